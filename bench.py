@@ -1,0 +1,385 @@
+"""Benchmark: images/s encode+decode (and achieved HBM GB/s vs peak) per BASELINE.json.
+
+Workload (BASELINE.json configs[1], "C2"): CIFAR-100-shaped synthetic dataset
+(50 000 x 32x32x3 u8, labels e % 100) resident in HBM; selective batch
+sampling with uniform weights over 100 classes, batch 512, seed 1234; every
+step is one epoch of the reference's draw stream (floor(50000/512) = 97
+batches per GPU): SBS draws (optb_sbs_next_dev) -> gather-encode of the
+drawn rows into exact128 containers (optb_encode_dev) -> decode of every
+container back to u8 rows (optb_decode_dev).  Containers are materialised in
+HBM between the kernels.  N GPUs: one process per GPU, each draws the global
+stream's batches t % N == rank (weak scaling, no collective on the data path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Rank 0 prints one JSON line.  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, compiled from /root/reference's sources)
+on the host cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_EXAMPLES = 50000
+N_CLASSES = 100
+BATCH = 512
+SEED = 1234
+DATA_SEED = 7  # RunConfig::data_seed (runner.hpp:34)
+P = 32 * 32 * 3
+BATCHES_PER_STEP = N_EXAMPLES // BATCH  # 97: one epoch (runner.cpp:52-57)
+MODE = 1  # ExactInt128, the reference default (runner.hpp:52)
+PER_CHUNK = 16
+METRIC = "images/sec encode+decode (and achieved HBM GB/s vs peak) at 1/2/4/8 B200"
+UNIT = "images/s"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def config(world):
+    return {"workload": "C2: CIFAR-100-shaped 50000x32x32x3 u8 dataset in HBM, SBS (uniform 100 classes, "
+                        "B=512, seed 1234) + exact128 gather-encode + decode to u8; 1 epoch = 97 batches "
+                        "per GPU per step",
+            "global_batch": BATCH, "batches_per_step_per_gpu": BATCHES_PER_STEP, "mode": "exact128",
+            "per_chunk": PER_CHUNK, "image": [32, 32, 3], "decode_out": "u8",
+            "parallelism": f"independent batch shards x{world} (t % N == rank)",
+            "l2": "flushed between steps (256 MiB write outside the per-step events)"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram read+write bytes per launch of the roofline kernel from the
+    committed ncu --set full summary (profiles/ncu_summary.json), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ---------------------------------------------------------------- reference arm
+def reference_rate(n_batches_sample: int, threads: int, repeats: int = 1):
+    """Time the reference CPU path (oracle/_ref = the reference compiled from
+    its own sources; else the C oracle port) on a bounded sample: SBS draws
+    with the reference BatchCursor, then per batch image_of gather +
+    codec::encode per chunk + codec::decode per chunk, batches split over
+    `threads` host threads.  Returns (images/s, kind, sample description)."""
+    import ctypes as ct
+
+    import oracle as O
+    labels = (np.arange(N_EXAMPLES) % N_CLASSES).astype(np.int32)
+    ds = O.synth_pixels(DATA_SEED, 0, N_EXAMPLES, P)
+    rates = []
+    if O.ref_available():
+        R = O.REF
+        off = np.zeros(N_CLASSES + 1, np.uint64)
+        mem = np.zeros(N_EXAMPLES, np.int64)
+        buf = ct.create_string_buffer(512)
+        R.ref_class_index(O.ptr(labels, O.i32p), N_EXAMPLES, N_CLASSES, O.ptr(off, O.u64p), O.ptr(mem, O.i64p),
+                          buf, 512)
+        w = np.full(N_CLASSES, 1.0 / N_CLASSES)
+        st = ct.c_int(0)
+        h = R.ref_cursor_create(O.ptr(w, O.f64p), N_CLASSES, BATCH, SEED, O.ptr(off, O.u64p), O.ptr(mem, O.i64p),
+                                ct.byref(st), buf, 512)
+        dsh = R.ref_dataset_create(O.ptr(ds, O.u8p), N_EXAMPLES, 32, 32, 3)
+        ex = np.zeros(n_batches_sample * BATCH, np.int64)
+        chk = ct.c_uint64(0)
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            R.ref_cursor_next(h, n_batches_sample, O.ptr(ex, O.i64p), None)
+            t_sbs = time.perf_counter() - t0
+            secs = R.ref_bench_roundtrip(dsh, MODE, O.ptr(ex, O.i64p), n_batches_sample, BATCH, threads, 0,
+                                         ct.byref(chk))
+            rates.append(n_batches_sample * BATCH / (secs + t_sbs))
+        R.ref_dataset_destroy(dsh)
+        R.ref_cursor_destroy(h)
+        kind = "reference"
+    else:
+        off, mem = O.class_index(labels, N_CLASSES)
+        cur = O.Cursor(O.sbs_plan([1.0 / N_CLASSES] * N_CLASSES, BATCH), off, mem, BATCH, SEED)
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            ex, _ = cur.next(n_batches_sample)
+            cont, _ = O.encode_stream(ds, ex, MODE, PER_CHUNK, BATCH, n_batches_sample)
+            O.decode_stream(cont, None, MODE, PER_CHUNK, P, BATCH, n_batches_sample)
+            rates.append(n_batches_sample * BATCH / (time.perf_counter() - t0))
+        kind, threads = "port", 1
+    sample = (f"{n_batches_sample} batches x {BATCH} images of the C2 stream (SBS draws + image_of gather + "
+              f"codec::encode/decode per 16-image chunk), {threads} host threads, median of {repeats}")
+    return statistics.median(rates), kind, sample, threads
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    sample_batches = max(threads * 2, 8)
+    for _ in range(args.warmup):
+        reference_rate(sample_batches, threads, 1)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, kind, sample, used = reference_rate(sample_batches, threads, 1)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": config(world), "impl": "reference",
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": kind, "sample": sample},
+            "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2105_00619_b200 as pkg
+    C, S = pkg.codec, pkg.sampler
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        ctx = pkg._lib.context(local)
+        ds = torch.empty((N_EXAMPLES, P), dtype=torch.uint8, device=dev)
+        pkg._lib.check(pkg._lib.lib.optb_synth_pixels_dev(ctx, DATA_SEED, 0, N_EXAMPLES, P,
+                                                          __import__("ctypes").c_void_p(ds.data_ptr()), P,
+                                                          __import__("ctypes").c_void_p(stream.cuda_stream)))
+        labels = torch.arange(N_EXAMPLES, device=dev, dtype=torch.int32) % N_CLASSES
+        plan = S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED)
+        offs, mem = S.class_index_dev(labels, N_CLASSES, device=local)
+        cur = S.BatchCursor.from_device_index(plan, offs, mem, device=local)
+        L = C.layout(MODE, PER_CHUNK, P, BATCH, BATCHES_PER_STEP)
+        cont, _ = C.alloc_stream(L, local)
+        rows = BATCH * BATCHES_PER_STEP
+        out = torch.empty((rows, P), dtype=torch.uint8, device=dev)
+        ex_buf = torch.empty(rows, dtype=torch.int64, device=dev)
+        cl_buf = torch.empty(rows, dtype=torch.int32, device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize(dev)
+    global_batches = BATCHES_PER_STEP * world
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def step(timed):
+        if timed:
+            ev[0].record(stream)
+        cur.next_dev(global_batches, shard=rank, n_shards=world, examples=ex_buf, classes=cl_buf, stream=stream)
+        if timed:
+            ev[1].record(stream)
+        C.encode_dev(L, ds, cont, row_index=ex_buf, stream=stream)
+        if timed:
+            ev[2].record(stream)
+        C.decode_dev(L, cont, out, stream=stream)
+        if timed:
+            ev[3].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step(False)
+        C.sync(local, stream)
+        launches0 = pkg._lib.launches(local)
+        per_step, t_sbs, t_enc, t_dec = [], [], [], []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with ClockSampler(local) as clk:
+            t_wall0 = time.perf_counter()
+            for _ in range(args.steps):
+                flush.zero_()
+                step(True)
+                ev[3].synchronize()
+                per_step.append(ev[0].elapsed_time(ev[3]))
+                t_sbs.append(ev[0].elapsed_time(ev[1]))
+                t_enc.append(ev[1].elapsed_time(ev[2]))
+                t_dec.append(ev[2].elapsed_time(ev[3]))
+            torch.cuda.synchronize(dev)
+            t_wall = time.perf_counter() - t_wall0
+        if world > 1:
+            dist.barrier()
+        C.sync(local, stream)
+        launches = pkg._lib.launches(local) - launches0
+
+    ms = sum(per_step) / len(per_step)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    images_per_step = rows * world
+    value = images_per_step / (ms / 1e3)
+
+    # roofline for the dominant kernel (per-launch algorithmic bytes / launch time)
+    enc_ms, dec_ms = statistics.mean(t_enc), statistics.mean(t_dec)
+    cont_bytes = C.container_bytes(L)
+    enc_bytes = rows * P + cont_bytes + rows * 8  # gathered rows + containers + row index
+    dec_bytes = cont_bytes + rows * P
+    peak, peak_kind = measured_peak()
+    if enc_ms >= dec_ms:
+        kname, kms, kbytes = "k_encode_exact_vec<16>", enc_ms, enc_bytes
+    else:
+        kname, kms, kbytes = "k_decode_exact_vec<16,u8>", dec_ms, dec_bytes
+    achieved = kbytes / (kms / 1e3) / 1e9
+    nsum = ncu_traffic()
+    traffic = None
+    if nsum and kname in nsum.get("kernels", {}):
+        traffic = nsum["kernels"][kname].get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
+                "algorithmic_bytes_per_launch": kbytes,
+                "kernels_ms": {"sbs": round(statistics.mean(t_sbs), 4), "encode": round(enc_ms, 4),
+                               "decode": round(dec_ms, 4)},
+                "encode_gbs": round(enc_bytes / (enc_ms / 1e3) / 1e9, 1),
+                "decode_gbs": round(dec_bytes / (dec_ms / 1e3) / 1e9, 1),
+                "step_gbs": round((enc_bytes + dec_bytes) / (ms / 1e3) / 1e9, 1)}
+
+    # e2e: dataset in pinned host memory; the gather-encode kernel reads the
+    # drawn rows over PCIe (H2D), decoded rows are copied back (D2H).
+    e2e = None
+    if args.e2e_steps > 0:
+        with torch.cuda.stream(stream):
+            ds_host = ds.cpu().pin_memory()
+            out_host = torch.empty((rows, P), dtype=torch.uint8).pin_memory()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+            def e2e_step():
+                cur.next_dev(global_batches, shard=rank, n_shards=world, examples=ex_buf, classes=cl_buf,
+                             stream=stream)
+                C.encode_dev(L, ds_host, cont, row_index=ex_buf, stream=stream)
+                C.decode_dev(L, cont, out, stream=stream)
+                out_host.copy_(out, non_blocking=True)
+            for _ in range(2):
+                e2e_step()
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            e0.record(stream)
+            for _ in range(args.e2e_steps):
+                e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+            ok = torch.equal(out_host[:BATCH], ds_host[ex_buf[:BATCH].cpu()])
+            if world > 1:
+                t = torch.tensor([e2e_ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e2e_ms = float(t.item())
+        e2e = {"value": round(images_per_step / (e2e_ms / 1e3), 1), "unit": UNIT,
+               "h2d_bytes_per_step": rows * P + 0, "d2h_bytes_per_step": rows * P,
+               "ms_per_step": round(e2e_ms, 3), "check": bool(ok),
+               "path": "optb_sbs_next_dev -> optb_encode_dev reading the pinned host dataset (zero-copy H2D of "
+                       "the drawn rows) -> optb_decode_dev -> D2H of the decoded rows to pinned host memory"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, kind, sample, used = reference_rate(max(threads * 2, 8), threads, 3)
+        cpu = {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": config(world),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 3)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,203 @@
+/*
+ * optb_cuda.h -- C ABI of the B200-native OpTorch data-flow path
+ * (encode / decode / selective batch sampling) for sm_100a.
+ *
+ * This is the drop-in boundary.  The reference (/root/reference/proj) has no
+ * FFI; its boundary is the C++ header API in include/optb/{codec,sampler}.hpp
+ * and nn.hpp.  Each entry point below names the reference function it
+ * replaces (file:line under /root/reference/proj).  The C++ headers with the
+ * reference's exact declarations are re-implemented over this ABI in
+ * paper_2105_00619_b200/csrc/shim (liboptb_shim.so), and bound from Python
+ * with ctypes in paper_2105_00619_b200/_lib.py; INTEGRATION.md shows both.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device memory;
+ *    "host" pointers are ordinary (pageable or pinned) host memory.
+ *  - Every function returns an optb_status.  On failure the message of the
+ *    calling thread is available from optb_last_error(); the text equals the
+ *    reference exception's what() (errors.hpp:9-42) wherever the reference
+ *    has one, so the shim rethrows the same class with the same message.
+ *  - *_dev entry points are asynchronous and stream-ordered (stream = a
+ *    cudaStream_t passed as void*, NULL = legacy default stream); they never
+ *    allocate.  Device-side format errors (decode range checks, bad labels)
+ *    are latched in the context and reported by optb_ctx_sync().  *_host
+ *    entry points are synchronous and report everything themselves.
+ *  - A context is bound to one device and is used by one host thread at a
+ *    time (the reference functions are reentrant: use one
+ *    context per thread).
+ *
+ * Device data layout
+ *  - images      rows of P = H*W*C u8 pixels, HWC (codec.hpp:56-62), rows
+ *                `row_stride` bytes apart.
+ *  - stream      n_batches batches of `batch` rows; batch b is split into
+ *                ceil(batch/per_chunk) chunks of per_chunk consecutive rows,
+ *                the last one partial (runner.cpp:77-90).
+ *  - containers  chunk k's plane is P words of Wc bytes at
+ *                containers + k*P*Wc, words little-endian (u64 / u128 lo,hi;
+ *                binary64 bits for f64) -- the OPTB payload order
+ *                (codec.cpp:298-312).  Wc = optb_container_value_bytes().
+ *  - offsets     (lossless modes) chunk k's parity plane, ceil(n_k*P/8)
+ *                bytes, bit i*P+p LSB-first (codec.cpp:101-104), at
+ *                offsets + k*optb_offsets_stride(mode, P, per_chunk).
+ *  - decoded     row r = b*batch + j*per_chunk + i at out + r*out_row_stride
+ *                elements (nn.cpp:177-191 row order).
+ */
+#ifndef OPTB_CUDA_H
+#define OPTB_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPTB_ABI_VERSION 1
+
+/* status codes <-> errors.hpp:9-42 */
+typedef enum optb_status {
+  OPTB_OK = 0,
+  OPTB_ERR = 1,          /* optb::Error (sampler and generic)      */
+  OPTB_ERR_SHAPE = 2,    /* optb::ShapeError                       */
+  OPTB_ERR_CAPACITY = 3, /* optb::CapacityError                    */
+  OPTB_ERR_FORMAT = 4,   /* optb::FormatError                      */
+  OPTB_ERR_CUDA = 5,     /* CUDA runtime failure (no reference twin) */
+  OPTB_ERR_ARG = 6       /* invalid argument to the C ABI itself   */
+} optb_status;
+
+/* codec modes -- CodecMode, codec.hpp:22-28 (same tags, also the OPTB tag) */
+enum { OPTB_EXACT64 = 0, OPTB_EXACT128 = 1, OPTB_F64 = 2, OPTB_LOSSLESS64 = 3, OPTB_LOSSLESS128 = 4 };
+/* decoded element types */
+enum { OPTB_OUT_U8 = 0, OPTB_OUT_F32 = 1, OPTB_OUT_F16 = 2, OPTB_OUT_BF16 = 3 };
+
+typedef struct optb_ctx optb_ctx;
+typedef struct optb_sbs optb_sbs;
+
+/* A batch stream (see "stream" above). */
+typedef struct optb_layout {
+  int32_t mode;        /* OPTB_EXACT64 ...                                  */
+  uint32_t per_chunk;  /* images per container, 1..optb_accept_limit(mode)  */
+  uint64_t pixels;     /* P = H*W*C                                         */
+  uint64_t batch;      /* rows per batch                                    */
+  uint64_t n_batches;  /* batches in the stream                             */
+} optb_layout;
+
+/* Decode epilogue (nn.cpp:183-189, 235).  For float outputs every element is
+ * RN(float(q) * scale) -- one binary32 multiply, never contracted -- then
+ * converted RNE to f16 (tensor.cpp:12-51) or bf16.  With per-class tables
+ * (the GPU form of the per-class preprocessing seam, sampler.hpp:39-40) row r
+ * uses c = row_class[r]: y = RN(RN(q*class_scale[c]) + class_bias[c]); a
+ * table of (scale, 0) reproduces the plain epilogue bit for bit. */
+typedef struct optb_epilogue {
+  int32_t out_dtype;          /* OPTB_OUT_*                                */
+  float scale;                /* e.g. 1/255 = 0x3b808081 (runner.hpp:22)  */
+  const float* class_scale;   /* dev, nullable                             */
+  const float* class_bias;    /* dev, nullable (requires class_scale)      */
+  const int32_t* row_class;   /* dev, required with class tables           */
+  uint64_t out_row_stride;    /* elements between output rows; 0 = P       */
+} optb_epilogue;
+
+/* ---------------------------------------------------------------- metadata
+ * codec.hpp:33-43, codec.cpp:13-62.  Unknown modes return 0 / "?". */
+uint32_t optb_abi_version(void);
+uint32_t optb_capacity(int32_t mode);
+uint32_t optb_accept_limit(int32_t mode);     /* capacity, or 16 for f64 (codec.hpp:36) */
+int32_t optb_capacity_is_hard(int32_t mode);
+const char* optb_mode_name(int32_t mode);
+int32_t optb_mode_has_offsets(int32_t mode);
+uint32_t optb_container_value_bytes(int32_t mode);
+uint64_t optb_offsets_plane_bytes(uint32_t n_images, uint64_t pixels); /* codec.cpp:75-77 */
+uint64_t optb_offsets_stride(int32_t mode, uint64_t pixels, uint32_t per_chunk);
+uint64_t optb_layout_chunks(const optb_layout* L);
+uint64_t optb_layout_rows(const optb_layout* L);
+uint64_t optb_layout_container_bytes(const optb_layout* L);
+uint64_t optb_layout_offsets_bytes(const optb_layout* L);
+/* Validates a layout like codec.cpp:79-97 (capacity message included). */
+int optb_layout_check(const optb_layout* L);
+
+/* ---------------------------------------------------------------- errors */
+const char* optb_last_error(void);  /* calling thread's last message ("" if none) */
+
+/* ---------------------------------------------------------------- context */
+int optb_ctx_create(int device, optb_ctx** out);
+void optb_ctx_destroy(optb_ctx* ctx);
+/* Synchronise `stream`, then report (and clear) any device-side error
+ * latched by earlier *_dev calls: decode range violations give
+ * OPTB_ERR_FORMAT with the reference message (codec.cpp:165-170, 191-194),
+ * bad labels give OPTB_ERR (sampler.cpp:58-61). */
+int optb_ctx_sync(optb_ctx* ctx, void* stream);
+/* Number of device kernels this context has launched (bench evidence). */
+uint64_t optb_ctx_launches(const optb_ctx* ctx);
+
+/* ---------------------------------------------------------------- codec, device
+ * Replaces codec::encode (codec.cpp:106-146) applied to every chunk of a
+ * stream, fused with the gather of Dataset::image_of (dataset.cpp:16-22) as
+ * driven by runner.cpp:77-90 / 278-290: stream row r reads image row
+ * row_index[r] (dev int64, nullable = identity) of `images`. */
+int optb_encode_dev(optb_ctx* ctx, const optb_layout* L, const uint8_t* images,
+                    uint64_t row_stride, const int64_t* row_index, void* containers,
+                    uint8_t* offsets, void* stream);
+
+/* Replaces codec::decode (codec.cpp:148-208) for every chunk, and with a
+ * float epilogue nn::decode_input (nn.cpp:153-192) + the MixedPrecision
+ * binary16 store (nn.cpp:141-146, 235): the layer input is written directly. */
+int optb_decode_dev(optb_ctx* ctx, const optb_layout* L, const void* containers,
+                    const uint8_t* offsets, const optb_epilogue* E, void* out, void* stream);
+
+/* ---------------------------------------------------------------- codec, host
+ * Same operations on host buffers (images [rows][P] contiguous; containers /
+ * offsets / decoded in the layouts above).  H2D and D2H run on side streams
+ * through pinned staging, overlapped slice by slice with the kernels.
+ * Synchronous; all errors reported on return. */
+int optb_encode_host(optb_ctx* ctx, const optb_layout* L, const uint8_t* images,
+                     void* containers, uint8_t* offsets);
+int optb_decode_host(optb_ctx* ctx, const optb_layout* L, const void* containers,
+                     const uint8_t* offsets, const optb_epilogue* E, void* out);
+
+/* ---------------------------------------------------------------- SBS
+ * sampler::plan (sampler.cpp:11-51): largest-remainder counts; host
+ * arithmetic (binary64), errors and messages as the reference. */
+int optb_sbs_plan(const double* weights, uint64_t n_classes, uint64_t batch, uint64_t* counts);
+
+/* ClassIndex::from_labels (sampler.cpp:53-65) on the GPU: a stable
+ * partition of [0,n) by label (warp match/ballot ranks + tile x class scan).
+ * class_offsets[C+1] and members[n] are dev outputs.  A label outside
+ * [0,C) latches OPTB_ERR "sampler: label L outside C classes" (first such
+ * example), reported by optb_ctx_sync. */
+int optb_class_index_dev(optb_ctx* ctx, const int32_t* labels, uint64_t n, uint64_t n_classes,
+                         uint64_t* class_offsets, int64_t* members, void* stream);
+
+/* BatchCursor(plan, index) (sampler.cpp:67-82): per-class permutations and
+ * the SplitMix64 chain live on the device.  counts[C] and class_offsets[C+1]
+ * are host arrays; members[class_offsets[C]] is dev (members_on_device=1) or
+ * host.  Runs the constructor's C reshuffles before returning. */
+int optb_sbs_create(optb_ctx* ctx, const uint64_t* counts, uint64_t n_classes, uint64_t batch,
+                    uint64_t seed, const uint64_t* class_offsets, const int64_t* members,
+                    int32_t members_on_device, optb_sbs** out);
+void optb_sbs_destroy(optb_sbs* sbs);
+
+/* BatchCursor::next (sampler.cpp:91-104) n_batches times.  Writes the
+ * class-major draws of the batches beta0 + t (t < n_batches) with
+ * t % n_shards == shard, in order, batch after batch: examples (dev int64)
+ * and classes (dev int32, nullable).  Every shard advances the cursor by
+ * n_batches, so n_shards processes calling with shard = 0..n_shards-1
+ * together reproduce the single-process stream with no communication. */
+int optb_sbs_next_dev(optb_sbs* sbs, uint64_t n_batches, uint32_t shard, uint32_t n_shards,
+                      int64_t* examples, int32_t* classes, void* stream);
+/* Same, all batches, host outputs (synchronous). */
+int optb_sbs_next_host(optb_sbs* sbs, uint64_t n_batches, int64_t* examples, int32_t* classes);
+uint64_t optb_sbs_batches_drawn(const optb_sbs* sbs);
+/* Testing aid: force the exact serial rejection-sampling path for every
+ * reshuffle (results are identical; only speed changes). */
+int optb_sbs_set_force_serial(optb_sbs* sbs, int32_t on);
+
+/* ---------------------------------------------------------------- synthetic data
+ * Counter-based u8 rows (bench / tests): w = mix(seed + (e*ceil(P/8) + p/8 + 1)*gamma),
+ * pixel = (w >> 8*(p%8)) & 0xff for dataset row e = first_row + r. */
+int optb_synth_pixels_dev(optb_ctx* ctx, uint64_t seed, uint64_t first_row, uint64_t n_rows,
+                          uint64_t pixels, uint8_t* out, uint64_t row_stride, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OPTB_CUDA_H */

@@ -1,0 +1,88 @@
+"""Build recipe for the native libraries (in-tree, sm_100a only).
+
+    liboptb_cuda.so  csrc/{codec,sbs,capi}.cu -> the C ABI of include/optb_cuda.h
+    liboptb_shim.so  csrc/shim/src/*.cpp       -> the reference's C++ API
+                     (optb::codec / optb::sampler / optb::Rng / decode_input)
+                     re-implemented over liboptb_cuda.so
+
+Called by __graft_entry__.build(); also runnable as
+``python -m paper_2105_00619_b200.build``.  Objects go to build/, the shared
+libraries next to this file so they travel with the repo snapshot.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+BUILD = os.path.join(ROOT, "build")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_LIB = "/usr/local/cuda/lib64"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+              "--expt-relaxed-constexpr", "-diag-suppress", "177", "-I" + INCLUDE]
+CUDA_SOURCES = ["codec.cu", "sbs.cu", "capi.cu"]
+CUDA_LIB_NAME = os.path.join(PKG, "liboptb_cuda.so")
+SHIM_LIB_NAME = os.path.join(PKG, "liboptb_shim.so")
+SHIM_SOURCES = ["codec.cpp", "sampler.cpp", "nn.cpp"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed: " + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    return r.stdout + r.stderr
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_cuda(force: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    headers = [os.path.join(CSRC, "internal.h"), os.path.join(INCLUDE, "optb_cuda.h")]
+    objs = []
+    jobs = []
+    for src in CUDA_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            jobs.append([NVCC] + ARCH + NVCC_FLAGS + ["-c", s, "-o", o])
+    with cf.ThreadPoolExecutor(max_workers=len(CUDA_SOURCES)) as ex:
+        list(ex.map(_run, jobs))
+    if force or _stale(CUDA_LIB_NAME, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", CUDA_LIB_NAME] + objs + ["-cudart", "static"])
+    return CUDA_LIB_NAME
+
+
+def build_shim(force: bool = False) -> str:
+    inc = os.path.join(CSRC, "shim", "include")
+    srcs = [os.path.join(CSRC, "shim", "src", f) for f in SHIM_SOURCES]
+    hdrs = [os.path.join(inc, "optb", h) for h in os.listdir(os.path.join(inc, "optb"))]
+    if force or _stale(SHIM_LIB_NAME, srcs + hdrs + [CUDA_LIB_NAME]):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + inc,
+              "-I" + INCLUDE] + srcs + ["-o", SHIM_LIB_NAME, "-L" + PKG, "-loptb_cuda",
+                                        "-Wl,-rpath,$ORIGIN"])
+    return SHIM_LIB_NAME
+
+
+def build(force: bool = False) -> None:
+    build_cuda(force)
+    if os.path.isdir(os.path.join(CSRC, "shim", "src")) and all(
+            os.path.exists(os.path.join(CSRC, "shim", "src", f)) for f in SHIM_SOURCES):
+        build_shim(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)
+    print("built", CUDA_LIB_NAME)

@@ -1,0 +1,1040 @@
+// capi.cu -- the C ABI (include/optb_cuda.h): validation with the reference's
+// error messages, contexts, the host staging pipeline, and the SBS host-side
+// event planner.  Kernels live in codec.cu and sbs.cu.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "optb_cuda.h"
+
+using namespace optb_b200;
+
+// ------------------------------------------------------------------ errors
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_err(cudaError_t e, const char* where) {
+  return set_err(OPTB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call, where)                          \
+  do {                                           \
+    cudaError_t _e = (call);                     \
+    if (_e != cudaSuccess) return cuda_err(_e, where); \
+  } while (0)
+
+bool valid_mode(int32_t m) { return m >= 0 && m <= 4; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ metadata
+extern "C" {
+
+uint32_t optb_abi_version(void) { return OPTB_ABI_VERSION; }
+
+uint32_t optb_capacity(int32_t mode) {  // codec.cpp:13-27
+  switch (mode) {
+    case OPTB_EXACT64: return 8;
+    case OPTB_EXACT128: return 16;
+    case OPTB_F64: return 6;
+    case OPTB_LOSSLESS64: return 9;
+    case OPTB_LOSSLESS128: return 18;
+  }
+  return 0;
+}
+
+uint32_t optb_accept_limit(int32_t mode) {
+  return mode == OPTB_F64 ? 16u : optb_capacity(mode);
+}
+
+int32_t optb_capacity_is_hard(int32_t mode) { return mode != OPTB_F64; }
+
+const char* optb_mode_name(int32_t mode) {  // codec.cpp:31-45
+  switch (mode) {
+    case OPTB_EXACT64: return "exact64";
+    case OPTB_EXACT128: return "exact128";
+    case OPTB_F64: return "f64";
+    case OPTB_LOSSLESS64: return "lossless64";
+    case OPTB_LOSSLESS128: return "lossless128";
+  }
+  return "?";
+}
+
+int32_t optb_mode_has_offsets(int32_t mode) {
+  return mode == OPTB_LOSSLESS64 || mode == OPTB_LOSSLESS128;
+}
+
+uint32_t optb_container_value_bytes(int32_t mode) {  // codec.cpp:51-62
+  switch (mode) {
+    case OPTB_EXACT64:
+    case OPTB_F64:
+    case OPTB_LOSSLESS64: return 8;
+    case OPTB_EXACT128:
+    case OPTB_LOSSLESS128: return 16;
+  }
+  return 0;
+}
+
+uint64_t optb_offsets_plane_bytes(uint32_t n, uint64_t pixels) {
+  return (static_cast<uint64_t>(n) * pixels + 7) / 8;
+}
+
+uint64_t optb_offsets_stride(int32_t mode, uint64_t pixels, uint32_t per_chunk) {
+  if (!optb_mode_has_offsets(mode)) return 0;
+  return (optb_offsets_plane_bytes(per_chunk, pixels) + 15) / 16 * 16;
+}
+
+uint64_t optb_layout_chunks(const optb_layout* L) {
+  if (!L || L->per_chunk == 0) return 0;
+  return L->n_batches * ((L->batch + L->per_chunk - 1) / L->per_chunk);
+}
+
+uint64_t optb_layout_rows(const optb_layout* L) { return L ? L->batch * L->n_batches : 0; }
+
+uint64_t optb_layout_container_bytes(const optb_layout* L) {
+  return optb_layout_chunks(L) * (L ? L->pixels : 0) * optb_container_value_bytes(L ? L->mode : -1);
+}
+
+uint64_t optb_layout_offsets_bytes(const optb_layout* L) {
+  if (!L) return 0;
+  return optb_layout_chunks(L) * optb_offsets_stride(L->mode, L->pixels, L->per_chunk);
+}
+
+int optb_layout_check(const optb_layout* L) {  // codec.cpp:79-97
+  if (!L) return set_err(OPTB_ERR_ARG, "layout: null");
+  if (!valid_mode(L->mode)) return set_err(OPTB_ERR, "unknown codec mode");
+  if (L->per_chunk == 0) return set_err(OPTB_ERR, "encode: batch must contain at least one image");
+  if (L->pixels == 0) return set_err(OPTB_ERR_SHAPE, "encode: image extents must be positive");
+  const uint32_t limit = optb_accept_limit(L->mode);
+  if (L->per_chunk > limit)
+    return set_err(OPTB_ERR_CAPACITY, "encode: %u images exceed %s capacity of %u", L->per_chunk,
+                   optb_mode_name(L->mode), limit);
+  if (L->batch == 0) return set_err(OPTB_ERR_ARG, "layout: batch must be positive");
+  g_err.clear();
+  return OPTB_OK;
+}
+
+const char* optb_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ context
+struct optb_ctx {
+  int device = 0;
+  int sms = 148;
+  DevError* d_err = nullptr;
+  uint64_t launches = 0;
+  cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  // host-API staging (2 slots)
+  static constexpr int kSlots = 2;
+  size_t slot_in = 0, slot_out = 0, slot_off = 0;
+  uint8_t* pin_in[kSlots] = {};
+  uint8_t* pin_out[kSlots] = {};
+  uint8_t* pin_off[kSlots] = {};
+  uint8_t* dev_in[kSlots] = {};
+  uint8_t* dev_out[kSlots] = {};
+  uint8_t* dev_off[kSlots] = {};
+  cudaEvent_t ev_h2d[kSlots] = {}, ev_kern[kSlots] = {}, ev_d2h[kSlots] = {};
+  // scratch for class index / sbs host outputs
+  uint32_t* ci_scratch = nullptr;
+  uint64_t ci_words = 0;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+};
+
+namespace {
+
+
+int reset_err(optb_ctx* c, cudaStream_t s) {
+  DevError z{0, 0, ~0ull, 0, 0};
+  CK(cudaMemcpyAsync(c->d_err, &z, sizeof z, cudaMemcpyHostToDevice, s), "reset error latch");
+  CK(cudaStreamSynchronize(s), "reset error latch");
+  return OPTB_OK;
+}
+
+Geom make_geom(const optb_layout* L) {
+  Geom g;
+  g.mode = L->mode;
+  g.per_chunk = L->per_chunk;
+  g.wc = optb_container_value_bytes(L->mode);
+  g.cpb = static_cast<uint32_t>((L->batch + L->per_chunk - 1) / L->per_chunk);
+  g.P = L->pixels;
+  g.B = L->batch;
+  g.chunks = optb_layout_chunks(L);
+  g.ostride = optb_offsets_stride(L->mode, L->pixels, L->per_chunk);
+  g.chunk_base = 0;
+  return g;
+}
+
+int check_epilogue(const optb_epilogue* E) {
+  if (!E) return set_err(OPTB_ERR_ARG, "decode: null epilogue");
+  if (E->out_dtype < OPTB_OUT_U8 || E->out_dtype > OPTB_OUT_BF16)
+    return set_err(OPTB_ERR_ARG, "decode: unknown output dtype %d", E->out_dtype);
+  if ((E->class_scale || E->class_bias) && !E->row_class)
+    return set_err(OPTB_ERR_ARG, "decode: class tables need row_class");
+  if (E->class_bias && !E->class_scale)
+    return set_err(OPTB_ERR_ARG, "decode: class_bias needs class_scale");
+  return OPTB_OK;
+}
+
+Epi make_epi(const optb_epilogue* E, uint64_t P) {
+  Epi e;
+  e.dtype = E->out_dtype;
+  e.scale = E->scale;
+  e.class_scale = E->class_scale;
+  e.class_bias = E->class_bias;
+  e.row_class = E->row_class;
+  e.row_stride = E->out_row_stride ? E->out_row_stride : P;
+  return e;
+}
+
+// Decode layout validation mirrors codec.cpp:150-158 (empty batch) and the
+// capacity header checks of read_optb (codec.cpp:338-344).
+int check_decode_layout(const optb_layout* L) {
+  if (!L) return set_err(OPTB_ERR_ARG, "layout: null");
+  if (!valid_mode(L->mode)) return set_err(OPTB_ERR, "unknown codec mode");
+  if (L->per_chunk == 0 || L->pixels == 0)
+    return set_err(OPTB_ERR_FORMAT, "decode: empty encoded batch");
+  if (L->per_chunk > optb_accept_limit(L->mode))
+    return set_err(OPTB_ERR_FORMAT, "optb: image count %u exceeds %s capacity", L->per_chunk,
+                   optb_mode_name(L->mode));
+  if (L->batch == 0) return set_err(OPTB_ERR_ARG, "layout: batch must be positive");
+  return OPTB_OK;
+}
+
+size_t out_elem_bytes(int dtype) {
+  return dtype == OPTB_OUT_U8 ? 1 : dtype == OPTB_OUT_F32 ? 4 : 2;
+}
+
+}  // namespace
+
+extern "C" {
+
+int optb_ctx_create(int device, optb_ctx** out) {
+  if (!out) return set_err(OPTB_ERR_ARG, "ctx: null output");
+  *out = nullptr;
+  int n = 0;
+  CK(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+  if (device < 0 || device >= n)
+    return set_err(OPTB_ERR_CUDA, "ctx: device %d not present (%d devices)", device, n);
+  CK(cudaSetDevice(device), "cudaSetDevice");
+  auto* c = new optb_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&c->d_err, sizeof(DevError)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->s_compute, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) != cudaSuccess) {
+    optb_ctx_destroy(c);
+    return cuda_err(cudaGetLastError(), "ctx create");
+  }
+  for (int i = 0; i < optb_ctx::kSlots; ++i) {
+    cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_kern[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming);
+  }
+  int st = reset_err(c, c->s_compute);
+  if (st) {
+    optb_ctx_destroy(c);
+    return st;
+  }
+  *out = c;
+  g_err.clear();
+  return OPTB_OK;
+}
+
+void optb_ctx_destroy(optb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < optb_ctx::kSlots; ++i) {
+    if (c->pin_in[i]) cudaFreeHost(c->pin_in[i]);
+    if (c->pin_out[i]) cudaFreeHost(c->pin_out[i]);
+    if (c->pin_off[i]) cudaFreeHost(c->pin_off[i]);
+    if (c->dev_in[i]) cudaFree(c->dev_in[i]);
+    if (c->dev_out[i]) cudaFree(c->dev_out[i]);
+    if (c->dev_off[i]) cudaFree(c->dev_off[i]);
+    if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+    if (c->ev_kern[i]) cudaEventDestroy(c->ev_kern[i]);
+    if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+  }
+  if (c->ci_scratch) cudaFree(c->ci_scratch);
+  if (c->tmp) cudaFree(c->tmp);
+  if (c->d_err) cudaFree(c->d_err);
+  if (c->s_compute) cudaStreamDestroy(c->s_compute);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  delete c;
+}
+
+uint64_t optb_ctx_launches(const optb_ctx* c) { return c ? c->launches : 0; }
+
+int optb_ctx_sync(optb_ctx* c, void* stream) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DevError h{};
+  CK(cudaStreamSynchronize(s), "stream synchronize");
+  CK(cudaMemcpyAsync(&h, c->d_err, sizeof h, cudaMemcpyDeviceToHost, c->s_compute), "read error latch");
+  CK(cudaStreamSynchronize(c->s_compute), "read error latch");
+  if (h.kind == kErrNone) {
+    g_err.clear();
+    return OPTB_OK;
+  }
+  int st = reset_err(c, c->s_compute);
+  if (st) return st;
+  const unsigned n = static_cast<unsigned>(h.key & 0xff);
+  switch (h.kind) {
+    case kErrIntRange:  // codec.cpp:191-194
+      return set_err(OPTB_ERR_FORMAT, "decode: container value exceeds range of %u packed images", n);
+    case kErrF64Range:  // codec.cpp:165-170
+      return set_err(OPTB_ERR_FORMAT, "decode: container value out of range for %u images", n);
+    case kErrLabel:  // sampler.cpp:58-61
+      return set_err(OPTB_ERR, "sampler: label %lld outside %llu classes",
+                     static_cast<long long>(h.label), static_cast<unsigned long long>(h.aux));
+  }
+  return set_err(OPTB_ERR, "device error %u", h.kind);
+}
+
+// ------------------------------------------------------------------ codec, device
+int optb_encode_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
+                    const int64_t* row_index, void* containers, uint8_t* offsets, void* stream) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!images || !containers || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "encode: null buffer");
+  if (row_stride == 0) row_stride = L->pixels;
+  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
+  const Geom g = make_geom(L);
+  cudaError_t e = launch_encode(g, images, row_stride, row_index, containers, offsets,
+                                static_cast<cudaStream_t>(stream), c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "encode launch");
+  return OPTB_OK;
+}
+
+int optb_decode_dev(optb_ctx* c, const optb_layout* L, const void* containers,
+                    const uint8_t* offsets, const optb_epilogue* E, void* out, void* stream) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = check_decode_layout(L);
+  if (st) return st;
+  st = check_epilogue(E);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "decode: null buffer");
+  const Epi ep = make_epi(E, L->pixels);
+  if (ep.row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "decode: out_row_stride < pixels");
+  const Geom g = make_geom(L);
+  cudaError_t e = launch_decode(g, containers, offsets, ep, out, c->d_err,
+                                static_cast<cudaStream_t>(stream), c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "decode launch");
+  return OPTB_OK;
+}
+
+int optb_synth_pixels_dev(optb_ctx* c, uint64_t seed, uint64_t first_row, uint64_t n_rows,
+                          uint64_t pixels, uint8_t* out, uint64_t row_stride, void* stream) {
+  if (!c || !out) return set_err(OPTB_ERR_ARG, "synth: null");
+  if (row_stride == 0) row_stride = pixels;
+  cudaError_t e = launch_synth(seed, first_row, n_rows, pixels, out, row_stride,
+                               static_cast<cudaStream_t>(stream), c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "synth launch");
+  return OPTB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ host pipeline
+namespace {
+
+struct Slice {
+  uint64_t row0, rows;       // stream rows [row0, row0 + rows)
+  uint64_t chunk0, chunks;   // chunks [chunk0, chunk0 + chunks)
+  optb_layout L;             // layout of the slice on its own
+};
+
+// Split a stream into slices of about `target` input bytes.  Whole batches
+// when a batch is small; otherwise runs of whole chunks inside one batch (a
+// run starting at a chunk boundary re-chunks identically).
+std::vector<Slice> plan_slices(const optb_layout* L, uint64_t bytes_per_row, uint64_t target) {
+  std::vector<Slice> out;
+  const uint64_t pc = L->per_chunk;
+  const uint64_t cpb = (L->batch + pc - 1) / pc;
+  const uint64_t batch_bytes = L->batch * bytes_per_row;
+  if (batch_bytes <= target) {
+    const uint64_t per = std::max<uint64_t>(1, target / batch_bytes);
+    for (uint64_t b = 0; b < L->n_batches; b += per) {
+      const uint64_t nb = std::min(per, L->n_batches - b);
+      Slice s;
+      s.row0 = b * L->batch;
+      s.rows = nb * L->batch;
+      s.chunk0 = b * cpb;
+      s.chunks = nb * cpb;
+      s.L = *L;
+      s.L.n_batches = nb;
+      out.push_back(s);
+    }
+    return out;
+  }
+  const uint64_t chunk_bytes = pc * bytes_per_row;
+  const uint64_t per_chunks = std::max<uint64_t>(1, target / chunk_bytes);
+  for (uint64_t b = 0; b < L->n_batches; ++b) {
+    for (uint64_t j = 0; j < cpb; j += per_chunks) {
+      const uint64_t nj = std::min(per_chunks, cpb - j);
+      const uint64_t r_begin = j * pc, r_end = std::min((j + nj) * pc, L->batch);
+      Slice s;
+      s.row0 = b * L->batch + r_begin;
+      s.rows = r_end - r_begin;
+      s.chunk0 = b * cpb + j;
+      s.chunks = nj;
+      s.L = *L;
+      s.L.batch = s.rows;
+      s.L.n_batches = 1;
+      out.push_back(s);
+    }
+  }
+  return out;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+int ensure_slots(optb_ctx* c, size_t in_b, size_t out_b, size_t off_b) {
+  if (c->slot_in < in_b || c->slot_out < out_b || c->slot_off < off_b) {
+    cudaDeviceSynchronize();
+    for (int i = 0; i < optb_ctx::kSlots; ++i) {
+      if (c->pin_in[i]) cudaFreeHost(c->pin_in[i]);
+      if (c->pin_out[i]) cudaFreeHost(c->pin_out[i]);
+      if (c->pin_off[i]) cudaFreeHost(c->pin_off[i]);
+      if (c->dev_in[i]) cudaFree(c->dev_in[i]);
+      if (c->dev_out[i]) cudaFree(c->dev_out[i]);
+      if (c->dev_off[i]) cudaFree(c->dev_off[i]);
+      c->pin_in[i] = c->pin_out[i] = c->pin_off[i] = nullptr;
+      c->dev_in[i] = c->dev_out[i] = c->dev_off[i] = nullptr;
+    }
+    c->slot_in = std::max(c->slot_in, in_b);
+    c->slot_out = std::max(c->slot_out, out_b);
+    c->slot_off = std::max<size_t>(std::max(c->slot_off, off_b), 16);
+    for (int i = 0; i < optb_ctx::kSlots; ++i) {
+      CK(cudaHostAlloc(&c->pin_in[i], c->slot_in, cudaHostAllocDefault), "pinned staging");
+      CK(cudaHostAlloc(&c->pin_out[i], c->slot_out, cudaHostAllocDefault), "pinned staging");
+      CK(cudaHostAlloc(&c->pin_off[i], c->slot_off, cudaHostAllocDefault), "pinned staging");
+      CK(cudaMalloc(&c->dev_in[i], c->slot_in), "device staging");
+      CK(cudaMalloc(&c->dev_out[i], c->slot_out), "device staging");
+      CK(cudaMalloc(&c->dev_off[i], c->slot_off), "device staging");
+    }
+  }
+  return OPTB_OK;
+}
+
+constexpr uint64_t kSliceTarget = 32ull << 20;
+
+}  // namespace
+
+extern "C" {
+
+// Host encode: images (host) -> containers/offsets (host).  Slices are
+// double-buffered: H2D on s_h2d, kernels on s_compute, D2H on s_d2h.
+int optb_encode_host(optb_ctx* c, const optb_layout* L, const uint8_t* images, void* containers,
+                     uint8_t* offsets) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const uint64_t P = L->pixels;
+  const uint32_t wc = optb_container_value_bytes(L->mode);
+  const uint64_t ost = optb_offsets_stride(L->mode, P, L->per_chunk);
+  const auto slices = plan_slices(L, P, kSliceTarget);
+  uint64_t max_rows = 0, max_chunks = 0;
+  for (const auto& s : slices) {
+    max_rows = std::max(max_rows, s.rows);
+    max_chunks = std::max(max_chunks, s.chunks);
+  }
+  st = ensure_slots(c, max_rows * P, max_chunks * P * wc, max_chunks * ost);
+  if (st) return st;
+  const bool pin_src = is_pinned(images), pin_dst = is_pinned(containers) &&
+                                                   (!ost || is_pinned(offsets));
+  auto copy_out = [&](size_t i) -> int {
+    const Slice& s = slices[i];
+    const int k = static_cast<int>(i % optb_ctx::kSlots);
+    CK(cudaEventSynchronize(c->ev_d2h[k]), "D2H");
+    if (!pin_dst) {
+      memcpy(static_cast<uint8_t*>(containers) + s.chunk0 * P * wc, c->pin_out[k], s.chunks * P * wc);
+      if (ost) memcpy(offsets + s.chunk0 * ost, c->pin_off[k], s.chunks * ost);
+    }
+    return OPTB_OK;
+  };
+  for (size_t i = 0; i < slices.size(); ++i) {
+    const Slice& s = slices[i];
+    const int k = static_cast<int>(i % optb_ctx::kSlots);
+    const uint8_t* src = images + s.row0 * P;
+    if (!pin_src) {
+      CK(cudaEventSynchronize(c->ev_h2d[k]), "H2D");
+      memcpy(c->pin_in[k], src, s.rows * P);
+      src = c->pin_in[k];
+    }
+    CK(cudaStreamWaitEvent(c->s_h2d, c->ev_kern[k], 0), "wait");
+    CK(cudaMemcpyAsync(c->dev_in[k], src, s.rows * P, cudaMemcpyHostToDevice, c->s_h2d), "H2D");
+    CK(cudaEventRecord(c->ev_h2d[k], c->s_h2d), "event");
+    CK(cudaStreamWaitEvent(c->s_compute, c->ev_h2d[k], 0), "wait");
+    CK(cudaStreamWaitEvent(c->s_compute, c->ev_d2h[k], 0), "wait");
+    const Geom g = make_geom(&s.L);
+    cudaError_t e = launch_encode(g, c->dev_in[k], P, nullptr, c->dev_out[k], c->dev_off[k],
+                                  c->s_compute, c->sms, &c->launches);
+    if (e != cudaSuccess) return cuda_err(e, "encode launch");
+    CK(cudaEventRecord(c->ev_kern[k], c->s_compute), "event");
+    CK(cudaStreamWaitEvent(c->s_d2h, c->ev_kern[k], 0), "wait");
+    uint8_t* dst = pin_dst ? static_cast<uint8_t*>(containers) + s.chunk0 * P * wc : c->pin_out[k];
+    CK(cudaMemcpyAsync(dst, c->dev_out[k], s.chunks * P * wc, cudaMemcpyDeviceToHost, c->s_d2h), "D2H");
+    if (ost) {
+      uint8_t* od = pin_dst ? offsets + s.chunk0 * ost : c->pin_off[k];
+      CK(cudaMemcpyAsync(od, c->dev_off[k], s.chunks * ost, cudaMemcpyDeviceToHost, c->s_d2h), "D2H");
+    }
+    CK(cudaEventRecord(c->ev_d2h[k], c->s_d2h), "event");
+    if (i >= 1) {
+      st = copy_out(i - 1);
+      if (st) return st;
+    }
+  }
+  st = copy_out(slices.size() - 1);
+  if (st) return st;
+  CK(cudaStreamSynchronize(c->s_d2h), "sync");
+  g_err.clear();
+  return OPTB_OK;
+}
+
+int optb_decode_host(optb_ctx* c, const optb_layout* L, const void* containers,
+                     const uint8_t* offsets, const optb_epilogue* E, void* out) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = check_decode_layout(L);
+  if (st) return st;
+  st = check_epilogue(E);
+  if (st) return st;
+  if (E->class_scale || E->row_class)
+    return set_err(OPTB_ERR_ARG, "decode_host: class tables are device-side; use optb_decode_dev");
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const uint64_t P = L->pixels;
+  const uint32_t wc = optb_container_value_bytes(L->mode);
+  const uint64_t ost = optb_offsets_stride(L->mode, P, L->per_chunk);
+  const size_t es = out_elem_bytes(E->out_dtype);
+  const uint64_t ors = E->out_row_stride ? E->out_row_stride : P;
+  if (ors != P) return set_err(OPTB_ERR_ARG, "decode_host: out_row_stride must be 0 or P");
+  // slice on container bytes per row (one chunk of per_chunk rows is P*wc)
+  const auto slices = plan_slices(L, (P * wc + L->per_chunk - 1) / L->per_chunk, kSliceTarget);
+  uint64_t max_rows = 0, max_chunks = 0;
+  for (const auto& s : slices) {
+    max_rows = std::max(max_rows, s.rows);
+    max_chunks = std::max(max_chunks, s.chunks);
+  }
+  st = ensure_slots(c, max_chunks * P * wc, max_rows * P * es, max_chunks * ost);
+  if (st) return st;
+  st = reset_err(c, c->s_compute);
+  if (st) return st;
+  const bool pin_src = is_pinned(containers) && (!ost || is_pinned(offsets));
+  const bool pin_dst = is_pinned(out);
+  auto copy_out = [&](size_t i) -> int {
+    const Slice& s = slices[i];
+    const int k = static_cast<int>(i % optb_ctx::kSlots);
+    CK(cudaEventSynchronize(c->ev_d2h[k]), "D2H");
+    if (!pin_dst) memcpy(static_cast<uint8_t*>(out) + s.row0 * P * es, c->pin_out[k], s.rows * P * es);
+    return OPTB_OK;
+  };
+  for (size_t i = 0; i < slices.size(); ++i) {
+    const Slice& s = slices[i];
+    const int k = static_cast<int>(i % optb_ctx::kSlots);
+    const uint8_t* src = static_cast<const uint8_t*>(containers) + s.chunk0 * P * wc;
+    const uint8_t* osrc = ost ? offsets + s.chunk0 * ost : nullptr;
+    if (!pin_src) {
+      CK(cudaEventSynchronize(c->ev_h2d[k]), "H2D");
+      memcpy(c->pin_in[k], src, s.chunks * P * wc);
+      src = c->pin_in[k];
+      if (ost) {
+        memcpy(c->pin_off[k], osrc, s.chunks * ost);
+        osrc = c->pin_off[k];
+      }
+    }
+    CK(cudaStreamWaitEvent(c->s_h2d, c->ev_kern[k], 0), "wait");
+    CK(cudaMemcpyAsync(c->dev_in[k], src, s.chunks * P * wc, cudaMemcpyHostToDevice, c->s_h2d), "H2D");
+    if (ost)
+      CK(cudaMemcpyAsync(c->dev_off[k], osrc, s.chunks * ost, cudaMemcpyHostToDevice, c->s_h2d), "H2D");
+    CK(cudaEventRecord(c->ev_h2d[k], c->s_h2d), "event");
+    CK(cudaStreamWaitEvent(c->s_compute, c->ev_h2d[k], 0), "wait");
+    CK(cudaStreamWaitEvent(c->s_compute, c->ev_d2h[k], 0), "wait");
+    Geom g = make_geom(&s.L);
+    g.chunk_base = s.chunk0;
+    Epi ep = make_epi(E, P);
+    cudaError_t e = launch_decode(g, c->dev_in[k], c->dev_off[k], ep, c->dev_out[k], c->d_err,
+                                  c->s_compute, c->sms, &c->launches);
+    if (e != cudaSuccess) return cuda_err(e, "decode launch");
+    CK(cudaEventRecord(c->ev_kern[k], c->s_compute), "event");
+    CK(cudaStreamWaitEvent(c->s_d2h, c->ev_kern[k], 0), "wait");
+    uint8_t* dst = pin_dst ? static_cast<uint8_t*>(out) + s.row0 * P * es : c->pin_out[k];
+    CK(cudaMemcpyAsync(dst, c->dev_out[k], s.rows * P * es, cudaMemcpyDeviceToHost, c->s_d2h), "D2H");
+    CK(cudaEventRecord(c->ev_d2h[k], c->s_d2h), "event");
+    if (i >= 1) {
+      st = copy_out(i - 1);
+      if (st) return st;
+    }
+  }
+  st = copy_out(slices.size() - 1);
+  if (st) return st;
+  return optb_ctx_sync(c, c->s_d2h);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ SBS
+struct optb_sbs {
+  optb_ctx* ctx = nullptr;
+  uint64_t C = 0, B = 0, N = 0;
+  std::vector<uint64_t> counts, m, off, prefix, gen;
+  uint64_t batches = 0;
+  int force_serial = 0;
+  bool small_ids = true;  // every example id < 2^32 (shared-memory shuffle)
+  uint32_t max_m = 0;
+  // device
+  int64_t* d_pool = nullptr;  // [N current permutations][generation area]
+  uint64_t pool_cap = 0;      // elements
+  unsigned long long* d_chain = nullptr;
+  uint8_t* d_static = nullptr;  // counts[C] prefix[C+1] size[C] row_cls[B]
+  uint8_t* d_call = nullptr;
+  size_t call_cap = 0;
+  uint8_t* h_call = nullptr;
+  size_t h_call_cap = 0;
+  cudaEvent_t uploaded = nullptr;
+  // scratch for next_host
+  int64_t* d_ex = nullptr;
+  int32_t* d_cl = nullptr;
+  uint64_t ex_cap = 0;
+};
+
+namespace {
+
+// Packs per-call arrays into one pinned block and uploads it.
+struct Packer {
+  std::vector<uint8_t> buf;
+  template <typename T>
+  size_t put(const T* p, size_t n) {
+    size_t at = (buf.size() + 15) / 16 * 16;
+    buf.resize(at + n * sizeof(T));
+    if (n) memcpy(buf.data() + at, p, n * sizeof(T));
+    return at;
+  }
+  size_t reserve(size_t bytes) {
+    size_t at = (buf.size() + 15) / 16 * 16;
+    buf.resize(at + bytes);
+    return at;
+  }
+};
+
+int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
+  const size_t bytes = std::max<size_t>(pk.buf.size(), 16);
+  if (s->uploaded) CK(cudaEventSynchronize(s->uploaded), "sbs upload");
+  if (s->h_call_cap < bytes) {
+    if (s->h_call) cudaFreeHost(s->h_call);
+    s->h_call = nullptr;
+    CK(cudaHostAlloc(&s->h_call, bytes * 2, cudaHostAllocDefault), "sbs pinned");
+    s->h_call_cap = bytes * 2;
+  }
+  if (s->call_cap < bytes) {
+    if (s->d_call) {
+      CK(cudaStreamSynchronize(st), "sbs sync");
+      cudaFree(s->d_call);
+    }
+    s->d_call = nullptr;
+    CK(cudaMalloc(&s->d_call, bytes * 2), "sbs call block");
+    s->call_cap = bytes * 2;
+  }
+  memcpy(s->h_call, pk.buf.data(), pk.buf.size());
+  CK(cudaMemcpyAsync(s->d_call, s->h_call, bytes, cudaMemcpyHostToDevice, st), "sbs upload");
+  CK(cudaEventRecord(s->uploaded, st), "sbs upload");
+  return OPTB_OK;
+}
+
+int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st) {
+  if (s->pool_cap >= elems) return OPTB_OK;
+  const uint64_t cap = std::max<uint64_t>(elems, s->pool_cap * 3 / 2);
+  int64_t* p = nullptr;
+  CK(cudaMalloc(&p, cap * sizeof(int64_t)), "sbs pool");
+  if (s->d_pool) {
+    CK(cudaMemcpyAsync(p, s->d_pool, s->N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st), "sbs pool");
+    CK(cudaStreamSynchronize(st), "sbs pool");
+    cudaFree(s->d_pool);
+  }
+  s->d_pool = p;
+  s->pool_cap = cap;
+  return OPTB_OK;
+}
+
+struct EvKey {
+  uint64_t beta, cls, g;
+  uint64_t t;  // index within the class's events of this call (1-based)
+};
+
+// Runs the chain + shuffle kernels for an ordered event list.  `evs` are in
+// chain order; per-class lists for K9 are derived here.
+int run_events(optb_sbs* s, const std::vector<SbsEvent>& evs, const std::vector<uint64_t>& cls_copy_of,
+               const std::vector<uint64_t>& cls_final_of, Packer& pk, size_t* off_gather,
+               cudaStream_t st, bool with_gather_block, const std::vector<uint64_t>& gather_arrays) {
+  const uint64_t E = evs.size();
+  // K9 work lists: classes (m >= 2) with events, events in generation order
+  std::vector<std::vector<uint32_t>> per(s->C);
+  for (uint64_t e = 0; e < E; ++e)
+    if (evs[e].m >= 2) per[evs[e].cls].push_back(static_cast<uint32_t>(e));
+  std::vector<uint32_t> begin{0}, list;
+  std::vector<uint64_t> ccopy, cfinal;
+  for (uint64_t c = 0; c < s->C; ++c) {
+    if (per[c].empty()) continue;
+    for (uint32_t e : per[c]) list.push_back(e);
+    begin.push_back(static_cast<uint32_t>(list.size()));
+    ccopy.push_back(cls_copy_of[c]);
+    cfinal.push_back(cls_final_of[c]);
+  }
+  const size_t o_ev = pk.put(evs.data(), E);
+  const size_t o_seeds = pk.reserve((E + 1) * sizeof(uint64_t));
+  const size_t o_flags = pk.reserve((E + 1) * sizeof(uint32_t));
+  const size_t o_begin = pk.put(begin.data(), begin.size());
+  const size_t o_list = pk.put(list.data(), list.size());
+  const size_t o_copy = pk.put(ccopy.data(), ccopy.size());
+  const size_t o_final = pk.put(cfinal.data(), cfinal.size());
+  if (with_gather_block) *off_gather = pk.put(gather_arrays.data(), gather_arrays.size());
+  int rc = upload_call(s, pk, st);
+  if (rc) return rc;
+  uint8_t* d = s->d_call;
+  const SbsEvent* d_ev = reinterpret_cast<const SbsEvent*>(d + o_ev);
+  uint64_t* d_seeds = reinterpret_cast<uint64_t*>(d + o_seeds);
+  uint32_t* d_flags = reinterpret_cast<uint32_t*>(d + o_flags);
+  if (E > 0) {
+    cudaError_t e = launch_sbs_chain(d_ev, E, s->d_chain, d_seeds, d_flags, s->force_serial, st,
+                                     &s->ctx->launches);
+    if (e != cudaSuccess) return cuda_err(e, "sbs chain");
+    const uint32_t ncls = static_cast<uint32_t>(ccopy.size());
+    e = launch_sbs_shuffle(d_ev, reinterpret_cast<const uint32_t*>(d + o_begin),
+                           reinterpret_cast<const uint32_t*>(d + o_list),
+                           reinterpret_cast<const uint64_t*>(d + o_copy),
+                           reinterpret_cast<const uint64_t*>(d + o_final), ncls, d_seeds, d_flags,
+                           s->d_pool, s->small_ids ? s->max_m : 0xffffffffu, st, &s->ctx->launches);
+    if (e != cudaSuccess) return cuda_err(e, "sbs shuffle");
+  }
+  return OPTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int optb_sbs_plan(const double* w, uint64_t C, uint64_t B, uint64_t* counts) {
+  // sampler.cpp:11-51
+  if (C == 0) return set_err(OPTB_ERR, "sampler: at least one class weight required");
+  if (B == 0) return set_err(OPTB_ERR, "sampler: batch size must be positive");
+  if (!w || !counts) return set_err(OPTB_ERR_ARG, "sampler: null buffer");
+  double sum = 0.0;
+  for (uint64_t c = 0; c < C; ++c) {
+    if (w[c] < 0.0)
+      return set_err(OPTB_ERR, "sampler: negative weight for class %llu", (unsigned long long)c);
+    sum += w[c];
+  }
+  if (std::abs(sum - 1.0) > 1e-9)
+    return set_err(OPTB_ERR, "sampler: class weights sum to %s, expected 1",
+                   std::to_string(sum).c_str());
+  std::vector<double> rem(C);
+  std::vector<uint64_t> order(C);
+  uint64_t assigned = 0;
+  for (uint64_t c = 0; c < C; ++c) {
+    const double exact = w[c] * static_cast<double>(B);
+    counts[c] = static_cast<uint64_t>(std::floor(exact));
+    rem[c] = exact - std::floor(exact);
+    assigned += counts[c];
+    order[c] = c;
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint64_t a, uint64_t b) { return rem[a] > rem[b]; });
+  for (uint64_t k = 0; assigned < B; ++k) {
+    counts[order[k % C]] += 1;
+    ++assigned;
+  }
+  g_err.clear();
+  return OPTB_OK;
+}
+
+int optb_class_index_dev(optb_ctx* c, const int32_t* labels, uint64_t n, uint64_t C,
+                         uint64_t* class_offsets, int64_t* members, void* stream) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  if (C == 0) return set_err(OPTB_ERR_ARG, "class index: no classes");
+  if (C > 50000) return set_err(OPTB_ERR_ARG, "class index: more than 50000 classes unsupported");
+  if (n >= (1ull << 32)) return set_err(OPTB_ERR_ARG, "class index: n >= 2^32 unsupported");
+  const uint64_t words = std::max<uint64_t>(class_index_scratch_words(n, C), 1);
+  if (c->ci_words < words) {
+    if (c->ci_scratch) cudaFree(c->ci_scratch);
+    c->ci_scratch = nullptr;
+    c->ci_words = 0;
+    CK(cudaMalloc(&c->ci_scratch, words * sizeof(uint32_t)), "class index scratch");
+    c->ci_words = words;
+  }
+  cudaError_t e = launch_class_index(labels, n, C, class_offsets, members, c->ci_scratch,
+                                     c->ci_words, c->d_err, static_cast<cudaStream_t>(stream),
+                                     &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "class index launch");
+  return OPTB_OK;
+}
+
+int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B, uint64_t seed,
+                    const uint64_t* class_offsets, const int64_t* members, int32_t on_dev,
+                    optb_sbs** out) {
+  if (!c || !out || !counts || !class_offsets) return set_err(OPTB_ERR_ARG, "sbs: null argument");
+  *out = nullptr;
+  if (C == 0) return set_err(OPTB_ERR, "sampler: at least one class weight required");
+  uint64_t total = 0;
+  for (uint64_t k = 0; k < C; ++k) total += counts[k];
+  if (total != B)
+    return set_err(OPTB_ERR_ARG, "sbs: counts sum to %llu, batch is %llu", (unsigned long long)total,
+                   (unsigned long long)B);
+  for (uint64_t k = 0; k < C; ++k) {  // sampler.cpp:75-79
+    if (class_offsets[k + 1] < class_offsets[k]) return set_err(OPTB_ERR_ARG, "sbs: offsets not monotone");
+    if (counts[k] > 0 && class_offsets[k + 1] == class_offsets[k])
+      return set_err(OPTB_ERR, "sampler: class %llu has no examples but a positive batch count",
+                     (unsigned long long)k);
+  }
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  auto* s = new optb_sbs();
+  s->ctx = c;
+  s->C = C;
+  s->B = B;
+  s->N = class_offsets[C];
+  s->counts.assign(counts, counts + C);
+  s->off.assign(class_offsets, class_offsets + C + 1);
+  s->m.resize(C);
+  s->gen.assign(C, 0);
+  s->prefix.assign(C + 1, 0);
+  for (uint64_t k = 0; k < C; ++k) {
+    s->m[k] = s->off[k + 1] - s->off[k];
+    s->prefix[k + 1] = s->prefix[k] + counts[k];
+    if (s->m[k] >= 2) s->max_m = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(s->max_m, s->m[k]), 0xffffffffull));
+    if (s->m[k] >= (1ull << 32)) s->small_ids = false;
+  }
+  cudaStream_t st = c->s_compute;
+  auto fail = [&](int code) {
+    optb_sbs_destroy(s);
+    return code;
+  };
+  if (cudaEventCreateWithFlags(&s->uploaded, cudaEventDisableTiming) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs event"));
+  if (cudaMalloc(&s->d_chain, sizeof(unsigned long long)) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs chain"));
+  int rc = ensure_pool(s, std::max<uint64_t>(s->N, 1), st);
+  if (rc) return fail(rc);
+  if (s->N) {
+    if (on_dev) {
+      if (cudaMemcpyAsync(s->d_pool, members, s->N * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return fail(cuda_err(cudaGetLastError(), "sbs members"));
+    } else {
+      for (uint64_t i = 0; i < s->N; ++i)
+        if (members[i] < 0 || static_cast<uint64_t>(members[i]) >= (1ull << 32)) s->small_ids = false;
+      if (cudaMemcpy(s->d_pool, members, s->N * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(cuda_err(cudaGetLastError(), "sbs members"));
+    }
+  }
+  // static device arrays: counts, prefix, class sizes, row -> class
+  {
+    std::vector<uint32_t> row_cls(B);
+    for (uint64_t k = 0; k < C; ++k)
+      for (uint64_t r = s->prefix[k]; r < s->prefix[k + 1]; ++r) row_cls[r] = static_cast<uint32_t>(k);
+    Packer pk;
+    pk.put(s->counts.data(), C);
+    pk.put(s->prefix.data(), C + 1);
+    pk.put(s->m.data(), C);
+    pk.put(row_cls.data(), B);
+    if (cudaMalloc(&s->d_static, pk.buf.size() + 16) != cudaSuccess ||
+        cudaMemcpy(s->d_static, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(cuda_err(cudaGetLastError(), "sbs static"));
+  }
+  const unsigned long long seed64 = seed;
+  if (cudaMemcpy(s->d_chain, &seed64, 8, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs seed"));
+  // constructor events: every class in order, shuffled in place (sampler.cpp:73-81)
+  std::vector<SbsEvent> evs(C);
+  std::vector<uint64_t> none(C, ~0ull);
+  for (uint64_t k = 0; k < C; ++k) {
+    evs[k].cls = static_cast<uint32_t>(k);
+    evs[k].m = static_cast<uint32_t>(std::min<uint64_t>(s->m[k], 0xffffffffull));
+    evs[k].slot = evs[k].src = s->off[k];
+  }
+  Packer pk;
+  size_t unused = 0;
+  rc = run_events(s, evs, none, none, pk, &unused, st, false, {});
+  if (rc) return fail(rc);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail(cuda_err(cudaGetLastError(), "sbs ctor"));
+  *out = s;
+  g_err.clear();
+  return OPTB_OK;
+}
+
+void optb_sbs_destroy(optb_sbs* s) {
+  if (!s) return;
+  cudaDeviceSynchronize();
+  if (s->d_pool) cudaFree(s->d_pool);
+  if (s->d_chain) cudaFree(s->d_chain);
+  if (s->d_static) cudaFree(s->d_static);
+  if (s->d_call) cudaFree(s->d_call);
+  if (s->h_call) cudaFreeHost(s->h_call);
+  if (s->uploaded) cudaEventDestroy(s->uploaded);
+  if (s->d_ex) cudaFree(s->d_ex);
+  if (s->d_cl) cudaFree(s->d_cl);
+  delete s;
+}
+
+uint64_t optb_sbs_batches_drawn(const optb_sbs* s) { return s ? s->batches : 0; }
+
+int optb_sbs_set_force_serial(optb_sbs* s, int32_t on) {
+  if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
+  s->force_serial = on ? 1 : 0;
+  return OPTB_OK;
+}
+
+int optb_sbs_next_dev(optb_sbs* s, uint64_t n, uint32_t shard, uint32_t n_shards,
+                      int64_t* examples, int32_t* classes, void* stream) {
+  if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
+  if (n_shards == 0 || shard >= n_shards) return set_err(OPTB_ERR_ARG, "sbs: bad shard %u of %u", shard, n_shards);
+  if (n == 0) return OPTB_OK;
+  if (!examples) return set_err(OPTB_ERR_ARG, "sbs: null examples");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t C = s->C;
+  // ---- events of this call (lazy reshuffles, sampler.cpp:97): class c's
+  // draw D triggers generation D/m when D % m == 0 and D > 0.
+  std::vector<EvKey> keys;
+  std::vector<uint64_t> ev_count(C, 0);
+  for (uint64_t c = 0; c < C; ++c) {
+    const uint64_t cnt = s->counts[c], m = s->m[c];
+    if (cnt == 0 || m == 0) continue;
+    const uint64_t D1 = (s->batches + n) * cnt;
+    for (uint64_t g = s->gen[c] + 1; g * m < D1; ++g) {
+      keys.push_back({(g * m) / cnt, c, g, g - s->gen[c]});
+      ++ev_count[c];
+    }
+  }
+  std::sort(keys.begin(), keys.end(), [](const EvKey& a, const EvKey& b) {
+    if (a.beta != b.beta) return a.beta < b.beta;
+    if (a.cls != b.cls) return a.cls < b.cls;
+    return a.g < b.g;
+  });
+  // ---- generation pool layout: class c with E_c events gets E_c + 1 slots
+  // (slot 0 = copy of the current generation) after the N current entries.
+  std::vector<uint64_t> base(C, 0), copy_of(C, ~0ull), final_of(C, ~0ull);
+  uint64_t cursor = s->N;
+  for (uint64_t c = 0; c < C; ++c) {
+    if (ev_count[c] == 0 || s->m[c] < 2) continue;
+    base[c] = cursor;
+    copy_of[c] = cursor;
+    final_of[c] = s->off[c];
+    cursor += (ev_count[c] + 1) * s->m[c];
+  }
+  int rc = ensure_pool(s, std::max<uint64_t>(cursor, 1), st);
+  if (rc) return rc;
+  std::vector<SbsEvent> evs(keys.size());
+  for (size_t e = 0; e < keys.size(); ++e) {
+    const uint64_t c = keys[e].cls, m = s->m[c], t = keys[e].t;
+    evs[e].cls = static_cast<uint32_t>(c);
+    evs[e].m = static_cast<uint32_t>(m);
+    if (m >= 2) {
+      evs[e].slot = base[c] + t * m;
+      evs[e].src = (t == 1) ? s->off[c] : base[c] + (t - 1) * m;
+    } else {
+      evs[e].slot = evs[e].src = s->off[c];
+    }
+  }
+  // ---- gather tables (K10)
+  std::vector<uint64_t> ga(4 * C);
+  for (uint64_t c = 0; c < C; ++c) {
+    const bool pooled = ev_count[c] > 0 && s->m[c] >= 2;
+    ga[c] = s->batches * s->counts[c];                   // drawn_before
+    ga[C + c] = s->gen[c];                               // generation in slot 0
+    ga[2 * C + c] = pooled ? base[c] : s->off[c];        // its pool offset
+    ga[3 * C + c] = s->m[c] >= 2 ? s->m[c] : 0;          // stride (0: never changes)
+  }
+  Packer pk;
+  size_t o_ga = 0;
+  rc = run_events(s, evs, copy_of, final_of, pk, &o_ga, st, true, ga);
+  if (rc) return rc;
+  const uint64_t* d_ga = reinterpret_cast<const uint64_t*>(s->d_call + o_ga);
+  SbsGatherArgs a;
+  const uint8_t* stat = s->d_static;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = (o + 15) / 16 * 16;
+    o = at + bytes;
+    return stat + at;
+  };
+  a.counts = reinterpret_cast<const uint64_t*>(take(C * 8));
+  a.prefix = reinterpret_cast<const uint64_t*>(take((C + 1) * 8));
+  a.class_size = reinterpret_cast<const uint64_t*>(take(C * 8));
+  a.row_cls = reinterpret_cast<const uint32_t*>(take(s->B * 4));
+  a.drawn_before = d_ga;
+  a.gen_base_gen = d_ga + C;
+  a.gen_base_off = d_ga + 2 * C;
+  a.gen_stride = d_ga + 3 * C;
+  a.pool = s->d_pool;
+  a.C = C;
+  a.B = s->B;
+  a.n_batches = n;
+  a.shard = shard;
+  a.n_shards = n_shards;
+  cudaError_t e = launch_sbs_gather(a, examples, classes, st, &s->ctx->launches);
+  if (e != cudaSuccess) return cuda_err(e, "sbs gather");
+  for (uint64_t c = 0; c < C; ++c) s->gen[c] += ev_count[c];
+  s->batches += n;
+  return OPTB_OK;
+}
+
+int optb_sbs_next_host(optb_sbs* s, uint64_t n, int64_t* examples, int32_t* classes) {
+  if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
+  if (n == 0) return OPTB_OK;
+  const uint64_t rows = n * s->B;
+  if (s->ex_cap < rows) {
+    if (s->d_ex) cudaFree(s->d_ex);
+    if (s->d_cl) cudaFree(s->d_cl);
+    s->d_ex = nullptr;
+    s->d_cl = nullptr;
+    s->ex_cap = 0;
+    CK(cudaMalloc(&s->d_ex, rows * 8), "sbs scratch");
+    CK(cudaMalloc(&s->d_cl, rows * 4), "sbs scratch");
+    s->ex_cap = rows;
+  }
+  cudaStream_t st = s->ctx->s_compute;
+  int rc = optb_sbs_next_dev(s, n, 0, 1, s->d_ex, s->d_cl, st);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(examples, s->d_ex, rows * 8, cudaMemcpyDeviceToHost, st), "sbs D2H");
+  if (classes) CK(cudaMemcpyAsync(classes, s->d_cl, rows * 4, cudaMemcpyDeviceToHost, st), "sbs D2H");
+  CK(cudaStreamSynchronize(st), "sbs sync");
+  g_err.clear();
+  return OPTB_OK;
+}
+
+}  // extern "C"

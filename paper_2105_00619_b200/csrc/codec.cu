@@ -1,0 +1,713 @@
+// codec.cu -- sm_100a encode / decode kernels for the optb container modes.
+//
+// Reference semantics (file:line under /root/reference/proj):
+//   encode  codec.cpp:106-146   decode  codec.cpp:148-208
+//   gather  dataset.cpp:16-22 + runner.cpp:77-90 (chunking of a batch)
+//   float epilogue  nn.cpp:183-189 (float(q)*scale), fp16 store nn.cpp:235 ->
+//   tensor.cpp:12-51 (RNE; __float2half_rn is bit-identical on q*scale values,
+//   SURVEY App. B).
+//
+// Kernel families:
+//   K1 encode_exact_vec<WC>   16-pixel x 16-image register byte transpose
+//                             (PRMT), 128-bit loads of gathered rows, XOR-
+//                             swizzled warp-private smem staging, fully
+//                             coalesced 128-bit container stores.
+//   K2 decode_exact_vec<WC,O> coalesced 128-bit container loads into swizzled
+//                             smem, register transpose, u8 rows stored
+//                             directly (128-bit) or via a u8 smem tile and a
+//                             fused float/half/bf16 epilogue (coalesced).
+//   K3/K4 lossless, K5/K6 f64 and unaligned shapes: one pixel per lane,
+//                             warp ballots for the parity plane.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace optb_b200 {
+namespace {
+
+constexpr int kWarps = 8;            // warps per CTA for the vector kernels
+constexpr int kThreads = kWarps * 32;
+
+__device__ __forceinline__ uint4 ldg16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg8(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg16(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void stg8(void* p, uint2 v) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// 4x4 byte transpose of rows a0..a3 (row r's byte c -> row c's byte r).
+__device__ __forceinline__ void t4x4(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+  const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a0, a1, 0x7362);
+  const uint32_t t2 = __byte_perm(a2, a3, 0x5140), t3 = __byte_perm(a2, a3, 0x7362);
+  a0 = __byte_perm(t0, t2, 0x5410);
+  a1 = __byte_perm(t0, t2, 0x7632);
+  a2 = __byte_perm(t1, t3, 0x5410);
+  a3 = __byte_perm(t1, t3, 0x7632);
+}
+
+// 16x16 byte transpose, m[r][q] holds bytes 4q..4q+3 of row r.  ROWS / COLS
+// bound the live part (rows >= ROWS are zero, columns >= COLS are unused):
+// exact64 uses 8 of the 16 image columns / rows.
+template <int ROWS, int COLS>
+__device__ __forceinline__ void transpose16(uint32_t (&m)[16][4]) {
+  uint32_t t[16][4];
+#pragma unroll
+  for (int R = 0; R < 4; ++R) {
+#pragma unroll
+    for (int Q = 0; Q < 4; ++Q) {
+      if (4 * Q >= COLS) continue;
+      uint32_t a0 = 4 * R + 0 < ROWS ? m[4 * R + 0][Q] : 0u;
+      uint32_t a1 = 4 * R + 1 < ROWS ? m[4 * R + 1][Q] : 0u;
+      uint32_t a2 = 4 * R + 2 < ROWS ? m[4 * R + 2][Q] : 0u;
+      uint32_t a3 = 4 * R + 3 < ROWS ? m[4 * R + 3][Q] : 0u;
+      t4x4(a0, a1, a2, a3);
+      t[4 * Q + 0][R] = a0;
+      t[4 * Q + 1][R] = a1;
+      t[4 * Q + 2][R] = a2;
+      t[4 * Q + 3][R] = a3;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m[r][q] = (r < COLS) ? t[r][q] : 0u;
+}
+
+struct ChunkPos {
+  uint64_t r0;  // first stream row of the chunk
+  uint32_t n;   // images in the chunk
+};
+
+__device__ __forceinline__ ChunkPos chunk_pos(const Geom& g, uint64_t k) {
+  const uint64_t b = k / g.cpb;
+  const uint32_t j = static_cast<uint32_t>(k - b * g.cpb);
+  const uint64_t first = static_cast<uint64_t>(j) * g.per_chunk;
+  const uint64_t left = g.B - first;
+  ChunkPos c;
+  c.r0 = b * g.B + first;
+  c.n = left < g.per_chunk ? static_cast<uint32_t>(left) : g.per_chunk;
+  return c;
+}
+
+__device__ __forceinline__ void latch_error(DevError* err, uint32_t kind, uint64_t chunk,
+                                            uint32_t n) {
+  atomicCAS(&err->kind, 0u, kind);
+  atomicMin(&err->key, static_cast<unsigned long long>((chunk << 8) | n));
+}
+
+// ------------------------------------------------------------------ epilogue
+struct Out4 {
+  // store 4 consecutive decoded pixels q (bytes of `q4`) of row `row` at `dst`
+  template <int O>
+  static __device__ __forceinline__ void put(void* dst, uint32_t q4, float s, float b, bool affine) {
+    float y[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float v = __fmul_rn(static_cast<float>((q4 >> (8 * k)) & 0xffu), s);
+      y[k] = affine ? __fadd_rn(v, b) : v;
+    }
+    if constexpr (O == OPTB_OUT_F32) {
+      float4 f = make_float4(y[0], y[1], y[2], y[3]);
+      stg16(dst, *reinterpret_cast<uint4*>(&f));
+    } else if constexpr (O == OPTB_OUT_F16) {
+      const __half h0 = __float2half_rn(y[0]), h1 = __float2half_rn(y[1]);
+      const __half h2 = __float2half_rn(y[2]), h3 = __float2half_rn(y[3]);
+      uint2 u;
+      u.x = static_cast<uint32_t>(__half_as_ushort(h0)) |
+            (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+      u.y = static_cast<uint32_t>(__half_as_ushort(h2)) |
+            (static_cast<uint32_t>(__half_as_ushort(h3)) << 16);
+      stg8(dst, u);
+    } else {
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(y[0]), h1 = __float2bfloat16_rn(y[1]);
+      const __nv_bfloat16 h2 = __float2bfloat16_rn(y[2]), h3 = __float2bfloat16_rn(y[3]);
+      uint2 u;
+      u.x = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
+            (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+      u.y = static_cast<uint32_t>(__bfloat16_as_ushort(h2)) |
+            (static_cast<uint32_t>(__bfloat16_as_ushort(h3)) << 16);
+      stg8(dst, u);
+    }
+  }
+};
+
+template <int O>
+__device__ __forceinline__ void put1(void* out, uint64_t idx, uint32_t q, float s, float b,
+                                     bool affine) {
+  if constexpr (O == OPTB_OUT_U8) {
+    static_cast<uint8_t*>(out)[idx] = static_cast<uint8_t>(q);
+  } else {
+    const float v0 = __fmul_rn(static_cast<float>(q), s);
+    const float y = affine ? __fadd_rn(v0, b) : v0;
+    if constexpr (O == OPTB_OUT_F32) {
+      static_cast<float*>(out)[idx] = y;
+    } else if constexpr (O == OPTB_OUT_F16) {
+      static_cast<__half*>(out)[idx] = __float2half_rn(y);
+    } else {
+      static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(y);
+    }
+  }
+}
+
+__device__ __forceinline__ void row_affine(const Epi& e, uint64_t row, float& s, float& b,
+                                           bool& affine) {
+  s = e.scale;
+  b = 0.0f;
+  affine = false;
+  if (e.class_scale) {
+    const int32_t c = __ldg(e.row_class + row);
+    s = __ldg(e.class_scale + c);
+    if (e.class_bias) {
+      b = __ldg(e.class_bias + c);
+      affine = true;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K1
+// One work item = 16 consecutive pixels of one chunk; items are linear in
+// (chunk, group) so a warp's 32 items cover 32*16*WC contiguous container
+// bytes.  Requires P % 16 == 0, 16-byte aligned rows and containers.
+template <int WC>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_encode_exact_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
+                       const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont) {
+  constexpr int NI = WC;  // images per container word
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* sw = smem_raw + warp * (32 * 16 * WC);
+  const uint64_t G = g.P / 16;
+  const uint64_t items = g.chunks * G;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
+  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32; base < items;
+       base += stride) {
+    const uint64_t t = base + lane;
+    uint32_t m[16][4];
+    if (t < items) {
+      const uint64_t k = t / G;
+      const uint64_t gi = t - k * G;
+      const ChunkPos c = chunk_pos(g, k);
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (i < static_cast<int>(c.n)) {
+          const uint64_t r = c.r0 + i;
+          const uint64_t src = row_index ? static_cast<uint64_t>(__ldg(row_index + r)) : r;
+          v = ldg16(images + src * row_stride + gi * 16);
+        }
+        m[i][0] = v.x;
+        m[i][1] = v.y;
+        m[i][2] = v.z;
+        m[i][3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NI; ++i) m[i][0] = m[i][1] = m[i][2] = m[i][3] = 0u;
+    }
+    transpose16<NI, 16>(m);  // m[p] = word of pixel p (bytes = images 0..15)
+    // stage: word p of lane L at slot (p ^ (L & SW)) of L's row (bank-conflict free)
+    constexpr int SW = (WC == 16) ? 7 : 15;
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const int slot = p ^ (lane & SW);
+      if constexpr (WC == 16) {
+        *reinterpret_cast<uint4*>(sw + (lane * 16 + slot) * 16) =
+            make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
+      } else {
+        *reinterpret_cast<uint2*>(sw + (lane * 16 + slot) * 8) = make_uint2(m[p][0], m[p][1]);
+      }
+    }
+    __syncwarp();
+    uint8_t* dst = cont + base * 16 * WC;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int W = q * 32 + lane, L = W >> 4, p = W & 15;
+      if (base + L < items) {
+        const int slot = p ^ (L & SW);
+        if constexpr (WC == 16) {
+          stg16(dst + W * 16, *reinterpret_cast<const uint4*>(sw + (L * 16 + slot) * 16));
+        } else {
+          stg8(dst + W * 8, *reinterpret_cast<const uint2*>(sw + (L * 16 + slot) * 8));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ K2
+template <int WC, int O>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_decode_exact_vec(Geom g, const uint8_t* __restrict__ cont, Epi e, void* __restrict__ out,
+                       DevError* err) {
+  constexpr int NI = WC;
+  constexpr int SW = (WC == 16) ? 7 : 15;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* sw = smem_raw + warp * (32 * 16 * 16);
+  const uint64_t G = g.P / 16;
+  const uint64_t items = g.chunks * G;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
+  const uint64_t ostride = e.row_stride;
+  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32; base < items;
+       base += stride) {
+    // coalesced container loads -> swizzled warp-private smem
+    const uint8_t* src = cont + base * 16 * WC;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int W = q * 32 + lane, L = W >> 4, p = W & 15;
+      if (base + L < items) {
+        const int slot = p ^ (L & SW);
+        if constexpr (WC == 16) {
+          *reinterpret_cast<uint4*>(sw + (L * 16 + slot) * 16) = ldg16(src + W * 16);
+        } else {
+          *reinterpret_cast<uint2*>(sw + (L * 16 + slot) * 8) = ldg8(src + W * 8);
+        }
+      }
+    }
+    __syncwarp();
+    uint32_t m[16][4];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const int slot = p ^ (lane & SW);
+      if constexpr (WC == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(sw + (lane * 16 + slot) * 16);
+        m[p][0] = v.x;
+        m[p][1] = v.y;
+        m[p][2] = v.z;
+        m[p][3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(sw + (lane * 16 + slot) * 8);
+        m[p][0] = v.x;
+        m[p][1] = v.y;
+        m[p][2] = 0u;
+        m[p][3] = 0u;
+      }
+    }
+    transpose16<16, NI>(m);  // m[i] = 16 pixels of image i
+    const uint64_t t = base + lane;
+    const bool valid = t < items;
+    uint64_t k = 0, gi = 0;
+    ChunkPos c{0, 0};
+    if (valid) {
+      k = t / G;
+      gi = t - k * G;
+      c = chunk_pos(g, k);
+      // range check (codec.cpp:189-194): bytes of images >= n must be zero
+      uint32_t hi = 0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
+      if (hi) latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
+    }
+    if constexpr (O == OPTB_OUT_U8) {
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+          if (i < static_cast<int>(c.n))
+            stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16,
+                  make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]));
+      }
+      __syncwarp();
+    } else {
+      __syncwarp();  // all lanes done reading the container stage
+      // u8 tile: image i, lane L's 16 pixels at (i*32 + L)*16
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        *reinterpret_cast<uint4*>(sw + (i * 32 + lane) * 16) =
+            make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]);
+      __syncwarp();
+      // epilogue: lane handles pixels 4*(lane%4).. of source lane L = lane/4 + 8*cc
+      constexpr int ES = (O == OPTB_OUT_F32) ? 4 : 2;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int L = (lane >> 2) + 8 * cc;
+        const uint32_t r0lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0), L);
+        const uint32_t r0hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0 >> 32), L);
+        const uint32_t nL = __shfl_sync(0xffffffffu, valid ? c.n : 0u, L);
+        const uint32_t glo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi), L);
+        const uint32_t ghi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi >> 32), L);
+        const uint64_t r0L = (static_cast<uint64_t>(r0hi) << 32) | r0lo;
+        const uint64_t gL = (static_cast<uint64_t>(ghi) << 32) | glo;
+        const uint64_t px = gL * 16 + 4 * (lane & 3);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          if (i < static_cast<int>(nL)) {
+            const uint32_t q4 = *reinterpret_cast<const uint32_t*>(sw + (i * 32 + L) * 16 +
+                                                                     4 * (lane & 3));
+            const uint64_t row = r0L + i;
+            float s, b;
+            bool aff;
+            row_affine(e, row, s, b, aff);
+            Out4::put<O>(static_cast<uint8_t*>(out) + (row * ostride + px) * ES, q4, s, b, aff);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ generic
+// One pixel per lane; any P, any alignment; all five modes.  Items are linear
+// in (chunk, pixel), so a warp's lanes are consecutive pixels of (at most two)
+// chunks.  Lossless parity bits are accumulated with warp ballots and written
+// with atomicOr into a zeroed plane (covers unaligned bit offsets).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_encode_generic(Geom g, const uint8_t* __restrict__ images,
+                                                        uint64_t row_stride,
+                                                        const int64_t* __restrict__ row_index,
+                                                        uint8_t* __restrict__ cont,
+                                                        uint8_t* __restrict__ offsets) {
+  constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
+  constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
+  constexpr int MAXN = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128) ? 16
+                       : (MODE == OPTB_F64) ? 16 : (MODE == OPTB_LOSSLESS64) ? 9 : 18;
+  const uint64_t items = g.chunks * g.P;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
+       t0 < items; t0 += gstride) {
+    const uint64_t t = t0 + lane;
+    const bool valid = t < items;
+    uint64_t k = 0, p = 0;
+    ChunkPos c{0, 0};
+    if (valid) {
+      k = t / g.P;
+      p = t - k * g.P;
+      c = chunk_pos(g, k);
+    }
+    unsigned __int128 acc = 0;
+    double dacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXN; ++i) {
+      uint32_t px = 0;
+      const bool has = valid && i < static_cast<int>(c.n);
+      if (has) {
+        const uint64_t r = c.r0 + i;
+        const uint64_t src = row_index ? static_cast<uint64_t>(__ldg(row_index + r)) : r;
+        px = __ldg(images + src * row_stride + p);
+        if constexpr (MODE == OPTB_F64) {
+          // codec.cpp:116-120: acc += px * 256^i in binary64, i ascending
+          dacc = __dadd_rn(dacc, __dmul_rn(static_cast<double>(px), ldexp(1.0, 8 * i)));
+        } else if constexpr (OFFS) {
+          acc |= static_cast<unsigned __int128>(px >> 1) << (7 * i);
+        } else {
+          acc |= static_cast<unsigned __int128>(px) << (8 * i);
+        }
+      }
+      if constexpr (OFFS) {
+        // parity bit i*P + p of chunk k (codec.cpp:132-133)
+        const uint32_t bits = __ballot_sync(0xffffffffu, has && (px & 1u));
+        const uint32_t inchunk = __ballot_sync(0xffffffffu, has);
+        if (has) {
+          // the first lane of each same-chunk run writes that run's bits
+          const uint32_t same = __match_any_sync(inchunk, k);
+          const int lead = __ffs(same) - 1;
+          if (lane == lead) {
+            const uint32_t seg = (bits & same) >> lead;
+            if (seg) {
+              const uint64_t bit = static_cast<uint64_t>(i) * g.P + p;  // p of the leader
+              uint32_t* plane = reinterpret_cast<uint32_t*>(offsets + k * g.ostride);
+              const uint64_t w = bit >> 5;
+              const uint32_t sh = static_cast<uint32_t>(bit & 31);
+              atomicOr(plane + w, seg << sh);
+              if (sh && (seg >> (32 - sh))) atomicOr(plane + w + 1, seg >> (32 - sh));
+            }
+          }
+        }
+      }
+    }
+    if (valid) {
+      uint8_t* w = cont + t * WC;
+      if constexpr (MODE == OPTB_F64) {
+        *reinterpret_cast<double*>(w) = dacc;
+      } else if constexpr (WC == 8) {
+        *reinterpret_cast<uint64_t*>(w) = static_cast<uint64_t>(acc);
+      } else {
+        reinterpret_cast<uint64_t*>(w)[0] = static_cast<uint64_t>(acc);
+        reinterpret_cast<uint64_t*>(w)[1] = static_cast<uint64_t>(acc >> 64);
+      }
+    }
+  }
+}
+
+template <int MODE, int O>
+__global__ void __launch_bounds__(256) k_decode_generic(Geom g, const uint8_t* __restrict__ cont,
+                                                        const uint8_t* __restrict__ offsets, Epi e,
+                                                        void* __restrict__ out, DevError* err) {
+  constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
+  constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
+  constexpr int MAXN = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128) ? 16
+                       : (MODE == OPTB_F64) ? 16 : (MODE == OPTB_LOSSLESS64) ? 9 : 18;
+  constexpr unsigned PER = OFFS ? 7u : 8u;
+  const uint64_t items = g.chunks * g.P;
+  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < items;
+       t += gstride) {
+    const uint64_t k = t / g.P;
+    const uint64_t p = t - k * g.P;
+    const ChunkPos c = chunk_pos(g, k);
+    const uint8_t* w = cont + t * WC;
+    if constexpr (MODE == OPTB_F64) {
+      double acc = *reinterpret_cast<const double*>(w);
+      // codec.cpp:163-170
+      const bool check = c.n <= 6u;
+      const double limit = ldexp(1.0, 8 * static_cast<int>(c.n));
+      if (!(acc >= 0.0) || (check && acc >= limit)) {
+        latch_error(err, kErrF64Range, g.chunk_base + k, c.n);
+        continue;
+      }
+#pragma unroll
+      for (int i = 0; i < MAXN; ++i) {
+        if (i < static_cast<int>(c.n)) {
+          const double q = fmod(acc, 256.0);           // exact
+          acc = __dmul_rn(__dsub_rn(acc, q), 0x1.0p-8);  // exact
+          const uint64_t row = c.r0 + i;
+          float s, b;
+          bool aff;
+          row_affine(e, row, s, b, aff);
+          put1<O>(out, row * e.row_stride + p, static_cast<uint32_t>(q), s, b, aff);
+        }
+      }
+    } else {
+      unsigned __int128 acc;
+      if constexpr (WC == 8) {
+        acc = *reinterpret_cast<const uint64_t*>(w);
+      } else {
+        acc = (static_cast<unsigned __int128>(reinterpret_cast<const uint64_t*>(w)[1]) << 64) |
+              reinterpret_cast<const uint64_t*>(w)[0];
+      }
+      const unsigned used = PER * c.n;
+      if (used < WC * 8u && (acc >> used) != 0) {  // codec.cpp:189-194
+        latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
+        continue;
+      }
+      const uint8_t* plane = OFFS ? offsets + k * g.ostride : nullptr;
+#pragma unroll
+      for (int i = 0; i < MAXN; ++i) {
+        if (i < static_cast<int>(c.n)) {
+          uint32_t q = static_cast<uint32_t>(acc >> (PER * i)) & ((1u << PER) - 1u);
+          if constexpr (OFFS) {
+            const uint64_t bit = static_cast<uint64_t>(i) * g.P + p;
+            q = (q << 1) | ((__ldg(plane + (bit >> 3)) >> (bit & 7)) & 1u);
+          }
+          const uint64_t row = c.r0 + i;
+          float s, b;
+          bool aff;
+          row_affine(e, row, s, b, aff);
+          put1<O>(out, row * e.row_stride + p, q, s, b, aff);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ synth
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uint64_t P,
+                        uint8_t* out, uint64_t row_stride) {
+  const uint64_t words = (P + 7) / 8;
+  const uint64_t total = n_rows * words;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = t / words, q = t - r * words;
+    const uint64_t w = mix64(seed + ((first_row + r) * words + q + 1) * 0x9e3779b97f4a7c15ull);
+    uint8_t* dst = out + r * row_stride + q * 8;
+    if (q * 8 + 8 <= P && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+      *reinterpret_cast<uint64_t*>(dst) = w;
+    } else {
+      for (uint64_t b = 0; b < 8 && q * 8 + b < P; ++b) dst[b] = static_cast<uint8_t>(w >> (8 * b));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+template <typename K>
+int grid_for(K kernel, int threads, size_t smem, int num_sms, uint64_t work_units) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t want = (work_units + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(per_sm) * num_sms;
+  return static_cast<int>(want < cap ? (want ? want : 1) : cap);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int MODE>
+cudaError_t enc_generic(const Geom& g, const uint8_t* images, uint64_t row_stride,
+                        const int64_t* idx, void* cont, uint8_t* offs, cudaStream_t s, int sms,
+                        uint64_t* launches) {
+  if (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128) {
+    cudaError_t st = cudaMemsetAsync(offs, 0, g.chunks * g.ostride, s);
+    if (st != cudaSuccess) return st;
+  }
+  const int grid = grid_for(k_encode_generic<MODE>, 256, 0, sms, g.chunks * g.P);
+  k_encode_generic<MODE><<<grid, 256, 0, s>>>(g, images, row_stride, idx,
+                                              static_cast<uint8_t*>(cont), offs);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int MODE, int O>
+cudaError_t dec_generic(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e,
+                        void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  const int grid = grid_for(k_decode_generic<MODE, O>, 256, 0, sms, g.chunks * g.P);
+  k_decode_generic<MODE, O><<<grid, 256, 0, s>>>(g, static_cast<const uint8_t*>(cont), offs, e,
+                                                 out, err);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int WC>
+cudaError_t enc_vec(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* idx,
+                    void* cont, cudaStream_t s, int sms, uint64_t* launches) {
+  const size_t smem = kWarps * 32 * 16 * WC;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_encode_exact_vec<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  const uint64_t items = g.chunks * (g.P / 16);
+  const int grid = grid_for(k_encode_exact_vec<WC>, kThreads, smem, sms, items);
+  k_encode_exact_vec<WC><<<grid, kThreads, smem, s>>>(g, images, row_stride, idx,
+                                                      static_cast<uint8_t*>(cont));
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int WC, int O>
+cudaError_t dec_vec(const Geom& g, const void* cont, const Epi& e, void* out, DevError* err,
+                    cudaStream_t s, int sms, uint64_t* launches) {
+  const size_t smem = kWarps * 32 * 16 * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_decode_exact_vec<WC, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  const uint64_t items = g.chunks * (g.P / 16);
+  const int grid = grid_for(k_decode_exact_vec<WC, O>, kThreads, smem, sms, items);
+  k_decode_exact_vec<WC, O><<<grid, kThreads, smem, s>>>(g, static_cast<const uint8_t*>(cont), e,
+                                                         out, err);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t dec_generic_any(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e,
+                            void* out, DevError* err, cudaStream_t s, int sms, uint64_t* l) {
+  switch (e.dtype) {
+    case OPTB_OUT_U8: return dec_generic<MODE, OPTB_OUT_U8>(g, cont, offs, e, out, err, s, sms, l);
+    case OPTB_OUT_F32: return dec_generic<MODE, OPTB_OUT_F32>(g, cont, offs, e, out, err, s, sms, l);
+    case OPTB_OUT_F16: return dec_generic<MODE, OPTB_OUT_F16>(g, cont, offs, e, out, err, s, sms, l);
+    default: return dec_generic<MODE, OPTB_OUT_BF16>(g, cont, offs, e, out, err, s, sms, l);
+  }
+}
+
+template <int WC>
+cudaError_t dec_vec_any(const Geom& g, const void* cont, const Epi& e, void* out, DevError* err,
+                        cudaStream_t s, int sms, uint64_t* l) {
+  switch (e.dtype) {
+    case OPTB_OUT_U8: return dec_vec<WC, OPTB_OUT_U8>(g, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_F32: return dec_vec<WC, OPTB_OUT_F32>(g, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_F16: return dec_vec<WC, OPTB_OUT_F16>(g, cont, e, out, err, s, sms, l);
+    default: return dec_vec<WC, OPTB_OUT_BF16>(g, cont, e, out, err, s, sms, l);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_stride,
+                          const int64_t* row_index, void* containers, uint8_t* offsets,
+                          cudaStream_t s, int sms, uint64_t* launches) {
+  const bool exact = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128;
+  const bool vec = exact && g.P % 16 == 0 && row_stride % 16 == 0 && aligned16(images) &&
+                   aligned16(containers);
+  if (vec) {
+    return g.wc == 16 ? enc_vec<16>(g, images, row_stride, row_index, containers, s, sms, launches)
+                      : enc_vec<8>(g, images, row_stride, row_index, containers, s, sms, launches);
+  }
+  switch (g.mode) {
+    case OPTB_EXACT64:
+      return enc_generic<OPTB_EXACT64>(g, images, row_stride, row_index, containers, offsets, s,
+                                       sms, launches);
+    case OPTB_EXACT128:
+      return enc_generic<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s,
+                                        sms, launches);
+    case OPTB_F64:
+      return enc_generic<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms,
+                                   launches);
+    case OPTB_LOSSLESS64:
+      return enc_generic<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s,
+                                          sms, launches);
+    default:
+      return enc_generic<OPTB_LOSSLESS128>(g, images, row_stride, row_index, containers, offsets,
+                                           s, sms, launches);
+  }
+}
+
+cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* offsets,
+                          const Epi& e, void* out, DevError* err, cudaStream_t s, int sms,
+                          uint64_t* launches) {
+  const bool exact = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128;
+  const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
+  const bool vec = exact && g.P % 16 == 0 && aligned16(containers) && aligned16(out) &&
+                   (e.row_stride * es) % 16 == 0;
+  if (vec) {
+    return g.wc == 16 ? dec_vec_any<16>(g, containers, e, out, err, s, sms, launches)
+                      : dec_vec_any<8>(g, containers, e, out, err, s, sms, launches);
+  }
+  switch (g.mode) {
+    case OPTB_EXACT64:
+      return dec_generic_any<OPTB_EXACT64>(g, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_EXACT128:
+      return dec_generic_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_F64:
+      return dec_generic_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_LOSSLESS64:
+      return dec_generic_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms,
+                                              launches);
+    default:
+      return dec_generic_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms,
+                                               launches);
+  }
+}
+
+cudaError_t launch_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uint64_t P,
+                         uint8_t* out, uint64_t row_stride, cudaStream_t s, int sms,
+                         uint64_t* launches) {
+  const uint64_t words = n_rows * ((P + 7) / 8);
+  const int grid = grid_for(k_synth, 256, 0, sms, words);
+  k_synth<<<grid, 256, 0, s>>>(seed, first_row, n_rows, P, out, row_stride);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace optb_b200

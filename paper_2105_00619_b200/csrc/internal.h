@@ -1,0 +1,99 @@
+// internal.h -- declarations shared between the C-ABI layer (capi.cu) and the
+// kernel translation units (codec.cu, sbs.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "optb_cuda.h"
+
+namespace optb_b200 {
+
+// Device-side error latch owned by a context (see optb_ctx_sync).
+struct DevError {
+  uint32_t kind;         // 0 none, 1 int range, 2 f64 range, 3 label
+  uint32_t pad;
+  unsigned long long key;  // int/f64 range: (chunk << 8) | n ; label: example index
+  long long label;         // offending label value (kind 3)
+  unsigned long long aux;  // label: number of classes
+};
+enum : uint32_t { kErrNone = 0, kErrIntRange = 1, kErrF64Range = 2, kErrLabel = 3 };
+
+// Geometry of a batch stream (optb_layout + derived values).
+struct Geom {
+  int32_t mode;
+  uint32_t per_chunk;
+  uint32_t wc;          // container bytes per pixel
+  uint32_t cpb;         // chunks per batch
+  uint64_t P;
+  uint64_t B;
+  uint64_t chunks;
+  uint64_t ostride;     // offsets bytes per chunk (0 without offsets)
+  uint64_t chunk_base;  // global index of chunk 0 (error reporting across slices)
+};
+
+struct Epi {
+  int32_t dtype;
+  float scale;
+  const float* class_scale;
+  const float* class_bias;
+  const int32_t* row_class;
+  uint64_t row_stride;  // elements
+};
+
+// Kernel launchers (codec.cu).  Return cudaError_t of the launch; `launches`
+// is incremented by the number of kernels enqueued.
+cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_stride,
+                          const int64_t* row_index, void* containers, uint8_t* offsets,
+                          cudaStream_t s, int num_sms, uint64_t* launches);
+cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* offsets,
+                          const Epi& e, void* out, DevError* err, cudaStream_t s, int num_sms,
+                          uint64_t* launches);
+cudaError_t launch_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uint64_t P,
+                         uint8_t* out, uint64_t row_stride, cudaStream_t s, int num_sms,
+                         uint64_t* launches);
+
+// SBS launchers (sbs.cu).
+cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
+                               uint64_t* class_offsets, int64_t* members, uint32_t* scratch,
+                               uint64_t scratch_words, DevError* err, cudaStream_t s,
+                               uint64_t* launches);
+uint64_t class_index_scratch_words(uint64_t n, uint64_t C);
+
+// One reshuffle event of the SplitMix64 chain.
+struct SbsEvent {
+  uint32_t cls;     // class
+  uint32_t m;       // class size
+  uint64_t slot;    // element offset of the output permutation in the generation pool
+  uint64_t src;     // element offset of the input permutation (previous generation)
+};
+
+cudaError_t launch_sbs_chain(const SbsEvent* ev, uint64_t n_events, unsigned long long* chain,
+                             uint64_t* seeds, uint32_t* flags, int force_serial, cudaStream_t s,
+                             uint64_t* launches);
+cudaError_t launch_sbs_shuffle(const SbsEvent* ev, const uint32_t* class_event_begin,
+                               const uint32_t* class_event_list, const uint64_t* cls_copy,
+                               const uint64_t* cls_final, uint32_t n_classes,
+                               const uint64_t* seeds, const uint32_t* flags, int64_t* pool,
+                               uint32_t max_m, cudaStream_t s, uint64_t* launches);
+
+struct SbsGatherArgs {
+  const uint32_t* row_cls;       // [B] class of each batch row (class-major)
+  const uint64_t* counts;        // [C]
+  const uint64_t* prefix;        // [C+1] exclusive scan of counts (row offset in batch)
+  const uint64_t* class_size;    // [C]
+  const uint64_t* drawn_before;  // [C] draws from class c before this call
+  const uint64_t* gen_base_gen;  // [C] generation held in pool slot 0 of class c
+  const uint64_t* gen_base_off;  // [C] pool offset of that generation
+  const uint64_t* gen_stride;    // [C] pool elements per generation (= m_c)
+  const int64_t* pool;
+  uint64_t C, B;
+  uint64_t n_batches;  // batches in this call
+  uint32_t shard, n_shards;
+};
+cudaError_t launch_sbs_gather(const SbsGatherArgs& a, int64_t* examples, int32_t* classes,
+                              cudaStream_t s, uint64_t* launches);
+
+}  // namespace optb_b200

@@ -1,0 +1,449 @@
+// sbs.cu -- selective batch sampling on sm_100a.
+//
+// Reference semantics (file:line under /root/reference/proj):
+//   ClassIndex::from_labels   sampler.cpp:53-65   (K7 below)
+//   BatchCursor ctor/reshuffle sampler.cpp:67-89, Rng rng.hpp:16-64 (K8, K9)
+//   BatchCursor::next         sampler.cpp:91-104  (K10)
+//
+// The reference stream is one sequential SplitMix64 chain threaded through
+// every reshuffle.  SplitMix64 is counter based (draw k from state s is
+// mix(s + k*gamma)), so a reshuffle of a class of m examples started at chain
+// state s consumes K = m-1 draws plus any rejections of next_below and leaves
+// the chain at mix(s + (K+1)*gamma) (rng.hpp:16-21, sampler.cpp:84-89).  The
+// chain therefore depends only on the event sequence (class sizes) and on
+// rejections, never on permutation contents:
+//   K8a  one thread walks the events assuming no rejection (1 mix / event),
+//   K8b  every draw of every event is checked for rejection in parallel,
+//   K8c  on any hit (probability <= m/2^64 per draw) one thread recomputes
+//        the chain exactly from the first hit -- correct, and never slow in
+//        practice; also forced by optb_sbs_set_force_serial for testing,
+//   K9   one CTA per class applies that class's Fisher-Yates passes in
+//        generation order in shared memory: lanes precompute the swap
+//        targets j = x mod i (x = mix(s + k*gamma)), one lane swaps,
+//   K10  gathers the class-major draws of any subset of batches (sharding).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace optb_b200 {
+namespace {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// next_below's acceptance bound (rng.hpp:31): x is rejected iff x > limit.
+__device__ __forceinline__ uint64_t below_limit(uint64_t n) {
+  const uint64_t all = ~0ull;
+  return all - (all % n + 1) % n;
+}
+
+// Rejection is possible only when x >= 2^64 - (2^64 mod n); for n <= 2^32
+// that needs the top 32 bits set, so the 64-bit modulus is rarely evaluated.
+__device__ __forceinline__ bool rejected(uint64_t x, uint64_t n) {
+  if (n <= (1ull << 32) && (x >> 32) != 0xffffffffull) return false;
+  return x > below_limit(n);
+}
+
+// ------------------------------------------------------------------ K7
+// Stable partition of [0,n) by label.  One warp per tile of kTile labels.
+constexpr int kTile = 1024;
+
+__global__ void k_ci_hist(const int32_t* __restrict__ labels, uint64_t n, uint32_t C,
+                          uint32_t tiles, uint32_t* __restrict__ hist, DevError* err) {
+  extern __shared__ uint32_t h[];
+  const uint32_t tile = blockIdx.x;
+  for (uint32_t c = threadIdx.x; c < C; c += 32) h[c] = 0;
+  __syncwarp();
+  const uint64_t begin = static_cast<uint64_t>(tile) * kTile;
+  for (uint32_t o = threadIdx.x; o < kTile; o += 32) {
+    const uint64_t i = begin + o;
+    if (i >= n) break;
+    const int32_t l = __ldg(labels + i);
+    if (l < 0 || static_cast<uint32_t>(l) >= C) {
+      atomicCAS(&err->kind, 0u, kErrLabel);
+      atomicMin(&err->key, static_cast<unsigned long long>(i));
+      continue;
+    }
+    atomicAdd(&h[l], 1u);
+  }
+  __syncwarp();
+  for (uint32_t c = threadIdx.x; c < C; c += 32) hist[static_cast<uint64_t>(c) * tiles + tile] = h[c];
+}
+
+// Exclusive scan of hist (class-major, tile-minor) in place; class_offsets[c]
+// = scan at (c, 0); class_offsets[C] = total.  Single CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k_ci_scan(uint32_t* __restrict__ hist, uint64_t total,
+                                                  uint32_t C, uint32_t tiles,
+                                                  uint64_t* __restrict__ class_offsets) {
+  __shared__ uint64_t warp_sums[32];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t base = 0; base < total; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t v = i < total ? hist[i] : 0;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const uint64_t excl = carry + (warp ? warp_sums[warp - 1] : 0) + x - v;
+    if (i < total) {
+      hist[i] = static_cast<uint32_t>(excl);
+      if (i % tiles == 0) class_offsets[i / tiles] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) class_offsets[C] = carry;
+}
+
+__global__ void k_ci_scatter(const int32_t* __restrict__ labels, uint64_t n, uint32_t C,
+                             uint32_t tiles, const uint32_t* __restrict__ offs,
+                             int64_t* __restrict__ members) {
+  extern __shared__ uint32_t run[];  // running position per class for this tile
+  const uint32_t tile = blockIdx.x;
+  const int lane = threadIdx.x;
+  for (uint32_t c = lane; c < C; c += 32) run[c] = offs[static_cast<uint64_t>(c) * tiles + tile];
+  __syncwarp();
+  const uint64_t begin = static_cast<uint64_t>(tile) * kTile;
+  for (uint32_t o = 0; o < kTile; o += 32) {
+    const uint64_t i = begin + o + lane;
+    const bool in = i < n;
+    int32_t l = in ? __ldg(labels + i) : -1;
+    const bool ok = in && l >= 0 && static_cast<uint32_t>(l) < C;
+    if (!ok) l = -1 - lane;  // unique, never matches a real class
+    const uint32_t peers = __match_any_sync(0xffffffffu, l);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    uint32_t pos = 0;
+    if (ok) pos = run[l] + rank;
+    __syncwarp();
+    if (ok) {
+      members[pos] = static_cast<int64_t>(i);
+      if (31 - __clz(peers) == lane) run[l] = pos + 1;  // highest peer advances the run
+    }
+    __syncwarp();
+    if (__all_sync(0xffffffffu, !in)) break;
+  }
+}
+
+__global__ void k_ci_label_value(const int32_t* labels, uint64_t C, DevError* err) {
+  if (err->kind == kErrLabel) {
+    err->label = labels[err->key];
+    err->aux = C;
+  }
+}
+
+// ------------------------------------------------------------------ K8
+__global__ void k_chain_spec(const SbsEvent* __restrict__ ev, uint64_t E,
+                             unsigned long long* chain, uint64_t* __restrict__ seeds) {
+  if (threadIdx.x != 0) return;
+  uint64_t s = *chain;
+  for (uint64_t e = 0; e < E; ++e) {
+    seeds[e] = s;
+    const uint64_t m = ev[e].m;
+    const uint64_t used = m >= 2 ? m : 1;  // K + 1 with K = m - 1 (or 0)
+    s = mix64(s + used * kGamma);
+  }
+  seeds[E] = s;
+}
+
+// Every draw of every event: event e's draw k (1..m-1) serves FY step
+// i = m - k + 1 (rng.hpp:57-64).  grid-stride over (event, k) pairs via a
+// per-event block loop.
+__global__ void k_chain_verify(const SbsEvent* __restrict__ ev, uint64_t E,
+                               const uint64_t* __restrict__ seeds, uint32_t* __restrict__ flags) {
+  for (uint64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    const uint64_t m = ev[e].m;
+    const uint64_t s = seeds[e];
+    bool bad = false;
+    for (uint64_t k = 1 + threadIdx.x; k + 1 <= m; k += blockDim.x) {
+      const uint64_t x = mix64(s + k * kGamma);
+      if (rejected(x, m - k + 1)) bad = true;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) {
+      flags[e] = 1u;
+      atomicMin(flags + E, static_cast<uint32_t>(e < 0xffffffffull ? e : 0xfffffffeull));
+    } else if (threadIdx.x == 0) {
+      flags[e] = 0u;
+    }
+  }
+}
+
+// Exact serial chain from the first event with a rejection (or from 0 when
+// forced).  flags[E] holds the first flagged event (0xffffffff = none).
+__global__ void k_chain_fixup(const SbsEvent* __restrict__ ev, uint64_t E,
+                              unsigned long long* chain, uint64_t* __restrict__ seeds,
+                              uint32_t* __restrict__ flags, int force) {
+  if (threadIdx.x != 0) return;
+  uint64_t first = flags[E];
+  if (force) first = 0;
+  if (first == 0xffffffffull || first >= E) {
+    *chain = seeds[E];
+    return;
+  }
+  uint64_t s = seeds[first];
+  for (uint64_t e = first; e < E; ++e) {
+    seeds[e] = s;
+    const uint64_t m = ev[e].m;
+    uint64_t st = s;
+    bool rej = false;
+    for (uint64_t i = m; i > 1; --i) {  // Rng::shuffle draws (rng.hpp:57-64)
+      const uint64_t lim = below_limit(i);
+      st += kGamma;
+      uint64_t x = mix64(st);
+      while (x > lim) {
+        rej = true;
+        st += kGamma;
+        x = mix64(st);
+      }
+    }
+    st += kGamma;  // rng_state_ = rng.next_u64() (sampler.cpp:87)
+    s = mix64(st);
+    flags[e] = (rej || force) ? 1u : 0u;
+  }
+  seeds[E] = s;
+  *chain = s;
+}
+
+// ------------------------------------------------------------------ K9
+// One CTA per class with events.  The class's permutation lives in shared
+// memory as u32 (host guarantees example ids < 2^32 when this path is used);
+// lanes precompute swap targets for a window of steps, thread 0 swaps.
+constexpr int kJWin = 2048;
+
+__global__ void __launch_bounds__(128) k_shuffle(const SbsEvent* __restrict__ ev,
+                                                 const uint32_t* __restrict__ cls_begin,
+                                                 const uint32_t* __restrict__ cls_list,
+                                                 const uint64_t* __restrict__ cls_copy,
+                                                 const uint64_t* __restrict__ cls_final,
+                                                 const uint64_t* __restrict__ seeds,
+                                                 const uint32_t* __restrict__ flags,
+                                                 int64_t* __restrict__ pool, int use_smem) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* js = sh;            // kJWin swap targets
+  uint32_t* perm = sh + kJWin;  // m entries (smem path)
+  const uint32_t b = cls_begin[blockIdx.x], end = cls_begin[blockIdx.x + 1];
+  const SbsEvent first = ev[cls_list[b]];
+  const uint32_t m = first.m;
+  const uint64_t copy_to = cls_copy[blockIdx.x], final_to = cls_final[blockIdx.x];
+  // load the input permutation (current generation); optionally keep a copy of
+  // it in the generation pool for the gather (draws before the first event)
+  if (use_smem) {
+    for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) {
+      const int64_t v = pool[first.src + x];
+      perm[x] = static_cast<uint32_t>(v);
+      if (copy_to != ~0ull) pool[copy_to + x] = v;
+    }
+  } else if (copy_to != ~0ull) {
+    for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) pool[copy_to + x] = pool[first.src + x];
+  }
+  __syncthreads();
+  uint64_t cur_src = first.src;
+  for (uint32_t q = b; q < end; ++q) {
+    const uint32_t e = cls_list[q];
+    const SbsEvent E = ev[e];
+    const uint64_t s = seeds[e];
+    int64_t* gperm = pool + E.slot;
+    if (!use_smem) {  // global path: copy previous generation into this slot
+      if (E.slot != cur_src)
+        for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) gperm[x] = pool[cur_src + x];
+      __syncthreads();
+    }
+    if (flags[e] == 0u) {
+      // no rejection: step i = m..2 uses draw k = m - i + 1
+      for (uint32_t w0 = m; w0 > 1; w0 = (w0 > kJWin + 1) ? w0 - kJWin : 1) {
+        const uint32_t cnt = (w0 - 1 < kJWin) ? w0 - 1 : kJWin;  // steps i = w0 .. w0-cnt+1
+        for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+          const uint32_t i = w0 - t;
+          const uint64_t k = static_cast<uint64_t>(m) - i + 1;
+          const uint64_t x = mix64(s + k * kGamma);
+          js[t] = static_cast<uint32_t>(x % i);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (use_smem) {
+            for (uint32_t t = 0; t < cnt; ++t) {
+              const uint32_t i = w0 - t, j = js[t];
+              const uint32_t a = perm[i - 1];
+              perm[i - 1] = perm[j];
+              perm[j] = a;
+            }
+          } else {
+            for (uint32_t t = 0; t < cnt; ++t) {
+              const uint32_t i = w0 - t, j = js[t];
+              const int64_t a = gperm[i - 1];
+              gperm[i - 1] = gperm[j];
+              gperm[j] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    } else if (threadIdx.x == 0) {
+      // exact serial draws with rejection (rng.hpp:29-35, 57-64)
+      uint64_t st = s;
+      for (uint32_t i = m; i > 1; --i) {
+        const uint64_t lim = below_limit(i);
+        st += kGamma;
+        uint64_t x = mix64(st);
+        while (x > lim) {
+          st += kGamma;
+          x = mix64(st);
+        }
+        const uint32_t j = static_cast<uint32_t>(x % i);
+        if (use_smem) {
+          const uint32_t a = perm[i - 1];
+          perm[i - 1] = perm[j];
+          perm[j] = a;
+        } else {
+          const int64_t a = gperm[i - 1];
+          gperm[i - 1] = gperm[j];
+          gperm[j] = a;
+        }
+      }
+    }
+    __syncthreads();
+    if (use_smem)
+      for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) gperm[x] = perm[x];
+    cur_src = E.slot;
+    __syncthreads();
+  }
+  if (final_to != ~0ull && final_to != cur_src) {  // write back the newest generation
+    if (use_smem)
+      for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) pool[final_to + x] = perm[x];
+    else
+      for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) pool[final_to + x] = pool[cur_src + x];
+  }
+}
+
+// ------------------------------------------------------------------ K10
+__global__ void k_gather(SbsGatherArgs a, int64_t* __restrict__ examples, int32_t* __restrict__ classes,
+                         uint64_t out_batches) {
+  const uint64_t total = out_batches * a.B;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t lb = t / a.B;
+    const uint64_t r = t - lb * a.B;
+    const uint32_t c = a.row_cls[r];
+    const uint64_t k = r - a.prefix[c];
+    const uint64_t beta = a.shard + lb * a.n_shards;  // batch within this call
+    const uint64_t D = a.drawn_before[c] + beta * a.counts[c] + k;
+    const uint64_t m = a.class_size[c];
+    const uint64_t gen = D / m;
+    const uint64_t off = a.gen_base_off[c] + (gen - a.gen_base_gen[c]) * a.gen_stride[c] + (D - gen * m);
+    examples[t] = a.pool[off];
+    if (classes) classes[t] = static_cast<int32_t>(c);
+  }
+}
+
+}  // namespace
+
+uint64_t class_index_scratch_words(uint64_t n, uint64_t C) {
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  return tiles * C;
+}
+
+cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
+                               uint64_t* class_offsets, int64_t* members, uint32_t* scratch,
+                               uint64_t scratch_words, DevError* err, cudaStream_t s,
+                               uint64_t* launches) {
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  if (tiles * C > scratch_words) return cudaErrorInvalidValue;
+  const size_t smem = C * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_ci_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_ci_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  if (tiles > 0) {
+    k_ci_hist<<<static_cast<unsigned>(tiles), 32, smem, s>>>(labels, n, (uint32_t)C,
+                                                             (uint32_t)tiles, scratch, err);
+    ++*launches;
+  }
+  k_ci_scan<<<1, 1024, 0, s>>>(scratch, tiles * C, (uint32_t)C, (uint32_t)(tiles ? tiles : 1),
+                               class_offsets);
+  ++*launches;
+  if (tiles > 0) {
+    k_ci_scatter<<<static_cast<unsigned>(tiles), 32, smem, s>>>(labels, n, (uint32_t)C,
+                                                                (uint32_t)tiles, scratch, members);
+    ++*launches;
+  }
+  k_ci_label_value<<<1, 1, 0, s>>>(labels, C, err);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sbs_chain(const SbsEvent* ev, uint64_t E, unsigned long long* chain,
+                             uint64_t* seeds, uint32_t* flags, int force_serial, cudaStream_t s,
+                             uint64_t* launches) {
+  k_chain_spec<<<1, 32, 0, s>>>(ev, E, chain, seeds);
+  cudaError_t st = cudaMemsetAsync(flags + E, 0xff, sizeof(uint32_t), s);
+  if (st != cudaSuccess) return st;
+  if (E > 0) {
+    const unsigned grid = static_cast<unsigned>(E < 4096 ? E : 4096);
+    k_chain_verify<<<grid, 256, 0, s>>>(ev, E, seeds, flags);
+    ++*launches;
+  }
+  k_chain_fixup<<<1, 32, 0, s>>>(ev, E, chain, seeds, flags, force_serial);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sbs_shuffle(const SbsEvent* ev, const uint32_t* cls_begin,
+                               const uint32_t* cls_list, const uint64_t* cls_copy,
+                               const uint64_t* cls_final, uint32_t n_classes, const uint64_t* seeds,
+                               const uint32_t* flags, int64_t* pool, uint32_t max_m,
+                               cudaStream_t s, uint64_t* launches) {
+  if (n_classes == 0) return cudaSuccess;
+  size_t smem = (kJWin + static_cast<size_t>(max_m)) * sizeof(uint32_t);
+  int use_smem = 1;
+  if (smem > 200 * 1024) {
+    use_smem = 0;
+    smem = kJWin * sizeof(uint32_t);
+  }
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_shuffle, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 8192);
+    attr = 200 * 1024 + 8192;
+  }
+  k_shuffle<<<n_classes, 128, smem, s>>>(ev, cls_begin, cls_list, cls_copy, cls_final, seeds,
+                                          flags, pool, use_smem);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sbs_gather(const SbsGatherArgs& a, int64_t* examples, int32_t* classes,
+                              cudaStream_t s, uint64_t* launches) {
+  const uint64_t out_batches =
+      a.n_batches > a.shard ? (a.n_batches - a.shard + a.n_shards - 1) / a.n_shards : 0;
+  const uint64_t total = out_batches * a.B;
+  if (total == 0) return cudaSuccess;
+  const uint64_t want = (total + 255) / 256;
+  const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+  k_gather<<<grid, 256, 0, s>>>(a, examples, classes, out_batches);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace optb_b200
