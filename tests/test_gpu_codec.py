@@ -111,7 +111,7 @@ def test_random_roundtrips_vs_oracle(pkg, oracle_mod, torch_cuda):
 def _stream_case(pkg, torch, O, mode, per_chunk, P, B, nb, rng, gather=True, out_dtype=None):
     C = pkg.codec
     dev = torch.device("cuda", 0)
-    n_ds = max(B * nb // 2, 1)
+    n_ds = max(B * nb // 2, 1) if gather else B * nb
     ds = rng.integers(0, 256, size=(n_ds, P), dtype=np.uint8)
     idx = rng.integers(0, n_ds, size=B * nb).astype(np.int64) if gather else None
     L = C.layout(mode, per_chunk, P, B, nb)
