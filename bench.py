@@ -56,7 +56,9 @@ def config(world):
             "global_batch": BATCH, "batches_per_step_per_gpu": BATCHES_PER_STEP, "mode": "exact128",
             "per_chunk": PER_CHUNK, "image": [32, 32, 3], "decode_out": "u8",
             "parallelism": f"independent batch shards x{world} (t % N == rank)",
-            "l2": "flushed between steps (256 MiB write outside the per-step events)"}
+            "l2": "inputs larger than L2: 153.6 MB dataset (> 126 MB L2), and every step streams 152.6 MB of "
+                  "containers + 152.6 MB of decoded rows through it",
+            "pipeline": "SBS draws of step k+1 on a side stream overlap encode/decode of step k"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -221,10 +223,13 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    import ctypes as ct
+
     import torch
     import torch.distributed as dist
 
     import paper_2105_00619_b200 as pkg
+    from paper_2105_00619_b200.pipeline import Pipeline
     C, S = pkg.codec, pkg.sampler
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -233,68 +238,51 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     stream = torch.cuda.Stream(dev)
+    rows = BATCH * BATCHES_PER_STEP
     with torch.cuda.stream(stream):
         ctx = pkg._lib.context(local)
         ds = torch.empty((N_EXAMPLES, P), dtype=torch.uint8, device=dev)
-        pkg._lib.check(pkg._lib.lib.optb_synth_pixels_dev(ctx, DATA_SEED, 0, N_EXAMPLES, P,
-                                                          __import__("ctypes").c_void_p(ds.data_ptr()), P,
-                                                          __import__("ctypes").c_void_p(stream.cuda_stream)))
+        pkg._lib.check(pkg._lib.lib.optb_synth_pixels_dev(ctx, DATA_SEED, 0, N_EXAMPLES, P, ct.c_void_p(ds.data_ptr()),
+                                                          P, ct.c_void_p(stream.cuda_stream)))
         labels = torch.arange(N_EXAMPLES, device=dev, dtype=torch.int32) % N_CLASSES
         plan = S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED)
         offs, mem = S.class_index_dev(labels, N_CLASSES, device=local)
         cur = S.BatchCursor.from_device_index(plan, offs, mem, device=local)
-        L = C.layout(MODE, PER_CHUNK, P, BATCH, BATCHES_PER_STEP)
-        cont, _ = C.alloc_stream(L, local)
-        rows = BATCH * BATCHES_PER_STEP
         out = torch.empty((rows, P), dtype=torch.uint8, device=dev)
-        ex_buf = torch.empty(rows, dtype=torch.int64, device=dev)
-        cl_buf = torch.empty(rows, dtype=torch.int32, device=dev)
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize(dev)
-    global_batches = BATCHES_PER_STEP * world
-
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-
-    def step(timed):
-        if timed:
-            ev[0].record(stream)
-        cur.next_dev(global_batches, shard=rank, n_shards=world, examples=ex_buf, classes=cl_buf, stream=stream)
-        if timed:
-            ev[1].record(stream)
-        C.encode_dev(L, ds, cont, row_index=ex_buf, stream=stream)
-        if timed:
-            ev[2].record(stream)
-        C.decode_dev(L, cont, out, stream=stream)
-        if timed:
-            ev[3].record(stream)
+    # The native E-D pipeline (optb_pipeline_*): per step, SBS draws of step
+    # k+1 on a side stream overlap gather-encode + decode of step k.
+    pipe = Pipeline(cur, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
+                    device=local, record_timings=True)
+    L = pipe.layout
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            step(False)
+            pipe.step(out, stream)
         C.sync(local, stream)
+        torch.cuda.synchronize(dev)
         launches0 = pkg._lib.launches(local)
-        per_step, t_sbs, t_enc, t_dec = [], [], [], []
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as clk:
             t_wall0 = time.perf_counter()
+            start.record(stream)
             for _ in range(args.steps):
-                flush.zero_()
-                step(True)
-                ev[3].synchronize()
-                per_step.append(ev[0].elapsed_time(ev[3]))
-                t_sbs.append(ev[0].elapsed_time(ev[1]))
-                t_enc.append(ev[1].elapsed_time(ev[2]))
-                t_dec.append(ev[2].elapsed_time(ev[3]))
-            torch.cuda.synchronize(dev)
+                pipe.step(out, stream)
+            end.record(stream)
+            t_enqueue = time.perf_counter() - t_wall0
+            end.synchronize()
             t_wall = time.perf_counter() - t_wall0
         if world > 1:
             dist.barrier()
         C.sync(local, stream)
         launches = pkg._lib.launches(local) - launches0
-
-    ms = sum(per_step) / len(per_step)
+    timed = range(args.warmup, args.warmup + args.steps)
+    tim = [pipe.timings(k) for k in timed]
+    t_sbs, t_enc, t_dec = [t[0] for t in tim], [t[1] for t in tim], [t[2] for t in tim]
+    ms = start.elapsed_time(end) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -320,26 +308,29 @@ def main():
     roofline = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
                 "algorithmic_bytes_per_launch": kbytes,
-                "kernels_ms": {"sbs": round(statistics.mean(t_sbs), 4), "encode": round(enc_ms, 4),
+                "host_enqueue_us_per_step": round(t_enqueue / args.steps * 1e6, 1),
+                "kernels_ms": {"sbs_side_stream": round(statistics.mean(t_sbs), 4), "encode": round(enc_ms, 4),
                                "decode": round(dec_ms, 4)},
                 "encode_gbs": round(enc_bytes / (enc_ms / 1e3) / 1e9, 1),
                 "decode_gbs": round(dec_bytes / (dec_ms / 1e3) / 1e9, 1),
                 "step_gbs": round((enc_bytes + dec_bytes) / (ms / 1e3) / 1e9, 1)}
 
-    # e2e: dataset in pinned host memory; the gather-encode kernel reads the
-    # drawn rows over PCIe (H2D), decoded rows are copied back (D2H).
+    # e2e: the same pipeline with the dataset in pinned host memory; the
+    # gather-encode kernel reads the drawn rows over PCIe (H2D) and the decoded
+    # rows are copied back to pinned host memory (D2H), every step.
     e2e = None
     if args.e2e_steps > 0:
         with torch.cuda.stream(stream):
             ds_host = ds.cpu().pin_memory()
             out_host = torch.empty((rows, P), dtype=torch.uint8).pin_memory()
+            plan2 = S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED)
+            cur2 = S.BatchCursor.from_device_index(plan2, offs, mem, device=local)
+            pipe2 = Pipeline(cur2, ds_host, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank,
+                             n_shards=world, device=local)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
             def e2e_step():
-                cur.next_dev(global_batches, shard=rank, n_shards=world, examples=ex_buf, classes=cl_buf,
-                             stream=stream)
-                C.encode_dev(L, ds_host, cont, row_index=ex_buf, stream=stream)
-                C.decode_dev(L, cont, out, stream=stream)
+                pipe2.step(out, stream)
                 out_host.copy_(out, non_blocking=True)
             for _ in range(2):
                 e2e_step()
@@ -352,16 +343,21 @@ def main():
             e1.record(stream)
             e1.synchronize()
             e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-            ok = torch.equal(out_host[:BATCH], ds_host[ex_buf[:BATCH].cpu()])
+            # check the last step against an independent cursor's draws
+            cur3 = S.BatchCursor.from_device_index(plan2, offs, mem, device=local)
+            for _ in range(pipe2.steps):
+                ex3, _ = cur3.next_dev(BATCHES_PER_STEP * world, shard=rank, n_shards=world)
+            ok = bool(torch.equal(out_host, ds_host[ex3.cpu()]))
+            pipe2.close()
             if world > 1:
                 t = torch.tensor([e2e_ms], device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 e2e_ms = float(t.item())
         e2e = {"value": round(images_per_step / (e2e_ms / 1e3), 1), "unit": UNIT,
-               "h2d_bytes_per_step": rows * P + 0, "d2h_bytes_per_step": rows * P,
-               "ms_per_step": round(e2e_ms, 3), "check": bool(ok),
-               "path": "optb_sbs_next_dev -> optb_encode_dev reading the pinned host dataset (zero-copy H2D of "
-                       "the drawn rows) -> optb_decode_dev -> D2H of the decoded rows to pinned host memory"}
+               "h2d_bytes_per_step": rows * P, "d2h_bytes_per_step": rows * P,
+               "ms_per_step": round(e2e_ms, 3), "check": ok,
+               "path": "optb_pipeline_step over a pinned-host dataset: SBS draws -> gather-encode reading the drawn "
+                       "rows over PCIe (zero-copy H2D) -> decode -> D2H copy of the decoded rows to pinned host"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -374,8 +370,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": config(world),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-                "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 3)}
+                "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 4)}
         print(json.dumps(line), flush=True)
+    pipe.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -191,6 +191,43 @@ uint64_t optb_sbs_batches_drawn(const optb_sbs* sbs);
  * reshuffle (results are identical; only speed changes). */
 int optb_sbs_set_force_serial(optb_sbs* sbs, int32_t on);
 
+/* ---------------------------------------------------------------- E-D pipeline
+ * The encode-while-train data path (replaces pipeline.cpp:37-97 HandoffSlot,
+ * :116-129 prepare_epoch, :181-244 run): each step gathers the SBS-drawn rows
+ * of `dataset` (device memory, or pinned host memory read zero-copy), encodes
+ * them into the pipeline's containers and decodes them with `epilogue` into
+ * the caller's layer-input buffer, all on the caller's stream; the draws of
+ * the next step run meanwhile on a side stream (two draw buffers, event
+ * hand-off, no host synchronisation).  `layout` describes one step of this
+ * shard: layout.n_batches of the global stream's layout.n_batches*n_shards
+ * batches per step (those with index % n_shards == shard).  With class
+ * tables in the epilogue and row_class NULL, the step's own draw classes are
+ * used (per-class preprocessing). */
+typedef struct optb_pipeline optb_pipeline;
+typedef struct optb_pipeline_desc {
+  optb_layout layout;
+  const uint8_t* dataset;
+  uint64_t row_stride;
+  optb_sbs* sbs;
+  uint32_t shard, n_shards;
+  optb_epilogue epilogue;
+  int32_t record_timings;  /* keep per-step CUDA events for optb_pipeline_timings */
+} optb_pipeline_desc;
+
+int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* desc, optb_pipeline** out);
+/* Enqueue the next step; `out` receives optb_layout_rows(layout) decoded rows. */
+int optb_pipeline_step(optb_pipeline* p, void* out, void* stream);
+/* Device draws (examples, classes) of a step still buffered (the last two). */
+int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
+                        const int32_t** classes);
+/* The pipeline's container planes (valid for the last enqueued step). */
+const void* optb_pipeline_containers(const optb_pipeline* p);
+/* Device-timed durations (ms) of a completed step (last 64 steps): its SBS
+ * draws (side stream), its gather-encode and its decode. */
+int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, float* enc_ms,
+                          float* dec_ms);
+void optb_pipeline_destroy(optb_pipeline* p);
+
 /* ---------------------------------------------------------------- synthetic data
  * Counter-based u8 rows (bench / tests): w = mix(seed + (e*ceil(P/8) + p/8 + 1)*gamma),
  * pixel = (w >> 8*(p%8)) & 0xff for dataset row e = first_row + r. */

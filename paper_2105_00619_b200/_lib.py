@@ -43,8 +43,16 @@ class Epilogue(ct.Structure):
                 ("class_bias", vp), ("row_class", vp), ("out_row_stride", ct.c_uint64)]
 
 
+class PipelineDesc(ct.Structure):
+    """optb_pipeline_desc"""
+    _fields_ = [("layout", Layout), ("dataset", vp), ("row_stride", ct.c_uint64), ("sbs", vp),
+                ("shard", ct.c_uint32), ("n_shards", ct.c_uint32), ("epilogue", Epilogue),
+                ("record_timings", ct.c_int32)]
+
+
 LP = ct.POINTER(Layout)
 EP = ct.POINTER(Epilogue)
+fp = ct.POINTER(ct.c_float)
 
 # name -> (restype, argtypes); exactly the declarations of include/optb_cuda.h
 SIGNATURES = {
@@ -80,7 +88,13 @@ SIGNATURES = {
     "optb_sbs_next_host": (ct.c_int, [vp, ct.c_uint64, vp, vp]),
     "optb_sbs_batches_drawn": (ct.c_uint64, [vp]),
     "optb_sbs_set_force_serial": (ct.c_int, [vp, ct.c_int32]),
-    "optb_synth_pixels_dev": (ct.c_int, [vp, ct.c_uint64, ct.c_uint64, ct.c_uint64, ct.c_uint64, vp,
+    "optb_pipeline_create": (ct.c_int, [vp, ct.POINTER(PipelineDesc), ct.POINTER(vp)]),
+    "optb_pipeline_step": (ct.c_int, [vp, vp, vp]),
+    "optb_pipeline_draws": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(vp), ct.POINTER(vp)]),
+    "optb_pipeline_containers": (vp, [vp]),
+    "optb_pipeline_timings": (ct.c_int, [vp, ct.c_uint64, fp, fp, fp]),
+    "optb_pipeline_destroy": (None, [vp]),
+    "optb_synth_pixels_dev":(ct.c_int, [vp, ct.c_uint64, ct.c_uint64, ct.c_uint64, ct.c_uint64, vp,
                                          ct.c_uint64, vp]),
 }
 

@@ -6,7 +6,7 @@
                      re-implemented over liboptb_cuda.so
 
 Called by __graft_entry__.build(); also runnable as
-``python -m paper_2105_00619_b200.build``.  Objects go to build/, the shared
+``python paper_2105_00619_b200/build.py``.  Objects go to build/, the shared
 libraries next to this file so they travel with the repo snapshot.
 """
 from __future__ import annotations
@@ -27,7 +27,7 @@ CUDA_LIB = "/usr/local/cuda/lib64"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
               "--expt-relaxed-constexpr", "-diag-suppress", "177", "-I" + INCLUDE]
-CUDA_SOURCES = ["codec.cu", "sbs.cu", "capi.cu"]
+CUDA_SOURCES = ["codec.cu", "sbs.cu", "capi.cu", "pipeline.cu"]
 CUDA_LIB_NAME = os.path.join(PKG, "liboptb_cuda.so")
 SHIM_LIB_NAME = os.path.join(PKG, "liboptb_shim.so")
 SHIM_SOURCES = ["codec.cpp", "sampler.cpp", "nn.cpp"]

@@ -612,6 +612,11 @@ int optb_decode_host(optb_ctx* c, const optb_layout* L, const void* containers,
 }  // extern "C"
 
 // ------------------------------------------------------------------ SBS
+// ------------------------------------------------------------------ SBS
+// Host side of the GPU BatchCursor: it only plans.  Per call it lists the
+// reshuffle events (class, generation) in the reference's chain order
+// (sampler.cpp:91-104: batch, then class, then draw), lays out the
+// generation pool, and uploads one small block; the kernels do the rest.
 struct optb_sbs {
   optb_ctx* ctx = nullptr;
   uint64_t C = 0, B = 0, N = 0;
@@ -625,11 +630,13 @@ struct optb_sbs {
   uint64_t pool_cap = 0;      // elements
   unsigned long long* d_chain = nullptr;
   uint8_t* d_static = nullptr;  // counts[C] prefix[C+1] size[C] row_cls[B]
-  uint8_t* d_call = nullptr;
+  uint8_t* d_call = nullptr;    // per-call block (stream ordered reuse)
   size_t call_cap = 0;
-  uint8_t* h_call = nullptr;
-  size_t h_call_cap = 0;
-  cudaEvent_t uploaded = nullptr;
+  static constexpr int kRing = 4;  // pinned upload buffers in flight
+  uint8_t* h_call[kRing] = {};
+  size_t h_call_cap[kRing] = {};
+  cudaEvent_t uploaded[kRing] = {};
+  int ring = 0;
   // scratch for next_host
   int64_t* d_ex = nullptr;
   int32_t* d_cl = nullptr;
@@ -638,7 +645,7 @@ struct optb_sbs {
 
 namespace {
 
-// Packs per-call arrays into one pinned block and uploads it.
+// Packs per-call arrays into one 16-byte aligned block.
 struct Packer {
   std::vector<uint8_t> buf;
   template <typename T>
@@ -650,19 +657,21 @@ struct Packer {
   }
   size_t reserve(size_t bytes) {
     size_t at = (buf.size() + 15) / 16 * 16;
-    buf.resize(at + bytes);
+    buf.resize(at + bytes, 0);
     return at;
   }
 };
 
 int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
   const size_t bytes = std::max<size_t>(pk.buf.size(), 16);
-  if (s->uploaded) CK(cudaEventSynchronize(s->uploaded), "sbs upload");
-  if (s->h_call_cap < bytes) {
-    if (s->h_call) cudaFreeHost(s->h_call);
-    s->h_call = nullptr;
-    CK(cudaHostAlloc(&s->h_call, bytes * 2, cudaHostAllocDefault), "sbs pinned");
-    s->h_call_cap = bytes * 2;
+  const int r = s->ring;
+  s->ring = (s->ring + 1) % optb_sbs::kRing;
+  CK(cudaEventSynchronize(s->uploaded[r]), "sbs upload");  // this pinned slot is free again
+  if (s->h_call_cap[r] < bytes) {
+    if (s->h_call[r]) cudaFreeHost(s->h_call[r]);
+    s->h_call[r] = nullptr;
+    CK(cudaHostAlloc(&s->h_call[r], bytes * 2, cudaHostAllocDefault), "sbs pinned");
+    s->h_call_cap[r] = bytes * 2;
   }
   if (s->call_cap < bytes) {
     if (s->d_call) {
@@ -673,9 +682,9 @@ int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
     CK(cudaMalloc(&s->d_call, bytes * 2), "sbs call block");
     s->call_cap = bytes * 2;
   }
-  memcpy(s->h_call, pk.buf.data(), pk.buf.size());
-  CK(cudaMemcpyAsync(s->d_call, s->h_call, bytes, cudaMemcpyHostToDevice, st), "sbs upload");
-  CK(cudaEventRecord(s->uploaded, st), "sbs upload");
+  memcpy(s->h_call[r], pk.buf.data(), pk.buf.size());
+  CK(cudaMemcpyAsync(s->d_call, s->h_call[r], bytes, cudaMemcpyHostToDevice, st), "sbs upload");
+  CK(cudaEventRecord(s->uploaded[r], st), "sbs upload");
   return OPTB_OK;
 }
 
@@ -683,6 +692,7 @@ int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st) {
   if (s->pool_cap >= elems) return OPTB_OK;
   const uint64_t cap = std::max<uint64_t>(elems, s->pool_cap * 3 / 2);
   int64_t* p = nullptr;
+  CK(cudaStreamSynchronize(st), "sbs pool");
   CK(cudaMalloc(&p, cap * sizeof(int64_t)), "sbs pool");
   if (s->d_pool) {
     CK(cudaMemcpyAsync(p, s->d_pool, s->N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st), "sbs pool");
@@ -696,54 +706,83 @@ int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st) {
 
 struct EvKey {
   uint64_t beta, cls, g;
-  uint64_t t;  // index within the class's events of this call (1-based)
+  uint64_t t;  // 1-based index of the event among its class's events in this call
 };
 
-// Runs the chain + shuffle kernels for an ordered event list.  `evs` are in
-// chain order; per-class lists for K9 are derived here.
-int run_events(optb_sbs* s, const std::vector<SbsEvent>& evs, const std::vector<uint64_t>& cls_copy_of,
-               const std::vector<uint64_t>& cls_final_of, Packer& pk, size_t* off_gather,
-               cudaStream_t st, bool with_gather_block, const std::vector<uint64_t>& gather_arrays) {
-  const uint64_t E = evs.size();
-  // K9 work lists: classes (m >= 2) with events, events in generation order
-  std::vector<std::vector<uint32_t>> per(s->C);
-  for (uint64_t e = 0; e < E; ++e)
-    if (evs[e].m >= 2) per[evs[e].cls].push_back(static_cast<uint32_t>(e));
+// Lays out the generation pool for `keys` (already in chain order) starting at
+// element N: a reshuffling class c with E_c events gets E_c + 1 slots of m_c
+// (slot 0 = copy of its pre-call permutation).  Fills the event records and
+// the per-class K9 lists, packs them and launches K9 + K8.  `gen_base` gets,
+// per class, the pool offset of the pre-call permutation the gather reads.
+int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
+               std::vector<uint64_t>* gen_base, size_t* o_extra, const std::vector<uint64_t>* extra,
+               cudaStream_t st) {
+  const uint64_t C = s->C, E = keys.size();
+  std::vector<uint64_t> ev_count(C, 0);
+  for (const auto& k : keys) ++ev_count[k.cls];
+  std::vector<uint64_t> base(C, 0);
+  uint64_t cursor = s->N;
+  for (uint64_t c = 0; c < C; ++c) {
+    if (ev_count[c] == 0 || s->m[c] < 2) continue;
+    base[c] = cursor;
+    cursor += (ev_count[c] + 1) * s->m[c];
+  }
+  int rc = ensure_pool(s, std::max<uint64_t>(cursor, 1), st);
+  if (rc) return rc;
+  std::vector<SbsEvent> evs(E);
+  std::vector<std::vector<uint32_t>> per(C);
+  for (uint64_t e = 0; e < E; ++e) {
+    const uint64_t c = keys[e].cls, mm = s->m[c], t = keys[e].t;
+    evs[e].cls = static_cast<uint32_t>(c);
+    evs[e].m = static_cast<uint32_t>(mm);
+    if (mm >= 2) {
+      evs[e].slot = base[c] + t * mm;
+      evs[e].src = (t == 1) ? s->off[c] : base[c] + (t - 1) * mm;
+      per[c].push_back(static_cast<uint32_t>(e));
+    } else {
+      evs[e].slot = evs[e].src = s->off[c];
+    }
+  }
   std::vector<uint32_t> begin{0}, list;
   std::vector<uint64_t> ccopy, cfinal;
-  for (uint64_t c = 0; c < s->C; ++c) {
+  for (uint64_t c = 0; c < C; ++c) {
     if (per[c].empty()) continue;
     for (uint32_t e : per[c]) list.push_back(e);
     begin.push_back(static_cast<uint32_t>(list.size()));
-    ccopy.push_back(cls_copy_of[c]);
-    cfinal.push_back(cls_final_of[c]);
+    ccopy.push_back(base[c]);
+    cfinal.push_back(s->off[c]);
+  }
+  if (gen_base) {
+    gen_base->assign(C, 0);
+    for (uint64_t c = 0; c < C; ++c) (*gen_base)[c] = per[c].empty() ? s->off[c] : base[c];
   }
   const size_t o_ev = pk.put(evs.data(), E);
-  const size_t o_seeds = pk.reserve((E + 1) * sizeof(uint64_t));
-  const size_t o_flags = pk.reserve((E + 1) * sizeof(uint32_t));
+  const size_t o_seeds = pk.reserve(std::max<uint64_t>(E, 1) * sizeof(uint64_t));
+  const size_t o_flag = pk.reserve(16);
   const size_t o_begin = pk.put(begin.data(), begin.size());
   const size_t o_list = pk.put(list.data(), list.size());
   const size_t o_copy = pk.put(ccopy.data(), ccopy.size());
   const size_t o_final = pk.put(cfinal.data(), cfinal.size());
-  if (with_gather_block) *off_gather = pk.put(gather_arrays.data(), gather_arrays.size());
-  int rc = upload_call(s, pk, st);
+  if (extra) *o_extra = pk.put(extra->data(), extra->size());
+  rc = upload_call(s, pk, st);
   if (rc) return rc;
+  if (E == 0) return OPTB_OK;
   uint8_t* d = s->d_call;
-  const SbsEvent* d_ev = reinterpret_cast<const SbsEvent*>(d + o_ev);
-  uint64_t* d_seeds = reinterpret_cast<uint64_t*>(d + o_seeds);
-  uint32_t* d_flags = reinterpret_cast<uint32_t*>(d + o_flags);
-  if (E > 0) {
-    cudaError_t e = launch_sbs_chain(d_ev, E, s->d_chain, d_seeds, d_flags, s->force_serial, st,
-                                     &s->ctx->launches);
-    if (e != cudaSuccess) return cuda_err(e, "sbs chain");
-    const uint32_t ncls = static_cast<uint32_t>(ccopy.size());
-    e = launch_sbs_shuffle(d_ev, reinterpret_cast<const uint32_t*>(d + o_begin),
-                           reinterpret_cast<const uint32_t*>(d + o_list),
-                           reinterpret_cast<const uint64_t*>(d + o_copy),
-                           reinterpret_cast<const uint64_t*>(d + o_final), ncls, d_seeds, d_flags,
-                           s->d_pool, s->small_ids ? s->max_m : 0xffffffffu, st, &s->ctx->launches);
-    if (e != cudaSuccess) return cuda_err(e, "sbs shuffle");
-  }
+  ChainArgs a;
+  a.ev = reinterpret_cast<const SbsEvent*>(d + o_ev);
+  a.E = E;
+  a.cls_begin = reinterpret_cast<const uint32_t*>(d + o_begin);
+  a.cls_list = reinterpret_cast<const uint32_t*>(d + o_list);
+  a.cls_copy = reinterpret_cast<const uint64_t*>(d + o_copy);
+  a.cls_final = reinterpret_cast<const uint64_t*>(d + o_final);
+  a.seeds = reinterpret_cast<uint64_t*>(d + o_seeds);
+  a.flag = reinterpret_cast<uint32_t*>(d + o_flag);
+  a.chain = s->d_chain;
+  a.pool = s->d_pool;
+  cudaError_t e = launch_sbs_events(a, static_cast<uint32_t>(ccopy.size()),
+                                    s->small_ids ? s->max_m : 0xffffffffu, s->force_serial, st,
+                                    &s->ctx->launches);
+  if (e != cudaSuccess) return cuda_err(e, "sbs events");
   return OPTB_OK;
 }
 
@@ -806,6 +845,7 @@ int optb_class_index_dev(optb_ctx* c, const int32_t* labels, uint64_t n, uint64_
   return OPTB_OK;
 }
 
+
 int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B, uint64_t seed,
                     const uint64_t* class_offsets, const int64_t* members, int32_t on_dev,
                     optb_sbs** out) {
@@ -837,16 +877,18 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
   for (uint64_t k = 0; k < C; ++k) {
     s->m[k] = s->off[k + 1] - s->off[k];
     s->prefix[k + 1] = s->prefix[k] + counts[k];
-    if (s->m[k] >= 2) s->max_m = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(s->max_m, s->m[k]), 0xffffffffull));
     if (s->m[k] >= (1ull << 32)) s->small_ids = false;
+    else if (s->m[k] >= 2) s->max_m = std::max<uint32_t>(s->max_m, static_cast<uint32_t>(s->m[k]));
   }
+  if (s->N >= (1ull << 32)) s->small_ids = false;
   cudaStream_t st = c->s_compute;
   auto fail = [&](int code) {
     optb_sbs_destroy(s);
     return code;
   };
-  if (cudaEventCreateWithFlags(&s->uploaded, cudaEventDisableTiming) != cudaSuccess)
-    return fail(cuda_err(cudaGetLastError(), "sbs event"));
+  for (int r = 0; r < optb_sbs::kRing; ++r)
+    if (cudaEventCreateWithFlags(&s->uploaded[r], cudaEventDisableTiming) != cudaSuccess)
+      return fail(cuda_err(cudaGetLastError(), "sbs event"));
   if (cudaMalloc(&s->d_chain, sizeof(unsigned long long)) != cudaSuccess)
     return fail(cuda_err(cudaGetLastError(), "sbs chain"));
   int rc = ensure_pool(s, std::max<uint64_t>(s->N, 1), st);
@@ -862,8 +904,7 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
         return fail(cuda_err(cudaGetLastError(), "sbs members"));
     }
   }
-  // static device arrays: counts, prefix, class sizes, row -> class
-  {
+  {  // static device arrays: counts, prefix, class sizes, row -> class
     std::vector<uint32_t> row_cls(B);
     for (uint64_t k = 0; k < C; ++k)
       for (uint64_t r = s->prefix[k]; r < s->prefix[k + 1]; ++r) row_cls[r] = static_cast<uint32_t>(k);
@@ -879,17 +920,12 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
   const unsigned long long seed64 = seed;
   if (cudaMemcpy(s->d_chain, &seed64, 8, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(cuda_err(cudaGetLastError(), "sbs seed"));
-  // constructor events: every class in order, shuffled in place (sampler.cpp:73-81)
-  std::vector<SbsEvent> evs(C);
-  std::vector<uint64_t> none(C, ~0ull);
-  for (uint64_t k = 0; k < C; ++k) {
-    evs[k].cls = static_cast<uint32_t>(k);
-    evs[k].m = static_cast<uint32_t>(std::min<uint64_t>(s->m[k], 0xffffffffull));
-    evs[k].slot = evs[k].src = s->off[k];
-  }
+  // constructor: reshuffle every class in class order (sampler.cpp:73-81),
+  // including empty and single-example classes (they still consume a draw)
+  std::vector<EvKey> keys(C);
+  for (uint64_t k = 0; k < C; ++k) keys[k] = {0, k, 0, 1};
   Packer pk;
-  size_t unused = 0;
-  rc = run_events(s, evs, none, none, pk, &unused, st, false, {});
+  rc = run_events(s, keys, pk, nullptr, nullptr, nullptr, st);
   if (rc) return fail(rc);
   if (cudaStreamSynchronize(st) != cudaSuccess) return fail(cuda_err(cudaGetLastError(), "sbs ctor"));
   *out = s;
@@ -904,8 +940,10 @@ void optb_sbs_destroy(optb_sbs* s) {
   if (s->d_chain) cudaFree(s->d_chain);
   if (s->d_static) cudaFree(s->d_static);
   if (s->d_call) cudaFree(s->d_call);
-  if (s->h_call) cudaFreeHost(s->h_call);
-  if (s->uploaded) cudaEventDestroy(s->uploaded);
+  for (int r = 0; r < optb_sbs::kRing; ++r) {
+    if (s->h_call[r]) cudaFreeHost(s->h_call[r]);
+    if (s->uploaded[r]) cudaEventDestroy(s->uploaded[r]);
+  }
   if (s->d_ex) cudaFree(s->d_ex);
   if (s->d_cl) cudaFree(s->d_cl);
   delete s;
@@ -922,21 +960,22 @@ int optb_sbs_set_force_serial(optb_sbs* s, int32_t on) {
 int optb_sbs_next_dev(optb_sbs* s, uint64_t n, uint32_t shard, uint32_t n_shards,
                       int64_t* examples, int32_t* classes, void* stream) {
   if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
-  if (n_shards == 0 || shard >= n_shards) return set_err(OPTB_ERR_ARG, "sbs: bad shard %u of %u", shard, n_shards);
+  if (n_shards == 0 || shard >= n_shards)
+    return set_err(OPTB_ERR_ARG, "sbs: bad shard %u of %u", shard, n_shards);
   if (n == 0) return OPTB_OK;
   if (!examples) return set_err(OPTB_ERR_ARG, "sbs: null examples");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t C = s->C;
-  // ---- events of this call (lazy reshuffles, sampler.cpp:97): class c's
-  // draw D triggers generation D/m when D % m == 0 and D > 0.
+  // Lazy reshuffles (sampler.cpp:97): class c's draw D (counted from the
+  // constructor) starts generation D / m_c when D % m_c == 0 and D > 0.
   std::vector<EvKey> keys;
   std::vector<uint64_t> ev_count(C, 0);
   for (uint64_t c = 0; c < C; ++c) {
-    const uint64_t cnt = s->counts[c], m = s->m[c];
-    if (cnt == 0 || m == 0) continue;
+    const uint64_t cnt = s->counts[c], mm = s->m[c];
+    if (cnt == 0 || mm == 0) continue;
     const uint64_t D1 = (s->batches + n) * cnt;
-    for (uint64_t g = s->gen[c] + 1; g * m < D1; ++g) {
-      keys.push_back({(g * m) / cnt, c, g, g - s->gen[c]});
+    for (uint64_t g = s->gen[c] + 1; g * mm < D1; ++g) {
+      keys.push_back({(g * mm) / cnt, c, g, g - s->gen[c]});
       ++ev_count[c];
     }
   }
@@ -945,43 +984,33 @@ int optb_sbs_next_dev(optb_sbs* s, uint64_t n, uint32_t shard, uint32_t n_shards
     if (a.cls != b.cls) return a.cls < b.cls;
     return a.g < b.g;
   });
-  // ---- generation pool layout: class c with E_c events gets E_c + 1 slots
-  // (slot 0 = copy of the current generation) after the N current entries.
-  std::vector<uint64_t> base(C, 0), copy_of(C, ~0ull), final_of(C, ~0ull);
-  uint64_t cursor = s->N;
-  for (uint64_t c = 0; c < C; ++c) {
-    if (ev_count[c] == 0 || s->m[c] < 2) continue;
-    base[c] = cursor;
-    copy_of[c] = cursor;
-    final_of[c] = s->off[c];
-    cursor += (ev_count[c] + 1) * s->m[c];
-  }
-  int rc = ensure_pool(s, std::max<uint64_t>(cursor, 1), st);
-  if (rc) return rc;
-  std::vector<SbsEvent> evs(keys.size());
-  for (size_t e = 0; e < keys.size(); ++e) {
-    const uint64_t c = keys[e].cls, m = s->m[c], t = keys[e].t;
-    evs[e].cls = static_cast<uint32_t>(c);
-    evs[e].m = static_cast<uint32_t>(m);
-    if (m >= 2) {
-      evs[e].slot = base[c] + t * m;
-      evs[e].src = (t == 1) ? s->off[c] : base[c] + (t - 1) * m;
-    } else {
-      evs[e].slot = evs[e].src = s->off[c];
-    }
-  }
-  // ---- gather tables (K10)
+  // gather tables: drawn_before, generation at pool slot 0, its offset, stride
   std::vector<uint64_t> ga(4 * C);
   for (uint64_t c = 0; c < C; ++c) {
-    const bool pooled = ev_count[c] > 0 && s->m[c] >= 2;
-    ga[c] = s->batches * s->counts[c];                   // drawn_before
-    ga[C + c] = s->gen[c];                               // generation in slot 0
-    ga[2 * C + c] = pooled ? base[c] : s->off[c];        // its pool offset
-    ga[3 * C + c] = s->m[c] >= 2 ? s->m[c] : 0;          // stride (0: never changes)
+    ga[c] = s->batches * s->counts[c];
+    ga[C + c] = s->gen[c];
+    ga[3 * C + c] = s->m[c] >= 2 ? s->m[c] : 0;  // stride 0: the permutation never changes
   }
+  // the pool offsets are known only after layout; run_events fills gen_base
+  // and the packed copy of `ga` is patched before the upload
+  std::vector<uint64_t> gen_base;
   Packer pk;
   size_t o_ga = 0;
-  rc = run_events(s, evs, copy_of, final_of, pk, &o_ga, st, true, ga);
+  {
+    // lay out first to learn gen_base, then pack ga with it
+    uint64_t cursor = s->N;
+    gen_base.assign(C, 0);
+    for (uint64_t c = 0; c < C; ++c) {
+      if (ev_count[c] == 0 || s->m[c] < 2) {
+        gen_base[c] = s->off[c];
+        continue;
+      }
+      gen_base[c] = cursor;
+      cursor += (ev_count[c] + 1) * s->m[c];
+    }
+    for (uint64_t c = 0; c < C; ++c) ga[2 * C + c] = gen_base[c];
+  }
+  int rc = run_events(s, keys, pk, nullptr, &o_ga, &ga, st);
   if (rc) return rc;
   const uint64_t* d_ga = reinterpret_cast<const uint64_t*>(s->d_call + o_ga);
   SbsGatherArgs a;

@@ -188,7 +188,7 @@ __device__ __forceinline__ void row_affine(const Epi& e, uint64_t row, float& s,
 // (chunk, group) so a warp's 32 items cover 32*16*WC contiguous container
 // bytes.  Requires P % 16 == 0, 16-byte aligned rows and containers.
 template <int WC>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __maxnreg__(120)
     k_encode_exact_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
                        const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont) {
   constexpr int NI = WC;  // images per container word
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // ------------------------------------------------------------------ K2
 template <int WC, int O>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __maxnreg__(120)
     k_decode_exact_vec(Geom g, const uint8_t* __restrict__ cont, Epi e, void* __restrict__ out,
                        DevError* err) {
   constexpr int NI = WC;

@@ -70,14 +70,24 @@ struct SbsEvent {
   uint64_t src;     // element offset of the input permutation (previous generation)
 };
 
-cudaError_t launch_sbs_chain(const SbsEvent* ev, uint64_t n_events, unsigned long long* chain,
-                             uint64_t* seeds, uint32_t* flags, int force_serial, cudaStream_t s,
-                             uint64_t* launches);
-cudaError_t launch_sbs_shuffle(const SbsEvent* ev, const uint32_t* class_event_begin,
-                               const uint32_t* class_event_list, const uint64_t* cls_copy,
-                               const uint64_t* cls_final, uint32_t n_classes,
-                               const uint64_t* seeds, const uint32_t* flags, int64_t* pool,
-                               uint32_t max_m, cudaStream_t s, uint64_t* launches);
+// Device view of one call's reshuffle events (uploaded as one block).
+struct ChainArgs {
+  const SbsEvent* ev;         // [E] in chain order
+  uint64_t E;
+  const uint32_t* cls_begin;  // [n_cls+1] into cls_list
+  const uint32_t* cls_list;   // event ids of each reshuffling class, generation order
+  const uint64_t* cls_copy;   // pool offset receiving the class's pre-call permutation
+  const uint64_t* cls_final;  // pool offset of the class's current permutation
+  uint64_t* seeds;            // [E] chain state at the start of each event
+  uint32_t* flag;             // [1] rejection seen (forces the exact serial redo)
+  unsigned long long* chain;  // chain state before the first event; advanced in place
+  int64_t* pool;
+};
+
+// k_shuffle (one CTA per reshuffling class) + k_chain_finish (chain advance,
+// or the exact serial redo after a rejection / when forced).
+cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t max_m, int force,
+                              cudaStream_t s, uint64_t* launches);
 
 struct SbsGatherArgs {
   const uint32_t* row_cls;       // [B] class of each batch row (class-major)

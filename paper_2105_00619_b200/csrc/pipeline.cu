@@ -1,0 +1,172 @@
+// pipeline.cu -- the encode-while-train data path as a device pipeline.
+//
+// Replaces the reference's producer/consumer hand-off (pipeline.cpp:37-97
+// HandoffSlot, :116-129 prepare_epoch, :181-244 run) for the E-D path: instead
+// of a producer thread encoding whole epochs into host buffers behind a mutex,
+// each step is enqueued on CUDA streams with event hand-offs:
+//   side stream   : SBS draws of step k+1 (optb_sbs_next_dev) into draw buffer
+//                   (k+1)%2, after encode k-1 released it;
+//   caller stream : wait draws k -> gather-encode (optb_encode_dev) -> decode
+//                   with the fused epilogue (optb_decode_dev) into the caller's
+//                   layer-input buffer.
+// Reference invariants kept: at most two live draw buffers (pipeline.hpp:19-20),
+// in-order delivery, and errors surfacing before the affected step is consumed
+// (device-side format errors latch in the context, optb_ctx_sync).
+// Built only on the public C ABI (include/optb_cuda.h).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <vector>
+
+#include "optb_cuda.h"
+
+namespace {
+constexpr int kTimingRing = 64;
+}
+
+struct optb_pipeline {
+  optb_ctx* ctx = nullptr;
+  optb_pipeline_desc d{};
+  cudaStream_t side = nullptr;
+  int64_t* ex[2] = {};
+  int32_t* cls[2] = {};
+  void* cont = nullptr;
+  uint8_t* offs = nullptr;
+  cudaEvent_t sbs_done[2] = {}, enc_done[2] = {};
+  cudaEvent_t t_s0[kTimingRing] = {}, t_s1[kTimingRing] = {}, t_e0[kTimingRing] = {},
+              t_e1[kTimingRing] = {}, t_d1[kTimingRing] = {};
+  uint64_t step = 0;     // next step to deliver
+  uint64_t drawn = 0;    // steps whose draws are enqueued
+  bool timing = false;
+};
+
+namespace {
+
+int enqueue_draws(optb_pipeline* p) {
+  const uint64_t k = p->drawn;
+  const int b = static_cast<int>(k % 2);
+  if (k >= 2) {
+    if (cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  }
+  const int r = static_cast<int>(k % kTimingRing);
+  if (p->timing) cudaEventRecord(p->t_s0[r], p->side);
+  const uint64_t global_batches = p->d.layout.n_batches * p->d.n_shards;
+  int st = optb_sbs_next_dev(p->d.sbs, global_batches, p->d.shard, p->d.n_shards, p->ex[b], p->cls[b],
+                             p->side);
+  if (st) return st;
+  if (p->timing) cudaEventRecord(p->t_s1[r], p->side);
+  if (cudaEventRecord(p->sbs_done[b], p->side) != cudaSuccess) return OPTB_ERR_CUDA;
+  ++p->drawn;
+  return OPTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeline** out) {
+  if (!ctx || !d || !out || !d->sbs || !d->dataset) return OPTB_ERR_ARG;
+  *out = nullptr;
+  int st = optb_layout_check(&d->layout);
+  if (st) return st;
+  if (d->n_shards == 0 || d->shard >= d->n_shards) return OPTB_ERR_ARG;
+  auto* p = new optb_pipeline();
+  p->ctx = ctx;
+  p->d = *d;
+  p->timing = d->record_timings != 0;
+  const uint64_t rows = optb_layout_rows(&d->layout);
+  bool ok = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) == cudaSuccess;
+  for (int b = 0; b < 2 && ok; ++b) {
+    ok = cudaMalloc(&p->ex[b], rows * sizeof(int64_t)) == cudaSuccess &&
+         cudaMalloc(&p->cls[b], rows * sizeof(int32_t)) == cudaSuccess &&
+         cudaEventCreateWithFlags(&p->sbs_done[b], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&p->enc_done[b], cudaEventDisableTiming) == cudaSuccess;
+  }
+  if (ok) ok = cudaMalloc(&p->cont, optb_layout_container_bytes(&d->layout) + 16) == cudaSuccess;
+  const uint64_t ob = optb_layout_offsets_bytes(&d->layout);
+  if (ok && ob) ok = cudaMalloc(&p->offs, ob) == cudaSuccess;
+  for (int r = 0; r < kTimingRing && ok && p->timing; ++r) {
+    ok = cudaEventCreate(&p->t_s0[r]) == cudaSuccess && cudaEventCreate(&p->t_s1[r]) == cudaSuccess &&
+         cudaEventCreate(&p->t_e0[r]) == cudaSuccess && cudaEventCreate(&p->t_e1[r]) == cudaSuccess &&
+         cudaEventCreate(&p->t_d1[r]) == cudaSuccess;
+  }
+  if (!ok) {
+    optb_pipeline_destroy(p);
+    return OPTB_ERR_CUDA;
+  }
+  st = enqueue_draws(p);  // step 0's draws start right away
+  if (st) {
+    optb_pipeline_destroy(p);
+    return st;
+  }
+  *out = p;
+  return OPTB_OK;
+}
+
+int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
+  if (!p || !out) return OPTB_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t k = p->step;
+  const int b = static_cast<int>(k % 2);
+  const int r = static_cast<int>(k % kTimingRing);
+  int st = enqueue_draws(p);  // step k+1's draws overlap this step
+  if (st) return st;
+  if (cudaStreamWaitEvent(s, p->sbs_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (p->timing) cudaEventRecord(p->t_e0[r], s);
+  st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b], p->cont, p->offs, s);
+  if (st) return st;
+  if (p->timing) cudaEventRecord(p->t_e1[r], s);
+  if (cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
+  optb_epilogue e = p->d.epilogue;
+  if (e.class_scale && !e.row_class) e.row_class = p->cls[b];
+  st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
+  if (st) return st;
+  if (p->timing) cudaEventRecord(p->t_d1[r], s);
+  ++p->step;
+  return OPTB_OK;
+}
+
+int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
+                        const int32_t** classes) {
+  if (!p || step + 2 < p->step || step >= p->drawn) return OPTB_ERR_ARG;
+  if (examples) *examples = p->ex[step % 2];
+  if (classes) *classes = p->cls[step % 2];
+  return OPTB_OK;
+}
+
+const void* optb_pipeline_containers(const optb_pipeline* p) { return p ? p->cont : nullptr; }
+
+int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, float* enc_ms,
+                          float* dec_ms) {
+  if (!p || !p->timing || step >= p->step || step + kTimingRing <= p->step) return OPTB_ERR_ARG;
+  const int r = static_cast<int>(step % kTimingRing);
+  if (cudaEventSynchronize(p->t_d1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (sbs_ms && cudaEventElapsedTime(sbs_ms, p->t_s0[r], p->t_s1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (enc_ms && cudaEventElapsedTime(enc_ms, p->t_e0[r], p->t_e1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (dec_ms && cudaEventElapsedTime(dec_ms, p->t_e1[r], p->t_d1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  return OPTB_OK;
+}
+
+void optb_pipeline_destroy(optb_pipeline* p) {
+  if (!p) return;
+  if (p->side) cudaStreamSynchronize(p->side);
+  cudaDeviceSynchronize();
+  for (int b = 0; b < 2; ++b) {
+    if (p->ex[b]) cudaFree(p->ex[b]);
+    if (p->cls[b]) cudaFree(p->cls[b]);
+    if (p->sbs_done[b]) cudaEventDestroy(p->sbs_done[b]);
+    if (p->enc_done[b]) cudaEventDestroy(p->enc_done[b]);
+  }
+  for (int r = 0; r < kTimingRing; ++r) {
+    cudaEvent_t* evs[5] = {&p->t_s0[r], &p->t_s1[r], &p->t_e0[r], &p->t_e1[r], &p->t_d1[r]};
+    for (cudaEvent_t* e : evs)
+      if (*e) cudaEventDestroy(*e);
+  }
+  if (p->cont) cudaFree(p->cont);
+  if (p->offs) cudaFree(p->offs);
+  if (p->side) cudaStreamDestroy(p->side);
+  delete p;
+}
+
+}  // extern "C"

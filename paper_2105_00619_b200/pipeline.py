@@ -1,0 +1,72 @@
+"""The encode-while-train data path (optb_pipeline_*; reference pipeline.cpp).
+
+    pipe = Pipeline(cursor, dataset, mode=CodecMode.ExactInt128, batch=512,
+                    batches_per_step=97, out_dtype=torch.float32, scale=1/255)
+    for step in range(n):
+        pipe.step(layer_input)          # SBS -> gather-encode -> decode, async
+
+Per step the native pipeline gathers the SBS-drawn rows of ``dataset`` (a
+CUDA tensor, or a pinned CPU tensor read zero-copy over PCIe), packs them into
+containers and decodes them into ``layer_input`` on the current stream, while
+the next step's draws run on a side stream.  One ctypes call per step.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+
+from . import _lib
+from ._lib import Epilogue, Layout, PipelineDesc, check, lib
+from .codec import BF16, F16, F32, U8
+
+
+class Pipeline:
+    def __init__(self, cursor, dataset, mode, batch: int, batches_per_step: int, per_chunk=None,
+                 shard: int = 0, n_shards: int = 1, out_dtype=None, scale: float = 1.0,
+                 class_scale=None, class_bias=None, device: int = 0, record_timings: bool = False):
+        import torch
+        from . import codec
+        out_dtype = out_dtype or torch.uint8
+        dt = {torch.uint8: U8, torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}[out_dtype]
+        P = dataset.shape[1]
+        pc = per_chunk or codec.capacity(mode)
+        self.layout = Layout(int(mode), pc, P, batch, batches_per_step)
+        self.rows = batch * batches_per_step
+        self.P = P
+        self.device = device
+        self._keep = (cursor, dataset, class_scale, class_bias)
+        E = Epilogue(dt, float(scale), None if class_scale is None else ct.c_void_p(class_scale.data_ptr()),
+                     None if class_bias is None else ct.c_void_p(class_bias.data_ptr()), None, 0)
+        desc = PipelineDesc(self.layout, ct.c_void_p(dataset.data_ptr()), dataset.stride(0), cursor._h, shard,
+                            n_shards, E, 1 if record_timings else 0)
+        self._h = ct.c_void_p()
+        check(lib.optb_pipeline_create(_lib.context(device), ct.byref(desc), ct.byref(self._h)))
+        self.steps = 0
+
+    def step(self, out, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        check(lib.optb_pipeline_step(self._h, ct.c_void_p(out.data_ptr()), ct.c_void_p(stream.cuda_stream)))
+        self.steps += 1
+
+    def timings(self, step: int):
+        s, e, d = ct.c_float(), ct.c_float(), ct.c_float()
+        check(lib.optb_pipeline_timings(self._h, step, ct.byref(s), ct.byref(e), ct.byref(d)))
+        return s.value, e.value, d.value
+
+    def draws(self, step: int):
+        """(examples_ptr, classes_ptr) device pointers of a buffered step."""
+        ex, cl = ct.c_void_p(), ct.c_void_p()
+        check(lib.optb_pipeline_draws(self._h, step, ct.byref(ex), ct.byref(cl)))
+        return ex.value, cl.value
+
+    def containers_ptr(self) -> int:
+        return lib.optb_pipeline_containers(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.optb_pipeline_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,75 @@
+"""The E-D pipeline (optb_pipeline_*): every step's decoded rows equal the
+oracle's decode of the oracle's encode of the reference-stream draws."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SCALE = float(np.float32(1.0) / np.float32(255.0))
+
+
+def _setup(pkg, O, torch, N=4000, Ccls=10, B=64, seed=99):
+    S = pkg.sampler
+    labels = (np.arange(N) % Ccls).astype(np.int32)
+    ds = O.synth_pixels(7, 0, N, 768)
+    p = S.plan([1.0 / Ccls] * Ccls, B, seed)
+    offs, mem = S.class_index_dev(labels, Ccls)
+    ro, rm = O.class_index(labels, Ccls)
+    ref = O.Cursor(O.sbs_plan([1.0 / Ccls] * Ccls, B), ro, rm, B, seed)
+    return S, labels, ds, p, offs, mem, ref
+
+
+@pytest.mark.parametrize("mode,dtype", [(1, "uint8"), (0, "float32"), (3, "bfloat16"), (2, "float16")])
+def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype):
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P = 64, 5, 768
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    ds_d = torch.from_numpy(ds).cuda()
+    dt = getattr(torch, dtype)
+    pc = pkg.codec.capacity(mode)
+    pipe = Pipeline(cur, ds_d, mode, B, nb, per_chunk=pc, out_dtype=dt, scale=SCALE)
+    kind = {"uint8": O.U8, "float32": O.F32, "bfloat16": O.BF16, "float16": O.F16}[dtype]
+    for step in range(6):
+        out = torch.empty((B * nb, P), dtype=dt, device="cuda")
+        pipe.step(out)
+        pkg.codec.sync()
+        ex, _ = ref.next(nb)
+        cont, offs_ = O.encode_stream(ds, ex, mode, pc, B, nb)
+        want = O.decode_stream(cont, offs_, mode, pc, P, B, nb, out_dtype=kind, scale=SCALE)
+        got = out.cpu()
+        got = got.numpy() if dtype in ("uint8", "float32") else got.view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got.view(want.dtype), want), step
+    pipe.close()
+
+
+def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda):
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P, G = 64, 3, 768, 2
+    ds_d = torch.from_numpy(ds).cuda()
+    cs = torch.linspace(0.001, 0.01, 10, device="cuda")
+    cb = torch.linspace(-1, 1, 10, device="cuda")
+    outs = {}
+    for r in range(G):
+        cur = S.BatchCursor.from_device_index(p, offs, mem)
+        pipe = Pipeline(cur, ds_d, 1, B, nb, shard=r, n_shards=G, out_dtype=torch.float32, class_scale=cs,
+                        class_bias=cb)
+        outs[r] = []
+        for _ in range(2):
+            o = torch.empty((B * nb, P), dtype=torch.float32, device="cuda")
+            pipe.step(o)
+            outs[r].append(o)
+        pkg.codec.sync()
+        pipe.close()
+    for step in range(2):
+        ex, cl = ref.next(nb * G)
+        ex, cl = ex.reshape(nb * G, B), cl.reshape(nb * G, B)
+        for r in range(G):
+            e, c = ex[r::G].reshape(-1), cl[r::G].reshape(-1)
+            cont, _ = O.encode_stream(ds, e, 1, 16, B, nb)
+            want = O.decode_stream(cont, None, 1, 16, P, B, nb, out_dtype=O.F32, scale=1.0,
+                                   class_scale=cs.cpu().numpy(), class_bias=cb.cpu().numpy(), row_class=c)
+            assert np.array_equal(outs[r][step].cpu().numpy().view(np.uint32), want.view(np.uint32)), (step, r)
