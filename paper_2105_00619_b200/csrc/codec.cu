@@ -150,6 +150,33 @@ struct Out4 {
   }
 };
 
+// 8 consecutive decoded pixels -> 8 binary16 / bfloat16 values, one 128-bit store.
+struct Out8 {
+  template <int O>
+  static __device__ __forceinline__ void put(void* dst, uint2 q8, float s, float b, bool affine) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t src = k < 2 ? q8.x : q8.y;
+      const int sh = 16 * (k & 1);
+      float y0 = __fmul_rn(static_cast<float>((src >> sh) & 0xffu), s);
+      float y1 = __fmul_rn(static_cast<float>((src >> (sh + 8)) & 0xffu), s);
+      if (affine) {
+        y0 = __fadd_rn(y0, b);
+        y1 = __fadd_rn(y1, b);
+      }
+      if constexpr (O == OPTB_OUT_F16) {
+        const __half2 h = __floats2half2_rn(y0, y1);
+        w[k] = *reinterpret_cast<const uint32_t*>(&h);
+      } else {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
+        w[k] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+    }
+    stg16(dst, make_uint4(w[0], w[1], w[2], w[3]));
+  }
+};
+
 template <int O>
 __device__ __forceinline__ void put1(void* out, uint64_t idx, uint32_t q, float s, float b,
                                      bool affine) {
@@ -183,57 +210,122 @@ __device__ __forceinline__ void row_affine(const Epi& e, uint64_t row, float& s,
   }
 }
 
-// ------------------------------------------------------------------ K1
-// One work item = 16 consecutive pixels of one chunk; items are linear in
-// (chunk, group) so a warp's 32 items cover 32*16*WC contiguous container
-// bytes.  Requires P % 16 == 0, 16-byte aligned rows and containers.
+// ------------------------------------------------------------------ async copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Work items: 16 consecutive pixels of one chunk, linear in (chunk, group),
+// so a warp's 32 items cover 32*16*WC contiguous container bytes.  Each warp
+// runs a kStages-deep cp.async pipeline over its tiles (one tile = the warp's
+// 32 items) in a warp-private ring of shared-memory slots: the copies of the
+// next kStages-1 tiles are in flight while the current tile is transposed.
+// Requires P % 16 == 0 and 16-byte aligned rows / containers / outputs.
+constexpr int kStages = 3;
+
 template <int WC>
-__global__ void __maxnreg__(120)
+struct VecShape {
+  static constexpr int NI = WC;                 // images per container word
+  static constexpr int SW = (WC == 16) ? 7 : 15;  // slot XOR swizzle mask
+  static constexpr int SLOT = 32 * 16 * WC;     // bytes per stage slot per warp
+};
+
+// ------------------------------------------------------------------ K1
+// Gather-encode.  Stage slot layout on input: row i of the chunk, lane L's
+// 16 pixels at (i*32 + L)*16 (conflict-free LDS.128); after the register
+// transpose the slot is reused as the output tile, word p of lane L at
+// (L*16 + (p ^ (L & SW)))*WC (conflict-free both ways), then copied out with
+// fully coalesced 128-bit (64-bit) stores.
+template <int WC>
+__global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
     k_encode_exact_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
                        const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont) {
-  constexpr int NI = WC;  // images per container word
+  using S = VecShape<WC>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* sw = smem_raw + warp * (32 * 16 * WC);
+  uint8_t* ring = smem_raw + warp * kStages * S::SLOT;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
-  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32; base < items;
-       base += stride) {
+  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
+
+  // Dataset row ids of a tile are fetched one stage before its copies are
+  // issued, so the dependent index loads never stall the pipeline.
+  auto fetch_rows = [&](uint64_t base, uint32_t (&rows)[S::NI]) {
     const uint64_t t = base + lane;
-    uint32_t m[16][4];
-    if (t < items) {
+    if (base < items && t < items) {
+      const ChunkPos c = chunk_pos(g, t / G);
+#pragma unroll
+      for (int i = 0; i < S::NI; ++i) {
+        const uint64_t r = c.r0 + i;
+        rows[i] = (i < static_cast<int>(c.n))
+                      ? static_cast<uint32_t>(row_index ? __ldg(row_index + r) : static_cast<int64_t>(r))
+                      : 0u;
+      }
+    }
+  };
+  auto issue = [&](uint64_t base, int stage, const uint32_t (&rows)[S::NI]) {
+    const uint64_t t = base + lane;
+    if (base < items && t < items) {
       const uint64_t k = t / G;
       const uint64_t gi = t - k * G;
-      const ChunkPos c = chunk_pos(g, k);
+      const uint32_t n = chunk_pos(g, k).n;
+      uint8_t* slot = ring + stage * S::SLOT;
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (i < static_cast<int>(c.n)) {
-          const uint64_t r = c.r0 + i;
-          const uint64_t src = row_index ? static_cast<uint64_t>(__ldg(row_index + r)) : r;
-          v = ldg16(images + src * row_stride + gi * 16);
-        }
-        m[i][0] = v.x;
-        m[i][1] = v.y;
-        m[i][2] = v.z;
-        m[i][3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < NI; ++i) m[i][0] = m[i][1] = m[i][2] = m[i][3] = 0u;
+      for (int i = 0; i < S::NI; ++i)
+        if (i < static_cast<int>(n))
+          cp_async16(slot + (i * 32 + lane) * 16, images + static_cast<uint64_t>(rows[i]) * row_stride + gi * 16);
     }
-    transpose16<NI, 16>(m);  // m[p] = word of pixel p (bytes = images 0..15)
-    // stage: word p of lane L at slot (p ^ (L & SW)) of L's row (bank-conflict free)
-    constexpr int SW = (WC == 16) ? 7 : 15;
+    cp_async_commit();
+  };
+
+  uint32_t rows[S::NI];
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    fetch_rows(first + s * stride, rows);
+    issue(first + s * stride, s, rows);
+  }
+  fetch_rows(first + (kStages - 1) * stride, rows);
+  int stage = 0;
+  for (uint64_t base = first; base < items; base += stride) {
+    issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages, rows);
+    fetch_rows(base + kStages * stride, rows);  // consumed by the next iteration's issue
+    cp_async_wait<kStages - 1>();
+    __syncwarp();
+    uint8_t* slot = ring + stage * S::SLOT;
+    const uint64_t t = base + lane;
+    uint32_t n = 0;
+    if (t < items) n = chunk_pos(g, t / G).n;
+    uint32_t m[16][4];
+#pragma unroll
+    for (int i = 0; i < S::NI; ++i) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (i < static_cast<int>(n)) v = *reinterpret_cast<const uint4*>(slot + (i * 32 + lane) * 16);
+      m[i][0] = v.x;
+      m[i][1] = v.y;
+      m[i][2] = v.z;
+      m[i][3] = v.w;
+    }
+    transpose16<S::NI, 16>(m);  // m[p] = word of pixel p (bytes = images 0..15)
+    __syncwarp();
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
-      const int slot = p ^ (lane & SW);
+      const int sl = p ^ (lane & S::SW);
       if constexpr (WC == 16) {
-        *reinterpret_cast<uint4*>(sw + (lane * 16 + slot) * 16) =
-            make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
+        *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
       } else {
-        *reinterpret_cast<uint2*>(sw + (lane * 16 + slot) * 8) = make_uint2(m[p][0], m[p][1]);
+        *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) = make_uint2(m[p][0], m[p][1]);
       }
     }
     __syncwarp();
@@ -242,105 +334,124 @@ __global__ void __maxnreg__(120)
     for (int q = 0; q < 16; ++q) {
       const int W = q * 32 + lane, L = W >> 4, p = W & 15;
       if (base + L < items) {
-        const int slot = p ^ (L & SW);
+        const int sl = p ^ (L & S::SW);
         if constexpr (WC == 16) {
-          stg16(dst + W * 16, *reinterpret_cast<const uint4*>(sw + (L * 16 + slot) * 16));
+          stg16(dst + W * 16, *reinterpret_cast<const uint4*>(slot + (L * 16 + sl) * 16));
         } else {
-          stg8(dst + W * 8, *reinterpret_cast<const uint2*>(sw + (L * 16 + slot) * 8));
+          stg8(dst + W * 8, *reinterpret_cast<const uint2*>(slot + (L * 16 + sl) * 8));
         }
       }
     }
     __syncwarp();
+    stage = (stage + 1) % kStages;
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ K2
+// Decode.  Container words arrive by cp.async straight into the swizzled slot
+// layout; after the register transpose each lane holds 16 pixels of every
+// image: u8 rows are stored directly (each warp instruction writes 512
+// contiguous bytes of one row); float outputs go through a u8 tile in the
+// same slot so that the epilogue stores are coalesced too.
 template <int WC, int O>
-__global__ void __maxnreg__(120)
+__global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
     k_decode_exact_vec(Geom g, const uint8_t* __restrict__ cont, Epi e, void* __restrict__ out,
                        DevError* err) {
-  constexpr int NI = WC;
-  constexpr int SW = (WC == 16) ? 7 : 15;
+  using S = VecShape<WC>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* sw = smem_raw + warp * (32 * 16 * 16);
+  uint8_t* ring = smem_raw + warp * kStages * S::SLOT;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
+  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
   const uint64_t ostride = e.row_stride;
-  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32; base < items;
-       base += stride) {
-    // coalesced container loads -> swizzled warp-private smem
-    const uint8_t* src = cont + base * 16 * WC;
+
+  auto issue = [&](uint64_t base, int stage) {
+    if (base < items) {
+      const uint8_t* src = cont + base * 16 * WC;
+      uint8_t* slot = ring + stage * S::SLOT;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int W = q * 32 + lane, L = W >> 4, p = W & 15;
-      if (base + L < items) {
-        const int slot = p ^ (L & SW);
-        if constexpr (WC == 16) {
-          *reinterpret_cast<uint4*>(sw + (L * 16 + slot) * 16) = ldg16(src + W * 16);
-        } else {
-          *reinterpret_cast<uint2*>(sw + (L * 16 + slot) * 8) = ldg8(src + W * 8);
+      for (int q = 0; q < 16; ++q) {
+        const int W = q * 32 + lane, L = W >> 4, p = W & 15;
+        if (base + L < items) {
+          const int sl = p ^ (L & S::SW);
+          if constexpr (WC == 16) {
+            cp_async16(slot + (L * 16 + sl) * 16, src + W * 16);
+          } else {
+            cp_async8(slot + (L * 16 + sl) * 8, src + W * 8);
+          }
         }
       }
     }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) issue(first + s * stride, s);
+  int stage = 0;
+  for (uint64_t base = first; base < items; base += stride) {
+    issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
+    cp_async_wait<kStages - 1>();
     __syncwarp();
+    uint8_t* slot = ring + stage * S::SLOT;
     uint32_t m[16][4];
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
-      const int slot = p ^ (lane & SW);
+      const int sl = p ^ (lane & S::SW);
       if constexpr (WC == 16) {
-        const uint4 v = *reinterpret_cast<const uint4*>(sw + (lane * 16 + slot) * 16);
+        const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
         m[p][0] = v.x;
         m[p][1] = v.y;
         m[p][2] = v.z;
         m[p][3] = v.w;
       } else {
-        const uint2 v = *reinterpret_cast<const uint2*>(sw + (lane * 16 + slot) * 8);
+        const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
         m[p][0] = v.x;
         m[p][1] = v.y;
         m[p][2] = 0u;
         m[p][3] = 0u;
       }
     }
-    transpose16<16, NI>(m);  // m[i] = 16 pixels of image i
+    transpose16<16, S::NI>(m);  // m[i] = 16 pixels of image i
     const uint64_t t = base + lane;
     const bool valid = t < items;
-    uint64_t k = 0, gi = 0;
+    uint64_t gi = 0;
     ChunkPos c{0, 0};
     if (valid) {
-      k = t / G;
+      const uint64_t k = t / G;
       gi = t - k * G;
       c = chunk_pos(g, k);
       // range check (codec.cpp:189-194): bytes of images >= n must be zero
       uint32_t hi = 0;
 #pragma unroll
-      for (int i = 0; i < NI; ++i)
+      for (int i = 0; i < S::NI; ++i)
         if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
       if (hi) latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
     }
     if constexpr (O == OPTB_OUT_U8) {
       if (valid) {
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
+        for (int i = 0; i < S::NI; ++i)
           if (i < static_cast<int>(c.n))
             stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16,
                   make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]));
       }
-      __syncwarp();
     } else {
-      __syncwarp();  // all lanes done reading the container stage
-      // u8 tile: image i, lane L's 16 pixels at (i*32 + L)*16
+      __syncwarp();  // all lanes done reading the container slot
+      // u8 tile in the same slot: image i, lane L's 16 pixels at (i*32 + L)*16
 #pragma unroll
-      for (int i = 0; i < NI; ++i)
-        *reinterpret_cast<uint4*>(sw + (i * 32 + lane) * 16) =
-            make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]);
+      for (int i = 0; i < S::NI; ++i)
+        *reinterpret_cast<uint4*>(slot + (i * 32 + lane) * 16) = make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]);
       __syncwarp();
-      // epilogue: lane handles pixels 4*(lane%4).. of source lane L = lane/4 + 8*cc
+      // epilogue: every lane stores 16 bytes per row -- PX = 4 fp32 or 8 half
+      // pixels, starting at pixel PX*(lane % LPS) of source lane L's group
       constexpr int ES = (O == OPTB_OUT_F32) ? 4 : 2;
+      constexpr int PX = 16 / ES, LPS = 16 / PX, ROUNDS = 32 / (32 / LPS);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int L = (lane >> 2) + 8 * cc;
+      for (int cc = 0; cc < ROUNDS; ++cc) {
+        const int L = lane / LPS + (32 / LPS) * cc;
         const uint32_t r0lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0), L);
         const uint32_t r0hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0 >> 32), L);
         const uint32_t nL = __shfl_sync(0xffffffffu, valid ? c.n : 0u, L);
@@ -348,23 +459,31 @@ __global__ void __maxnreg__(120)
         const uint32_t ghi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi >> 32), L);
         const uint64_t r0L = (static_cast<uint64_t>(r0hi) << 32) | r0lo;
         const uint64_t gL = (static_cast<uint64_t>(ghi) << 32) | glo;
-        const uint64_t px = gL * 16 + 4 * (lane & 3);
+        const int sub = PX * (lane % LPS);
+        const uint64_t px = gL * 16 + sub;
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
+        for (int i = 0; i < S::NI; ++i) {
           if (i < static_cast<int>(nL)) {
-            const uint32_t q4 = *reinterpret_cast<const uint32_t*>(sw + (i * 32 + L) * 16 +
-                                                                     4 * (lane & 3));
             const uint64_t row = r0L + i;
             float s, b;
             bool aff;
             row_affine(e, row, s, b, aff);
-            Out4::put<O>(static_cast<uint8_t*>(out) + (row * ostride + px) * ES, q4, s, b, aff);
+            uint8_t* dst = static_cast<uint8_t*>(out) + (row * ostride + px) * ES;
+            if constexpr (PX == 4) {
+              const uint32_t q4 = *reinterpret_cast<const uint32_t*>(slot + (i * 32 + L) * 16 + sub);
+              Out4::put<O>(dst, q4, s, b, aff);
+            } else {
+              const uint2 q8 = *reinterpret_cast<const uint2*>(slot + (i * 32 + L) * 16 + sub);
+              Out8::put<O>(dst, q8, s, b, aff);
+            }
           }
         }
       }
-      __syncwarp();
     }
+    __syncwarp();
+    stage = (stage + 1) % kStages;
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ generic
@@ -587,7 +706,7 @@ cudaError_t dec_generic(const Geom& g, const void* cont, const uint8_t* offs, co
 template <int WC>
 cudaError_t enc_vec(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* idx,
                     void* cont, cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = kWarps * 32 * 16 * WC;
+  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecShape<WC>::SLOT;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_encode_exact_vec<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -605,7 +724,7 @@ cudaError_t enc_vec(const Geom& g, const uint8_t* images, uint64_t row_stride, c
 template <int WC, int O>
 cudaError_t dec_vec(const Geom& g, const void* cont, const Epi& e, void* out, DevError* err,
                     cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = kWarps * 32 * 16 * 16;
+  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecShape<WC>::SLOT;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_decode_exact_vec<WC, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,

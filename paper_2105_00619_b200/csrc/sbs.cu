@@ -310,7 +310,7 @@ __global__ void k_chain_finish(ChainArgs a, uint32_t n_cls, int force) {
 }
 
 // ------------------------------------------------------------------ K10
-__global__ void k_gather(SbsGatherArgs a, int64_t* __restrict__ examples, int32_t* __restrict__ classes,
+__global__ void __maxnreg__(32) k_gather(SbsGatherArgs a, int64_t* __restrict__ examples, int32_t* __restrict__ classes,
                          uint64_t out_batches) {
   const uint64_t total = out_batches * a.B;
   for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
@@ -394,9 +394,11 @@ cudaError_t launch_sbs_gather(const SbsGatherArgs& a, int64_t* examples, int32_t
       a.n_batches > a.shard ? (a.n_batches - a.shard + a.n_shards - 1) / a.n_shards : 0;
   const uint64_t total = out_batches * a.B;
   if (total == 0) return cudaSuccess;
-  const uint64_t want = (total + 255) / 256;
-  const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
-  k_gather<<<grid, 256, 0, s>>>(a, examples, classes, out_batches);
+  // Small CTAs (64 threads x <= 32 registers) so the gather co-resides with
+  // the encode/decode CTAs of the previous step when it runs on a side stream.
+  const uint64_t want = (total + 63) / 64;
+  const unsigned grid = static_cast<unsigned>(want < 148 * 2 ? want : 148 * 2);
+  k_gather<<<grid, 64, 0, s>>>(a, examples, classes, out_batches);
   ++*launches;
   return cudaGetLastError();
 }
