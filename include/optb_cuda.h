@@ -190,6 +190,10 @@ uint64_t optb_sbs_batches_drawn(const optb_sbs* sbs);
 /* Testing aid: force the exact serial rejection-sampling path for every
  * reshuffle (results are identical; only speed changes). */
 int optb_sbs_set_force_serial(optb_sbs* sbs, int32_t on);
+/* Tuning aid: time each next call's phases with CUDA events; report the last
+ * call's upload, reshuffle (K9+K8) and gather (K10) durations in ms. */
+int optb_sbs_set_profiling(optb_sbs* sbs, int32_t on);
+int optb_sbs_profile(optb_sbs* sbs, float* upload_ms, float* reshuffle_ms, float* gather_ms);
 
 /* ---------------------------------------------------------------- E-D pipeline
  * The encode-while-train data path (replaces pipeline.cpp:37-97 HandoffSlot,

@@ -623,6 +623,8 @@ struct optb_sbs {
   std::vector<uint64_t> counts, m, off, prefix, gen;
   uint64_t batches = 0;
   int force_serial = 0;
+  bool prof = false;               // optb_sbs_set_profiling
+  cudaEvent_t pe[4] = {};          // call start, uploaded, reshuffled, gathered
   bool small_ids = true;  // every example id < 2^32 (shared-memory shuffle)
   uint32_t max_m = 0;
   // device
@@ -764,7 +766,9 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
   const size_t o_copy = pk.put(ccopy.data(), ccopy.size());
   const size_t o_final = pk.put(cfinal.data(), cfinal.size());
   if (extra) *o_extra = pk.put(extra->data(), extra->size());
+  if (s->prof) cudaEventRecord(s->pe[0], st);
   rc = upload_call(s, pk, st);
+  if (s->prof) cudaEventRecord(s->pe[1], st);
   if (rc) return rc;
   if (E == 0) return OPTB_OK;
   uint8_t* d = s->d_call;
@@ -783,6 +787,7 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
                                     s->small_ids ? s->max_m : 0xffffffffu, s->force_serial, st,
                                     &s->ctx->launches);
   if (e != cudaSuccess) return cuda_err(e, "sbs events");
+  if (s->prof) cudaEventRecord(s->pe[2], st);
   return OPTB_OK;
 }
 
@@ -946,10 +951,29 @@ void optb_sbs_destroy(optb_sbs* s) {
   }
   if (s->d_ex) cudaFree(s->d_ex);
   if (s->d_cl) cudaFree(s->d_cl);
+  for (auto& e : s->pe)
+    if (e) cudaEventDestroy(e);
   delete s;
 }
 
 uint64_t optb_sbs_batches_drawn(const optb_sbs* s) { return s ? s->batches : 0; }
+
+int optb_sbs_set_profiling(optb_sbs* s, int32_t on) {
+  if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
+  if (on && !s->pe[0])
+    for (auto& e : s->pe) CK(cudaEventCreate(&e), "sbs profiling events");
+  s->prof = on != 0;
+  return OPTB_OK;
+}
+
+int optb_sbs_profile(optb_sbs* s, float* upload_ms, float* reshuffle_ms, float* gather_ms) {
+  if (!s || !s->prof) return set_err(OPTB_ERR_ARG, "sbs: profiling is off");
+  CK(cudaEventSynchronize(s->pe[3]), "sbs profile");
+  if (upload_ms) CK(cudaEventElapsedTime(upload_ms, s->pe[0], s->pe[1]), "sbs profile");
+  if (reshuffle_ms) CK(cudaEventElapsedTime(reshuffle_ms, s->pe[1], s->pe[2]), "sbs profile");
+  if (gather_ms) CK(cudaEventElapsedTime(gather_ms, s->pe[2], s->pe[3]), "sbs profile");
+  return OPTB_OK;
+}
 
 int optb_sbs_set_force_serial(optb_sbs* s, int32_t on) {
   if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
@@ -1037,6 +1061,7 @@ int optb_sbs_next_dev(optb_sbs* s, uint64_t n, uint32_t shard, uint32_t n_shards
   a.n_shards = n_shards;
   cudaError_t e = launch_sbs_gather(a, examples, classes, st, &s->ctx->launches);
   if (e != cudaSuccess) return cuda_err(e, "sbs gather");
+  if (s->prof) cudaEventRecord(s->pe[3], st);
   for (uint64_t c = 0; c < C; ++c) s->gen[c] += ev_count[c];
   s->batches += n;
   return OPTB_OK;

@@ -166,24 +166,48 @@ __global__ void k_ci_label_value(const int32_t* labels, uint64_t C, DevError* er
 // call exactly (serially).  The permutation lives in shared memory as u32 when
 // it fits (host guarantees ids < 2^32 then), else in the generation pool.
 constexpr int kJWin = 2048;
+constexpr int kWalk = 1024;
+
+// Called by every thread of a block.  Thread 0 walks the event list assuming
+// no rejection (one mix per event: K = m-1, or 0 for m <= 1); the list is
+// staged into shared memory chunk by chunk by the whole block first, so the
+// serial walk never waits on a global load (it runs next to bandwidth-bound
+// encode/decode kernels).  Optionally records the start state of `cls`'s
+// events in a.seeds.  Returns the chain state after the last event.
+__device__ uint64_t chain_walk(const ChainArgs& a, uint32_t cls, bool want_seeds) {
+  __shared__ uint2 evs[kWalk];
+  __shared__ uint64_t s_sh;
+  if (threadIdx.x == 0) s_sh = *a.chain;
+  for (uint64_t base = 0; base < a.E; base += kWalk) {
+    const uint32_t cnt = static_cast<uint32_t>(a.E - base < kWalk ? a.E - base : kWalk);
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < cnt; x += blockDim.x) {
+      const SbsEvent ev = a.ev[base + x];
+      evs[x] = make_uint2(ev.cls, ev.m);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t s = s_sh;
+      for (uint32_t x = 0; x < cnt; ++x) {
+        const uint2 ev = evs[x];
+        if (want_seeds && ev.x == cls) a.seeds[base + x] = s;
+        s = mix64(s + (ev.y >= 2 ? static_cast<uint64_t>(ev.y) : 1ull) * kGamma);
+      }
+      s_sh = s;
+    }
+  }
+  __syncthreads();
+  return s_sh;
+}
 
 __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
   extern __shared__ uint32_t sh[];
   uint32_t* js = sh;            // kJWin swap targets
   uint32_t* perm = sh + kJWin;  // m entries (smem path)
-  __shared__ int bad;
   const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
   const SbsEvent first = a.ev[a.cls_list[b]];
   const uint32_t cls = first.cls, m = first.m;
-  if (threadIdx.x == 0) {
-    bad = 0;
-    uint64_t s = *a.chain;
-    for (uint64_t e = 0; e < a.E; ++e) {  // speculative chain: K = m-1 (or 0)
-      const SbsEvent ev = a.ev[e];
-      if (ev.cls == cls) a.seeds[e] = s;
-      s = mix64(s + (ev.m >= 2 ? static_cast<uint64_t>(ev.m) : 1ull) * kGamma);
-    }
-  }
+  chain_walk(a, cls, true);  // this class's event start states -> a.seeds
   const uint64_t copy_to = a.cls_copy[blockIdx.x];
   if (use_smem) {
     for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) {
@@ -252,6 +276,123 @@ __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
     for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) a.pool[final_to + x] = a.pool[cur_src + x];
 }
 
+// ------------------------------------------------------------------ K9 (parallel)
+// Fisher-Yates with known swap targets, evaluated for all output positions at
+// once.  Let A_k be the array after steps m..k (step i swaps [i-1] and [j_i],
+// rng.hpp:57-64; A_{m+1} = input).  For x < k-1, A_k[x] is A_{k+1}[k-1] if
+// j_k == x and A_{k+1}[x] otherwise, so
+//   A_k[x] = input[x]                       if no step s >= k has j_s == x,
+//          = A_{s+1}[s-1]  (s = the smallest such step)   otherwise,
+// and the output is out[p] = A_{p+2}[j_{p+1}] for p >= 1, out[0] = A_2[0].
+// Each position follows its own short chain through the steps bucketed by
+// j, so the pass is one histogram + scan + scatter + chain-follow in shared
+// memory -- no serial swap loop (tests/test_chain_model.py and the GPU parity
+// tests pin it against the reference sequence).
+constexpr int kParThreads = 256;
+constexpr uint32_t kParMaxM = 11776;  // 18 bytes of shared memory per element
+
+size_t par_smem_bytes(uint32_t m) { return 4ull * (4ull * m + 2) + 2ull * (m + 2); }
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kParThreads / 32 ? warp_tot[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kParThreads / 32) warp_tot[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t before = warp ? warp_tot[warp - 1] : 0u;
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(kParThreads) k_shuffle_par(ChainArgs a) {
+  extern __shared__ uint32_t sh[];
+  __shared__ uint32_t warp_tot[kParThreads / 32];
+  const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
+  const SbsEvent first = a.ev[a.cls_list[b]];
+  const uint32_t cls = first.cls, m = first.m;
+  uint32_t* js = sh;               // [m + 1]  swap target of step i (i = 2..m)
+  uint32_t* off = js + (m + 1);    // [m + 1]  bucket starts, then ends
+  uint32_t* bk = off + (m + 1);    // [m]      steps bucketed by target
+  uint32_t* pa = bk + m;           // [m]      input permutation
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(pa + m);  // [m] bucket sizes
+  chain_walk(a, cls, true);
+  const uint64_t copy_to = a.cls_copy[blockIdx.x];
+  for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) {
+    const int64_t v = a.pool[first.src + x];
+    pa[x] = static_cast<uint32_t>(v);
+    a.pool[copy_to + x] = v;
+  }
+  __syncthreads();
+  // per-thread contiguous ranges for the scan
+  const uint32_t per = (m + kParThreads - 1) / kParThreads;
+  const uint32_t lo = min(m, threadIdx.x * per), hi = min(m, lo + per);
+  for (uint32_t q = b; q < end; ++q) {
+    const uint32_t e = a.cls_list[q];
+    const SbsEvent E = a.ev[e];
+    const uint64_t s = a.seeds[e];
+    bool rej = false;
+    for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) cnt[x] = 0;
+    __syncthreads();
+    for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) {
+      const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
+      rej |= rejected(x, i);
+      const uint32_t j = static_cast<uint32_t>(x % i);
+      js[i] = j;
+      atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
+    }
+    if (__syncthreads_or(rej)) {
+      if (threadIdx.x == 0) atomicExch(a.flag, 1u);
+      return;  // k_chain_finish redoes this call serially
+    }
+    uint32_t local = 0;
+    for (uint32_t x = lo; x < hi; ++x) local += cnt[x];
+    uint32_t run = block_exclusive_scan(local, warp_tot);
+    for (uint32_t x = lo; x < hi; ++x) {
+      off[x] = run;
+      run += cnt[x];
+    }
+    __syncthreads();
+    for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) bk[atomicAdd(&off[js[i]], 1u)] = i;
+    __syncthreads();  // off[x] now holds the end of bucket x
+    int64_t* gout = a.pool + E.slot;
+    for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+      uint32_t x = p >= 1 ? js[p + 1] : 0u;
+      uint32_t k = p >= 1 ? p + 2 : 2u;
+      for (;;) {
+        const uint32_t hi_b = off[x], lo_b = hi_b - cnt[x];
+        uint32_t best = 0xffffffffu;
+        for (uint32_t t = lo_b; t < hi_b; ++t) {
+          const uint32_t st = bk[t];
+          if (st >= k && st < best) best = st;
+        }
+        if (best == 0xffffffffu) break;
+        x = best - 1;
+        k = best + 1;
+      }
+      gout[p] = pa[x];
+    }
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) pa[x] = static_cast<uint32_t>(gout[x]);
+    __syncthreads();
+  }
+  const uint64_t final_to = a.cls_final[blockIdx.x];
+  for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) a.pool[final_to + x] = pa[x];
+}
+
 // ------------------------------------------------------------------ K8
 // Runs after k_shuffle.  Common case: advance the chain past this call's
 // events (one mix each).  If a draw was rejected (or the cursor forces the
@@ -260,16 +401,13 @@ __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
 // generation pool starting from each class's pre-call copy, then write back
 // the newest generations.
 __global__ void k_chain_finish(ChainArgs a, uint32_t n_cls, int force) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  uint64_t s = *a.chain;
   if (!force && *a.flag == 0u) {
-    for (uint64_t e = 0; e < a.E; ++e) {
-      const uint64_t m = a.ev[e].m;
-      s = mix64(s + (m >= 2 ? m : 1ull) * kGamma);
-    }
-    *a.chain = s;
+    const uint64_t s = chain_walk(a, 0xffffffffu, false);
+    if (threadIdx.x == 0) *a.chain = s;
     return;
   }
+  if (threadIdx.x != 0) return;
+  uint64_t s = *a.chain;
   for (uint64_t e = 0; e < a.E; ++e) {
     const SbsEvent ev = a.ev[e];
     uint64_t st = s;
@@ -368,7 +506,16 @@ cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
 
 cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t max_m, int force,
                               cudaStream_t s, uint64_t* launches) {
-  if (n_cls > 0) {
+  if (n_cls > 0 && max_m != 0xffffffffu && max_m <= kParMaxM) {
+    static bool par_attr = false;
+    if (!par_attr) {
+      cudaFuncSetAttribute(k_shuffle_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(par_smem_bytes(kParMaxM)));
+      par_attr = true;
+    }
+    k_shuffle_par<<<n_cls, kParThreads, par_smem_bytes(max_m), s>>>(a);
+    ++*launches;
+  } else if (n_cls > 0) {
     size_t smem = (kJWin + static_cast<size_t>(max_m)) * sizeof(uint32_t);
     int use_smem = 1;
     if (max_m == 0xffffffffu || smem > 200 * 1024) {
@@ -383,7 +530,7 @@ cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t max_m
     k_shuffle<<<n_cls, 64, smem, s>>>(a, use_smem);
     ++*launches;
   }
-  k_chain_finish<<<1, 32, 0, s>>>(a, n_cls, force);
+  k_chain_finish<<<1, 128, 0, s>>>(a, n_cls, force);
   ++*launches;
   return cudaGetLastError();
 }

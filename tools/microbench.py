@@ -77,10 +77,20 @@ def main():
         t_cp = timeit(lambda: copy_dst.copy_(copy_src), s)
         res["torch_copy_152MB"] = {"us": round(statistics.median(t_cp), 2),
                                    "GBps": round(2 * rows * P / statistics.median(t_cp) / 1e3, 1)}
+        lib = pkg._lib.lib
+        prof = lambda: [ct.c_float() for _ in range(3)]  # noqa: E731
+        pkg._lib.check(lib.optb_sbs_set_profiling(cur._h, 1))
+        cur.next_dev(NB, examples=ex_b, classes=cl_b, stream=s)
+        p3 = prof()
+        pkg._lib.check(lib.optb_sbs_profile(cur._h, *[ct.byref(x) for x in p3]))
+        res["sbs_alone_phases_us"] = [round(x.value * 1e3, 1) for x in p3]
         out = torch.empty((rows, P), dtype=torch.uint8, device=dev)
         pipe = Pipeline(cur, ds, 1, B, NB)
         t_pipe = timeit(lambda: pipe.step(out, s), s, reps=30)
         res["pipeline_step"] = {"us": round(statistics.median(t_pipe), 2)}
+        p3 = prof()
+        pkg._lib.check(lib.optb_sbs_profile(cur._h, *[ct.byref(x) for x in p3]))
+        res["sbs_in_pipeline_phases_us"] = [round(x.value * 1e3, 1) for x in p3]
         import time
         t0 = time.perf_counter()
         for _ in range(50):
