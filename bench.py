@@ -58,7 +58,8 @@ def config(world):
             "parallelism": f"independent batch shards x{world} (t % N == rank)",
             "l2": "inputs larger than L2: 153.6 MB dataset (> 126 MB L2), and every step streams 152.6 MB of "
                   "containers + 152.6 MB of decoded rows through it",
-            "pipeline": "SBS draws of step k+1 on a side stream overlap encode/decode of step k"}
+            "pipeline": "native optb_pipeline: SBS draws for the next steps on a side stream overlap "
+                        "encode/decode of the current step (steps_per_draw epochs per sampler call)"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -218,6 +219,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--steps-per-draw", type=int, default=2,
+                    help="epochs of SBS draws computed per sampler call (amortises its fixed cost)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -253,7 +256,7 @@ def main():
     # The native E-D pipeline (optb_pipeline_*): per step, SBS draws of step
     # k+1 on a side stream overlap gather-encode + decode of step k.
     pipe = Pipeline(cur, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
-                    device=local, record_timings=True)
+                    device=local, record_timings=True, steps_per_draw=args.steps_per_draw)
     L = pipe.layout
 
     with torch.cuda.stream(stream):

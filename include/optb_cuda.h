@@ -216,6 +216,8 @@ typedef struct optb_pipeline_desc {
   uint32_t shard, n_shards;
   optb_epilogue epilogue;
   int32_t record_timings;  /* keep per-step CUDA events for optb_pipeline_timings */
+  uint32_t steps_per_draw; /* SBS calls cover this many steps (0 = 1): amortises the
+                              per-call reshuffle work when steps are short */
 } optb_pipeline_desc;
 
 int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* desc, optb_pipeline** out);

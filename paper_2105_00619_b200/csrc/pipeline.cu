@@ -4,11 +4,12 @@
 // HandoffSlot, :116-129 prepare_epoch, :181-244 run) for the E-D path: instead
 // of a producer thread encoding whole epochs into host buffers behind a mutex,
 // each step is enqueued on CUDA streams with event hand-offs:
-//   side stream   : SBS draws of step k+1 (optb_sbs_next_dev) into draw buffer
-//                   (k+1)%2, after encode k-1 released it;
-//   caller stream : wait draws k -> gather-encode (optb_encode_dev) -> decode
-//                   with the fused epilogue (optb_decode_dev) into the caller's
-//                   layer-input buffer.
+//   side stream   : SBS draws (optb_sbs_next_dev) of the next `steps_per_draw`
+//                   steps into draw buffer (call+1)%2, once the encodes of the
+//                   call that last used that buffer are done;
+//   caller stream : wait for the step's draws -> gather-encode
+//                   (optb_encode_dev) -> decode with the fused epilogue
+//                   (optb_decode_dev) into the caller's layer-input buffer.
 // Reference invariants kept: at most two live draw buffers (pipeline.hpp:19-20),
 // in-order delivery, and errors surfacing before the affected step is consumed
 // (device-side format errors latch in the context, optb_ctx_sync).
@@ -16,8 +17,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
-
-#include <vector>
 
 #include "optb_cuda.h"
 
@@ -28,6 +27,8 @@ constexpr int kTimingRing = 64;
 struct optb_pipeline {
   optb_ctx* ctx = nullptr;
   optb_pipeline_desc d{};
+  uint32_t spd = 1;       // steps per SBS call
+  uint64_t rows = 0;      // rows per step
   cudaStream_t side = nullptr;
   int64_t* ex[2] = {};
   int32_t* cls[2] = {};
@@ -36,28 +37,25 @@ struct optb_pipeline {
   cudaEvent_t sbs_done[2] = {}, enc_done[2] = {};
   cudaEvent_t t_s0[kTimingRing] = {}, t_s1[kTimingRing] = {}, t_e0[kTimingRing] = {},
               t_e1[kTimingRing] = {}, t_d1[kTimingRing] = {};
-  uint64_t step = 0;     // next step to deliver
-  uint64_t drawn = 0;    // steps whose draws are enqueued
+  uint64_t step = 0;   // next step to deliver
+  uint64_t calls = 0;  // SBS calls enqueued
   bool timing = false;
 };
 
 namespace {
 
 int enqueue_draws(optb_pipeline* p) {
-  const uint64_t k = p->drawn;
-  const int b = static_cast<int>(k % 2);
-  if (k >= 2) {
-    if (cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
-  }
-  const int r = static_cast<int>(k % kTimingRing);
+  const uint64_t c = p->calls;
+  const int b = static_cast<int>(c % 2);
+  if (c >= 2 && cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  const int r = static_cast<int>(c % kTimingRing);
   if (p->timing) cudaEventRecord(p->t_s0[r], p->side);
-  const uint64_t global_batches = p->d.layout.n_batches * p->d.n_shards;
-  int st = optb_sbs_next_dev(p->d.sbs, global_batches, p->d.shard, p->d.n_shards, p->ex[b], p->cls[b],
-                             p->side);
+  const uint64_t n = p->d.layout.n_batches * p->d.n_shards * p->spd;
+  int st = optb_sbs_next_dev(p->d.sbs, n, p->d.shard, p->d.n_shards, p->ex[b], p->cls[b], p->side);
   if (st) return st;
   if (p->timing) cudaEventRecord(p->t_s1[r], p->side);
   if (cudaEventRecord(p->sbs_done[b], p->side) != cudaSuccess) return OPTB_ERR_CUDA;
-  ++p->drawn;
+  ++p->calls;
   return OPTB_OK;
 }
 
@@ -74,12 +72,13 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
   auto* p = new optb_pipeline();
   p->ctx = ctx;
   p->d = *d;
+  p->spd = d->steps_per_draw ? d->steps_per_draw : 1;
   p->timing = d->record_timings != 0;
-  const uint64_t rows = optb_layout_rows(&d->layout);
+  p->rows = optb_layout_rows(&d->layout);
   bool ok = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) == cudaSuccess;
   for (int b = 0; b < 2 && ok; ++b) {
-    ok = cudaMalloc(&p->ex[b], rows * sizeof(int64_t)) == cudaSuccess &&
-         cudaMalloc(&p->cls[b], rows * sizeof(int32_t)) == cudaSuccess &&
+    ok = cudaMalloc(&p->ex[b], p->rows * p->spd * sizeof(int64_t)) == cudaSuccess &&
+         cudaMalloc(&p->cls[b], p->rows * p->spd * sizeof(int32_t)) == cudaSuccess &&
          cudaEventCreateWithFlags(&p->sbs_done[b], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&p->enc_done[b], cudaEventDisableTiming) == cudaSuccess;
   }
@@ -95,7 +94,7 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
     optb_pipeline_destroy(p);
     return OPTB_ERR_CUDA;
   }
-  st = enqueue_draws(p);  // step 0's draws start right away
+  st = enqueue_draws(p);  // the first call's draws start right away
   if (st) {
     optb_pipeline_destroy(p);
     return st;
@@ -108,18 +107,23 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   if (!p || !out) return OPTB_ERR_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t k = p->step;
-  const int b = static_cast<int>(k % 2);
+  const uint64_t call = k / p->spd, sub = k % p->spd;
+  const int b = static_cast<int>(call % 2);
   const int r = static_cast<int>(k % kTimingRing);
-  int st = enqueue_draws(p);  // step k+1's draws overlap this step
-  if (st) return st;
-  if (cudaStreamWaitEvent(s, p->sbs_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  int st;
+  if (sub == 0) {
+    st = enqueue_draws(p);  // the next call's draws overlap this call's steps
+    if (st) return st;
+    if (cudaStreamWaitEvent(s, p->sbs_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  }
   if (p->timing) cudaEventRecord(p->t_e0[r], s);
-  st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b], p->cont, p->offs, s);
+  st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
+                       p->cont, p->offs, s);
   if (st) return st;
   if (p->timing) cudaEventRecord(p->t_e1[r], s);
-  if (cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
   optb_epilogue e = p->d.epilogue;
-  if (e.class_scale && !e.row_class) e.row_class = p->cls[b];
+  if (e.class_scale && !e.row_class) e.row_class = p->cls[b] + sub * p->rows;
   st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
   if (st) return st;
   if (p->timing) cudaEventRecord(p->t_d1[r], s);
@@ -129,9 +133,12 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
 
 int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
                         const int32_t** classes) {
-  if (!p || step + 2 < p->step || step >= p->drawn) return OPTB_ERR_ARG;
-  if (examples) *examples = p->ex[step % 2];
-  if (classes) *classes = p->cls[step % 2];
+  if (!p || step >= p->calls * p->spd) return OPTB_ERR_ARG;
+  const uint64_t call = step / p->spd;
+  if (call + 2 < p->calls) return OPTB_ERR_ARG;  // buffer already reused
+  const uint64_t sub = step % p->spd;
+  if (examples) *examples = p->ex[call % 2] + sub * p->rows;
+  if (classes) *classes = p->cls[call % 2] + sub * p->rows;
   return OPTB_OK;
 }
 
@@ -141,8 +148,12 @@ int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, 
                           float* dec_ms) {
   if (!p || !p->timing || step >= p->step || step + kTimingRing <= p->step) return OPTB_ERR_ARG;
   const int r = static_cast<int>(step % kTimingRing);
+  const int rc = static_cast<int>((step / p->spd) % kTimingRing);
   if (cudaEventSynchronize(p->t_d1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
-  if (sbs_ms && cudaEventElapsedTime(sbs_ms, p->t_s0[r], p->t_s1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (sbs_ms) {  // the SBS call that produced this step's draws, per step
+    if (cudaEventElapsedTime(sbs_ms, p->t_s0[rc], p->t_s1[rc]) != cudaSuccess) return OPTB_ERR_CUDA;
+    *sbs_ms /= static_cast<float>(p->spd);
+  }
   if (enc_ms && cudaEventElapsedTime(enc_ms, p->t_e0[r], p->t_e1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
   if (dec_ms && cudaEventElapsedTime(dec_ms, p->t_e1[r], p->t_d1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
   return OPTB_OK;

@@ -19,8 +19,9 @@ def _setup(pkg, O, torch, N=4000, Ccls=10, B=64, seed=99):
     return S, labels, ds, p, offs, mem, ref
 
 
-@pytest.mark.parametrize("mode,dtype", [(1, "uint8"), (0, "float32"), (3, "bfloat16"), (2, "float16")])
-def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype):
+@pytest.mark.parametrize("mode,dtype,spd", [(1, "uint8", 1), (0, "float32", 1), (3, "bfloat16", 2),
+                                            (2, "float16", 3), (1, "uint8", 4)])
+def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype, spd):
     torch, O = torch_cuda, oracle_mod
     from paper_2105_00619_b200.pipeline import Pipeline
     S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
@@ -29,7 +30,7 @@ def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype):
     ds_d = torch.from_numpy(ds).cuda()
     dt = getattr(torch, dtype)
     pc = pkg.codec.capacity(mode)
-    pipe = Pipeline(cur, ds_d, mode, B, nb, per_chunk=pc, out_dtype=dt, scale=SCALE)
+    pipe = Pipeline(cur, ds_d, mode, B, nb, per_chunk=pc, out_dtype=dt, scale=SCALE, steps_per_draw=spd)
     kind = {"uint8": O.U8, "float32": O.F32, "bfloat16": O.BF16, "float16": O.F16}[dtype]
     for step in range(6):
         out = torch.empty((B * nb, P), dtype=dt, device="cuda")

@@ -85,9 +85,14 @@ def main():
         pkg._lib.check(lib.optb_sbs_profile(cur._h, *[ct.byref(x) for x in p3]))
         res["sbs_alone_phases_us"] = [round(x.value * 1e3, 1) for x in p3]
         out = torch.empty((rows, P), dtype=torch.uint8, device=dev)
+        for spd in (2, 4):
+            pipe = Pipeline(cur, ds, 1, B, NB, steps_per_draw=spd)
+            t_pipe = timeit(lambda: pipe.step(out, s), s, reps=32)
+            res[f"pipeline_step_spd{spd}"] = {"us": round(statistics.mean(t_pipe), 2)}
+            pipe.close()
         pipe = Pipeline(cur, ds, 1, B, NB)
         t_pipe = timeit(lambda: pipe.step(out, s), s, reps=30)
-        res["pipeline_step"] = {"us": round(statistics.median(t_pipe), 2)}
+        res["pipeline_step"] = {"us": round(statistics.mean(t_pipe), 2)}
         p3 = prof()
         pkg._lib.check(lib.optb_sbs_profile(cur._h, *[ct.byref(x) for x in p3]))
         res["sbs_in_pipeline_phases_us"] = [round(x.value * 1e3, 1) for x in p3]
