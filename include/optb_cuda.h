@@ -167,6 +167,11 @@ int optb_sbs_plan(const double* weights, uint64_t n_classes, uint64_t batch, uin
 int optb_class_index_dev(optb_ctx* ctx, const int32_t* labels, uint64_t n, uint64_t n_classes,
                          uint64_t* class_offsets, int64_t* members, void* stream);
 
+/* Same partition with host labels in and host outputs back (synchronous;
+ * errors reported on return) -- the form ClassIndex::from_labels returns. */
+int optb_class_index_host(optb_ctx* ctx, const int32_t* labels, uint64_t n, uint64_t n_classes,
+                          uint64_t* class_offsets, int64_t* members);
+
 /* BatchCursor(plan, index) (sampler.cpp:67-82): per-class permutations and
  * the SplitMix64 chain live on the device.  counts[C] and class_offsets[C+1]
  * are host arrays; members[class_offsets[C]] is dev (members_on_device=1) or

@@ -81,7 +81,8 @@ SIGNATURES = {
     "optb_decode_host": (ct.c_int, [vp, LP, vp, vp, EP, vp]),
     "optb_sbs_plan": (ct.c_int, [f64p, ct.c_uint64, ct.c_uint64, u64p]),
     "optb_class_index_dev": (ct.c_int, [vp, vp, ct.c_uint64, ct.c_uint64, vp, vp, vp]),
-    "optb_sbs_create": (ct.c_int, [vp, u64p, ct.c_uint64, ct.c_uint64, ct.c_uint64, u64p, vp,
+    "optb_class_index_host": (ct.c_int, [vp, vp, ct.c_uint64, ct.c_uint64, vp, vp]),
+    "optb_sbs_create":(ct.c_int, [vp, u64p, ct.c_uint64, ct.c_uint64, ct.c_uint64, u64p, vp,
                                    ct.c_int32, ct.POINTER(vp)]),
     "optb_sbs_destroy": (None, [vp]),
     "optb_sbs_next_dev": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, vp, vp, vp]),

@@ -76,11 +76,37 @@ def build_shim(force: bool = False) -> str:
     return SHIM_LIB_NAME
 
 
+REF_TESTS = "/root/reference/proj/tests"
+REF_SUITES = ["test_codec.cpp", "test_sampler.cpp"]
+REF_SUITES_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "ref_suites_on_b200")
+
+
+def build_ref_suites(force: bool = False):
+    """Compile the REFERENCE's own unit suites (test_codec.cpp,
+    test_sampler.cpp and its doctest_main.cpp), in place from
+    /root/reference, against the drop-in shim headers + libraries -- the
+    drop-in proof.  Uses tests/cpp/doctest.h (written for this repo) since
+    the reference's vendor/doctest.h is not shipped.  Only where the
+    reference exists; the binary travels to the GPU box like the .so files."""
+    if not os.path.isdir(REF_TESTS):
+        return None
+    srcs = [os.path.join(REF_TESTS, f) for f in REF_SUITES + ["doctest_main.cpp"]]
+    if not force and not _stale(REF_SUITES_BIN, srcs + [SHIM_LIB_NAME, CUDA_LIB_NAME]):
+        return REF_SUITES_BIN
+    os.makedirs(os.path.dirname(REF_SUITES_BIN), exist_ok=True)
+    _run(["g++", "-std=c++20", "-O2", "-w", "-I" + os.path.join(ROOT, "tests", "cpp"),
+          "-I" + os.path.join(CSRC, "shim", "include"), "-I" + INCLUDE, "-I" + REF_TESTS] + srcs +
+         ["-o", REF_SUITES_BIN, "-L" + PKG, "-loptb_shim", "-loptb_cuda", "-Wl,-rpath," + PKG,
+          "-Wl,-rpath,$ORIGIN/../../../paper_2105_00619_b200"])
+    return REF_SUITES_BIN
+
+
 def build(force: bool = False) -> None:
     build_cuda(force)
     if os.path.isdir(os.path.join(CSRC, "shim", "src")) and all(
             os.path.exists(os.path.join(CSRC, "shim", "src", f)) for f in SHIM_SOURCES):
         build_shim(force)
+        build_ref_suites(force)
 
 
 if __name__ == "__main__":

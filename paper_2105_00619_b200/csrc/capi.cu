@@ -851,6 +851,37 @@ int optb_class_index_dev(optb_ctx* c, const int32_t* labels, uint64_t n, uint64_
 }
 
 
+int optb_class_index_host(optb_ctx* c, const int32_t* labels, uint64_t n, uint64_t C,
+                          uint64_t* class_offsets, int64_t* members) {
+  if (!c || (!labels && n) || !class_offsets || (!members && n)) return set_err(OPTB_ERR_ARG, "class index: null");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  int32_t* d_lab = nullptr;
+  uint64_t* d_off = nullptr;
+  int64_t* d_mem = nullptr;
+  auto release = [&] {
+    if (d_lab) cudaFree(d_lab);
+    if (d_off) cudaFree(d_off);
+    if (d_mem) cudaFree(d_mem);
+  };
+  if (cudaMalloc(&d_lab, std::max<uint64_t>(n, 1) * 4) != cudaSuccess ||
+      cudaMalloc(&d_off, (C + 1) * 8) != cudaSuccess ||
+      cudaMalloc(&d_mem, std::max<uint64_t>(n, 1) * 8) != cudaSuccess) {
+    release();
+    return cuda_err(cudaGetLastError(), "class index buffers");
+  }
+  cudaStream_t st = c->s_compute;
+  int rc = OPTB_OK;
+  if (n && cudaMemcpyAsync(d_lab, labels, n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    rc = cuda_err(cudaGetLastError(), "class index upload");
+  if (!rc) rc = optb_class_index_dev(c, d_lab, n, C, d_off, d_mem, st);
+  if (!rc) rc = optb_ctx_sync(c, st);
+  if (!rc && (cudaMemcpy(class_offsets, d_off, (C + 1) * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+              (n && cudaMemcpy(members, d_mem, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess)))
+    rc = cuda_err(cudaGetLastError(), "class index download");
+  release();
+  return rc;
+}
+
 int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B, uint64_t seed,
                     const uint64_t* class_offsets, const int64_t* members, int32_t on_dev,
                     optb_sbs** out) {
