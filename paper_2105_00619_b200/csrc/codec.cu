@@ -234,27 +234,57 @@ __device__ __forceinline__ void cp_async_wait() {
 // Requires P % 16 == 0 and 16-byte aligned rows / containers / outputs.
 constexpr int kStages = 3;
 
-template <int WC>
-struct VecShape {
-  static constexpr int NI = WC;                 // images per container word
-  static constexpr int SW = (WC == 16) ? 7 : 15;  // slot XOR swizzle mask
-  static constexpr int SLOT = 32 * 16 * WC;     // bytes per stage slot per warp
+
+// ------------------------------------------------------------------ K1 / K3
+// Gather-encode for the exact and lossless modes.  Stage slot layout on
+// input: row i of the chunk, lane L's 16 pixels at i*512 + L*16
+// (conflict-free); after the register transpose the slot is reused as the
+// output tile, word p of lane L at (L*16 + (p ^ (L & SW)))*WC (conflict-free
+// both ways), then copied out with fully coalesced 128-bit (64-bit) stores.
+// Lossless (codec.cpp:125-135): each pixel's 7-bit fields (px >> 1) are
+// compacted from byte lanes with three mask/shift steps; the parity bits
+// (px & 1) of a lane's 16 pixels of image i are one 16-bit store at plane bit
+// i*P + 16*group (aligned: the vector path needs P % 32 == 0 in these modes).
+template <int MODE>
+struct VecMode {
+  static constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
+  static constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
+  static constexpr int NI = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128) ? 16
+                            : (MODE == OPTB_LOSSLESS64) ? 9 : 18;      // images per word
+  static constexpr int NT = NI < 16 ? NI : 16;                         // images in the 16x16 transpose
+  static constexpr int SW = (WC == 16) ? 7 : 15;                       // slot XOR swizzle mask
+  static constexpr int ROWS_B = NI * 512;                              // staged input rows
+  static constexpr int WORDS_B = 512 * WC;                             // container words of a tile
+  static constexpr int PAR_B = OFFS ? NI * 64 : 0;                     // staged parity bits (decode)
+  static constexpr int ENC_SLOT = ROWS_B > WORDS_B ? ROWS_B : WORDS_B;
+  static constexpr int DEC_SLOT = (WORDS_B + PAR_B) > ROWS_B ? (WORDS_B + PAR_B) : ROWS_B;
+  static constexpr int MIN_BLOCKS = WC == 16 ? 1 : 2;
 };
 
-// ------------------------------------------------------------------ K1
-// Gather-encode.  Stage slot layout on input: row i of the chunk, lane L's
-// 16 pixels at (i*32 + L)*16 (conflict-free LDS.128); after the register
-// transpose the slot is reused as the output tile, word p of lane L at
-// (L*16 + (p ^ (L & SW)))*WC (conflict-free both ways), then copied out with
-// fully coalesced 128-bit (64-bit) stores.
-template <int WC>
-__global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
-    k_encode_exact_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
-                       const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont) {
-  using S = VecShape<WC>;
+__device__ __forceinline__ uint64_t compact7(uint64_t x) {  // 8 byte lanes -> 8 x 7-bit fields
+  x = (x & 0x007F007F007F007Full) | ((x & 0x7F007F007F007F00ull) >> 1);
+  x = (x & 0x00003FFF00003FFFull) | ((x & 0x3FFF00003FFF0000ull) >> 2);
+  return (x & 0x000000000FFFFFFFull) | ((x & 0x0FFFFFFF00000000ull) >> 4);
+}
+__device__ __forceinline__ uint64_t expand7(uint64_t x) {  // inverse of compact7
+  x = (x & 0x0FFFFFFFull) | ((x << 4) & 0x0FFFFFFF00000000ull);
+  x = (x & 0x00003FFF00003FFFull) | ((x << 2) & 0x3FFF00003FFF0000ull);
+  return (x & 0x007F007F007F007Full) | ((x << 1) & 0x7F007F007F007F00ull);
+}
+__device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> bytes' LSBs
+  return (b * 0x00204081u) & 0x01010101u;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+    k_encode_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
+                 const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont,
+                 uint8_t* __restrict__ offsets) {
+  using S = VecMode<MODE>;
+  constexpr int WC = S::WC;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_raw + warp * kStages * S::SLOT;
+  uint8_t* ring = smem_raw + warp * kStages * S::ENC_SLOT;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
@@ -281,11 +311,11 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
       const uint64_t k = t / G;
       const uint64_t gi = t - k * G;
       const uint32_t n = chunk_pos(g, k).n;
-      uint8_t* slot = ring + stage * S::SLOT;
+      uint8_t* slot = ring + stage * S::ENC_SLOT;
 #pragma unroll
       for (int i = 0; i < S::NI; ++i)
         if (i < static_cast<int>(n))
-          cp_async16(slot + (i * 32 + lane) * 16, images + static_cast<uint64_t>(rows[i]) * row_stride + gi * 16);
+          cp_async16(slot + i * 512 + lane * 16, images + static_cast<uint64_t>(rows[i]) * row_stride + gi * 16);
     }
     cp_async_commit();
   };
@@ -303,26 +333,74 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
     fetch_rows(base + kStages * stride, rows);  // consumed by the next iteration's issue
     cp_async_wait<kStages - 1>();
     __syncwarp();
-    uint8_t* slot = ring + stage * S::SLOT;
+    uint8_t* slot = ring + stage * S::ENC_SLOT;
     const uint64_t t = base + lane;
     uint32_t n = 0;
-    if (t < items) n = chunk_pos(g, t / G).n;
+    uint64_t k = 0, gi = 0;
+    if (t < items) {
+      k = t / G;
+      gi = t - k * G;
+      n = chunk_pos(g, k).n;
+    }
     uint32_t m[16][4];
+    uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};  // images 16, 17 (lossless128)
 #pragma unroll
     for (int i = 0; i < S::NI; ++i) {
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (i < static_cast<int>(n)) v = *reinterpret_cast<const uint4*>(slot + (i * 32 + lane) * 16);
-      m[i][0] = v.x;
-      m[i][1] = v.y;
-      m[i][2] = v.z;
-      m[i][3] = v.w;
+      if (i < static_cast<int>(n)) v = *reinterpret_cast<const uint4*>(slot + i * 512 + lane * 16);
+      if constexpr (S::OFFS) {
+        // parity bits of 16 pixels at plane bit i*P + 16*gi (codec.cpp:132-133);
+        // images in [n, per_chunk) (partial chunk) write zeros so the padded
+        // plane is deterministic; the plane holds per_chunk images
+        if (t < items && i < static_cast<int>(g.per_chunk)) {
+          const uint32_t bits = (((v.x & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) |
+                                ((((v.y & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 4) |
+                                ((((v.z & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 8) |
+                                ((((v.w & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 12);
+          *reinterpret_cast<uint16_t*>(offsets + k * g.ostride + (static_cast<uint64_t>(i) * g.P) / 8 + 2 * gi) =
+              static_cast<uint16_t>(bits);
+        }
+      }
+      if (i < 16) {
+        m[i][0] = v.x;
+        m[i][1] = v.y;
+        m[i][2] = v.z;
+        m[i][3] = v.w;
+      } else if (i == 16) {
+        x16[0] = v.x; x16[1] = v.y; x16[2] = v.z; x16[3] = v.w;
+      } else {
+        x17[0] = v.x; x17[1] = v.y; x17[2] = v.z; x17[3] = v.w;
+      }
     }
-    transpose16<S::NI, 16>(m);  // m[p] = word of pixel p (bytes = images 0..15)
+    if constexpr (S::OFFS) {
+      if (t < items && gi == 0) {  // zero the plane's stride padding once per chunk
+        for (uint64_t b = (static_cast<uint64_t>(g.per_chunk) * g.P) / 8; b < g.ostride; b += 4)
+          *reinterpret_cast<uint32_t*>(offsets + k * g.ostride + b) = 0u;
+      }
+    }
+    transpose16<S::NT, 16>(m);  // m[p] = bytes of images 0..15 at pixel p
     __syncwarp();
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
       const int sl = p ^ (lane & S::SW);
-      if constexpr (WC == 16) {
+      if constexpr (S::OFFS) {
+        const uint64_t lo8 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];  // images 0..7
+        const uint64_t lo = compact7((lo8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
+        if constexpr (WC == 8) {  // lossless64: fields 0..7 + image 8's field at bit 56
+          const uint64_t f8 = (m[p][2] & 0xFFu) >> 1;
+          *reinterpret_cast<uint64_t*>(slot + (lane * 16 + sl) * 8) = lo | (f8 << 56);
+        } else {  // lossless128: fields 0..15, images 16/17 at bits 112/119
+          const uint64_t hi8 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
+          const uint64_t hi = compact7((hi8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
+          const uint64_t f16 = ((x16[p >> 2] >> (8 * (p & 3))) & 0xFFu) >> 1;
+          const uint64_t f17 = ((x17[p >> 2] >> (8 * (p & 3))) & 0xFFu) >> 1;
+          const uint64_t w0 = lo | (hi << 56);
+          const uint64_t w1 = (hi >> 8) | (f16 << 48) | (f17 << 55);
+          *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) =
+              make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1),
+                         static_cast<uint32_t>(w1 >> 32));
+        }
+      } else if constexpr (WC == 16) {
         *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
       } else {
         *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) = make_uint2(m[p][0], m[p][1]);
@@ -348,20 +426,23 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
   cp_async_wait<0>();
 }
 
-// ------------------------------------------------------------------ K2
-// Decode.  Container words arrive by cp.async straight into the swizzled slot
-// layout; after the register transpose each lane holds 16 pixels of every
-// image: u8 rows are stored directly (each warp instruction writes 512
-// contiguous bytes of one row); float outputs go through a u8 tile in the
-// same slot so that the epilogue stores are coalesced too.
-template <int WC, int O>
-__global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
-    k_decode_exact_vec(Geom g, const uint8_t* __restrict__ cont, Epi e, void* __restrict__ out,
-                       DevError* err) {
-  using S = VecShape<WC>;
+// ------------------------------------------------------------------ K2 / K4
+// Decode.  Container words (and, lossless, the tile's parity bits) arrive by
+// cp.async straight into the swizzled slot; each pixel's word is range
+// checked, lossless fields are expanded back to byte lanes, the 16x16
+// transpose gives 16 pixels of every image per lane, lossless rows get
+// (field << 1) | parity; u8 rows are stored directly (each warp instruction
+// writes 512 contiguous bytes of one row); float outputs go through a u8
+// tile in the same slot so that the epilogue stores are coalesced too.
+template <int MODE, int O>
+__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+    k_decode_vec(Geom g, const uint8_t* __restrict__ cont, const uint8_t* __restrict__ offsets, Epi e,
+                 void* __restrict__ out, DevError* err) {
+  using S = VecMode<MODE>;
+  constexpr int WC = S::WC;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_raw + warp * kStages * S::SLOT;
+  uint8_t* ring = smem_raw + warp * kStages * S::DEC_SLOT;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
@@ -371,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
   auto issue = [&](uint64_t base, int stage) {
     if (base < items) {
       const uint8_t* src = cont + base * 16 * WC;
-      uint8_t* slot = ring + stage * S::SLOT;
+      uint8_t* slot = ring + stage * S::DEC_SLOT;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int W = q * 32 + lane, L = W >> 4, p = W & 15;
@@ -381,6 +462,27 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
             cp_async16(slot + (L * 16 + sl) * 16, src + W * 16);
           } else {
             cp_async8(slot + (L * 16 + sl) * 8, src + W * 8);
+          }
+        }
+      }
+      if constexpr (S::OFFS) {
+        // parity bits of lane pairs (4 bytes, 4-aligned as P % 32 == 0)
+        const uint64_t t = base + lane;
+        if ((lane & 1) == 0 && t < items) {
+          const uint64_t k = t / G, gi = t - k * G;
+          const uint32_t n = chunk_pos(g, k).n;
+          const bool pair = (t + 1 < items) && ((t + 1) / G == k);
+#pragma unroll
+          for (int i = 0; i < S::NI; ++i) {
+            if (i < static_cast<int>(n)) {
+              const uint8_t* ps = offsets + k * g.ostride + (static_cast<uint64_t>(i) * g.P) / 8 + 2 * gi;
+              uint8_t* pd = slot + S::WORDS_B + i * 64 + lane * 2;
+              if (pair) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(pd)), "l"(ps) : "memory");
+              } else {
+                *reinterpret_cast<uint16_t*>(pd) = *reinterpret_cast<const uint16_t*>(ps);
+              }
+            }
           }
         }
       }
@@ -395,55 +497,96 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
     issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
     cp_async_wait<kStages - 1>();
     __syncwarp();
-    uint8_t* slot = ring + stage * S::SLOT;
+    uint8_t* slot = ring + stage * S::DEC_SLOT;
+    const uint64_t t = base + lane;
+    const bool valid = t < items;
+    uint64_t k = 0, gi = 0;
+    ChunkPos c{0, 0};
+    if (valid) {
+      k = t / G;
+      gi = t - k * G;
+      c = chunk_pos(g, k);
+    }
     uint32_t m[16][4];
+    uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
+    bool bad = false;
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
       const int sl = p ^ (lane & S::SW);
+      uint64_t w0, w1 = 0;
       if constexpr (WC == 16) {
         const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
-        m[p][0] = v.x;
-        m[p][1] = v.y;
-        m[p][2] = v.z;
-        m[p][3] = v.w;
+        w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+        w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
       } else {
         const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
-        m[p][0] = v.x;
-        m[p][1] = v.y;
-        m[p][2] = 0u;
-        m[p][3] = 0u;
+        w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
+      }
+      if constexpr (S::OFFS) {
+        // range check (codec.cpp:189-194): bits >= 7n must be zero
+        const unsigned used = 7u * c.n;
+        if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
+        else bad |= (w1 >> (used - 64u)) != 0;
+        const uint64_t lo = expand7(w0 & 0x00FFFFFFFFFFFFFFull);  // images 0..7
+        m[p][0] = static_cast<uint32_t>(lo);
+        m[p][1] = static_cast<uint32_t>(lo >> 32);
+        if constexpr (WC == 8) {
+          m[p][2] = static_cast<uint32_t>(w0 >> 56) & 0x7Fu;  // image 8
+          m[p][3] = 0u;
+        } else {
+          const uint64_t hi = expand7(((w0 >> 56) | (w1 << 8)) & 0x00FFFFFFFFFFFFFFull);  // images 8..15
+          m[p][2] = static_cast<uint32_t>(hi);
+          m[p][3] = static_cast<uint32_t>(hi >> 32);
+          x16[p >> 2] |= static_cast<uint32_t>((w1 >> 48) & 0x7Fu) << (8 * (p & 3));
+          x17[p >> 2] |= static_cast<uint32_t>((w1 >> 55) & 0x7Fu) << (8 * (p & 3));
+        }
+      } else {
+        m[p][0] = static_cast<uint32_t>(w0);
+        m[p][1] = static_cast<uint32_t>(w0 >> 32);
+        m[p][2] = static_cast<uint32_t>(w1);
+        m[p][3] = static_cast<uint32_t>(w1 >> 32);
       }
     }
-    transpose16<16, S::NI>(m);  // m[i] = 16 pixels of image i
-    const uint64_t t = base + lane;
-    const bool valid = t < items;
-    uint64_t gi = 0;
-    ChunkPos c{0, 0};
+    transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (fields for lossless)
     if (valid) {
-      const uint64_t k = t / G;
-      gi = t - k * G;
-      c = chunk_pos(g, k);
-      // range check (codec.cpp:189-194): bytes of images >= n must be zero
-      uint32_t hi = 0;
+      if constexpr (!S::OFFS) {
+        // range check (codec.cpp:189-194): bytes of images >= n must be zero
+        uint32_t hi = 0;
 #pragma unroll
-      for (int i = 0; i < S::NI; ++i)
-        if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
-      if (hi) latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
+        for (int i = 0; i < S::NI; ++i)
+          if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
+        bad = hi != 0;
+      }
+      if (bad) latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
     }
+    if constexpr (S::OFFS) {
+      // pixel = (field << 1) | parity (codec.cpp:196-201)
+#pragma unroll
+      for (int i = 0; i < S::NI; ++i) {
+        uint32_t bits = 0;
+        if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
+        uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) row[q] = (row[q] << 1) | nibble_lsbs((bits >> (4 * q)) & 0xFu);
+      }
+    }
+    auto row_vec = [&](int i) -> uint4 {
+      if (i < 16) return make_uint4(m[i < 16 ? i : 0][0], m[i < 16 ? i : 0][1], m[i < 16 ? i : 0][2], m[i < 16 ? i : 0][3]);
+      if (i == 16) return make_uint4(x16[0], x16[1], x16[2], x16[3]);
+      return make_uint4(x17[0], x17[1], x17[2], x17[3]);
+    };
     if constexpr (O == OPTB_OUT_U8) {
       if (valid) {
 #pragma unroll
         for (int i = 0; i < S::NI; ++i)
           if (i < static_cast<int>(c.n))
-            stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16,
-                  make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]));
+            stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16, row_vec(i));
       }
     } else {
-      __syncwarp();  // all lanes done reading the container slot
-      // u8 tile in the same slot: image i, lane L's 16 pixels at (i*32 + L)*16
+      __syncwarp();  // all lanes done reading the slot
+      // u8 tile in the same slot: image i, lane L's 16 pixels at i*512 + L*16
 #pragma unroll
-      for (int i = 0; i < S::NI; ++i)
-        *reinterpret_cast<uint4*>(slot + (i * 32 + lane) * 16) = make_uint4(m[i][0], m[i][1], m[i][2], m[i][3]);
+      for (int i = 0; i < S::NI; ++i) *reinterpret_cast<uint4*>(slot + i * 512 + lane * 16) = row_vec(i);
       __syncwarp();
       // epilogue: every lane stores 16 bytes per row -- PX = 4 fp32 or 8 half
       // pixels, starting at pixel PX*(lane % LPS) of source lane L's group
@@ -470,10 +613,10 @@ __global__ void __launch_bounds__(kThreads, (WC == 16) ? 1 : 2)
             row_affine(e, row, s, b, aff);
             uint8_t* dst = static_cast<uint8_t*>(out) + (row * ostride + px) * ES;
             if constexpr (PX == 4) {
-              const uint32_t q4 = *reinterpret_cast<const uint32_t*>(slot + (i * 32 + L) * 16 + sub);
+              const uint32_t q4 = *reinterpret_cast<const uint32_t*>(slot + i * 512 + L * 16 + sub);
               Out4::put<O>(dst, q4, s, b, aff);
             } else {
-              const uint2 q8 = *reinterpret_cast<const uint2*>(slot + (i * 32 + L) * 16 + sub);
+              const uint2 q8 = *reinterpret_cast<const uint2*>(slot + i * 512 + L * 16 + sub);
               Out8::put<O>(dst, q8, s, b, aff);
             }
           }
@@ -596,11 +739,23 @@ __global__ void __launch_bounds__(256) k_decode_generic(Geom g, const uint8_t* _
         latch_error(err, kErrF64Range, g.chunk_base + k, c.n);
         continue;
       }
+      // codec.cpp:171-175 peels with q = fmod(acc, 256), acc = (acc - q) / 256.
+      // For 0 <= acc < 2^64 that is exactly the integer peel of trunc(acc):
+      // fmod keeps acc's fraction in q, (u8)q drops it, and (acc - q)/256 is
+      // trunc(acc/256).  Only lossy sums >= 2^64 (n >= 9) need fmod itself.
+      const bool small = acc < 0x1.0p64;
+      uint64_t iacc = small ? static_cast<uint64_t>(acc) : 0ull;
 #pragma unroll
       for (int i = 0; i < MAXN; ++i) {
         if (i < static_cast<int>(c.n)) {
-          const double q = fmod(acc, 256.0);           // exact
-          acc = __dmul_rn(__dsub_rn(acc, q), 0x1.0p-8);  // exact
+          double q;
+          if (small) {
+            q = static_cast<double>(iacc & 0xffull);
+            iacc >>= 8;
+          } else {
+            q = fmod(acc, 256.0);                          // exact
+            acc = __dmul_rn(__dsub_rn(acc, q), 0x1.0p-8);  // exact
+          }
           const uint64_t row = c.r0 + i;
           float s, b;
           bool aff;
@@ -703,38 +858,37 @@ cudaError_t dec_generic(const Geom& g, const void* cont, const uint8_t* offs, co
   return cudaGetLastError();
 }
 
-template <int WC>
+template <int MODE>
 cudaError_t enc_vec(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* idx,
-                    void* cont, cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecShape<WC>::SLOT;
+                    void* cont, uint8_t* offs, cudaStream_t s, int sms, uint64_t* launches) {
+  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_encode_exact_vec<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_encode_vec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
   const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_encode_exact_vec<WC>, kThreads, smem, sms, items);
-  k_encode_exact_vec<WC><<<grid, kThreads, smem, s>>>(g, images, row_stride, idx,
-                                                      static_cast<uint8_t*>(cont));
+  const int grid = grid_for(k_encode_vec<MODE>, kThreads, smem, sms, items);
+  k_encode_vec<MODE><<<grid, kThreads, smem, s>>>(g, images, row_stride, idx, static_cast<uint8_t*>(cont),
+                                                  offs);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int WC, int O>
-cudaError_t dec_vec(const Geom& g, const void* cont, const Epi& e, void* out, DevError* err,
-                    cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecShape<WC>::SLOT;
+template <int MODE, int O>
+cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
+                    DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::DEC_SLOT;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_decode_exact_vec<WC, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_decode_vec<MODE, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
   const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_decode_exact_vec<WC, O>, kThreads, smem, sms, items);
-  k_decode_exact_vec<WC, O><<<grid, kThreads, smem, s>>>(g, static_cast<const uint8_t*>(cont), e,
-                                                         out, err);
+  const int grid = grid_for(k_decode_vec<MODE, O>, kThreads, smem, sms, items);
+  k_decode_vec<MODE, O><<<grid, kThreads, smem, s>>>(g, static_cast<const uint8_t*>(cont), offs, e, out, err);
   ++*launches;
   return cudaGetLastError();
 }
@@ -750,15 +904,23 @@ cudaError_t dec_generic_any(const Geom& g, const void* cont, const uint8_t* offs
   }
 }
 
-template <int WC>
-cudaError_t dec_vec_any(const Geom& g, const void* cont, const Epi& e, void* out, DevError* err,
-                        cudaStream_t s, int sms, uint64_t* l) {
+template <int MODE>
+cudaError_t dec_vec_any(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
+                        DevError* err, cudaStream_t s, int sms, uint64_t* l) {
   switch (e.dtype) {
-    case OPTB_OUT_U8: return dec_vec<WC, OPTB_OUT_U8>(g, cont, e, out, err, s, sms, l);
-    case OPTB_OUT_F32: return dec_vec<WC, OPTB_OUT_F32>(g, cont, e, out, err, s, sms, l);
-    case OPTB_OUT_F16: return dec_vec<WC, OPTB_OUT_F16>(g, cont, e, out, err, s, sms, l);
-    default: return dec_vec<WC, OPTB_OUT_BF16>(g, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_U8: return dec_vec<MODE, OPTB_OUT_U8>(g, cont, offs, e, out, err, s, sms, l);
+    case OPTB_OUT_F32: return dec_vec<MODE, OPTB_OUT_F32>(g, cont, offs, e, out, err, s, sms, l);
+    case OPTB_OUT_F16: return dec_vec<MODE, OPTB_OUT_F16>(g, cont, offs, e, out, err, s, sms, l);
+    default: return dec_vec<MODE, OPTB_OUT_BF16>(g, cont, offs, e, out, err, s, sms, l);
   }
+}
+
+// The vector kernels need 16-pixel groups (P % 16), 16-byte aligned rows and
+// planes; the lossless ones also 32-pixel aligned parity words (P % 32).
+bool vec_ok(const Geom& g) {
+  const bool lossless = g.mode == OPTB_LOSSLESS64 || g.mode == OPTB_LOSSLESS128;
+  if (g.mode == OPTB_F64) return false;
+  return lossless ? g.P % 32 == 0 : g.P % 16 == 0;
 }
 
 }  // namespace
@@ -766,56 +928,45 @@ cudaError_t dec_vec_any(const Geom& g, const void* cont, const Epi& e, void* out
 cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_stride,
                           const int64_t* row_index, void* containers, uint8_t* offsets,
                           cudaStream_t s, int sms, uint64_t* launches) {
-  const bool exact = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128;
-  const bool vec = exact && g.P % 16 == 0 && row_stride % 16 == 0 && aligned16(images) &&
-                   aligned16(containers);
-  if (vec) {
-    return g.wc == 16 ? enc_vec<16>(g, images, row_stride, row_index, containers, s, sms, launches)
-                      : enc_vec<8>(g, images, row_stride, row_index, containers, s, sms, launches);
-  }
+  const bool vec = vec_ok(g) && row_stride % 16 == 0 && aligned16(images) && aligned16(containers);
   switch (g.mode) {
     case OPTB_EXACT64:
-      return enc_generic<OPTB_EXACT64>(g, images, row_stride, row_index, containers, offsets, s,
-                                       sms, launches);
+      if (vec) return enc_vec<OPTB_EXACT64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_EXACT64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_EXACT128:
-      return enc_generic<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s,
-                                        sms, launches);
+      if (vec) return enc_vec<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_F64:
-      return enc_generic<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms,
-                                   launches);
+      return enc_generic<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_LOSSLESS64:
-      return enc_generic<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s,
-                                          sms, launches);
+      if (vec) return enc_vec<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     default:
-      return enc_generic<OPTB_LOSSLESS128>(g, images, row_stride, row_index, containers, offsets,
-                                           s, sms, launches);
+      if (vec) return enc_vec<OPTB_LOSSLESS128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_LOSSLESS128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
   }
 }
 
 cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* offsets,
                           const Epi& e, void* out, DevError* err, cudaStream_t s, int sms,
                           uint64_t* launches) {
-  const bool exact = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128;
   const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
-  const bool vec = exact && g.P % 16 == 0 && aligned16(containers) && aligned16(out) &&
-                   (e.row_stride * es) % 16 == 0;
-  if (vec) {
-    return g.wc == 16 ? dec_vec_any<16>(g, containers, e, out, err, s, sms, launches)
-                      : dec_vec_any<8>(g, containers, e, out, err, s, sms, launches);
-  }
+  const bool vec = vec_ok(g) && aligned16(containers) && aligned16(out) && (e.row_stride * es) % 16 == 0;
   switch (g.mode) {
     case OPTB_EXACT64:
+      if (vec) return dec_vec_any<OPTB_EXACT64>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_EXACT64>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_EXACT128:
+      if (vec) return dec_vec_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_F64:
       return dec_generic_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_LOSSLESS64:
-      return dec_generic_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms,
-                                              launches);
+      if (vec) return dec_vec_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms, launches);
+      return dec_generic_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms, launches);
     default:
-      return dec_generic_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms,
-                                               launches);
+      if (vec) return dec_vec_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms, launches);
+      return dec_generic_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms, launches);
   }
 }
 

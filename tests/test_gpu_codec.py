@@ -190,6 +190,9 @@ def test_stream_golden_gather_and_epilogues(golden, pkg, torch_cuda):
     (2, 6, 3072, 256, 1),      # f64 exact range
     (2, 16, 3072, 64, 1),      # f64 lossy range
     (3, 9, 108, 40, 2),        # lossless, unaligned bit offsets
+    (3, 5, 3072, 23, 2),       # lossless64 vector path, per_chunk < capacity, partial chunks
+    (4, 11, 768, 50, 2),       # lossless128 vector path, per_chunk < capacity, partial chunks
+    (4, 18, 1568, 36, 1),      # lossless128, P % 32 == 0 but odd group count per chunk
     (1, 16, 108, 40, 2),       # exact, P%16 != 0 (generic path)
     (0, 5, 27, 13, 3),         # odd everything
 ])
@@ -267,6 +270,32 @@ def test_unaligned_pointers_and_strides(pkg, oracle_mod, torch_cuda):
     C.sync()
     assert np.array_equal(big[:, :P].cpu().numpy(), ds.cpu().numpy()[idx])
     assert int(big[:, P:].sum()) == 0
+
+
+def test_f64_decode_arbitrary_containers_vs_oracle(pkg, oracle_mod, torch_cuda):
+    """f64 decode on arbitrary (also fractional, huge and lossy) binary64
+    containers equals the oracle's fmod peel (codec.cpp:159-178)."""
+    torch = torch_cuda
+    C, O = pkg.codec, oracle_mod
+    rng = np.random.default_rng(64)
+    for n in (1, 3, 6, 7, 9, 12, 16):
+        P = 96
+        vals = rng.random(P) * 2.0 ** rng.integers(0, 8 * n + 1, size=P)
+        vals[::7] = np.floor(vals[::7])
+        plane = vals.astype(np.float64).view(np.uint8)
+        try:
+            want = O.decode(plane, None, n, P, O.F64)
+        except O.OracleError:
+            want = None
+        L = C.layout(2, n, P, n, 1)
+        out = torch.empty((n, P), dtype=torch.uint8, device="cuda")
+        C.decode_dev(L, torch.from_numpy(plane.copy()).cuda(), out)
+        if want is None:
+            with pytest.raises(pkg.errors.FormatError):
+                C.sync()
+        else:
+            C.sync()
+            assert np.array_equal(out.cpu().numpy(), want), n
 
 
 def test_device_range_check_reports_first_chunk(pkg, torch_cuda):
