@@ -8,16 +8,18 @@
 //   SURVEY App. B).
 //
 // Kernel families:
-//   K1 encode_exact_vec<WC>   16-pixel x 16-image register byte transpose
-//                             (PRMT), 128-bit loads of gathered rows, XOR-
-//                             swizzled warp-private smem staging, fully
-//                             coalesced 128-bit container stores.
-//   K2 decode_exact_vec<WC,O> coalesced 128-bit container loads into swizzled
-//                             smem, register transpose, u8 rows stored
-//                             directly (128-bit) or via a u8 smem tile and a
-//                             fused float/half/bf16 epilogue (coalesced).
-//   K3/K4 lossless, K5/K6 f64 and unaligned shapes: one pixel per lane,
-//                             warp ballots for the parity plane.
+//   k_encode_vec<MODE>    K1/K3/K5: gathered rows by cp.async into a 3-stage
+//                         warp-private smem ring, 16-pixel x 16-image register
+//                         byte transpose (PRMT), per-mode word build (exact
+//                         bytes, lossless 7-bit compaction + 16-bit parity
+//                         stores, f64 ordered binary64 adds), XOR-swizzled
+//                         staging, fully coalesced 128/64-bit container stores.
+//   k_decode_vec<MODE,O>  K2/K4/K6: container words (+ parity) by cp.async
+//                         into swizzled slots, per-mode range check and
+//                         unpack, transpose, u8 rows stored directly or through
+//                         a u8 tile with the fused fp32/fp16/bf16 epilogue.
+//   k_{en,de}code_generic any P / stride / alignment: one pixel per lane,
+//                         warp ballots for the parity plane.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -112,6 +114,11 @@ __device__ __forceinline__ void latch_error(DevError* err, uint32_t kind, uint64
                                             uint32_t n) {
   atomicCAS(&err->kind, 0u, kind);
   atomicMin(&err->key, static_cast<unsigned long long>((chunk << 8) | n));
+}
+
+// 256^i as an exact binary64 built from its exponent bits (0 <= i <= 16).
+__device__ __forceinline__ double pow256(int i) {
+  return __longlong_as_double(static_cast<long long>(1023 + 8 * i) << 52);
 }
 
 // ------------------------------------------------------------------ epilogue
@@ -249,7 +256,8 @@ template <int MODE>
 struct VecMode {
   static constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
   static constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
-  static constexpr int NI = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128) ? 16
+  static constexpr bool F64 = MODE == OPTB_F64;
+  static constexpr int NI = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128 || F64) ? 16
                             : (MODE == OPTB_LOSSLESS64) ? 9 : 18;      // images per word
   static constexpr int NT = NI < 16 ? NI : 16;                         // images in the 16x16 transpose
   static constexpr int SW = (WC == 16) ? 7 : 15;                       // slot XOR swizzle mask
@@ -258,8 +266,36 @@ struct VecMode {
   static constexpr int PAR_B = OFFS ? NI * 64 : 0;                     // staged parity bits (decode)
   static constexpr int ENC_SLOT = ROWS_B > WORDS_B ? ROWS_B : WORDS_B;
   static constexpr int DEC_SLOT = (WORDS_B + PAR_B) > ROWS_B ? (WORDS_B + PAR_B) : ROWS_B;
-  static constexpr int MIN_BLOCKS = WC == 16 ? 1 : 2;
+  static constexpr int MIN_BLOCKS = (WC == 16 || F64) ? 1 : 2;
 };
+
+// Float64Faithful peel of one container value into 16 image bytes
+// (codec.cpp:171-175: q = fmod(acc, 256), acc = (acc - q) / 256, pixel =
+// (u8)q), without fmod:
+//  * 0 <= acc < 2^64: the peel is exactly the integer peel of trunc(acc) --
+//    fmod keeps acc's fraction in q, (u8)q drops it, (acc - q)/256 is
+//    trunc(acc/256);
+//  * acc >= 2^64: acc is a multiple of 2^12, so q = 0 and acc/256 is exact;
+//  * +inf / NaN: q is NaN -> pixel 0 (the reference's x86 conversion), and
+//    acc stays non-finite; the acc >= 2^64 branch yields the same bytes.
+__device__ __forceinline__ void f64_peel16(double acc, uint32_t (&b)[4]) {
+  b[0] = b[1] = b[2] = b[3] = 0u;
+  bool small = acc < 0x1.0p64;
+  uint64_t iacc = small ? static_cast<uint64_t>(acc) : 0ull;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    uint32_t q = 0u;
+    if (small) {
+      q = static_cast<uint32_t>(iacc & 0xffull);
+      iacc >>= 8;
+    } else {
+      acc = __dmul_rn(acc, 0x1.0p-8);
+      small = acc < 0x1.0p64;
+      if (small) iacc = static_cast<uint64_t>(acc);
+    }
+    b[i >> 2] |= q << (8 * (i & 3));
+  }
+}
 
 __device__ __forceinline__ uint64_t compact7(uint64_t x) {  // 8 byte lanes -> 8 x 7-bit fields
   x = (x & 0x007F007F007F007Full) | ((x & 0x7F007F007F007F00ull) >> 1);
@@ -383,7 +419,17 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
       const int sl = p ^ (lane & S::SW);
-      if constexpr (S::OFFS) {
+      if constexpr (S::F64) {
+        // acc += px_i * 256^i in binary64, i ascending (codec.cpp:116-120); the
+        // products are exact, the adds round in the reference's order
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < static_cast<int>(n))
+            acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
+                                           pow256(i)));
+        *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
+      } else if constexpr (S::OFFS) {
         const uint64_t lo8 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];  // images 0..7
         const uint64_t lo = compact7((lo8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
         if constexpr (WC == 8) {  // lossless64: fields 0..7 + image 8's field at bit 56
@@ -522,7 +568,12 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
         const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
         w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
       }
-      if constexpr (S::OFFS) {
+      if constexpr (S::F64) {
+        // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
+        const double acc = __longlong_as_double(static_cast<long long>(w0));
+        bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
+        f64_peel16(acc, m[p]);
+      } else if constexpr (S::OFFS) {
         // range check (codec.cpp:189-194): bits >= 7n must be zero
         const unsigned used = 7u * c.n;
         if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
@@ -549,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
     }
     transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (fields for lossless)
     if (valid) {
-      if constexpr (!S::OFFS) {
+      if constexpr (!S::OFFS && !S::F64) {
         // range check (codec.cpp:189-194): bytes of images >= n must be zero
         uint32_t hi = 0;
 #pragma unroll
@@ -557,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
           if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
         bad = hi != 0;
       }
-      if (bad) latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
+      if (bad) latch_error(err, S::F64 ? kErrF64Range : kErrIntRange, g.chunk_base + k, c.n);
     }
     if constexpr (S::OFFS) {
       // pixel = (field << 1) | parity (codec.cpp:196-201)
@@ -670,7 +721,7 @@ __global__ void __launch_bounds__(256) k_encode_generic(Geom g, const uint8_t* _
         px = __ldg(images + src * row_stride + p);
         if constexpr (MODE == OPTB_F64) {
           // codec.cpp:116-120: acc += px * 256^i in binary64, i ascending
-          dacc = __dadd_rn(dacc, __dmul_rn(static_cast<double>(px), ldexp(1.0, 8 * i)));
+          dacc = __dadd_rn(dacc, __dmul_rn(static_cast<double>(px), pow256(i)));
         } else if constexpr (OFFS) {
           acc |= static_cast<unsigned __int128>(px >> 1) << (7 * i);
         } else {
@@ -734,7 +785,7 @@ __global__ void __launch_bounds__(256) k_decode_generic(Geom g, const uint8_t* _
       double acc = *reinterpret_cast<const double*>(w);
       // codec.cpp:163-170
       const bool check = c.n <= 6u;
-      const double limit = ldexp(1.0, 8 * static_cast<int>(c.n));
+      const double limit = pow256(static_cast<int>(c.n));
       if (!(acc >= 0.0) || (check && acc >= limit)) {
         latch_error(err, kErrF64Range, g.chunk_base + k, c.n);
         continue;
@@ -919,7 +970,6 @@ cudaError_t dec_vec_any(const Geom& g, const void* cont, const uint8_t* offs, co
 // planes; the lossless ones also 32-pixel aligned parity words (P % 32).
 bool vec_ok(const Geom& g) {
   const bool lossless = g.mode == OPTB_LOSSLESS64 || g.mode == OPTB_LOSSLESS128;
-  if (g.mode == OPTB_F64) return false;
   return lossless ? g.P % 32 == 0 : g.P % 16 == 0;
 }
 
@@ -937,6 +987,7 @@ cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_str
       if (vec) return enc_vec<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
       return enc_generic<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_F64:
+      if (vec) return enc_vec<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
       return enc_generic<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_LOSSLESS64:
       if (vec) return enc_vec<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
@@ -960,6 +1011,7 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
       if (vec) return dec_vec_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_F64:
+      if (vec) return dec_vec_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_LOSSLESS64:
       if (vec) return dec_vec_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms, launches);
