@@ -200,6 +200,22 @@ int optb_sbs_set_force_serial(optb_sbs* sbs, int32_t on);
 int optb_sbs_set_profiling(optb_sbs* sbs, int32_t on);
 int optb_sbs_profile(optb_sbs* sbs, float* upload_ms, float* reshuffle_ms, float* gather_ms);
 
+/* ---------------------------------------------------------------- OPTB files
+ * pipeline::dump / load (pipeline.cpp:246-271) for device streams: chunk k of
+ * a stream is the file <dir>/batch_<epoch>_<k>.optb holding write_optb's
+ * bytes (codec.cpp:283-317).  The device container planes already are the
+ * OPTB payload (little-endian words, binary64 bits for f64) followed by the
+ * parity plane, so a file is the 20-byte header plus one D2H copy per plane
+ * (staged through pinned memory).  (h, w, c) is the image shape, h*w*c must
+ * equal layout.pixels.  Load validates every header like read_optb
+ * (codec.cpp:319-367: magic, version, mode tag, capacity) and against the
+ * expected layout; a missing file or any mismatch is OPTB_ERR_FORMAT. */
+int optb_dump_dev(optb_ctx* ctx, const optb_layout* L, const void* containers,
+                  const uint8_t* offsets, uint32_t h, uint32_t w, uint32_t c, const char* dir,
+                  uint64_t epoch);
+int optb_load_dev(optb_ctx* ctx, const optb_layout* L, uint32_t h, uint32_t w, uint32_t c,
+                  const char* dir, uint64_t epoch, void* containers, uint8_t* offsets);
+
 /* ---------------------------------------------------------------- E-D pipeline
  * The encode-while-train data path (replaces pipeline.cpp:37-97 HandoffSlot,
  * :116-129 prepare_epoch, :181-244 run): each step gathers the SBS-drawn rows

@@ -91,7 +91,9 @@ SIGNATURES = {
     "optb_sbs_set_force_serial": (ct.c_int, [vp, ct.c_int32]),
     "optb_sbs_set_profiling": (ct.c_int, [vp, ct.c_int32]),
     "optb_sbs_profile": (ct.c_int, [vp, fp, fp, fp]),
-    "optb_pipeline_create": (ct.c_int, [vp, ct.POINTER(PipelineDesc), ct.POINTER(vp)]),
+    "optb_dump_dev": (ct.c_int, [vp, LP, vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64]),
+    "optb_load_dev": (ct.c_int, [vp, LP, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64, vp, vp]),
+    "optb_pipeline_create":(ct.c_int, [vp, ct.POINTER(PipelineDesc), ct.POINTER(vp)]),
     "optb_pipeline_step": (ct.c_int, [vp, vp, vp]),
     "optb_pipeline_draws": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(vp), ct.POINTER(vp)]),
     "optb_pipeline_containers": (vp, [vp]),

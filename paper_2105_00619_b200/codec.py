@@ -274,6 +274,61 @@ def sync(device: int = 0, stream=None) -> None:
     check(lib.optb_ctx_sync(_lib.context(device), _stream(stream, device)))
 
 
+def dump_dev(L: Layout, containers, offsets, shape: ImageShape, directory: str, epoch: int) -> None:
+    """pipeline::dump for a device stream (optb_dump_dev): chunk k ->
+    <directory>/batch_<epoch>_<k>.optb in write_optb's format."""
+    dev = containers.device.index or 0
+    check(lib.optb_dump_dev(_lib.context(dev), ct.byref(L), _dptr(containers), _dptr(offsets), shape.height,
+                            shape.width, shape.channels, str(directory).encode(), epoch))
+
+
+def load_dev(L: Layout, shape: ImageShape, directory: str, epoch: int, device=0):
+    """pipeline::load into device planes (optb_load_dev); validates headers."""
+    cont, offs = alloc_stream(L, device)
+    check(lib.optb_load_dev(_lib.context(device), ct.byref(L), shape.height, shape.width, shape.channels,
+                            str(directory).encode(), epoch, _dptr(cont), _dptr(offs)))
+    return cont, offs
+
+
+def write_optb(stream, enc: EncodedBatch) -> None:
+    """codec::write_optb (codec.cpp:283-317): header + LE plane + parity plane."""
+    if enc.n_images == 0:
+        raise Error("optb: refusing to write an empty batch")
+    hdr = b"OPTB" + (1).to_bytes(2, "little") + bytes([int(enc.mode), int(enc.n_images)])
+    hdr += b"".join(int(v).to_bytes(4, "little") for v in (enc.shape.height, enc.shape.width, enc.shape.channels))
+    stream.write(hdr + np.ascontiguousarray(enc.plane, np.uint8).tobytes()
+                 + (np.ascontiguousarray(enc.offsets, np.uint8).tobytes() if mode_has_offsets(enc.mode) else b""))
+
+
+def read_optb(stream) -> EncodedBatch:
+    """codec::read_optb (codec.cpp:319-367) with the same checks and messages."""
+    def take(n):
+        b = stream.read(n)
+        if len(b) != n:
+            raise FormatError("optb: truncated stream")
+        return b
+    if take(4) != b"OPTB":
+        raise FormatError("optb: bad magic")
+    version = int.from_bytes(take(2), "little")
+    if version != 1:
+        raise FormatError(f"optb: unsupported version {version}")
+    tag, n = take(1)[0], take(1)[0]
+    if tag > 4:
+        raise FormatError(f"optb: unknown mode tag {tag}")
+    mode = CodecMode(tag)
+    h, w, c = (int.from_bytes(take(4), "little") for _ in range(3))
+    shape = ImageShape(h, w, c)
+    P = shape.pixel_count()
+    if n == 0 or P == 0:
+        raise FormatError("optb: empty batch header")
+    limit = capacity(mode) if capacity_is_hard(mode) else kFloat64AcceptLimit
+    if n > limit:
+        raise FormatError(f"optb: image count {n} exceeds {mode_name(mode)} capacity")
+    plane = np.frombuffer(take(P * container_value_bytes(mode)), np.uint8).copy()
+    offsets = np.frombuffer(take((n * P + 7) // 8), np.uint8).copy() if mode_has_offsets(mode) else np.zeros(0, np.uint8)
+    return EncodedBatch(mode, shape, n, plane, offsets)
+
+
 def encode_host(L: Layout, images: np.ndarray):
     """optb_encode_host over a whole host stream ([rows, P] u8)."""
     cont = np.zeros(container_bytes(L), np.uint8)

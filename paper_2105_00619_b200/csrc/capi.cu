@@ -33,6 +33,15 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+int optb_b200::set_error_text(int code, const std::string& message) {
+  g_err = message;
+  return code;
+}
+
+namespace {
+
 int cuda_err(cudaError_t e, const char* where) {
   return set_err(OPTB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }

@@ -11,6 +11,9 @@
 
 namespace optb_b200 {
 
+// Sets the calling thread's optb_last_error() text; returns `code`.
+int set_error_text(int code, const std::string& message);
+
 // Device-side error latch owned by a context (see optb_ctx_sync).
 struct DevError {
   uint32_t kind;         // 0 none, 1 int range, 2 f64 range, 3 label

@@ -1,0 +1,193 @@
+// io.cu -- OPTB epoch dump / load for device streams (optb_dump_dev,
+// optb_load_dev).  Replaces pipeline::dump / pipeline::load
+// (pipeline.cpp:246-271) over codec::write_optb / read_optb
+// (codec.cpp:283-367) for the GPU path: the container planes are already in
+// OPTB payload order, so no pack/unpack kernel is needed -- each chunk is a
+// header plus a D2H (or H2D) copy staged through a ring of pinned buffers,
+// with file I/O of chunk k overlapping the copy of chunk k+1.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/stat.h>
+
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "optb_cuda.h"
+
+namespace {
+
+int io_fail(int code, const std::string& msg) { return optb_b200::set_error_text(code, msg); }
+
+std::string chunk_path(const char* dir, uint64_t epoch, uint64_t k) {
+  return std::string(dir) + "/batch_" + std::to_string(epoch) + "_" + std::to_string(k) + ".optb";
+}
+
+void put_le(uint8_t* p, uint64_t v, int n) {
+  for (int i = 0; i < n; ++i) p[i] = static_cast<uint8_t>(v >> (8 * i));
+}
+uint64_t get_le(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = n - 1; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+struct ChunkGeom {
+  uint64_t n;       // images in chunk k
+  uint64_t bytes;   // plane bytes
+  uint64_t obytes;  // parity plane bytes (exact, ceil(n*P/8))
+};
+
+ChunkGeom chunk_geom(const optb_layout* L, uint64_t k) {
+  const uint64_t cpb = (L->batch + L->per_chunk - 1) / L->per_chunk;
+  const uint64_t j = k % cpb;
+  const uint64_t left = L->batch - j * L->per_chunk;
+  ChunkGeom g;
+  g.n = left < L->per_chunk ? left : L->per_chunk;
+  g.bytes = L->pixels * optb_container_value_bytes(L->mode);
+  g.obytes = optb_mode_has_offsets(L->mode) ? optb_offsets_plane_bytes(static_cast<uint32_t>(g.n), L->pixels) : 0;
+  return g;
+}
+
+struct Staging {
+  static constexpr int kRing = 4;
+  uint8_t* buf[kRing] = {};
+  cudaEvent_t ev[kRing] = {};
+  size_t cap = 0;
+  cudaStream_t s = nullptr;
+  ~Staging() {
+    for (int i = 0; i < kRing; ++i) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+    if (s) cudaStreamDestroy(s);
+  }
+  bool init(size_t bytes) {
+    cap = bytes;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return false;
+    for (int i = 0; i < kRing; ++i)
+      if (cudaHostAlloc(&buf[i], bytes, cudaHostAllocDefault) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess)
+        return false;
+    return true;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int optb_dump_dev(optb_ctx* ctx, const optb_layout* L, const void* containers, const uint8_t* offsets,
+                  uint32_t h, uint32_t w, uint32_t c, const char* dir, uint64_t epoch) {
+  if (!ctx || !L || !containers || !dir) return io_fail(OPTB_ERR_ARG, "dump: null argument");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  if (static_cast<uint64_t>(h) * w * c != L->pixels) return io_fail(OPTB_ERR_SHAPE, "dump: h*w*c != pixels");
+  if (optb_mode_has_offsets(L->mode) && !offsets) return io_fail(OPTB_ERR_ARG, "dump: null offsets");
+  mkdir(dir, 0755);  // create_directories for the last level (pipeline.cpp:248-250)
+  struct stat sb;
+  if (stat(dir, &sb) != 0 || !S_ISDIR(sb.st_mode))
+    return io_fail(OPTB_ERR_FORMAT, std::string("dump: cannot create directory ") + dir);
+  const uint64_t chunks = optb_layout_chunks(L);
+  const uint64_t ostride = optb_offsets_stride(L->mode, L->pixels, L->per_chunk);
+  const ChunkGeom full = chunk_geom(L, 0);
+  Staging stg;
+  if (!stg.init(20 + full.bytes + (full.obytes ? ostride : 0)))
+    return io_fail(OPTB_ERR_CUDA, "dump: pinned staging");
+  auto write_out = [&](uint64_t k) -> int {
+    const int r = static_cast<int>(k % Staging::kRing);
+    if (cudaEventSynchronize(stg.ev[r]) != cudaSuccess) return io_fail(OPTB_ERR_CUDA, "dump: D2H");
+    const ChunkGeom g = chunk_geom(L, k);
+    uint8_t* b = stg.buf[r];
+    memcpy(b, "OPTB", 4);
+    put_le(b + 4, 1, 2);
+    put_le(b + 6, static_cast<uint64_t>(L->mode), 1);
+    put_le(b + 7, g.n, 1);
+    put_le(b + 8, h, 4);
+    put_le(b + 12, w, 4);
+    put_le(b + 16, c, 4);
+    const std::string path = chunk_path(dir, epoch, k);
+    FILE* f = fopen(path.c_str(), "wb");
+    if (!f) return io_fail(OPTB_ERR_FORMAT, "optb: cannot open for writing: " + path);
+    const size_t total = 20 + g.bytes + g.obytes;
+    const size_t wr = fwrite(b, 1, total, f);
+    const int cl = fclose(f);
+    if (wr != total || cl != 0) return io_fail(OPTB_ERR_FORMAT, "optb: write failed: " + path);
+    return OPTB_OK;
+  };
+  for (uint64_t k = 0; k < chunks; ++k) {
+    const int r = static_cast<int>(k % Staging::kRing);
+    if (k >= Staging::kRing) {
+      st = write_out(k - Staging::kRing);
+      if (st) return st;
+    }
+    const ChunkGeom g = chunk_geom(L, k);
+    if (cudaMemcpyAsync(stg.buf[r] + 20, static_cast<const uint8_t*>(containers) + k * g.bytes, g.bytes,
+                        cudaMemcpyDeviceToHost, stg.s) != cudaSuccess ||
+        (g.obytes && cudaMemcpyAsync(stg.buf[r] + 20 + g.bytes, offsets + k * ostride, g.obytes,
+                                     cudaMemcpyDeviceToHost, stg.s) != cudaSuccess) ||
+        cudaEventRecord(stg.ev[r], stg.s) != cudaSuccess)
+      return io_fail(OPTB_ERR_CUDA, "dump: D2H");
+  }
+  for (uint64_t k = chunks > Staging::kRing ? chunks - Staging::kRing : 0; k < chunks; ++k) {
+    st = write_out(k);
+    if (st) return st;
+  }
+  return OPTB_OK;
+}
+
+int optb_load_dev(optb_ctx* ctx, const optb_layout* L, uint32_t h, uint32_t w, uint32_t c,
+                  const char* dir, uint64_t epoch, void* containers, uint8_t* offsets) {
+  if (!ctx || !L || !containers || !dir) return io_fail(OPTB_ERR_ARG, "load: null argument");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  if (static_cast<uint64_t>(h) * w * c != L->pixels) return io_fail(OPTB_ERR_SHAPE, "load: h*w*c != pixels");
+  if (optb_mode_has_offsets(L->mode) && !offsets) return io_fail(OPTB_ERR_ARG, "load: null offsets");
+  const uint64_t chunks = optb_layout_chunks(L);
+  const uint64_t ostride = optb_offsets_stride(L->mode, L->pixels, L->per_chunk);
+  const ChunkGeom full = chunk_geom(L, 0);
+  Staging stg;
+  if (!stg.init(20 + full.bytes + (full.obytes ? ostride : 0)))
+    return io_fail(OPTB_ERR_CUDA, "load: pinned staging");
+  if (chunks == 0) return OPTB_OK;
+  for (uint64_t k = 0; k < chunks; ++k) {
+    const int r = static_cast<int>(k % Staging::kRing);
+    if (cudaEventSynchronize(stg.ev[r]) != cudaSuccess) return io_fail(OPTB_ERR_CUDA, "load: H2D");
+    const ChunkGeom g = chunk_geom(L, k);
+    const std::string path = chunk_path(dir, epoch, k);
+    FILE* f = fopen(path.c_str(), "rb");
+    if (!f)
+      return io_fail(OPTB_ERR_FORMAT, "load: missing batch file " + path + " for epoch " + std::to_string(epoch));
+    uint8_t* b = stg.buf[r];
+    const size_t want = 20 + g.bytes + g.obytes;
+    const size_t got = fread(b, 1, want, f);
+    const bool extra = fgetc(f) != EOF;
+    fclose(f);
+    // read_optb's checks, in its order (codec.cpp:319-344)
+    if (got < 4) return io_fail(OPTB_ERR_FORMAT, "optb: truncated stream");
+    if (memcmp(b, "OPTB", 4) != 0) return io_fail(OPTB_ERR_FORMAT, "optb: bad magic");
+    if (got < 6) return io_fail(OPTB_ERR_FORMAT, "optb: truncated stream");
+    const uint64_t version = get_le(b + 4, 2);
+    if (version != 1) return io_fail(OPTB_ERR_FORMAT, "optb: unsupported version " + std::to_string(version));
+    if (got < 20) return io_fail(OPTB_ERR_FORMAT, "optb: truncated stream");
+    const uint64_t tag = b[6], n = b[7];
+    if (tag > 4) return io_fail(OPTB_ERR_FORMAT, "optb: unknown mode tag " + std::to_string(tag));
+    if (tag != static_cast<uint64_t>(L->mode) || n != g.n || get_le(b + 8, 4) != h || get_le(b + 12, 4) != w ||
+        get_le(b + 16, 4) != c)
+      return io_fail(OPTB_ERR_FORMAT, "load: " + path + " does not match the expected layout");
+    if (got != want) return io_fail(OPTB_ERR_FORMAT, "optb: truncated stream");
+    (void)extra;  // like read_optb_file, bytes after the parity plane are ignored
+    if (cudaMemcpyAsync(static_cast<uint8_t*>(containers) + k * g.bytes, b + 20, g.bytes, cudaMemcpyHostToDevice,
+                        stg.s) != cudaSuccess ||
+        (g.obytes && cudaMemcpyAsync(offsets + k * ostride, b + 20 + g.bytes, g.obytes, cudaMemcpyHostToDevice,
+                                     stg.s) != cudaSuccess) ||
+        cudaEventRecord(stg.ev[r], stg.s) != cudaSuccess)
+      return io_fail(OPTB_ERR_CUDA, "load: H2D");
+  }
+  if (cudaStreamSynchronize(stg.s) != cudaSuccess) return io_fail(OPTB_ERR_CUDA, "load: H2D");
+  return OPTB_OK;
+}
+
+}  // extern "C"
