@@ -216,6 +216,18 @@ int optb_dump_dev(optb_ctx* ctx, const optb_layout* L, const void* containers,
 int optb_load_dev(optb_ctx* ctx, const optb_layout* L, uint32_t h, uint32_t w, uint32_t c,
                   const char* dir, uint64_t epoch, void* containers, uint8_t* offsets);
 
+/* data::load_records (dataset.cpp:65-99) onto the device: a file of
+ * CIFAR-style records (1 label byte + C planes of H*W bytes) is read into
+ * pinned memory, copied up, and one kernel de-interleaves planar CHW into the
+ * HWC rows the codec packs (pixels[r][hw*C + c] = plane c byte hw) and
+ * extracts the labels (int32).  Errors and messages are the reference's
+ * ("records: cannot open ...", "... label L outside K classes in ...",
+ * "... trailing partial record in ...", "... no records in ...").
+ * *n_records gets the count; at most max_records are accepted. */
+int optb_load_records_dev(optb_ctx* ctx, const char* path, uint32_t h, uint32_t w, uint32_t c,
+                          uint32_t n_classes, uint8_t* pixels, int32_t* labels,
+                          uint64_t max_records, uint64_t* n_records);
+
 /* ---------------------------------------------------------------- E-D pipeline
  * The encode-while-train data path (replaces pipeline.cpp:37-97 HandoffSlot,
  * :116-129 prepare_epoch, :181-244 run): each step gathers the SBS-drawn rows

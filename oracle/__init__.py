@@ -284,6 +284,17 @@ def float_to_bf16(v: float) -> int:
     return C.orc_float_to_bf16(ct.c_float(v))
 
 
+def records_to_hwc(raw: bytes, h: int, w: int, c: int):
+    """data::load_records' record parse (dataset.cpp:65-99): each record is a
+    label byte then C planes of H*W bytes; pixels[hw*C + c] = plane c [hw]
+    (dataset.cpp:84-91).  Returns (pixels [N, P] u8, labels [N] int32)."""
+    P = h * w * c
+    arr = np.frombuffer(raw, np.uint8).reshape(-1, P + 1)
+    labels = arr[:, 0].astype(np.int32)
+    pixels = arr[:, 1:].reshape(-1, c, h * w).transpose(0, 2, 1).reshape(-1, P)
+    return np.ascontiguousarray(pixels), labels
+
+
 # ------------------------------------------------------------------ reference (compiled)
 def ref_available() -> bool:
     return REF is not None

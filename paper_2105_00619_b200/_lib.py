@@ -93,6 +93,8 @@ SIGNATURES = {
     "optb_sbs_profile": (ct.c_int, [vp, fp, fp, fp]),
     "optb_dump_dev": (ct.c_int, [vp, LP, vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64]),
     "optb_load_dev": (ct.c_int, [vp, LP, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64, vp, vp]),
+    "optb_load_records_dev": (ct.c_int, [vp, ct.c_char_p, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp,
+                                         vp, ct.c_uint64, u64p]),
     "optb_pipeline_create":(ct.c_int, [vp, ct.POINTER(PipelineDesc), ct.POINTER(vp)]),
     "optb_pipeline_step": (ct.c_int, [vp, vp, vp]),
     "optb_pipeline_draws": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(vp), ct.POINTER(vp)]),

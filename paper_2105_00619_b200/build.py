@@ -101,11 +101,24 @@ def build_ref_suites(force: bool = False):
     return REF_SUITES_BIN
 
 
+CLI_SRC = os.path.join(ROOT, "tools", "optb_cli.cpp")
+CLI_BIN = os.path.join(PKG, "optb_b200")
+
+
+def build_cli(force: bool = False) -> str:
+    """The reference CLI's encode/decode subcommands over the shim."""
+    if force or _stale(CLI_BIN, [CLI_SRC, SHIM_LIB_NAME]):
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-I" + os.path.join(CSRC, "shim", "include"), CLI_SRC,
+              "-o", CLI_BIN, "-L" + PKG, "-loptb_shim", "-loptb_cuda", "-Wl,-rpath,$ORIGIN"])
+    return CLI_BIN
+
+
 def build(force: bool = False) -> None:
     build_cuda(force)
     if os.path.isdir(os.path.join(CSRC, "shim", "src")) and all(
             os.path.exists(os.path.join(CSRC, "shim", "src", f)) for f in SHIM_SOURCES):
         build_shim(force)
+        build_cli(force)
         build_ref_suites(force)
 
 

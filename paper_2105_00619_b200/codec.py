@@ -290,6 +290,21 @@ def load_dev(L: Layout, shape: ImageShape, directory: str, epoch: int, device=0)
     return cont, offs
 
 
+def load_records_dev(path: str, shape: ImageShape, num_classes: int, max_records: int, device=0):
+    """data::load_records (dataset.cpp:65-99) onto the device: returns
+    (pixels [N, P] u8 HWC rows, labels [N] int32) tensors."""
+    import torch
+    dev = torch.device("cuda", device)
+    P = shape.pixel_count()
+    pixels = torch.empty((max(max_records, 1), max(P, 1)), dtype=torch.uint8, device=dev)
+    labels = torch.empty(max(max_records, 1), dtype=torch.int32, device=dev)
+    n = ct.c_uint64(0)
+    check(lib.optb_load_records_dev(_lib.context(device), str(path).encode(), shape.height, shape.width,
+                                    shape.channels, num_classes, _dptr(pixels), _dptr(labels), max_records,
+                                    ct.byref(n)))
+    return pixels[: n.value], labels[: n.value]
+
+
 def write_optb(stream, enc: EncodedBatch) -> None:
     """codec::write_optb (codec.cpp:283-317): header + LE plane + parity plane."""
     if enc.n_images == 0:

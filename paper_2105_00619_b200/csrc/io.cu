@@ -191,3 +191,100 @@ int optb_load_dev(optb_ctx* ctx, const optb_layout* L, uint32_t h, uint32_t w, u
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- records
+namespace {
+
+// One CTA per record at a time: the record (1 + C*H*W bytes, not aligned) is
+// staged in shared memory with coalesced byte loads, then written out
+// channel-interleaved with coalesced byte stores (dataset.cpp:84-91).
+__global__ void k_records_to_hwc(const uint8_t* __restrict__ src, uint64_t n_rec, uint32_t hw, uint32_t ch,
+                                 uint32_t n_classes, uint8_t* __restrict__ dst, int32_t* __restrict__ labels,
+                                 unsigned long long* bad) {
+  extern __shared__ uint8_t rec[];
+  const uint64_t P = static_cast<uint64_t>(hw) * ch;
+  for (uint64_t r = blockIdx.x; r < n_rec; r += gridDim.x) {
+    const uint8_t* s = src + r * (P + 1);
+    for (uint64_t i = threadIdx.x; i < P + 1; i += blockDim.x) rec[i] = s[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      labels[r] = rec[0];
+      if (rec[0] >= n_classes) atomicMin(bad, static_cast<unsigned long long>(r));
+    }
+    for (uint64_t o = threadIdx.x; o < P; o += blockDim.x) {
+      const uint64_t px = o / ch, cc = o - px * ch;
+      dst[r * P + o] = rec[1 + cc * hw + px];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+extern "C" int optb_load_records_dev(optb_ctx* ctx, const char* path, uint32_t h, uint32_t w, uint32_t c,
+                                     uint32_t n_classes, uint8_t* pixels, int32_t* labels, uint64_t max_records,
+                                     uint64_t* n_records) {
+  if (!ctx || !path || !pixels || !labels || !n_records) return io_fail(OPTB_ERR_ARG, "records: null argument");
+  const uint64_t P = static_cast<uint64_t>(h) * w * c;
+  if (P == 0) return io_fail(OPTB_ERR_SHAPE, "records: image extents must be positive");
+  FILE* f = fopen(path, "rb");
+  if (!f) return io_fail(OPTB_ERR_FORMAT, std::string("records: cannot open ") + path);
+  fseek(f, 0, SEEK_END);
+  const long size = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  const uint64_t n = static_cast<uint64_t>(size) / (P + 1);
+  if (static_cast<uint64_t>(size) % (P + 1) != 0) {
+    fclose(f);
+    return io_fail(OPTB_ERR_FORMAT, std::string("records: trailing partial record in ") + path);
+  }
+  if (n == 0) {
+    fclose(f);
+    return io_fail(OPTB_ERR_FORMAT, std::string("records: no records in ") + path);
+  }
+  if (n > max_records) {
+    fclose(f);
+    return io_fail(OPTB_ERR_ARG, "records: " + std::to_string(n) + " records exceed the output capacity");
+  }
+  uint8_t* host = nullptr;
+  uint8_t* dev = nullptr;
+  unsigned long long* bad = nullptr;
+  auto release = [&] {
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    if (bad) cudaFree(bad);
+  };
+  if (cudaHostAlloc(&host, size, cudaHostAllocDefault) != cudaSuccess || cudaMalloc(&dev, size) != cudaSuccess ||
+      cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess) {
+    fclose(f);
+    release();
+    return io_fail(OPTB_ERR_CUDA, "records: staging buffers");
+  }
+  const size_t got = fread(host, 1, size, f);
+  fclose(f);
+  if (got != static_cast<size_t>(size)) {
+    release();
+    return io_fail(OPTB_ERR_FORMAT, std::string("records: cannot read ") + path);
+  }
+  const unsigned long long none = ~0ull;
+  cudaMemcpy(bad, &none, sizeof none, cudaMemcpyHostToDevice);
+  cudaMemcpy(dev, host, size, cudaMemcpyHostToDevice);
+  const unsigned grid = static_cast<unsigned>(n < 148 * 8 ? n : 148 * 8);
+  if (P + 1 > 48 * 1024)
+    cudaFuncSetAttribute(k_records_to_hwc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P + 1));
+  k_records_to_hwc<<<grid, 256, P + 1>>>(dev, n, h * w, c, n_classes, pixels, labels, bad);
+  unsigned long long first_bad = none;
+  const cudaError_t e = cudaMemcpy(&first_bad, bad, sizeof first_bad, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    release();
+    return io_fail(OPTB_ERR_CUDA, std::string("records: ") + cudaGetErrorString(e));
+  }
+  int rc = OPTB_OK;
+  if (first_bad != none) {  // dataset.cpp:78-82 names the first offending label
+    const int label = host[first_bad * (P + 1)];
+    rc = io_fail(OPTB_ERR_FORMAT, "records: label " + std::to_string(label) + " outside " +
+                                      std::to_string(n_classes) + " classes in " + path);
+  }
+  release();
+  *n_records = n;
+  return rc;
+}
