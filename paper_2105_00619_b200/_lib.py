@@ -14,7 +14,9 @@ import threading
 from .errors import raise_for
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liboptb_cuda.so")
+# OPTB_CUDA_LIB selects an alternative build of the same library (tuning
+# experiments, tools/tune_vec.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("OPTB_CUDA_LIB", os.path.join(PKG, "liboptb_cuda.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

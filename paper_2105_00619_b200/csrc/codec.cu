@@ -30,7 +30,13 @@
 namespace optb_b200 {
 namespace {
 
-constexpr int kWarps = 8;            // warps per CTA for the vector kernels
+#ifndef OPTB_VEC_WARPS
+#define OPTB_VEC_WARPS 8
+#endif
+#ifndef OPTB_VEC_STAGES
+#define OPTB_VEC_STAGES 3
+#endif
+constexpr int kWarps = OPTB_VEC_WARPS;  // warps per CTA for the vector kernels
 constexpr int kThreads = kWarps * 32;
 
 __device__ __forceinline__ uint4 ldg16(const void* p) {
@@ -239,7 +245,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // 32 items) in a warp-private ring of shared-memory slots: the copies of the
 // next kStages-1 tiles are in flight while the current tile is transposed.
 // Requires P % 16 == 0 and 16-byte aligned rows / containers / outputs.
-constexpr int kStages = 3;
+constexpr int kStages = OPTB_VEC_STAGES;
 
 
 // ------------------------------------------------------------------ K1 / K3

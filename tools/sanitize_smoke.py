@@ -1,0 +1,90 @@
+"""Exercise every kernel once on small inputs, for compute-sanitizer:
+
+    compute-sanitizer --tool memcheck  python tools/sanitize_smoke.py
+    compute-sanitizer --tool racecheck python tools/sanitize_smoke.py
+    compute-sanitizer --tool synccheck python tools/sanitize_smoke.py
+
+Covers the vector and generic codec paths for all modes and output types,
+partial chunks, gathers, the range-error latch, the class index, the SBS
+cursor (parallel Fisher-Yates and the forced serial redo), the pipeline,
+OPTB dump/load and the record loader.  Results are checked against the
+oracle so a sanitizer run is also a parity run.
+"""
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    import oracle as O
+    import paper_2105_00619_b200 as pkg
+    from paper_2105_00619_b200.pipeline import Pipeline
+    C, S = pkg.codec, pkg.sampler
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(0)
+    n_checks = 0
+    for mode in range(5):
+        for P, B, nb in ((768, 40, 2), (108, 21, 2)):  # vector path, generic path
+            pc = C.capacity(mode)
+            ds = rng.integers(0, 256, (64, P), dtype=np.uint8)
+            idx = rng.integers(0, 64, B * nb).astype(np.int64)
+            L = C.layout(mode, pc, P, B, nb)
+            cont, offs = C.alloc_stream(L)
+            C.encode_dev(L, torch.from_numpy(ds).to(dev), cont, offs, row_index=torch.from_numpy(idx).to(dev))
+            rc, ro = O.encode_stream(ds, idx, mode, pc, B, nb)
+            assert np.array_equal(cont.cpu().numpy()[: rc.size], rc)
+            for dt in (torch.uint8, torch.float32, torch.float16, torch.bfloat16):
+                out = torch.empty((B * nb, P), dtype=dt, device=dev)
+                C.decode_dev(L, cont, out, offsets=offs, scale=1 / 255)
+                C.sync()
+                n_checks += 1
+            bad = cont.clone()
+            bad.view(torch.uint8)[7] = 0xFF  # high byte of pixel 0's word in chunk 0
+            if mode != 2:
+                C.decode_dev(L, bad, torch.empty((B * nb, P), dtype=torch.uint8, device=dev), offsets=offs)
+                try:
+                    C.sync()
+                except pkg.errors.FormatError:
+                    pass
+    labels = (np.arange(3000) % 7).astype(np.int32)
+    offs_d, mem_d = S.class_index_dev(labels, 7)
+    p = S.plan([1 / 7] * 7, 21, 5)
+    ro, rm = O.class_index(labels, 7)
+    for serial in (False, True):
+        cur = S.BatchCursor.from_device_index(p, offs_d, mem_d)
+        cur.set_force_serial(serial)
+        ex, _ = cur.next_dev(300)
+        oc = O.Cursor(O.sbs_plan([1 / 7] * 7, 21), ro, rm, 21, 5)
+        assert np.array_equal(ex.cpu().numpy(), oc.next(300)[0])
+    ds = torch.randint(0, 256, (3000, 768), dtype=torch.uint8, device=dev)
+    cur = S.BatchCursor.from_device_index(p, offs_d, mem_d)
+    pipe = Pipeline(cur, ds, 1, 21, 4, steps_per_draw=2)
+    out = torch.empty((84, 768), dtype=torch.uint8, device=dev)
+    for _ in range(5):
+        pipe.step(out)
+    C.sync()
+    pipe.close()
+    with tempfile.TemporaryDirectory() as d:
+        L = C.layout(3, 9, 768, 40, 2)
+        cont, offs = C.alloc_stream(L)
+        C.encode_dev(L, ds[:80], cont, offs)
+        C.dump_dev(L, cont, offs, C.ImageShape(16, 16, 3), d, 0)
+        c2, o2 = C.load_dev(L, C.ImageShape(16, 16, 3), d, 0)
+        assert torch.equal(c2[: C.container_bytes(L)], cont[: C.container_bytes(L)])
+        rec = np.concatenate([np.full((50, 1), 3, np.uint8), rng.integers(0, 256, (50, 3072), dtype=np.uint8)], 1)
+        open(os.path.join(d, "r.bin"), "wb").write(rec.tobytes())
+        px, lab = C.load_records_dev(os.path.join(d, "r.bin"), C.ImageShape(32, 32, 3), 10, 50)
+        assert np.array_equal(px.cpu().numpy(), O.records_to_hwc(rec.tobytes(), 32, 32, 3)[0])
+    torch.cuda.synchronize()
+    print(f"sanitize smoke ok ({n_checks} decode variants)")
+
+
+if __name__ == "__main__":
+    main()
