@@ -940,6 +940,8 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
   if (rc) return fail(rc);
   if (s->N) {
     if (on_dev) {
+      // device members may still be in flight on the caller's stream
+      if (cudaDeviceSynchronize() != cudaSuccess) return fail(cuda_err(cudaGetLastError(), "sbs members"));
       if (cudaMemcpyAsync(s->d_pool, members, s->N * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return fail(cuda_err(cudaGetLastError(), "sbs members"));
     } else {

@@ -86,6 +86,8 @@ int optb_dump_dev(optb_ctx* ctx, const optb_layout* L, const void* containers, c
   if (st) return st;
   if (static_cast<uint64_t>(h) * w * c != L->pixels) return io_fail(OPTB_ERR_SHAPE, "dump: h*w*c != pixels");
   if (optb_mode_has_offsets(L->mode) && !offsets) return io_fail(OPTB_ERR_ARG, "dump: null offsets");
+  // synchronous: the planes may still be written by kernels queued on any stream
+  if (cudaDeviceSynchronize() != cudaSuccess) return io_fail(OPTB_ERR_CUDA, "dump: device synchronize");
   mkdir(dir, 0755);  // create_directories for the last level (pipeline.cpp:248-250)
   struct stat sb;
   if (stat(dir, &sb) != 0 || !S_ISDIR(sb.st_mode))
@@ -145,6 +147,8 @@ int optb_load_dev(optb_ctx* ctx, const optb_layout* L, uint32_t h, uint32_t w, u
   if (st) return st;
   if (static_cast<uint64_t>(h) * w * c != L->pixels) return io_fail(OPTB_ERR_SHAPE, "load: h*w*c != pixels");
   if (optb_mode_has_offsets(L->mode) && !offsets) return io_fail(OPTB_ERR_ARG, "load: null offsets");
+  // synchronous: queued kernels may still read the destination planes
+  if (cudaDeviceSynchronize() != cudaSuccess) return io_fail(OPTB_ERR_CUDA, "load: device synchronize");
   const uint64_t chunks = optb_layout_chunks(L);
   const uint64_t ostride = optb_offsets_stride(L->mode, L->pixels, L->per_chunk);
   const ChunkGeom full = chunk_geom(L, 0);
