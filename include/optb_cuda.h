@@ -256,6 +256,9 @@ typedef struct optb_pipeline_desc {
 int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* desc, optb_pipeline** out);
 /* Enqueue the next step; `out` receives optb_layout_rows(layout) decoded rows. */
 int optb_pipeline_step(optb_pipeline* p, void* out, void* stream);
+/* Rows for subsequent steps come from `dataset` (e.g. a double-buffered
+ * device copy of a host dataset refreshed by the caller every step). */
+int optb_pipeline_set_dataset(optb_pipeline* p, const uint8_t* dataset, uint64_t row_stride);
 /* Device draws (examples, classes) of a step still buffered (the last two). */
 int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
                         const int32_t** classes);

@@ -131,6 +131,13 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   return OPTB_OK;
 }
 
+int optb_pipeline_set_dataset(optb_pipeline* p, const uint8_t* dataset, uint64_t row_stride) {
+  if (!p || !dataset) return OPTB_ERR_ARG;
+  p->d.dataset = dataset;
+  p->d.row_stride = row_stride;
+  return OPTB_OK;
+}
+
 int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
                         const int32_t** classes) {
   if (!p || step >= p->calls * p->spd) return OPTB_ERR_ARG;

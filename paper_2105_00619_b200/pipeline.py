@@ -50,6 +50,11 @@ class Pipeline:
         check(lib.optb_pipeline_step(self._h, ct.c_void_p(out.data_ptr()), ct.c_void_p(stream.cuda_stream)))
         self.steps += 1
 
+    def set_dataset(self, dataset):
+        """Rows for subsequent steps come from `dataset` (same shape)."""
+        self._keep = self._keep + (dataset,)
+        check(lib.optb_pipeline_set_dataset(self._h, ct.c_void_p(dataset.data_ptr()), dataset.stride(0)))
+
     def timings(self, step: int):
         s, e, d = ct.c_float(), ct.c_float(), ct.c_float()
         check(lib.optb_pipeline_timings(self._h, step, ct.byref(s), ct.byref(e), ct.byref(d)))
