@@ -258,12 +258,18 @@ constexpr int kStages = OPTB_VEC_STAGES;
 // compacted from byte lanes with three mask/shift steps; the parity bits
 // (px & 1) of a lane's 16 pixels of image i are one 16-bit store at plane bit
 // i*P + 16*group (aligned: the vector path needs P % 32 == 0 in these modes).
+// kF64Narrow: Float64Faithful with at most 8 images per container (the
+// common case, capacity 6): half the staging and transpose work of the
+// 16-image (lossy) variant, two CTAs per SM.
+constexpr int kF64Narrow = 5;
+
 template <int MODE>
 struct VecMode {
   static constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
   static constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
-  static constexpr bool F64 = MODE == OPTB_F64;
-  static constexpr int NI = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128 || F64) ? 16
+  static constexpr bool F64 = MODE == OPTB_F64 || MODE == kF64Narrow;
+  static constexpr int NI = (MODE == OPTB_EXACT64 || MODE == kF64Narrow) ? 8
+                            : (MODE == OPTB_EXACT128 || F64) ? 16
                             : (MODE == OPTB_LOSSLESS64) ? 9 : 18;      // images per word
   static constexpr int NT = NI < 16 ? NI : 16;                         // images in the 16x16 transpose
   static constexpr int SW = (WC == 16) ? 7 : 15;                       // slot XOR swizzle mask
@@ -272,7 +278,7 @@ struct VecMode {
   static constexpr int PAR_B = OFFS ? NI * 64 : 0;                     // staged parity bits (decode)
   static constexpr int ENC_SLOT = ROWS_B > WORDS_B ? ROWS_B : WORDS_B;
   static constexpr int DEC_SLOT = (WORDS_B + PAR_B) > ROWS_B ? (WORDS_B + PAR_B) : ROWS_B;
-  static constexpr int MIN_BLOCKS = (WC == 16 || F64) ? 1 : 2;
+  static constexpr int MIN_BLOCKS = (WC == 16 || NI == 16) ? 1 : 2;
 };
 
 // Float64Faithful peel of one container value into 16 image bytes
@@ -301,6 +307,17 @@ __device__ __forceinline__ void f64_peel16(double acc, uint32_t (&b)[4]) {
     }
     b[i >> 2] |= q << (8 * (i & 3));
   }
+}
+
+// Out-of-line so the rare lossy >= 2^64 case does not bloat the unrolled
+// per-pixel loops of the decode kernel.
+__device__ __noinline__ void f64_peel_big(double acc, uint32_t* b) {
+  uint32_t t[4];
+  f64_peel16(acc, t);
+  b[0] = t[0];
+  b[1] = t[1];
+  b[2] = t[2];
+  b[3] = t[3];
 }
 
 __device__ __forceinline__ uint64_t compact7(uint64_t x) {  // 8 byte lanes -> 8 x 7-bit fields
@@ -429,11 +446,18 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
         // acc += px_i * 256^i in binary64, i ascending (codec.cpp:116-120); the
         // products are exact, the adds round in the reference's order
         double acc = 0.0;
+        if (n <= 6u) {
+          // every partial sum is an integer < 2^48: exact, so the ordered sum
+          // is the packed integer itself (one conversion instead of 2n ops)
+          const uint64_t word = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
+          acc = static_cast<double>(word & ((1ull << (8 * n)) - 1ull));
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (i < static_cast<int>(n))
-            acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
-                                           pow256(i)));
+          for (int i = 0; i < 16; ++i)
+            if (i < static_cast<int>(n))
+              acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
+                                             pow256(i)));
+        }
         *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
       } else if constexpr (S::OFFS) {
         const uint64_t lo8 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];  // images 0..7
@@ -578,7 +602,14 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
         // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
         const double acc = __longlong_as_double(static_cast<long long>(w0));
         bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
-        f64_peel16(acc, m[p]);
+        if (acc < 0x1.0p64) {  // common case: the peel is the integer's bytes
+          const uint64_t iacc = static_cast<uint64_t>(acc);
+          m[p][0] = static_cast<uint32_t>(iacc);
+          m[p][1] = static_cast<uint32_t>(iacc >> 32);
+          m[p][2] = m[p][3] = 0u;
+        } else {
+          f64_peel_big(acc, m[p]);
+        }
       } else if constexpr (S::OFFS) {
         // range check (codec.cpp:189-194): bits >= 7n must be zero
         const unsigned used = 7u * c.n;
@@ -993,6 +1024,8 @@ cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_str
       if (vec) return enc_vec<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
       return enc_generic<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_F64:
+      if (vec && g.per_chunk <= 8)
+        return enc_vec<kF64Narrow>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
       if (vec) return enc_vec<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
       return enc_generic<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
     case OPTB_LOSSLESS64:
@@ -1017,6 +1050,8 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
       if (vec) return dec_vec_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_F64:
+      if (vec && g.per_chunk <= 8)
+        return dec_vec_any<kF64Narrow>(g, containers, offsets, e, out, err, s, sms, launches);
       if (vec) return dec_vec_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
     case OPTB_LOSSLESS64:
