@@ -200,6 +200,25 @@ int optb_sbs_set_force_serial(optb_sbs* sbs, int32_t on);
 int optb_sbs_set_profiling(optb_sbs* sbs, int32_t on);
 int optb_sbs_profile(optb_sbs* sbs, float* upload_ms, float* reshuffle_ms, float* gather_ms);
 
+/* ---------------------------------------------------------------- sharded dataset
+ * Building blocks of the optional dataset-sharded global gather (SURVEY
+ * §8(e)): when every rank holds only rows [begin, end) of the dataset, the
+ * rows a step draws are exchanged with one all-to-all (NCCL over NVLink;
+ * paper_2105_00619_b200/sharded.py).  The exchange plan is a stable
+ * partition of each rank's draws by owner rank (optb_class_index_dev with
+ * labels = owner); these two kernels pack the outgoing rows and turn the
+ * incoming order into a row index for optb_encode_dev.
+ *
+ * dst row i = src row (index[i] - bias) (16-byte vector copies when aligned). */
+int optb_gather_rows_dev(optb_ctx* ctx, const uint8_t* src, uint64_t src_stride, const int64_t* index,
+                         uint64_t n, int64_t bias, uint64_t pixels, uint8_t* dst, uint64_t dst_stride,
+                         void* stream);
+/* inv[perm[j]] = j for j < n (perm a permutation of [0, n)). */
+int optb_inverse_perm_dev(optb_ctx* ctx, const int64_t* perm, uint64_t n, int64_t* inv, void* stream);
+/* owner[i] = (int32)((examples[i] - 0) / rows_per_shard), clamped to n_shards - 1. */
+int optb_owner_labels_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, uint64_t rows_per_shard,
+                          uint32_t n_shards, int32_t* owner, void* stream);
+
 /* ---------------------------------------------------------------- OPTB files
  * pipeline::dump / load (pipeline.cpp:246-271) for device streams: chunk k of
  * a stream is the file <dir>/batch_<epoch>_<k>.optb holding write_optb's

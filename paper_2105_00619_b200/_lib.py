@@ -93,6 +93,10 @@ SIGNATURES = {
     "optb_sbs_set_force_serial": (ct.c_int, [vp, ct.c_int32]),
     "optb_sbs_set_profiling": (ct.c_int, [vp, ct.c_int32]),
     "optb_sbs_profile": (ct.c_int, [vp, fp, fp, fp]),
+    "optb_gather_rows_dev": (ct.c_int, [vp, vp, ct.c_uint64, vp, ct.c_uint64, ct.c_int64, ct.c_uint64, vp,
+                                        ct.c_uint64, vp]),
+    "optb_inverse_perm_dev": (ct.c_int, [vp, vp, ct.c_uint64, vp, vp]),
+    "optb_owner_labels_dev": (ct.c_int, [vp, vp, ct.c_uint64, ct.c_uint64, ct.c_uint32, vp, vp]),
     "optb_dump_dev": (ct.c_int, [vp, LP, vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64]),
     "optb_load_dev": (ct.c_int, [vp, LP, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64, vp, vp]),
     "optb_load_records_dev": (ct.c_int, [vp, ct.c_char_p, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp,

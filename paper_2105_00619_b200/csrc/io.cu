@@ -292,3 +292,77 @@ extern "C" int optb_load_records_dev(optb_ctx* ctx, const char* path, uint32_t h
   *n_records = n;
   return rc;
 }
+
+// ---------------------------------------------------------------- sharded dataset helpers
+namespace {
+
+// One warp per row; 16-byte copies when both rows are 16-byte aligned.
+__global__ void k_gather_rows(const uint8_t* __restrict__ src, uint64_t src_stride,
+                              const int64_t* __restrict__ index, uint64_t n, int64_t bias, uint64_t P,
+                              uint8_t* __restrict__ dst, uint64_t dst_stride) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < n; i += warps) {
+    const uint8_t* s = src + static_cast<uint64_t>(index[i] - bias) * src_stride;
+    uint8_t* d = dst + i * dst_stride;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0;
+    uint64_t done = 0;
+    if (vec) {
+      const uint64_t v = P / 16;
+      for (uint64_t k = lane; k < v; k += 32)
+        reinterpret_cast<uint4*>(d)[k] = __ldg(reinterpret_cast<const uint4*>(s) + k);
+      done = v * 16;
+    }
+    for (uint64_t k = done + lane; k < P; k += 32) d[k] = s[k];
+  }
+}
+
+__global__ void k_inverse_perm(const int64_t* __restrict__ perm, uint64_t n, int64_t* __restrict__ inv) {
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    inv[perm[j]] = static_cast<int64_t>(j);
+}
+
+__global__ void k_owner_labels(const int64_t* __restrict__ ex, uint64_t n, uint64_t per, uint32_t shards,
+                               int32_t* __restrict__ owner) {
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t o = static_cast<uint64_t>(ex[j]) / per;
+    owner[j] = static_cast<int32_t>(o < shards ? o : shards - 1);
+  }
+}
+
+unsigned grid_of(uint64_t work, unsigned per_block) {
+  const uint64_t g = (work + per_block - 1) / per_block;
+  return static_cast<unsigned>(g < 148 * 8 ? (g ? g : 1) : 148 * 8);
+}
+
+}  // namespace
+
+extern "C" int optb_gather_rows_dev(optb_ctx* ctx, const uint8_t* src, uint64_t src_stride, const int64_t* index,
+                                    uint64_t n, int64_t bias, uint64_t pixels, uint8_t* dst, uint64_t dst_stride,
+                                    void* stream) {
+  if (!ctx || (!n)) return ctx ? OPTB_OK : io_fail(OPTB_ERR_ARG, "gather_rows: null ctx");
+  if (!src || !index || !dst) return io_fail(OPTB_ERR_ARG, "gather_rows: null buffer");
+  k_gather_rows<<<grid_of(n * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      src, src_stride ? src_stride : pixels, index, n, bias, pixels, dst, dst_stride ? dst_stride : pixels);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OPTB_OK : io_fail(OPTB_ERR_CUDA, cudaGetErrorString(e));
+}
+
+extern "C" int optb_inverse_perm_dev(optb_ctx* ctx, const int64_t* perm, uint64_t n, int64_t* inv, void* stream) {
+  if (!ctx || (n && (!perm || !inv))) return io_fail(OPTB_ERR_ARG, "inverse_perm: null argument");
+  if (!n) return OPTB_OK;
+  k_inverse_perm<<<grid_of(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(perm, n, inv);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OPTB_OK : io_fail(OPTB_ERR_CUDA, cudaGetErrorString(e));
+}
+
+extern "C" int optb_owner_labels_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, uint64_t per,
+                                     uint32_t shards, int32_t* owner, void* stream) {
+  if (!ctx || !shards || !per || (n && (!examples || !owner))) return io_fail(OPTB_ERR_ARG, "owner_labels: bad argument");
+  if (!n) return OPTB_OK;
+  k_owner_labels<<<grid_of(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(examples, n, per, shards, owner);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OPTB_OK : io_fail(OPTB_ERR_CUDA, cudaGetErrorString(e));
+}
