@@ -58,8 +58,10 @@ def config(world):
             "parallelism": f"independent batch shards x{world} (t % N == rank)",
             "l2": "inputs larger than L2: 153.6 MB dataset (> 126 MB L2), and every step streams 152.6 MB of "
                   "containers + 152.6 MB of decoded rows through it",
-            "pipeline": "native optb_pipeline: SBS draws for the next steps on a side stream overlap "
-                        "encode/decode of the current step (steps_per_draw epochs per sampler call)"}
+            "pipeline": "native optb_pipeline: SBS draws for the next steps on a side stream overlap the "
+                        "current step's gather-encode + decode, one optb_roundtrip_dev launch per step (every warp "
+                        "encodes its tiles into the HBM container stream, then decodes them back in write order); "
+                        "steps_per_draw epochs per sampler call"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -304,6 +306,10 @@ def main():
     ap.add_argument("--sharded-steps", type=int, default=3,
                     help="N > 1 only: steps of the dataset-sharded (all-to-all) variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-steps", type=int, default=50,
+                    help="steps of the same pipeline with separate encode / decode launches (per-kernel view)")
+    ap.add_argument("--split-kernels", action="store_true",
+                    help="headline with separate encode / decode launches instead of the fused round trip")
     ap.add_argument("--steps-per-draw", type=int, default=2,
                     help="epochs of SBS draws computed per sampler call (amortises its fixed cost)")
     args = ap.parse_args()
@@ -350,7 +356,8 @@ def main():
     # The native E-D pipeline (optb_pipeline_*): per step, SBS draws of step
     # k+1 on a side stream overlap gather-encode + decode of step k.
     pipe = Pipeline(cur, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
-                    device=local, record_timings=True, steps_per_draw=args.steps_per_draw)
+                    device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
+                    split_kernels=args.split_kernels)
     L = pipe.layout
 
     with torch.cuda.stream(stream):
@@ -395,7 +402,12 @@ def main():
     enc_bytes = rows * P + cont_bytes + rows * 8  # gathered rows + containers + row index
     dec_bytes = cont_bytes + rows * P
     peak, peak_kind = measured_peak()
-    if enc_ms >= dec_ms:
+    fused = pipe.fused
+    if fused and statistics.mean(t_dec) > 0.005:
+        raise RuntimeError("pipeline reported separate decode launches on the fused path")
+    if fused:  # one optb_roundtrip_dev launch per step: encode + decode bytes
+        kname, kms, kbytes = "k_roundtrip_vec<exact128,u8>", enc_ms, enc_bytes + dec_bytes
+    elif enc_ms >= dec_ms:
         kname, kms, kbytes = "k_encode_vec<exact128>", enc_ms, enc_bytes
     else:
         kname, kms, kbytes = "k_decode_vec<exact128,u8>", dec_ms, dec_bytes
@@ -408,11 +420,42 @@ def main():
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
                 "algorithmic_bytes_per_launch": kbytes,
                 "host_enqueue_us_per_step": round(t_enqueue / args.steps * 1e6, 1),
-                "kernels_ms": {"sbs_side_stream": round(statistics.mean(t_sbs), 4), "encode": round(enc_ms, 4),
-                               "decode": round(dec_ms, 4)},
-                "encode_gbs": round(enc_bytes / (enc_ms / 1e3) / 1e9, 1),
-                "decode_gbs": round(dec_bytes / (dec_ms / 1e3) / 1e9, 1),
-                "step_gbs": round((enc_bytes + dec_bytes) / (ms / 1e3) / 1e9, 1)}
+                "kernels_ms": ({"sbs_side_stream": round(statistics.mean(t_sbs), 4),
+                                "roundtrip": round(enc_ms, 4)} if fused else
+                               {"sbs_side_stream": round(statistics.mean(t_sbs), 4), "encode": round(enc_ms, 4),
+                                "decode": round(dec_ms, 4)}),
+                "step_gbs": round((enc_bytes + dec_bytes) / (ms / 1e3) / 1e9, 1),
+                "step_frac": round((enc_bytes + dec_bytes) / (ms / 1e3) / 1e9 / peak, 4)}
+    if not fused:
+        roofline["encode_gbs"] = round(enc_bytes / (enc_ms / 1e3) / 1e9, 1)
+        roofline["decode_gbs"] = round(dec_bytes / (dec_ms / 1e3) / 1e9, 1)
+    # the same pipeline with separate encode / decode launches per step
+    # (optb_encode_dev + optb_decode_dev), for the per-kernel view
+    split = None
+    if fused and args.split_steps > 0:
+        with torch.cuda.stream(stream):
+            cur5 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                   device=local)
+            pipe5 = Pipeline(cur5, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank,
+                             n_shards=world, device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
+                             split_kernels=True)
+            for _ in range(args.warmup):
+                pipe5.step(out, stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.split_steps):
+                pipe5.step(out, stream)
+            e1.record(stream)
+            e1.synchronize()
+            sms_ = e0.elapsed_time(e1) / args.split_steps
+            tim5 = [pipe5.timings(k) for k in range(max(args.warmup, args.warmup + args.split_steps - 60),
+                                                     args.warmup + args.split_steps)]
+            pipe5.close()
+        e5, d5 = statistics.mean(t[1] for t in tim5), statistics.mean(t[2] for t in tim5)
+        split = {"ms_per_step": round(sms_, 4), "value": round(images_per_step / (sms_ / 1e3), 1),
+                 "encode_ms": round(e5, 4), "decode_ms": round(d5, 4),
+                 "encode_gbs": round(enc_bytes / (e5 / 1e3) / 1e9, 1),
+                 "decode_gbs": round(dec_bytes / (d5 / 1e3) / 1e9, 1)}
 
     # e2e: host buffers in and out, every step.  The epoch's input rows live
     # in pinned host memory; each step uploads the dataset epoch with one bulk
@@ -426,6 +469,15 @@ def main():
     if args.e2e_steps > 0:
         e2e, e2e_zc = run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, world, rows,
                               images_per_step, red_dev)
+        # this box's pinned-memory PCIe bandwidth (same-size copies, same
+        # run): the e2e leg is transfer-bound, so its bound is what these allow
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import pcie_probe
+        pc = pcie_probe.measure(torch, BATCH * BATCHES_PER_STEP * P)
+        bound_ms = max(e2e["h2d_bytes_per_step"] / pc["h2d_gbs"], e2e["d2h_bytes_per_step"] / pc["d2h_gbs"],
+                       (e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]) / pc["bidir_gbs"]) / 1e6
+        e2e["pcie"] = dict(pc, bound_ms_per_step=round(bound_ms, 3),
+                           frac_of_pcie_bound=round(bound_ms / e2e["ms_per_step"], 3))
     # N > 1: the optional dataset-sharded variant (each rank holds 1/N of the
     # dataset; drawn rows cross ranks in one all-to-all per step) -- exchange
     # bound, reported separately from the headline.
@@ -467,7 +519,8 @@ def main():
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": config(world),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_zero_copy": e2e_zc,
+                "roofline": roofline, "split_kernels": split, "cpu_baseline": cpu, "e2e": e2e,
+                "e2e_zero_copy": e2e_zc,
                 "sharded_dataset": sharded, "clocks": clk.summary(),
                 "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 4)}
         print(json.dumps(line), flush=True)

@@ -144,6 +144,16 @@ int optb_encode_dev(optb_ctx* ctx, const optb_layout* L, const uint8_t* images,
 int optb_decode_dev(optb_ctx* ctx, const optb_layout* L, const void* containers,
                     const uint8_t* offsets, const optb_epilogue* E, void* out, void* stream);
 
+/* optb_encode_dev followed by optb_decode_dev of the same stream (same
+ * results, containers and offsets materialised as by the two calls): one
+ * persistent launch for the exact and f64 modes on the vector path (each
+ * warp encodes its tiles, then decodes them back from HBM), otherwise the two
+ * launches.  The E-D pipeline step (pipeline.cpp:197-216 encode +
+ * runner.cpp:292-309 decode) uses it. */
+int optb_roundtrip_dev(optb_ctx* ctx, const optb_layout* L, const uint8_t* images,
+                       uint64_t row_stride, const int64_t* row_index, void* containers,
+                       uint8_t* offsets, const optb_epilogue* E, void* out, void* stream);
+
 /* ---------------------------------------------------------------- codec, host
  * Same operations on host buffers (images [rows][P] contiguous; containers /
  * offsets / decoded in the layouts above).  H2D and D2H run on side streams
@@ -270,6 +280,8 @@ typedef struct optb_pipeline_desc {
   int32_t record_timings;  /* keep per-step CUDA events for optb_pipeline_timings */
   uint32_t steps_per_draw; /* SBS calls cover this many steps (0 = 1): amortises the
                               per-call reshuffle work when steps are short */
+  uint32_t split_kernels;  /* 1: separate encode and decode launches per step;
+                              0: optb_roundtrip_dev (one launch where it applies) */
 } optb_pipeline_desc;
 
 int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* desc, optb_pipeline** out);
@@ -284,7 +296,8 @@ int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** e
 /* The pipeline's container planes (valid for the last enqueued step). */
 const void* optb_pipeline_containers(const optb_pipeline* p);
 /* Device-timed durations (ms) of a completed step (last 64 steps): its SBS
- * draws (side stream), its gather-encode and its decode. */
+ * draws (side stream), its gather-encode and its decode (for a fused
+ * round-trip step: the whole launch in enc_ms and 0 in dec_ms). */
 int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, float* enc_ms,
                           float* dec_ms);
 void optb_pipeline_destroy(optb_pipeline* p);

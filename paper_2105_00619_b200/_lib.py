@@ -49,7 +49,7 @@ class PipelineDesc(ct.Structure):
     """optb_pipeline_desc"""
     _fields_ = [("layout", Layout), ("dataset", vp), ("row_stride", ct.c_uint64), ("sbs", vp),
                 ("shard", ct.c_uint32), ("n_shards", ct.c_uint32), ("epilogue", Epilogue),
-                ("record_timings", ct.c_int32), ("steps_per_draw", ct.c_uint32)]
+                ("record_timings", ct.c_int32), ("steps_per_draw", ct.c_uint32), ("split_kernels", ct.c_uint32)]
 
 
 LP = ct.POINTER(Layout)
@@ -79,6 +79,7 @@ SIGNATURES = {
     "optb_ctx_launches": (ct.c_uint64, [vp]),
     "optb_encode_dev": (ct.c_int, [vp, LP, vp, ct.c_uint64, vp, vp, vp, vp]),
     "optb_decode_dev": (ct.c_int, [vp, LP, vp, vp, EP, vp, vp]),
+    "optb_roundtrip_dev": (ct.c_int, [vp, LP, vp, ct.c_uint64, vp, vp, vp, EP, vp, vp]),
     "optb_encode_host": (ct.c_int, [vp, LP, vp, vp, vp]),
     "optb_decode_host": (ct.c_int, [vp, LP, vp, vp, EP, vp]),
     "optb_sbs_plan": (ct.c_int, [f64p, ct.c_uint64, ct.c_uint64, u64p]),

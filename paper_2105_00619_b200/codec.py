@@ -269,6 +269,20 @@ def decode_dev(L: Layout, containers, out, offsets=None, scale: float = 1.0, cla
                               ct.byref(E), _dptr(out), _stream(stream, dev)))
 
 
+def roundtrip_dev(L: Layout, images, containers, out, offsets=None, row_index=None, scale: float = 1.0,
+                  class_scale=None, class_bias=None, row_class=None, stream=None):
+    """encode_dev then decode_dev of the same stream (optb_roundtrip_dev): one
+    fused launch for the exact / f64 modes, the two launches otherwise; the
+    containers (and offsets) are materialised exactly as by the two calls."""
+    import torch
+    dt = {torch.uint8: U8, torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}[out.dtype]
+    dev = out.device.index or 0
+    E = Epilogue(dt, float(scale), _dptr(class_scale), _dptr(class_bias), _dptr(row_class), out.stride(0))
+    check(lib.optb_roundtrip_dev(_lib.context(dev), ct.byref(L), _dptr(images), images.stride(0),
+                                 _dptr(row_index), _dptr(containers), _dptr(offsets), ct.byref(E), _dptr(out),
+                                 _stream(stream, dev)))
+
+
 def sync(device: int = 0, stream=None) -> None:
     """Synchronise and raise any latched device-side FormatError (optb_ctx_sync)."""
     check(lib.optb_ctx_sync(_lib.context(device), _stream(stream, device)))

@@ -361,6 +361,38 @@ int optb_decode_dev(optb_ctx* c, const optb_layout* L, const void* containers,
   return OPTB_OK;
 }
 
+int optb_roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
+                       const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E,
+                       void* out, void* stream) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  st = check_decode_layout(L);
+  if (st) return st;
+  st = check_epilogue(E);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!images || !containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "roundtrip: null buffer");
+  if (row_stride == 0) row_stride = L->pixels;
+  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
+  const Epi ep = make_epi(E, L->pixels);
+  if (ep.row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "decode: out_row_stride < pixels");
+  const Geom g = make_geom(L);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_roundtrip(g, images, row_stride, row_index, containers, ep, out, c->d_err, s, c->sms,
+                                   &c->launches);
+  if (e == cudaErrorNotSupported) {
+    e = launch_encode(g, images, row_stride, row_index, containers, offsets, s, c->sms, &c->launches);
+    if (e != cudaSuccess) return cuda_err(e, "encode launch");
+    e = launch_decode(g, containers, offsets, ep, out, c->d_err, s, c->sms, &c->launches);
+    if (e != cudaSuccess) return cuda_err(e, "decode launch");
+    return OPTB_OK;
+  }
+  if (e != cudaSuccess) return cuda_err(e, "roundtrip launch");
+  return OPTB_OK;
+}
+
 int optb_synth_pixels_dev(optb_ctx* c, uint64_t seed, uint64_t first_row, uint64_t n_rows,
                           uint64_t pixels, uint8_t* out, uint64_t row_stride, void* stream) {
   if (!c || !out) return set_err(OPTB_ERR_ARG, "synth: null");

@@ -8,22 +8,31 @@
 //   SURVEY App. B).
 //
 // Kernel families:
-//   k_encode_vec<MODE>    K1/K3/K5: gathered rows by cp.async into a 3-stage
+//   k_encode_vec<MODE>    K1/K3/K5: gathered rows by cp.async into a 2-stage
 //                         warp-private smem ring, 16-pixel x 16-image register
 //                         byte transpose (PRMT), per-mode word build (exact
 //                         bytes, lossless 7-bit compaction + 16-bit parity
 //                         stores, f64 ordered binary64 adds), XOR-swizzled
 //                         staging, fully coalesced 128/64-bit container stores.
-//   k_decode_vec<MODE,O>  K2/K4/K6: container words (+ parity) by cp.async
-//                         into swizzled slots, per-mode range check and
-//                         unpack, transpose, u8 rows stored directly or through
-//                         a u8 tile with the fused fp32/fp16/bf16 epilogue.
+//   k_decode_vec<MODE,O,TMA>  K2/K4/K6: container words by one 2D TMA tensor
+//                         load per tile (128-byte hardware swizzle, mbarrier
+//                         completion; exact / f64 modes) or by cp.async into
+//                         XOR-swizzled slots (+ lossless parity bits), per-mode
+//                         range check and unpack, transpose, u8 rows stored
+//                         directly or through a u8 tile with the fused
+//                         fp32/fp16/bf16 epilogue.
+//   k_roundtrip_vec<MODE,O>  K1+K2 in one persistent launch (optb_roundtrip_dev,
+//                         the E-D pipeline step): each warp encodes its tiles
+//                         into HBM, then decodes the same tiles back.
 //   k_{en,de}code_generic any P / stride / alignment: one pixel per lane,
 //                         warp ballots for the parity plane.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "internal.h"
 
@@ -34,7 +43,7 @@ namespace {
 #define OPTB_VEC_WARPS 8
 #endif
 #ifndef OPTB_VEC_STAGES
-#define OPTB_VEC_STAGES 3
+#define OPTB_VEC_STAGES 2
 #endif
 constexpr int kWarps = OPTB_VEC_WARPS;  // warps per CTA for the vector kernels
 constexpr int kThreads = kWarps * 32;
@@ -112,6 +121,60 @@ __device__ __forceinline__ ChunkPos chunk_pos(const Geom& g, uint64_t k) {
   const uint64_t left = g.B - first;
   ChunkPos c;
   c.r0 = b * g.B + first;
+  c.n = left < g.per_chunk ? static_cast<uint32_t>(left) : g.per_chunk;
+  return c;
+}
+
+// A lane's work item t = k*G + gi (chunk k = b*cpb + j, G = items per chunk)
+// along its grid-stride sequence.  The hot loops advance it with adds and
+// compares only; the 64-bit divisions happen once, at kernel start.
+struct Walk {
+  uint64_t t, k, gi, b;
+  uint32_t j;
+};
+struct WalkStep {
+  uint64_t dt, dk, dgi, db;
+  uint32_t dj;
+};
+__device__ __forceinline__ Walk walk_at(const Geom& g, uint64_t G, uint64_t t) {
+  Walk w;
+  w.t = t;
+  w.k = t / G;
+  w.gi = t - w.k * G;
+  w.b = w.k / g.cpb;
+  w.j = static_cast<uint32_t>(w.k - w.b * g.cpb);
+  return w;
+}
+__device__ __forceinline__ WalkStep walk_step(const Geom& g, uint64_t G, uint64_t dt) {
+  WalkStep s;
+  s.dt = dt;
+  s.dk = dt / G;
+  s.dgi = dt - s.dk * G;
+  s.db = s.dk / g.cpb;
+  s.dj = static_cast<uint32_t>(s.dk - s.db * g.cpb);
+  return s;
+}
+__device__ __forceinline__ void walk_advance(Walk& w, const WalkStep& s, const Geom& g, uint64_t G) {
+  w.t += s.dt;
+  w.gi += s.dgi;
+  w.k += s.dk;
+  w.b += s.db;
+  w.j += s.dj;
+  if (w.gi >= G) {  // gi, dgi < G: at most one carry
+    w.gi -= G;
+    ++w.k;
+    ++w.j;
+  }
+  if (w.j >= g.cpb) {  // j, dj < cpb, carry <= 1: at most one wrap
+    w.j -= g.cpb;
+    ++w.b;
+  }
+}
+__device__ __forceinline__ ChunkPos walk_chunk(const Geom& g, const Walk& w) {
+  const uint64_t first = static_cast<uint64_t>(w.j) * g.per_chunk;
+  const uint64_t left = g.B - first;
+  ChunkPos c;
+  c.r0 = w.b * g.B + first;
   c.n = left < g.per_chunk ? static_cast<uint32_t>(left) : g.per_chunk;
   return c;
 }
@@ -239,6 +302,40 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ------------------------------------------------------------------ TMA / mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n OPTB_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra OPTB_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+// 2D tensor-map tile load into shared memory, completing on mbarrier `b`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(c0), "r"(c1), "r"(smem_u32(b))
+      : "memory");
+}
+// order this thread's generic-proxy accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Work items: 16 consecutive pixels of one chunk, linear in (chunk, group),
 // so a warp's 32 items cover 32*16*WC contiguous container bytes.  Each warp
 // runs a kStages-deep cp.async pipeline over its tiles (one tile = the warp's
@@ -311,13 +408,10 @@ __device__ __forceinline__ void f64_peel16(double acc, uint32_t (&b)[4]) {
 
 // Out-of-line so the rare lossy >= 2^64 case does not bloat the unrolled
 // per-pixel loops of the decode kernel.
-__device__ __noinline__ void f64_peel_big(double acc, uint32_t* b) {
+__device__ __noinline__ uint4 f64_peel_big(double acc) {
   uint32_t t[4];
   f64_peel16(acc, t);
-  b[0] = t[0];
-  b[1] = t[1];
-  b[2] = t[2];
-  b[3] = t[3];
+  return make_uint4(t[0], t[1], t[2], t[3]);
 }
 
 __device__ __forceinline__ uint64_t compact7(uint64_t x) {  // 8 byte lanes -> 8 x 7-bit fields
@@ -335,26 +429,31 @@ __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> byte
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_encode_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
-                 const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont,
-                 uint8_t* __restrict__ offsets) {
+__device__ __forceinline__ void encode_body(const Geom& g, const uint8_t* __restrict__ images, uint64_t row_stride,
+                                            const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont,
+                                            uint8_t* __restrict__ offsets, uint8_t* smem_base) {
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_raw + warp * kStages * S::ENC_SLOT;
+  uint8_t* ring = smem_base + warp * kStages * S::ENC_SLOT;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
   const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
 
+  const WalkStep step = walk_step(g, G, stride);
   // Dataset row ids of a tile are fetched one stage before its copies are
   // issued, so the dependent index loads never stall the pipeline.
-  auto fetch_rows = [&](uint64_t base, uint32_t (&rows)[S::NI]) {
-    const uint64_t t = base + lane;
-    if (base < items && t < items) {
-      const ChunkPos c = chunk_pos(g, t / G);
+  Walk wf = walk_at(g, G, first + lane);  // next tile to fetch row ids for
+  uint32_t rows[S::NI];
+  uint64_t pend_gi = 0;  // group and image count of the fetched tile
+  uint32_t pend_n = 0;
+  auto fetch_rows = [&]() {
+    pend_n = 0;
+    if (wf.t < items) {
+      const ChunkPos c = walk_chunk(g, wf);
+      pend_n = c.n;
+      pend_gi = wf.gi;
 #pragma unroll
       for (int i = 0; i < S::NI; ++i) {
         const uint64_t r = c.r0 + i;
@@ -363,44 +462,36 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
                       : 0u;
       }
     }
+    walk_advance(wf, step, g, G);
   };
-  auto issue = [&](uint64_t base, int stage, const uint32_t (&rows)[S::NI]) {
-    const uint64_t t = base + lane;
-    if (base < items && t < items) {
-      const uint64_t k = t / G;
-      const uint64_t gi = t - k * G;
-      const uint32_t n = chunk_pos(g, k).n;
-      uint8_t* slot = ring + stage * S::ENC_SLOT;
+  auto issue = [&](int stage) {
+    uint8_t* slot = ring + stage * S::ENC_SLOT;
 #pragma unroll
-      for (int i = 0; i < S::NI; ++i)
-        if (i < static_cast<int>(n))
-          cp_async16(slot + i * 512 + lane * 16, images + static_cast<uint64_t>(rows[i]) * row_stride + gi * 16);
-    }
+    for (int i = 0; i < S::NI; ++i)
+      if (i < static_cast<int>(pend_n))
+        cp_async16(slot + i * 512 + lane * 16, images + static_cast<uint64_t>(rows[i]) * row_stride + pend_gi * 16);
     cp_async_commit();
   };
 
-  uint32_t rows[S::NI];
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
-    fetch_rows(first + s * stride, rows);
-    issue(first + s * stride, s, rows);
+    fetch_rows();
+    issue(s);
   }
-  fetch_rows(first + (kStages - 1) * stride, rows);
+  fetch_rows();
   int stage = 0;
+  Walk wc = walk_at(g, G, first + lane);  // the tile being transposed
   for (uint64_t base = first; base < items; base += stride) {
-    issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages, rows);
-    fetch_rows(base + kStages * stride, rows);  // consumed by the next iteration's issue
+    issue((stage + kStages - 1) % kStages);
+    fetch_rows();  // consumed by the next iteration's issue
     cp_async_wait<kStages - 1>();
     __syncwarp();
     uint8_t* slot = ring + stage * S::ENC_SLOT;
-    const uint64_t t = base + lane;
+    const uint64_t t = wc.t;
     uint32_t n = 0;
-    uint64_t k = 0, gi = 0;
-    if (t < items) {
-      k = t / G;
-      gi = t - k * G;
-      n = chunk_pos(g, k).n;
-    }
+    const uint64_t k = wc.k, gi = wc.gi;
+    if (t < items) n = walk_chunk(g, wc).n;
+    walk_advance(wc, step, g, G);
     uint32_t m[16][4];
     uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};  // images 16, 17 (lossless128)
 #pragma unroll
@@ -502,52 +593,104 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
   cp_async_wait<0>();
 }
 
-// ------------------------------------------------------------------ K2 / K4
-// Decode.  Container words (and, lossless, the tile's parity bits) arrive by
-// cp.async straight into the swizzled slot; each pixel's word is range
-// checked, lossless fields are expanded back to byte lanes, the 16x16
-// transpose gives 16 pixels of every image per lane, lossless rows get
-// (field << 1) | parity; u8 rows are stored directly (each warp instruction
-// writes 512 contiguous bytes of one row); float outputs go through a u8
-// tile in the same slot so that the epilogue stores are coalesced too.
-template <int MODE, int O>
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_decode_vec(Geom g, const uint8_t* __restrict__ cont, const uint8_t* __restrict__ offsets, Epi e,
-                 void* __restrict__ out, DevError* err) {
+    k_encode_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
+                 const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont,
+                 uint8_t* __restrict__ offsets) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  encode_body<MODE>(g, images, row_stride, row_index, cont, offsets, smem_raw);
+}
+
+// ------------------------------------------------------------------ K2 / K4
+// Decode.  Container words (and, lossless, the tile's parity bits) arrive in
+// a warp-private ring slot, either by cp.async straight into the XOR-swizzled
+// slot (any mode) or, for the exact and f64 modes, as ONE 2D TMA tensor load
+// per tile (the tile's 512*WC contiguous bytes as a [rows][128 B] box with the
+// hardware's 128-byte swizzle, completion on a per-stage mbarrier).  Each
+// pixel's word is range checked, lossless fields are expanded back to byte
+// lanes, the 16x16 transpose gives 16 pixels of every image per lane,
+// lossless rows get (field << 1) | parity; u8 rows are stored directly (each
+// warp instruction writes 512 contiguous bytes of one row); float outputs go
+// through a u8 tile in the same slot so that the epilogue stores are
+// coalesced too.
+//
+// TMA slot layout (SWIZZLE_128B, slot 1024-byte aligned): byte b of the tile
+// sits at row r = b / 128, 16-byte chunk c = (b % 128) / 16, stored at
+// r*128 + ((c ^ (r & 7)) << 4) + b % 16.  Lane L's word p is tile byte
+// (16L + p) * WC.  The read order below keeps the 8 lanes of each
+// quarter-warp on 8 distinct chunks (conflict-free):
+//   WC = 16: r = 2L + p/8, c = p%8; at step j lane L reads p = j and j+8,
+//            lanes with L & 4 the high half first;
+//   WC = 8 : r = L, c = p/2; at step c lane L reads words 2c, 2c+1.
+template <int MODE>
+struct DecSlot {
+  static constexpr int RAW = VecMode<MODE>::DEC_SLOT;
+  static constexpr int TMA = (RAW + 1023) / 1024 * 1024;
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  const uint32_t a = smem_u32(p);
+  return p + (((a + 1023u) & ~1023u) - a);
+}
+
+template <int MODE, int O, bool TMA>
+__device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom& g, const uint8_t* __restrict__ cont,
+                                            const uint8_t* __restrict__ offsets, const Epi& e,
+                                            void* __restrict__ out, DevError* err, uint8_t* smem_base,
+                                            uint64_t* bars) {
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  constexpr int SLOT = TMA ? DecSlot<MODE>::TMA : DecSlot<MODE>::RAW;
+  static_assert(!TMA || !S::OFFS, "TMA decode covers the exact and f64 modes");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_raw + warp * kStages * S::DEC_SLOT;
+  uint8_t* ring = smem_base + warp * kStages * SLOT;
+  uint64_t* bar = bars + warp * kStages;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
   const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
   const uint64_t ostride = e.row_stride;
+  if constexpr (TMA) {
+    if (lane == 0)
+      for (int st = 0; st < kStages; ++st) mbar_init(bar + st, 1);
+    fence_mbar_init();
+    __syncwarp();
+  }
 
+  const WalkStep step = walk_step(g, G, stride);
+  Walk wi = walk_at(g, G, first + lane);  // next tile to issue (parity planes)
+  Walk wc = wi;                           // the tile being decoded
   auto issue = [&](uint64_t base, int stage) {
     if (base < items) {
-      const uint8_t* src = cont + base * 16 * WC;
-      uint8_t* slot = ring + stage * S::DEC_SLOT;
+      uint8_t* slot = ring + stage * SLOT;
+      if constexpr (TMA) {
+        if (lane == 0) {
+          mbar_expect_tx(bar + stage, 512 * WC);
+          tma_load_2d(slot, cmap, 0, static_cast<int>((base * 16 * WC) >> 7), bar + stage);
+        }
+      } else {
+        const uint8_t* src = cont + base * 16 * WC;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int W = q * 32 + lane, L = W >> 4, p = W & 15;
-        if (base + L < items) {
-          const int sl = p ^ (L & S::SW);
-          if constexpr (WC == 16) {
-            cp_async16(slot + (L * 16 + sl) * 16, src + W * 16);
-          } else {
-            cp_async8(slot + (L * 16 + sl) * 8, src + W * 8);
+        for (int q = 0; q < 16; ++q) {
+          const int W = q * 32 + lane, L = W >> 4, p = W & 15;
+          if (base + L < items) {
+            const int sl = p ^ (L & S::SW);
+            if constexpr (WC == 16) {
+              cp_async16(slot + (L * 16 + sl) * 16, src + W * 16);
+            } else {
+              cp_async8(slot + (L * 16 + sl) * 8, src + W * 8);
+            }
           }
         }
       }
       if constexpr (S::OFFS) {
         // parity bits of lane pairs (4 bytes, 4-aligned as P % 32 == 0)
-        const uint64_t t = base + lane;
+        const uint64_t t = wi.t;
         if ((lane & 1) == 0 && t < items) {
-          const uint64_t k = t / G, gi = t - k * G;
-          const uint32_t n = chunk_pos(g, k).n;
-          const bool pair = (t + 1 < items) && ((t + 1) / G == k);
+          const uint64_t k = wi.k, gi = wi.gi;
+          const uint32_t n = walk_chunk(g, wi).n;
+          const bool pair = (t + 1 < items) && (gi + 1 < G);
 #pragma unroll
           for (int i = 0; i < S::NI; ++i) {
             if (i < static_cast<int>(n)) {
@@ -563,41 +706,80 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
         }
       }
     }
-    cp_async_commit();
+    if constexpr (!TMA) cp_async_commit();
+    if constexpr (S::OFFS) walk_advance(wi, step, g, G);
   };
 
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) issue(first + s * stride, s);
   int stage = 0;
+  uint32_t phase = 0;
   for (uint64_t base = first; base < items; base += stride) {
     issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
-    cp_async_wait<kStages - 1>();
-    __syncwarp();
-    uint8_t* slot = ring + stage * S::DEC_SLOT;
-    const uint64_t t = base + lane;
-    const bool valid = t < items;
-    uint64_t k = 0, gi = 0;
-    ChunkPos c{0, 0};
-    if (valid) {
-      k = t / G;
-      gi = t - k * G;
-      c = chunk_pos(g, k);
+    if constexpr (TMA) {
+      mbar_wait(bar + stage, phase);
+    } else {
+      cp_async_wait<kStages - 1>();
+      __syncwarp();
     }
+    uint8_t* slot = ring + stage * SLOT;
+    const bool valid = wc.t < items;
+    const uint64_t k = wc.k, gi = wc.gi;
+    ChunkPos c{0, 0};
+    if (valid) c = walk_chunk(g, wc);
+    walk_advance(wc, step, g, G);
+    // raw words: m[p] = word of pixel 16*gi + p (low 8 bytes in [0..1] for WC 8)
     uint32_t m[16][4];
+    if constexpr (TMA && WC == 16) {
+      const bool hi = (lane >> 2) & 1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int ra = 2 * lane + (hi ? 1 : 0), rb = 2 * lane + (hi ? 0 : 1);
+        const uint4 a = *reinterpret_cast<const uint4*>(slot + ra * 128 + ((j ^ (ra & 7)) << 4));
+        const uint4 b = *reinterpret_cast<const uint4*>(slot + rb * 128 + ((j ^ (rb & 7)) << 4));
+        m[j][0] = hi ? b.x : a.x;
+        m[j][1] = hi ? b.y : a.y;
+        m[j][2] = hi ? b.z : a.z;
+        m[j][3] = hi ? b.w : a.w;
+        m[j + 8][0] = hi ? a.x : b.x;
+        m[j + 8][1] = hi ? a.y : b.y;
+        m[j + 8][2] = hi ? a.z : b.z;
+        m[j + 8][3] = hi ? a.w : b.w;
+      }
+    } else if constexpr (TMA) {
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const uint4 v = *reinterpret_cast<const uint4*>(slot + lane * 128 + ((cc ^ (lane & 7)) << 4));
+        m[2 * cc][0] = v.x;
+        m[2 * cc][1] = v.y;
+        m[2 * cc + 1][0] = v.z;
+        m[2 * cc + 1][1] = v.w;
+        m[2 * cc][2] = m[2 * cc][3] = m[2 * cc + 1][2] = m[2 * cc + 1][3] = 0u;
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        const int sl = p ^ (lane & S::SW);
+        if constexpr (WC == 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
+          m[p][0] = v.x;
+          m[p][1] = v.y;
+          m[p][2] = v.z;
+          m[p][3] = v.w;
+        } else {
+          const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
+          m[p][0] = v.x;
+          m[p][1] = v.y;
+          m[p][2] = m[p][3] = 0u;
+        }
+      }
+    }
     uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
-      const int sl = p ^ (lane & S::SW);
-      uint64_t w0, w1 = 0;
-      if constexpr (WC == 16) {
-        const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
-        w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
-        w1 = (static_cast<uint64_t>(v.w) << 32) | v.z;
-      } else {
-        const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
-        w0 = (static_cast<uint64_t>(v.y) << 32) | v.x;
-      }
+      const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
+      const uint64_t w1 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
       if constexpr (S::F64) {
         // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
         const double acc = __longlong_as_double(static_cast<long long>(w0));
@@ -608,7 +790,11 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
           m[p][1] = static_cast<uint32_t>(iacc >> 32);
           m[p][2] = m[p][3] = 0u;
         } else {
-          f64_peel_big(acc, m[p]);
+          const uint4 v = f64_peel_big(acc);
+          m[p][0] = v.x;
+          m[p][1] = v.y;
+          m[p][2] = v.z;
+          m[p][3] = v.w;
         }
       } else if constexpr (S::OFFS) {
         // range check (codec.cpp:189-194): bits >= 7n must be zero
@@ -628,11 +814,6 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
           x16[p >> 2] |= static_cast<uint32_t>((w1 >> 48) & 0x7Fu) << (8 * (p & 3));
           x17[p >> 2] |= static_cast<uint32_t>((w1 >> 55) & 0x7Fu) << (8 * (p & 3));
         }
-      } else {
-        m[p][0] = static_cast<uint32_t>(w0);
-        m[p][1] = static_cast<uint32_t>(w0 >> 32);
-        m[p][2] = static_cast<uint32_t>(w1);
-        m[p][3] = static_cast<uint32_t>(w1 >> 32);
       }
     }
     transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (fields for lossless)
@@ -710,11 +891,52 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
           }
         }
       }
+      // the slot's next fill is an async-proxy (TMA) write
+      if constexpr (TMA) fence_proxy_async_smem();
     }
     __syncwarp();
-    stage = (stage + 1) % kStages;
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
   }
-  cp_async_wait<0>();
+  if constexpr (!TMA) cp_async_wait<0>();
+}
+
+template <int MODE, int O, bool TMA>
+__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+    k_decode_vec(const __grid_constant__ CUtensorMap cmap, Geom g, const uint8_t* __restrict__ cont,
+                 const uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ uint64_t bars[TMA ? kWarps * kStages : 1];
+  decode_body<MODE, O, TMA>(&cmap, g, cont, offsets, e, out, err, TMA ? align1024(smem_raw) : smem_raw, bars);
+}
+
+// ------------------------------------------------------------------ K1+K2 fused
+// One step's round trip in one persistent launch (the E-D pipeline step,
+// pipeline.cpp:197-216 producer encode + runner.cpp:292-309 consumer decode):
+// every warp gather-encodes its tiles into the container stream in HBM, then
+// decodes the same tiles back -- in the order it wrote them, so by the time a
+// tile is read back the rest of the step's ~150 MB of traffic has gone
+// through L2 and the read is served by HBM like a separate decode launch.
+// No warp reads another warp's containers, so no grid-wide barrier is needed;
+// the kernel saves one launch's ramp-up and tail.  Exact and f64 modes (the
+// decode half reads each tile with one TMA tensor load).
+template <int MODE, int O>
+__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+    k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, const uint8_t* __restrict__ images,
+                    uint64_t row_stride, const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont, Epi e,
+                    void* __restrict__ out, DevError* err) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ uint64_t bars[kWarps * kStages];
+  uint8_t* base = align1024(smem_raw);
+  encode_body<MODE>(g, images, row_stride, row_index, cont, nullptr, base);
+  // this warp's container stores (generic proxy) before its TMA reads of
+  // them, and its staging writes before the TMA fills of the same slots
+  fence_proxy_async_global();
+  fence_proxy_async_smem();
+  __syncwarp();
+  decode_body<MODE, O, true>(&cmap, g, cont, nullptr, e, out, err, base, bars);
 }
 
 // ------------------------------------------------------------------ generic
@@ -964,21 +1186,107 @@ cudaError_t enc_vec(const Geom& g, const uint8_t* images, uint64_t row_stride, c
   return cudaGetLastError();
 }
 
-template <int MODE, int O>
-cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
-                    DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::DEC_SLOT;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// The container stream as a [bytes/128][128] u8 tensor, box = one decode tile
+// (512 words = 512*WC bytes), 128-byte hardware swizzle (see decode_body).
+bool container_map(CUtensorMap* m, const void* cont, uint64_t bytes, int wc) {
+  const EncodeTiledFn fn = encode_tiled();
+  if (!fn || bytes % 128 || bytes / 128 > 0x7fffffffull) return false;
+  const cuuint64_t dims[2] = {128, bytes / 128};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(512 * wc / 128)};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(cont), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// OPTB_DECODE_TMA=0 selects the cp.async decode (A/B measurements)
+bool tma_decode_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("OPTB_DECODE_TMA");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <int MODE, int O, bool TMA>
+cudaError_t dec_vec_launch(const CUtensorMap& cm, const Geom& g, const void* cont, const uint8_t* offs,
+                           const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  const size_t smem = TMA ? static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA + 1024
+                          : static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::RAW;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_decode_vec<MODE, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_decode_vec<MODE, O, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
   const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_decode_vec<MODE, O>, kThreads, smem, sms, items);
-  k_decode_vec<MODE, O><<<grid, kThreads, smem, s>>>(g, static_cast<const uint8_t*>(cont), offs, e, out, err);
+  const int grid = grid_for(k_decode_vec<MODE, O, TMA>, kThreads, smem, sms, items);
+  k_decode_vec<MODE, O, TMA><<<grid, kThreads, smem, s>>>(cm, g, static_cast<const uint8_t*>(cont), offs, e, out,
+                                                          err);
   ++*launches;
   return cudaGetLastError();
+}
+
+template <int MODE, int O>
+cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
+                    DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  CUtensorMap cm;
+  if constexpr (!VecMode<MODE>::OFFS) {
+    if (tma_decode_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
+      return dec_vec_launch<MODE, O, true>(cm, g, cont, offs, e, out, err, s, sms, launches);
+  }
+  memset(&cm, 0, sizeof cm);
+  return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
+}
+
+template <int MODE, int O>
+cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const uint8_t* images, uint64_t row_stride,
+                   const int64_t* idx, void* cont, const Epi& e, void* out, DevError* err, cudaStream_t s, int sms,
+                   uint64_t* launches) {
+  constexpr size_t enc = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
+  constexpr size_t dec = static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA;
+  constexpr size_t smem = (enc > dec ? enc : dec) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_roundtrip_vec<MODE, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  const uint64_t items = g.chunks * (g.P / 16);
+  const int grid = grid_for(k_roundtrip_vec<MODE, O>, kThreads, smem, sms, items);
+  k_roundtrip_vec<MODE, O><<<grid, kThreads, smem, s>>>(cm, g, images, row_stride, idx,
+                                                        static_cast<uint8_t*>(cont), e, out, err);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t rt_vec_any(const CUtensorMap& cm, const Geom& g, const uint8_t* images, uint64_t row_stride,
+                       const int64_t* idx, void* cont, const Epi& e, void* out, DevError* err, cudaStream_t s,
+                       int sms, uint64_t* l) {
+  switch (e.dtype) {
+    case OPTB_OUT_U8: return rt_vec<MODE, OPTB_OUT_U8>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_F32: return rt_vec<MODE, OPTB_OUT_F32>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_F16: return rt_vec<MODE, OPTB_OUT_F16>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
+    default: return rt_vec<MODE, OPTB_OUT_BF16>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
+  }
 }
 
 template <int MODE>
@@ -1060,6 +1368,26 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
     default:
       if (vec) return dec_vec_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms, launches);
       return dec_generic_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms, launches);
+  }
+}
+
+cudaError_t launch_roundtrip(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* row_index,
+                             void* containers, const Epi& e, void* out, DevError* err, cudaStream_t s, int sms,
+                             uint64_t* launches) {
+  const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
+  const bool vec = vec_ok(g) && row_stride % 16 == 0 && aligned16(images) && aligned16(containers) &&
+                   aligned16(out) && (e.row_stride * es) % 16 == 0;
+  const bool tma_mode = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128 || g.mode == OPTB_F64;
+  CUtensorMap cm;
+  if (!vec || !tma_mode || !tma_decode_enabled() || !container_map(&cm, containers, g.chunks * g.P * g.wc, g.wc))
+    return cudaErrorNotSupported;  // caller: separate encode + decode launches
+  switch (g.mode) {
+    case OPTB_EXACT64: return rt_vec_any<OPTB_EXACT64>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
+    case OPTB_EXACT128: return rt_vec_any<OPTB_EXACT128>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
+    default:
+      if (g.per_chunk <= 8)
+        return rt_vec_any<kF64Narrow>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
+      return rt_vec_any<OPTB_F64>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
   }
 }
 

@@ -7,9 +7,10 @@
 //   side stream   : SBS draws (optb_sbs_next_dev) of the next `steps_per_draw`
 //                   steps into draw buffer (call+1)%2, once the encodes of the
 //                   call that last used that buffer are done;
-//   caller stream : wait for the step's draws -> gather-encode
-//                   (optb_encode_dev) -> decode with the fused epilogue
-//                   (optb_decode_dev) into the caller's layer-input buffer.
+//   caller stream : wait for the step's draws -> gather-encode + decode with
+//                   the fused epilogue into the caller's layer-input buffer:
+//                   one optb_roundtrip_dev launch, or (split_kernels)
+//                   optb_encode_dev then optb_decode_dev.
 // Reference invariants kept: at most two live draw buffers (pipeline.hpp:19-20),
 // in-order delivery, and errors surfacing before the affected step is consumed
 // (device-side format errors latch in the context, optb_ctx_sync).
@@ -116,16 +117,24 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
     if (st) return st;
     if (cudaStreamWaitEvent(s, p->sbs_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
   }
-  if (p->timing) cudaEventRecord(p->t_e0[r], s);
-  st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
-                       p->cont, p->offs, s);
-  if (st) return st;
-  if (p->timing) cudaEventRecord(p->t_e1[r], s);
-  if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
   optb_epilogue e = p->d.epilogue;
   if (e.class_scale && !e.row_class) e.row_class = p->cls[b] + sub * p->rows;
-  st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
-  if (st) return st;
+  if (p->timing) cudaEventRecord(p->t_e0[r], s);
+  if (p->d.split_kernels) {
+    st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
+                         p->cont, p->offs, s);
+    if (st) return st;
+    if (p->timing) cudaEventRecord(p->t_e1[r], s);
+    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
+    st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
+    if (st) return st;
+  } else {
+    st = optb_roundtrip_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
+                            p->cont, p->offs, &e, out, s);
+    if (st) return st;
+    if (p->timing) cudaEventRecord(p->t_e1[r], s);
+    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
+  }
   if (p->timing) cudaEventRecord(p->t_d1[r], s);
   ++p->step;
   return OPTB_OK;

@@ -8,7 +8,9 @@
 Per step the native pipeline gathers the SBS-drawn rows of ``dataset`` (a
 CUDA tensor, or a pinned CPU tensor read zero-copy over PCIe), packs them into
 containers and decodes them into ``layer_input`` on the current stream, while
-the next step's draws run on a side stream.  One ctypes call per step.
+the next step's draws run on a side stream.  One ctypes call per step; the
+gather-encode and decode are one fused launch where the mode allows it
+(optb_roundtrip_dev), or two launches with ``split_kernels=True``.
 """
 from __future__ import annotations
 
@@ -23,7 +25,7 @@ class Pipeline:
     def __init__(self, cursor, dataset, mode, batch: int, batches_per_step: int, per_chunk=None,
                  shard: int = 0, n_shards: int = 1, out_dtype=None, scale: float = 1.0,
                  class_scale=None, class_bias=None, device: int = 0, record_timings: bool = False,
-                 steps_per_draw: int = 1):
+                 steps_per_draw: int = 1, split_kernels: bool = False):
         import torch
         from . import codec
         out_dtype = out_dtype or torch.uint8
@@ -38,9 +40,13 @@ class Pipeline:
         E = Epilogue(dt, float(scale), None if class_scale is None else ct.c_void_p(class_scale.data_ptr()),
                      None if class_bias is None else ct.c_void_p(class_bias.data_ptr()), None, 0)
         desc = PipelineDesc(self.layout, ct.c_void_p(dataset.data_ptr()), dataset.stride(0), cursor._h, shard,
-                            n_shards, E, 1 if record_timings else 0, steps_per_draw)
+                            n_shards, E, 1 if record_timings else 0, steps_per_draw, 1 if split_kernels else 0)
         self._h = ct.c_void_p()
         check(lib.optb_pipeline_create(_lib.context(device), ct.byref(desc), ct.byref(self._h)))
+        # one fused launch per step (optb_roundtrip_dev) for the exact / f64
+        # modes on the vector path; the library falls back to two launches
+        self.fused = (not split_kernels and int(mode) in (0, 1, 2) and P % 16 == 0 and dataset.stride(0) % 16 == 0
+                      and dataset.data_ptr() % 16 == 0)
         self.steps = 0
 
     def step(self, out, stream=None):

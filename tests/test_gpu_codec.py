@@ -202,6 +202,63 @@ def test_stream_parity_vs_oracle(pkg, oracle_mod, torch_cuda, mode, per_chunk, P
     _stream_case(pkg, torch_cuda, oracle_mod, mode, per_chunk, P, B, nb, rng, gather=False)
 
 
+@pytest.mark.parametrize("mode,per_chunk,P,B,nb", [
+    (1, 16, 3072, 512, 2),     # C2 shape, exact128 (fused launch)
+    (0, 8, 3072, 128, 3),      # C1 exact64 (fused)
+    (1, 16, 3072, 100, 3),     # partial last chunk, partial last tile
+    (0, 5, 48, 37, 5),         # tiny P, per_chunk < capacity
+    (2, 6, 3072, 256, 1),      # f64 narrow (fused)
+    (2, 16, 3072, 64, 2),      # f64 lossy (fused, 16-image variant)
+    (1, 16, 768, 1000, 1),     # items not a multiple of the warp tile
+    (3, 9, 3072, 512, 1),      # lossless: separate launches
+    (1, 16, 108, 40, 2),       # generic path: separate launches
+])
+@pytest.mark.parametrize("dtype", ["uint8", "float32", "bfloat16"])
+def test_roundtrip_dev_vs_oracle(pkg, oracle_mod, torch_cuda, mode, per_chunk, P, B, nb, dtype):
+    """optb_roundtrip_dev (one launch where it applies) == oracle encode_stream
+    + decode_stream: containers, parity planes and the decoded layer input."""
+    torch, C, O = torch_cuda, pkg.codec, oracle_mod
+    rng = np.random.default_rng(mode * 31 + per_chunk + P + B + nb)
+    n_ds = max(B * nb // 2, 1)
+    ds = rng.integers(0, 256, size=(n_ds, P), dtype=np.uint8)
+    idx = rng.integers(0, n_ds, size=B * nb).astype(np.int64)
+    L = C.layout(mode, per_chunk, P, B, nb)
+    cont, offs = C.alloc_stream(L)
+    dt = getattr(torch, dtype)
+    out = torch.empty((B * nb, P), dtype=dt, device="cuda")
+    C.roundtrip_dev(L, torch.from_numpy(ds).cuda(), cont, out, offsets=offs, row_index=torch.from_numpy(idx).cuda(),
+                    scale=float(SCALE) if dtype != "uint8" else 1.0)
+    C.sync()
+    rc, ro = O.encode_stream(ds, idx, mode, per_chunk, B, nb)
+    assert np.array_equal(cont.cpu().numpy()[: rc.size], rc)
+    if ro is not None:
+        assert np.array_equal(offs.cpu().numpy()[: ro.size], ro)
+    kind = {"uint8": O.U8, "float32": O.F32, "bfloat16": O.BF16}[dtype]
+    want = O.decode_stream(rc, ro, mode, per_chunk, P, B, nb, out_dtype=kind,
+                           scale=float(SCALE) if dtype != "uint8" else 1.0)
+    got = out.cpu()
+    got = got.view(torch.int16).numpy() if dtype == "bfloat16" else got.numpy()
+    assert np.array_equal(got.view(want.dtype), want)
+
+
+def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
+    """The exact / f64 vector geometries take the fused single launch."""
+    torch, C = torch_cuda, pkg.codec
+    P, B, nb = 3072, 512, 2
+    ds = torch.randint(0, 256, (B * nb, P), dtype=torch.uint8, device="cuda")
+    for mode, pc, launches in ((1, 16, 1), (0, 8, 1), (2, 6, 1), (3, 9, 2)):
+        L = C.layout(mode, pc, P, B, nb)
+        cont, offs = C.alloc_stream(L)
+        out = torch.empty((B * nb, P), dtype=torch.uint8, device="cuda")
+        C.sync()
+        n0 = pkg._lib.launches(0)
+        C.roundtrip_dev(L, ds, cont, out, offsets=offs)
+        C.sync()
+        assert pkg._lib.launches(0) - n0 == launches, mode
+        if pc <= C.capacity(mode):
+            assert torch.equal(out, ds)
+
+
 @pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("dtype", ["float32", "float16", "bfloat16"])
 def test_float_epilogue_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype):

@@ -19,9 +19,10 @@ def _setup(pkg, O, torch, N=4000, Ccls=10, B=64, seed=99):
     return S, labels, ds, p, offs, mem, ref
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("mode,dtype,spd", [(1, "uint8", 1), (0, "float32", 1), (3, "bfloat16", 2),
                                             (2, "float16", 3), (1, "uint8", 4)])
-def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype, spd):
+def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype, spd, split):
     torch, O = torch_cuda, oracle_mod
     from paper_2105_00619_b200.pipeline import Pipeline
     S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
@@ -30,7 +31,8 @@ def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype, spd)
     ds_d = torch.from_numpy(ds).cuda()
     dt = getattr(torch, dtype)
     pc = pkg.codec.capacity(mode)
-    pipe = Pipeline(cur, ds_d, mode, B, nb, per_chunk=pc, out_dtype=dt, scale=SCALE, steps_per_draw=spd)
+    pipe = Pipeline(cur, ds_d, mode, B, nb, per_chunk=pc, out_dtype=dt, scale=SCALE, steps_per_draw=spd,
+                    split_kernels=split)
     kind = {"uint8": O.U8, "float32": O.F32, "bfloat16": O.BF16, "float16": O.F16}[dtype]
     for step in range(6):
         out = torch.empty((B * nb, P), dtype=dt, device="cuda")

@@ -60,8 +60,10 @@ def main():
             t_dec = timeit(lambda: C.decode_dev(L, cont, out, stream=s), s)
             t_decf = timeit(lambda: C.decode_dev(L, cont, outf, scale=1 / 255, stream=s), s)
             t_decb = timeit(lambda: C.decode_dev(L, cont, outb, scale=1 / 255, stream=s), s)
+            t_rt = timeit(lambda: C.roundtrip_dev(L, ds, cont, out, row_index=ex, stream=s), s)
             m = C.mode_name(mode)
-            for name, t, byts in (("encode_gather", t_enc, rows * P + cb + rows * 8),
+            for name, t, byts in (("roundtrip_gather_u8", t_rt, 2 * (rows * P + cb) + rows * 8),
+                                  ("encode_gather", t_enc, rows * P + cb + rows * 8),
                                   ("encode_seq", t_encs, rows * P + cb),
                                   ("decode_u8", t_dec, cb + rows * P),
                                   ("decode_f32", t_decf, cb + rows * P * 4),
@@ -86,10 +88,11 @@ def main():
         res["sbs_alone_phases_us"] = [round(x.value * 1e3, 1) for x in p3]
         out = torch.empty((rows, P), dtype=torch.uint8, device=dev)
         for spd in (2, 4):
-            pipe = Pipeline(cur, ds, 1, B, NB, steps_per_draw=spd)
-            t_pipe = timeit(lambda: pipe.step(out, s), s, reps=32)
-            res[f"pipeline_step_spd{spd}"] = {"us": round(statistics.mean(t_pipe), 2)}
-            pipe.close()
+            for split in (False, True):
+                pipe = Pipeline(cur, ds, 1, B, NB, steps_per_draw=spd, split_kernels=split)
+                t_pipe = timeit(lambda: pipe.step(out, s), s, reps=32)
+                res[f"pipeline_step_spd{spd}{'_split' if split else ''}"] = {"us": round(statistics.mean(t_pipe), 2)}
+                pipe.close()
         pipe = Pipeline(cur, ds, 1, B, NB)
         t_pipe = timeit(lambda: pipe.step(out, s), s, reps=30)
         res["pipeline_step"] = {"us": round(statistics.mean(t_pipe), 2)}
