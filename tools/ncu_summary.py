@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (run here, on the CPU box).
 
-    python tools/ncu_summary.py gpurun_out/launches3.csv gpurun_out/prof3.ncu-rep r01
+    python tools/ncu_summary.py gpurun_out/launches3.csv gpurun_out/prof3.ncu-rep [more.ncu-rep ...] r01
 
 Writes profiles/<tag>_launches.csv (kernel, duration per launch: the
 `--metrics gpu__time_duration.sum` launch list) and profiles/ncu_summary.json
@@ -28,9 +28,10 @@ def short(name):
     n = n.replace("unnamed>::", "").strip()
     if "<" in n:
         base, args = n.split("<", 1)
-        args = [a.strip().replace("(int)", "") for a in args.rstrip(">").split(",")]
-        if base in ("k_encode_vec", "k_decode_vec", "k_encode_generic", "k_decode_generic"):
-            args = [MODES.get(args[0], args[0])] + [OUTS.get(a, a) for a in args[1:]]
+        args = [a.strip().replace("(int)", "").replace("(bool)", "") for a in args.rstrip(">").split(",")]
+        if base in ("k_encode_vec", "k_decode_vec", "k_encode_generic", "k_decode_generic", "k_roundtrip_vec"):
+            args = [MODES.get(args[0], args[0])] + [OUTS.get(a, a) for a in args[1:2]] + \
+                   [{"1": "true", "0": "false"}.get(a, a) for a in args[2:]]
         n = f"{base}<{','.join(args)}>"
     return n
 
@@ -49,7 +50,8 @@ def launches(path, tag):
     dst = os.path.join(ROOT, "profiles", f"{tag}_launches.csv")
     with open(dst, "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised replay:\n"
-                "# compare shares of the step, not absolutes); bench.py --steps 4 --warmup 3 --e2e-steps 0\n")
+                "# compare shares of the step, not absolutes); bench.py --steps 4 --warmup 3 --e2e-steps 0 "
+                "--split-steps 4 --no-cpu-baseline\n")
         f.write("id,kernel,duration_ns\n")
         for i, k, t in out:
             f.write(f"{i},{k},{t:.0f}\n")
@@ -78,20 +80,26 @@ def full(path):
 
 
 def main():
-    lcsv, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    lcsv, tag, reps = sys.argv[1], sys.argv[-1], sys.argv[2:-1]
     out = launches(lcsv, tag)
-    kern = full(rep)
+    kern = {}
+    for rep in reps:
+        kern.update(full(rep))
     rows, P = 97 * 512, 3072
     summ = {"source": f"ncu --set full --clock-control none --import-source on on bench.py (tag {tag}, B200)",
             "note": "ncu flushes caches before each replayed kernel; writes still dirty in L2 at kernel end are "
                     "not counted in dram__bytes_write, so traffic is below the algorithmic bytes for the "
                     "write-heavy kernels",
             "algorithmic_bytes_per_launch": {"k_encode_vec<exact128>": rows * P * 2 + rows * 8,
-                                             "k_decode_vec<exact128,u8>": rows * P * 2},
+                                             "k_decode_vec<exact128,u8,true>": rows * P * 2,
+                                             "k_roundtrip_vec<exact128,u8>": rows * P * 4 + rows * 8},
             "kernels": kern}
     json.dump(summ, open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w"), indent=1)
     step = {}
-    for _, k, t in out[-10:]:
+    # the last fused-pipeline step of the launch list: its roundtrip launch and
+    # the SBS launches of the draw call that fed it
+    last_rt = max(i for i, (_, k, _) in enumerate(out) if k.startswith("k_roundtrip_vec"))
+    for _, k, t in out[last_rt - 4:last_rt + 1]:
         step[k] = step.get(k, 0) + t
     tot = sum(step.values())
     for k, t in sorted(step.items(), key=lambda x: -x[1]):
