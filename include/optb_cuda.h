@@ -229,6 +229,35 @@ int optb_inverse_perm_dev(optb_ctx* ctx, const int64_t* perm, uint64_t n, int64_
 int optb_owner_labels_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, uint64_t rows_per_shard,
                           uint32_t n_shards, int32_t* owner, void* stream);
 
+/* Peer-memory variant (no all-to-all, no staging, no host synchronisation):
+ * every rank maps its peers' dataset shards into its address space with CUDA
+ * IPC (NVLink / NVSwitch peer access) and the gather-encode kernel loads each
+ * drawn row from the GPU that holds it, tile by tile.
+ *
+ * row_ptrs[i] = bases[o] + (examples[i] - o*rows_per_shard) * row_stride with
+ * o = examples[i] / rows_per_shard clamped to n_shards - 1 (bases: device
+ * array of the shards' base addresses as seen by this process). */
+int optb_shard_row_ptrs_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, const uint64_t* bases,
+                            uint32_t n_shards, uint64_t rows_per_shard, uint64_t row_stride,
+                            uint64_t* row_ptrs, void* stream);
+/* optb_encode_dev / optb_roundtrip_dev reading stream row r from the absolute
+ * device-accessible address row_ptrs[r] (device array): this GPU's HBM, a
+ * peer GPU's HBM opened with optb_ipc_open, or mapped pinned host memory.
+ * rows_aligned16 != 0 asserts every address is 16-byte aligned, which (with
+ * pixels % 16 == 0) selects the vector kernels. */
+int optb_encode_rows_dev(optb_ctx* ctx, const optb_layout* L, const uint64_t* row_ptrs,
+                         int32_t rows_aligned16, void* containers, uint8_t* offsets, void* stream);
+int optb_roundtrip_rows_dev(optb_ctx* ctx, const optb_layout* L, const uint64_t* row_ptrs,
+                            int32_t rows_aligned16, void* containers, uint8_t* offsets,
+                            const optb_epilogue* E, void* out, void* stream);
+/* CUDA IPC of the device allocation holding dev_ptr: the 64-byte handle and
+ * dev_ptr's offset inside the allocation; open maps it on `device` in another
+ * process (peer access enabled lazily); close unmaps (pass the same offset). */
+#define OPTB_IPC_HANDLE_BYTES 64
+int optb_ipc_export(const void* dev_ptr, uint8_t* handle, uint64_t* offset);
+int optb_ipc_open(int device, const uint8_t* handle, uint64_t offset, void** dev_ptr);
+int optb_ipc_close(void* dev_ptr, uint64_t offset);
+
 /* ---------------------------------------------------------------- OPTB files
  * pipeline::dump / load (pipeline.cpp:246-271) for device streams: chunk k of
  * a stream is the file <dir>/batch_<epoch>_<k>.optb holding write_optb's

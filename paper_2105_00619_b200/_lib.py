@@ -98,6 +98,13 @@ SIGNATURES = {
                                         ct.c_uint64, vp]),
     "optb_inverse_perm_dev": (ct.c_int, [vp, vp, ct.c_uint64, vp, vp]),
     "optb_owner_labels_dev": (ct.c_int, [vp, vp, ct.c_uint64, ct.c_uint64, ct.c_uint32, vp, vp]),
+    "optb_shard_row_ptrs_dev": (ct.c_int, [vp, vp, ct.c_uint64, vp, ct.c_uint32, ct.c_uint64, ct.c_uint64, vp,
+                                           vp]),
+    "optb_encode_rows_dev": (ct.c_int, [vp, LP, vp, ct.c_int32, vp, vp, vp]),
+    "optb_roundtrip_rows_dev": (ct.c_int, [vp, LP, vp, ct.c_int32, vp, vp, EP, vp, vp]),
+    "optb_ipc_export": (ct.c_int, [vp, vp, u64p]),
+    "optb_ipc_open": (ct.c_int, [ct.c_int, vp, ct.c_uint64, ct.POINTER(vp)]),
+    "optb_ipc_close": (ct.c_int, [vp, ct.c_uint64]),
     "optb_dump_dev": (ct.c_int, [vp, LP, vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64]),
     "optb_load_dev": (ct.c_int, [vp, LP, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint64, vp, vp]),
     "optb_load_records_dev": (ct.c_int, [vp, ct.c_char_p, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp,

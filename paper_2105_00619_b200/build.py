@@ -27,7 +27,7 @@ CUDA_LIB = "/usr/local/cuda/lib64"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
               "--expt-relaxed-constexpr", "-diag-suppress", "177", "-I" + INCLUDE]
-CUDA_SOURCES = ["codec.cu", "sbs.cu", "capi.cu", "pipeline.cu", "io.cu"]
+CUDA_SOURCES = ["codec.cu", "sbs.cu", "capi.cu", "pipeline.cu", "io.cu", "peer.cu"]
 CUDA_LIB_NAME = os.path.join(PKG, "liboptb_cuda.so")
 SHIM_LIB_NAME = os.path.join(PKG, "liboptb_shim.so")
 SHIM_SOURCES = ["codec.cpp", "sampler.cpp", "nn.cpp"]

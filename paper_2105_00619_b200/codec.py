@@ -283,6 +283,42 @@ def roundtrip_dev(L: Layout, images, containers, out, offsets=None, row_index=No
                                  _stream(stream, dev)))
 
 
+def encode_rows_dev(L: Layout, row_ptrs, containers, offsets=None, aligned16: bool = True, stream=None):
+    """Gather-encode from absolute row addresses (optb_encode_rows_dev):
+    stream row r packs the P bytes at row_ptrs[r] (int64 device tensor of
+    addresses -- this GPU's HBM, a peer GPU's HBM opened over IPC, mapped
+    host memory).  ``aligned16`` asserts 16-byte aligned rows (vector path)."""
+    dev = containers.device.index or 0
+    check(lib.optb_encode_rows_dev(_lib.context(dev), ct.byref(L), _dptr(row_ptrs), 1 if aligned16 else 0,
+                                   _dptr(containers), _dptr(offsets), _stream(stream, dev)))
+
+
+def roundtrip_rows_dev(L: Layout, row_ptrs, containers, out, offsets=None, aligned16: bool = True,
+                       scale: float = 1.0, class_scale=None, class_bias=None, row_class=None, stream=None):
+    """roundtrip_dev reading stream row r from row_ptrs[r] (optb_roundtrip_rows_dev)."""
+    import torch
+    dt = {torch.uint8: U8, torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}[out.dtype]
+    dev = out.device.index or 0
+    E = Epilogue(dt, float(scale), _dptr(class_scale), _dptr(class_bias), _dptr(row_class), out.stride(0))
+    check(lib.optb_roundtrip_rows_dev(_lib.context(dev), ct.byref(L), _dptr(row_ptrs), 1 if aligned16 else 0,
+                                      _dptr(containers), _dptr(offsets), ct.byref(E), _dptr(out),
+                                      _stream(stream, dev)))
+
+
+def shard_row_ptrs_dev(examples, bases, rows_per_shard: int, row_stride: int, out=None, stream=None):
+    """Drawn example ids -> absolute row addresses in the shard that owns
+    them (optb_shard_row_ptrs_dev); ``bases`` is an int64 device tensor of
+    the shards' base addresses in this process."""
+    import torch
+    dev = examples.device.index or 0
+    n = examples.numel()
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int64, device=examples.device)
+    check(lib.optb_shard_row_ptrs_dev(_lib.context(dev), _dptr(examples), n, _dptr(bases), bases.numel(),
+                                      rows_per_shard, row_stride, _dptr(out), _stream(stream, dev)))
+    return out[:n]
+
+
 def sync(device: int = 0, stream=None) -> None:
     """Synchronise and raise any latched device-side FormatError (optb_ctx_sync)."""
     check(lib.optb_ctx_sync(_lib.context(device), _stream(stream, device)))

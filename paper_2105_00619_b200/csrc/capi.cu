@@ -336,8 +336,23 @@ int optb_encode_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, ui
   if (row_stride == 0) row_stride = L->pixels;
   if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
   const Geom g = make_geom(L);
-  cudaError_t e = launch_encode(g, images, row_stride, row_index, containers, offsets,
-                                static_cast<cudaStream_t>(stream), c->sms, &c->launches);
+  const RowSrc rs{images, row_stride, row_index, nullptr, 0};
+  cudaError_t e = launch_encode(g, rs, containers, offsets, static_cast<cudaStream_t>(stream), c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "encode launch");
+  return OPTB_OK;
+}
+
+int optb_encode_rows_dev(optb_ctx* c, const optb_layout* L, const uint64_t* row_ptrs, int32_t rows_aligned16,
+                         void* containers, uint8_t* offsets, void* stream) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!row_ptrs || !containers || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "encode: null buffer");
+  const Geom g = make_geom(L);
+  const RowSrc rs{nullptr, 0, nullptr, row_ptrs, rows_aligned16};
+  cudaError_t e = launch_encode(g, rs, containers, offsets, static_cast<cudaStream_t>(stream), c->sms, &c->launches);
   if (e != cudaSuccess) return cuda_err(e, "encode launch");
   return OPTB_OK;
 }
@@ -361,29 +376,17 @@ int optb_decode_dev(optb_ctx* c, const optb_layout* L, const void* containers,
   return OPTB_OK;
 }
 
-int optb_roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
-                       const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E,
-                       void* out, void* stream) {
-  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
-  int st = optb_layout_check(L);
-  if (st) return st;
-  st = check_decode_layout(L);
-  if (st) return st;
-  st = check_epilogue(E);
-  if (st) return st;
-  if (optb_layout_rows(L) == 0) return OPTB_OK;
-  if (!images || !containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
-    return set_err(OPTB_ERR_ARG, "roundtrip: null buffer");
-  if (row_stride == 0) row_stride = L->pixels;
-  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
+namespace {
+
+int roundtrip(optb_ctx* c, const optb_layout* L, const RowSrc& rs, void* containers, uint8_t* offsets,
+              const optb_epilogue* E, void* out, void* stream) {
   const Epi ep = make_epi(E, L->pixels);
   if (ep.row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "decode: out_row_stride < pixels");
   const Geom g = make_geom(L);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_roundtrip(g, images, row_stride, row_index, containers, ep, out, c->d_err, s, c->sms,
-                                   &c->launches);
+  cudaError_t e = launch_roundtrip(g, rs, containers, ep, out, c->d_err, s, c->sms, &c->launches);
   if (e == cudaErrorNotSupported) {
-    e = launch_encode(g, images, row_stride, row_index, containers, offsets, s, c->sms, &c->launches);
+    e = launch_encode(g, rs, containers, offsets, s, c->sms, &c->launches);
     if (e != cudaSuccess) return cuda_err(e, "encode launch");
     e = launch_decode(g, containers, offsets, ep, out, c->d_err, s, c->sms, &c->launches);
     if (e != cudaSuccess) return cuda_err(e, "decode launch");
@@ -391,6 +394,41 @@ int optb_roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images,
   }
   if (e != cudaSuccess) return cuda_err(e, "roundtrip launch");
   return OPTB_OK;
+}
+
+int roundtrip_checks(optb_ctx* c, const optb_layout* L, const optb_epilogue* E) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  st = check_decode_layout(L);
+  if (st) return st;
+  return check_epilogue(E);
+}
+
+}  // namespace
+
+int optb_roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
+                       const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E,
+                       void* out, void* stream) {
+  int st = roundtrip_checks(c, L, E);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!images || !containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "roundtrip: null buffer");
+  if (row_stride == 0) row_stride = L->pixels;
+  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
+  return roundtrip(c, L, RowSrc{images, row_stride, row_index, nullptr, 0}, containers, offsets, E, out, stream);
+}
+
+int optb_roundtrip_rows_dev(optb_ctx* c, const optb_layout* L, const uint64_t* row_ptrs, int32_t rows_aligned16,
+                            void* containers, uint8_t* offsets, const optb_epilogue* E, void* out, void* stream) {
+  int st = roundtrip_checks(c, L, E);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!row_ptrs || !containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "roundtrip: null buffer");
+  return roundtrip(c, L, RowSrc{nullptr, 0, nullptr, row_ptrs, rows_aligned16}, containers, offsets, E, out,
+                   stream);
 }
 
 int optb_synth_pixels_dev(optb_ctx* c, uint64_t seed, uint64_t first_row, uint64_t n_rows,
@@ -547,7 +585,7 @@ int optb_encode_host(optb_ctx* c, const optb_layout* L, const uint8_t* images, v
     CK(cudaStreamWaitEvent(c->s_compute, c->ev_h2d[k], 0), "wait");
     CK(cudaStreamWaitEvent(c->s_compute, c->ev_d2h[k], 0), "wait");
     const Geom g = make_geom(&s.L);
-    cudaError_t e = launch_encode(g, c->dev_in[k], P, nullptr, c->dev_out[k], c->dev_off[k],
+    cudaError_t e = launch_encode(g, RowSrc{c->dev_in[k], P, nullptr, nullptr, 0}, c->dev_out[k], c->dev_off[k],
                                   c->s_compute, c->sms, &c->launches);
     if (e != cudaSuccess) return cuda_err(e, "encode launch");
     CK(cudaEventRecord(c->ev_kern[k], c->s_compute), "event");

@@ -34,6 +34,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace optb_b200 {
@@ -428,10 +430,15 @@ __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> byte
   return (b * 0x00204081u) & 0x01010101u;
 }
 
-template <int MODE>
-__device__ __forceinline__ void encode_body(const Geom& g, const uint8_t* __restrict__ images, uint64_t row_stride,
-                                            const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont,
+// PTRS: stream row r is read from the absolute address src.ptrs[r] (this
+// GPU's HBM, a peer GPU's HBM over NVLink, mapped pinned host memory) instead
+// of src.images + src.index[r] * src.stride.
+template <int MODE, bool PTRS>
+__device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
                                             uint8_t* __restrict__ offsets, uint8_t* smem_base) {
+  const uint8_t* __restrict__ images = src.images;
+  const uint64_t row_stride = src.stride;
+  const int64_t* __restrict__ row_index = src.index;
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -445,7 +452,8 @@ __device__ __forceinline__ void encode_body(const Geom& g, const uint8_t* __rest
   // Dataset row ids of a tile are fetched one stage before its copies are
   // issued, so the dependent index loads never stall the pipeline.
   Walk wf = walk_at(g, G, first + lane);  // next tile to fetch row ids for
-  uint32_t rows[S::NI];
+  using RowT = typename std::conditional<PTRS, uint64_t, uint32_t>::type;
+  RowT rows[S::NI];
   uint64_t pend_gi = 0;  // group and image count of the fetched tile
   uint32_t pend_n = 0;
   auto fetch_rows = [&]() {
@@ -457,9 +465,14 @@ __device__ __forceinline__ void encode_body(const Geom& g, const uint8_t* __rest
 #pragma unroll
       for (int i = 0; i < S::NI; ++i) {
         const uint64_t r = c.r0 + i;
-        rows[i] = (i < static_cast<int>(c.n))
-                      ? static_cast<uint32_t>(row_index ? __ldg(row_index + r) : static_cast<int64_t>(r))
-                      : 0u;
+        if constexpr (PTRS) {
+          rows[i] = (i < static_cast<int>(c.n)) ? __ldg(reinterpret_cast<const unsigned long long*>(src.ptrs) + r)
+                                                : 0ull;
+        } else {
+          rows[i] = (i < static_cast<int>(c.n))
+                        ? static_cast<uint32_t>(row_index ? __ldg(row_index + r) : static_cast<int64_t>(r))
+                        : 0u;
+        }
       }
     }
     walk_advance(wf, step, g, G);
@@ -467,9 +480,13 @@ __device__ __forceinline__ void encode_body(const Geom& g, const uint8_t* __rest
   auto issue = [&](int stage) {
     uint8_t* slot = ring + stage * S::ENC_SLOT;
 #pragma unroll
-    for (int i = 0; i < S::NI; ++i)
-      if (i < static_cast<int>(pend_n))
-        cp_async16(slot + i * 512 + lane * 16, images + static_cast<uint64_t>(rows[i]) * row_stride + pend_gi * 16);
+    for (int i = 0; i < S::NI; ++i) {
+      if (i < static_cast<int>(pend_n)) {
+        const uint8_t* row = PTRS ? reinterpret_cast<const uint8_t*>(static_cast<uintptr_t>(rows[i]))
+                                  : images + static_cast<uint64_t>(rows[i]) * row_stride;
+        cp_async16(slot + i * 512 + lane * 16, row + pend_gi * 16);
+      }
+    }
     cp_async_commit();
   };
 
@@ -593,13 +610,11 @@ __device__ __forceinline__ void encode_body(const Geom& g, const uint8_t* __rest
   cp_async_wait<0>();
 }
 
-template <int MODE>
+template <int MODE, bool PTRS>
 __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_encode_vec(Geom g, const uint8_t* __restrict__ images, uint64_t row_stride,
-                 const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont,
-                 uint8_t* __restrict__ offsets) {
+    k_encode_vec(Geom g, RowSrc src, uint8_t* __restrict__ cont, uint8_t* __restrict__ offsets) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  encode_body<MODE>(g, images, row_stride, row_index, cont, offsets, smem_raw);
+  encode_body<MODE, PTRS>(g, src, cont, offsets, smem_raw);
 }
 
 // ------------------------------------------------------------------ K2 / K4
@@ -922,15 +937,14 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
 // No warp reads another warp's containers, so no grid-wide barrier is needed;
 // the kernel saves one launch's ramp-up and tail.  Exact and f64 modes (the
 // decode half reads each tile with one TMA tensor load).
-template <int MODE, int O>
+template <int MODE, int O, bool PTRS>
 __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, const uint8_t* __restrict__ images,
-                    uint64_t row_stride, const int64_t* __restrict__ row_index, uint8_t* __restrict__ cont, Epi e,
+    k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont, Epi e,
                     void* __restrict__ out, DevError* err) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bars[kWarps * kStages];
   uint8_t* base = align1024(smem_raw);
-  encode_body<MODE>(g, images, row_stride, row_index, cont, nullptr, base);
+  encode_body<MODE, PTRS>(g, src, cont, nullptr, base);
   // this warp's container stores (generic proxy) before its TMA reads of
   // them, and its staging writes before the TMA fills of the same slots
   fence_proxy_async_global();
@@ -945,10 +959,7 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
 // chunks.  Lossless parity bits are accumulated with warp ballots and written
 // with atomicOr into a zeroed plane (covers unaligned bit offsets).
 template <int MODE>
-__global__ void __launch_bounds__(256) k_encode_generic(Geom g, const uint8_t* __restrict__ images,
-                                                        uint64_t row_stride,
-                                                        const int64_t* __restrict__ row_index,
-                                                        uint8_t* __restrict__ cont,
+__global__ void __launch_bounds__(256) k_encode_generic(Geom g, RowSrc rs, uint8_t* __restrict__ cont,
                                                         uint8_t* __restrict__ offsets) {
   constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
   constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
@@ -976,8 +987,13 @@ __global__ void __launch_bounds__(256) k_encode_generic(Geom g, const uint8_t* _
       const bool has = valid && i < static_cast<int>(c.n);
       if (has) {
         const uint64_t r = c.r0 + i;
-        const uint64_t src = row_index ? static_cast<uint64_t>(__ldg(row_index + r)) : r;
-        px = __ldg(images + src * row_stride + p);
+        if (rs.ptrs) {
+          px = __ldg(reinterpret_cast<const uint8_t*>(static_cast<uintptr_t>(__ldg(
+                         reinterpret_cast<const unsigned long long*>(rs.ptrs) + r))) + p);
+        } else {
+          const uint64_t src = rs.index ? static_cast<uint64_t>(__ldg(rs.index + r)) : r;
+          px = __ldg(rs.images + src * rs.stride + p);
+        }
         if constexpr (MODE == OPTB_F64) {
           // codec.cpp:116-120: acc += px * 256^i in binary64, i ascending
           dacc = __dadd_rn(dacc, __dmul_rn(static_cast<double>(px), pow256(i)));
@@ -1144,16 +1160,14 @@ int grid_for(K kernel, int threads, size_t smem, int num_sms, uint64_t work_unit
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <int MODE>
-cudaError_t enc_generic(const Geom& g, const uint8_t* images, uint64_t row_stride,
-                        const int64_t* idx, void* cont, uint8_t* offs, cudaStream_t s, int sms,
+cudaError_t enc_generic(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
                         uint64_t* launches) {
   if (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128) {
     cudaError_t st = cudaMemsetAsync(offs, 0, g.chunks * g.ostride, s);
     if (st != cudaSuccess) return st;
   }
   const int grid = grid_for(k_encode_generic<MODE>, 256, 0, sms, g.chunks * g.P);
-  k_encode_generic<MODE><<<grid, 256, 0, s>>>(g, images, row_stride, idx,
-                                              static_cast<uint8_t*>(cont), offs);
+  k_encode_generic<MODE><<<grid, 256, 0, s>>>(g, rs, static_cast<uint8_t*>(cont), offs);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1168,22 +1182,28 @@ cudaError_t dec_generic(const Geom& g, const void* cont, const uint8_t* offs, co
   return cudaGetLastError();
 }
 
-template <int MODE>
-cudaError_t enc_vec(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* idx,
-                    void* cont, uint8_t* offs, cudaStream_t s, int sms, uint64_t* launches) {
+template <int MODE, bool PTRS>
+cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
+                      uint64_t* launches) {
   const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_encode_vec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_encode_vec<MODE, PTRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
   const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_encode_vec<MODE>, kThreads, smem, sms, items);
-  k_encode_vec<MODE><<<grid, kThreads, smem, s>>>(g, images, row_stride, idx, static_cast<uint8_t*>(cont),
-                                                  offs);
+  const int grid = grid_for(k_encode_vec<MODE, PTRS>, kThreads, smem, sms, items);
+  k_encode_vec<MODE, PTRS><<<grid, kThreads, smem, s>>>(g, rs, static_cast<uint8_t*>(cont), offs);
   ++*launches;
   return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t enc_vec(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
+                    uint64_t* launches) {
+  if (rs.ptrs) return enc_vec_t<MODE, true>(g, rs, cont, offs, s, sms, launches);
+  return enc_vec_t<MODE, false>(g, rs, cont, offs, s, sms, launches);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -1256,37 +1276,41 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
   return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
 
-template <int MODE, int O>
-cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const uint8_t* images, uint64_t row_stride,
-                   const int64_t* idx, void* cont, const Epi& e, void* out, DevError* err, cudaStream_t s, int sms,
-                   uint64_t* launches) {
+template <int MODE, int O, bool PTRS>
+cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, const Epi& e, void* out,
+                   DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   constexpr size_t enc = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
   constexpr size_t dec = static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA;
   constexpr size_t smem = (enc > dec ? enc : dec) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_roundtrip_vec<MODE, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_roundtrip_vec<MODE, O, PTRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     attr = true;
   }
   const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_roundtrip_vec<MODE, O>, kThreads, smem, sms, items);
-  k_roundtrip_vec<MODE, O><<<grid, kThreads, smem, s>>>(cm, g, images, row_stride, idx,
-                                                        static_cast<uint8_t*>(cont), e, out, err);
+  const int grid = grid_for(k_roundtrip_vec<MODE, O, PTRS>, kThreads, smem, sms, items);
+  k_roundtrip_vec<MODE, O, PTRS><<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), e, out, err);
   ++*launches;
   return cudaGetLastError();
 }
 
-template <int MODE>
-cudaError_t rt_vec_any(const CUtensorMap& cm, const Geom& g, const uint8_t* images, uint64_t row_stride,
-                       const int64_t* idx, void* cont, const Epi& e, void* out, DevError* err, cudaStream_t s,
-                       int sms, uint64_t* l) {
+template <int MODE, bool PTRS>
+cudaError_t rt_vec_out(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, const Epi& e, void* out,
+                       DevError* err, cudaStream_t s, int sms, uint64_t* l) {
   switch (e.dtype) {
-    case OPTB_OUT_U8: return rt_vec<MODE, OPTB_OUT_U8>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
-    case OPTB_OUT_F32: return rt_vec<MODE, OPTB_OUT_F32>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
-    case OPTB_OUT_F16: return rt_vec<MODE, OPTB_OUT_F16>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
-    default: return rt_vec<MODE, OPTB_OUT_BF16>(cm, g, images, row_stride, idx, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_U8: return rt_vec<MODE, OPTB_OUT_U8, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_F32: return rt_vec<MODE, OPTB_OUT_F32, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_F16: return rt_vec<MODE, OPTB_OUT_F16, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
+    default: return rt_vec<MODE, OPTB_OUT_BF16, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
   }
+}
+
+template <int MODE>
+cudaError_t rt_vec_any(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, const Epi& e, void* out,
+                       DevError* err, cudaStream_t s, int sms, uint64_t* l) {
+  if (rs.ptrs) return rt_vec_out<MODE, true>(cm, g, rs, cont, e, out, err, s, sms, l);
+  return rt_vec_out<MODE, false>(cm, g, rs, cont, e, out, err, s, sms, l);
 }
 
 template <int MODE>
@@ -1320,28 +1344,32 @@ bool vec_ok(const Geom& g) {
 
 }  // namespace
 
-cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_stride,
-                          const int64_t* row_index, void* containers, uint8_t* offsets,
-                          cudaStream_t s, int sms, uint64_t* launches) {
-  const bool vec = vec_ok(g) && row_stride % 16 == 0 && aligned16(images) && aligned16(containers);
+// Row sources qualify for the vector path when every row is 16-byte aligned:
+// index mode checks base and stride, pointer mode trusts the caller's flag.
+bool rows_vec_ok(const RowSrc& rs) {
+  return rs.ptrs ? rs.ptrs_aligned16 != 0 : (rs.stride % 16 == 0 && aligned16(rs.images));
+}
+
+cudaError_t launch_encode(const Geom& g, const RowSrc& rs, void* containers, uint8_t* offsets, cudaStream_t s,
+                          int sms, uint64_t* launches) {
+  const bool vec = vec_ok(g) && rows_vec_ok(rs) && aligned16(containers);
   switch (g.mode) {
     case OPTB_EXACT64:
-      if (vec) return enc_vec<OPTB_EXACT64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_EXACT64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      if (vec) return enc_vec<OPTB_EXACT64>(g, rs, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_EXACT64>(g, rs, containers, offsets, s, sms, launches);
     case OPTB_EXACT128:
-      if (vec) return enc_vec<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_EXACT128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      if (vec) return enc_vec<OPTB_EXACT128>(g, rs, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_EXACT128>(g, rs, containers, offsets, s, sms, launches);
     case OPTB_F64:
-      if (vec && g.per_chunk <= 8)
-        return enc_vec<kF64Narrow>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
-      if (vec) return enc_vec<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_F64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      if (vec && g.per_chunk <= 8) return enc_vec<kF64Narrow>(g, rs, containers, offsets, s, sms, launches);
+      if (vec) return enc_vec<OPTB_F64>(g, rs, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_F64>(g, rs, containers, offsets, s, sms, launches);
     case OPTB_LOSSLESS64:
-      if (vec) return enc_vec<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_LOSSLESS64>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      if (vec) return enc_vec<OPTB_LOSSLESS64>(g, rs, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_LOSSLESS64>(g, rs, containers, offsets, s, sms, launches);
     default:
-      if (vec) return enc_vec<OPTB_LOSSLESS128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_LOSSLESS128>(g, images, row_stride, row_index, containers, offsets, s, sms, launches);
+      if (vec) return enc_vec<OPTB_LOSSLESS128>(g, rs, containers, offsets, s, sms, launches);
+      return enc_generic<OPTB_LOSSLESS128>(g, rs, containers, offsets, s, sms, launches);
   }
 }
 
@@ -1371,23 +1399,21 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
   }
 }
 
-cudaError_t launch_roundtrip(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* row_index,
-                             void* containers, const Epi& e, void* out, DevError* err, cudaStream_t s, int sms,
-                             uint64_t* launches) {
+cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rs, void* containers, const Epi& e, void* out,
+                             DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
-  const bool vec = vec_ok(g) && row_stride % 16 == 0 && aligned16(images) && aligned16(containers) &&
-                   aligned16(out) && (e.row_stride * es) % 16 == 0;
+  const bool vec = vec_ok(g) && rows_vec_ok(rs) && aligned16(containers) && aligned16(out) &&
+                   (e.row_stride * es) % 16 == 0;
   const bool tma_mode = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128 || g.mode == OPTB_F64;
   CUtensorMap cm;
   if (!vec || !tma_mode || !tma_decode_enabled() || !container_map(&cm, containers, g.chunks * g.P * g.wc, g.wc))
     return cudaErrorNotSupported;  // caller: separate encode + decode launches
   switch (g.mode) {
-    case OPTB_EXACT64: return rt_vec_any<OPTB_EXACT64>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
-    case OPTB_EXACT128: return rt_vec_any<OPTB_EXACT128>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
+    case OPTB_EXACT64: return rt_vec_any<OPTB_EXACT64>(cm, g, rs, containers, e, out, err, s, sms, launches);
+    case OPTB_EXACT128: return rt_vec_any<OPTB_EXACT128>(cm, g, rs, containers, e, out, err, s, sms, launches);
     default:
-      if (g.per_chunk <= 8)
-        return rt_vec_any<kF64Narrow>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
-      return rt_vec_any<OPTB_F64>(cm, g, images, row_stride, row_index, containers, e, out, err, s, sms, launches);
+      if (g.per_chunk <= 8) return rt_vec_any<kF64Narrow>(cm, g, rs, containers, e, out, err, s, sms, launches);
+      return rt_vec_any<OPTB_F64>(cm, g, rs, containers, e, out, err, s, sms, launches);
   }
 }
 

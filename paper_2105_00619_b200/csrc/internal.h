@@ -46,19 +46,28 @@ struct Epi {
   uint64_t row_stride;  // elements
 };
 
+// Where the gather-encode reads stream row r: images + index[r] * stride
+// (index NULL = identity), or the absolute address ptrs[r] when ptrs is set
+// (peer-GPU HBM over NVLink, mapped host memory, ...).
+struct RowSrc {
+  const uint8_t* images;
+  uint64_t stride;
+  const int64_t* index;
+  const uint64_t* ptrs;
+  int32_t ptrs_aligned16;  // every ptrs[r] is 16-byte aligned (vector path)
+};
+
 // Kernel launchers (codec.cu).  Return cudaError_t of the launch; `launches`
 // is incremented by the number of kernels enqueued.
-cudaError_t launch_encode(const Geom& g, const uint8_t* images, uint64_t row_stride,
-                          const int64_t* row_index, void* containers, uint8_t* offsets,
+cudaError_t launch_encode(const Geom& g, const RowSrc& rows, void* containers, uint8_t* offsets,
                           cudaStream_t s, int num_sms, uint64_t* launches);
 cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* offsets,
                           const Epi& e, void* out, DevError* err, cudaStream_t s, int num_sms,
                           uint64_t* launches);
 // Encode + decode of the same stream in one launch (exact / f64 vector path);
 // cudaErrorNotSupported when the geometry needs the separate launches.
-cudaError_t launch_roundtrip(const Geom& g, const uint8_t* images, uint64_t row_stride, const int64_t* row_index,
-                             void* containers, const Epi& e, void* out, DevError* err, cudaStream_t s,
-                             int num_sms, uint64_t* launches);
+cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rows, void* containers, const Epi& e, void* out,
+                             DevError* err, cudaStream_t s, int num_sms, uint64_t* launches);
 cudaError_t launch_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uint64_t P,
                          uint8_t* out, uint64_t row_stride, cudaStream_t s, int num_sms,
                          uint64_t* launches);

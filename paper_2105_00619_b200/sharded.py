@@ -17,6 +17,14 @@ Rank r owns dataset rows [r*per, min((r+1)*per, N)).  Per step:
      replicated-dataset path -- and decode runs as usual.
 The exchange moves (G-1)/G of the step's rows across NVLink (~7x slower
 than HBM), so this variant is exchange-bound and reported separately.
+
+PeerShardedGather is the B200-native form of the same step: the shards are
+mapped into every rank's address space (CUDA IPC over NVLink / NVSwitch peer
+access), a tiny kernel turns the step's draws into absolute row addresses,
+and ONE launch (optb_roundtrip_rows_dev) gathers each drawn row from the GPU
+that owns it -- the NVLink transfer overlapped tile by tile with the packing
+-- encodes it and decodes it: no staging buffer, no all-to-all, no host
+synchronisation, no index exchange.
 """
 from __future__ import annotations
 
@@ -109,3 +117,76 @@ class ShardedGather:
         codec.encode_dev(self.layout, recv, self.cont, self.offs, row_index=inv, stream=s)
         codec.decode_dev(self.layout, self.cont, out, offsets=self.offs, stream=s)
         return send_counts, recv_counts
+
+
+class PeerShardedGather:
+    """Dataset-sharded step over peer memory (see the module docstring).
+
+    Every rank holds rows [rank*per, (rank+1)*per) in ``local_rows`` (a CUDA
+    tensor, same row stride on every rank); construction is collective
+    (exchanges the IPC handles, then a barrier).  ``step(out)`` enqueues the
+    step on the current stream and returns immediately."""
+
+    def __init__(self, cursor, local_rows, n_examples: int, rank: int, world: int, batch: int,
+                 batches_per_step: int, mode=codec.CodecMode.ExactInt128, group=None, device: int = 0,
+                 out_dtype=None, scale: float = 1.0):
+        import torch
+        import torch.distributed as dist
+        self.cursor, self.local, self.N = cursor, local_rows, n_examples
+        self.rank, self.world, self.B, self.nb = rank, world, batch, batches_per_step
+        self.per = (n_examples + world - 1) // world
+        self.P = local_rows.shape[1]
+        self.stride = local_rows.stride(0)
+        self.device, self.scale, self.group = device, scale, group
+        self.rows = batch * batches_per_step
+        self.layout = codec.layout(mode, codec.capacity(mode), self.P, batch, batches_per_step)
+        self.cont, self.offs = codec.alloc_stream(self.layout, device)
+        dev = torch.device("cuda", device)
+        handle = (ct.c_uint8 * 64)()
+        off = ct.c_uint64()
+        check(lib.optb_ipc_export(ct.c_void_p(local_rows.data_ptr()), handle, ct.byref(off)))
+        mine = (bytes(handle), off.value, self.stride)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        if any(e[2] != self.stride for e in everyone):
+            raise ValueError("PeerShardedGather: shards must share one row stride")
+        bases, self._opened = [], []
+        for q, (h, o, _) in enumerate(everyone):
+            if q == rank:
+                bases.append(local_rows.data_ptr())
+                continue
+            p = ct.c_void_p()
+            check(lib.optb_ipc_open(device, (ct.c_uint8 * 64).from_buffer_copy(h), o, ct.byref(p)))
+            self._opened.append((p.value, o))
+            bases.append(p.value)
+        self.aligned16 = all(b % 16 == 0 for b in bases) and self.stride % 16 == 0
+        self.bases = torch.tensor(bases, dtype=torch.int64, device=dev)
+        self.ptrs = torch.empty(max(self.rows, 1), dtype=torch.int64, device=dev)
+        self.ex = torch.empty(max(self.rows, 1), dtype=torch.int64, device=dev)
+        self.cls = torch.empty(max(self.rows, 1), dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)  # every shard written and mapped before anyone reads
+
+    def step(self, out, stream=None):
+        """Draw this rank's batches of the step, resolve their rows to peer
+        addresses, then gather (over NVLink) + encode + decode in one launch."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        s = stream or torch.cuda.current_stream(dev)
+        ex, _ = self.cursor.next_dev(self.nb * self.world, shard=self.rank, n_shards=self.world,
+                                     examples=self.ex, classes=self.cls, stream=s)
+        codec.shard_row_ptrs_dev(ex, self.bases, self.per, self.stride, out=self.ptrs, stream=s)
+        codec.roundtrip_rows_dev(self.layout, self.ptrs, self.cont, out, offsets=self.offs,
+                                 aligned16=self.aligned16, scale=self.scale, stream=s)
+
+    def close(self):
+        """Collective: unmap the peers' shards once every rank is done."""
+        import torch
+        import torch.distributed as dist
+        if getattr(self, "_opened", None) is None:
+            return
+        torch.cuda.synchronize(torch.device("cuda", self.device))
+        dist.barrier(group=self.group)
+        for p, o in self._opened:
+            check(lib.optb_ipc_close(ct.c_void_p(p), o))
+        self._opened = None

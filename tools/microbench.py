@@ -61,8 +61,12 @@ def main():
             t_decf = timeit(lambda: C.decode_dev(L, cont, outf, scale=1 / 255, stream=s), s)
             t_decb = timeit(lambda: C.decode_dev(L, cont, outb, scale=1 / 255, stream=s), s)
             t_rt = timeit(lambda: C.roundtrip_dev(L, ds, cont, out, row_index=ex, stream=s), s)
+            bases = torch.tensor([ds.data_ptr()], dtype=torch.int64, device=dev)
+            ptrs = C.shard_row_ptrs_dev(ex, bases, N, P, stream=s)
+            t_rtp = timeit(lambda: C.roundtrip_rows_dev(L, ptrs, cont, out, stream=s), s)
             m = C.mode_name(mode)
             for name, t, byts in (("roundtrip_gather_u8", t_rt, 2 * (rows * P + cb) + rows * 8),
+                                  ("roundtrip_rowptrs_u8", t_rtp, 2 * (rows * P + cb) + rows * 8),
                                   ("encode_gather", t_enc, rows * P + cb + rows * 8),
                                   ("encode_seq", t_encs, rows * P + cb),
                                   ("decode_u8", t_dec, cb + rows * P),

@@ -14,5 +14,5 @@ done
 wait
 for v in "$@"; do
   d=build/tune/$v
-  nvcc $ARCH -shared -o $d/liboptb_cuda.so $d/codec.o build/sbs.o build/capi.o build/pipeline.o build/io.o -cudart static
+  nvcc $ARCH -shared -o $d/liboptb_cuda.so $d/codec.o build/sbs.o build/capi.o build/pipeline.o build/io.o build/peer.o -cudart static
 done
