@@ -260,7 +260,7 @@ def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, wo
             k_state[0] += 1
 
         with torch.cuda.stream(stream):
-            for _ in range(2):
+            for _ in range(max(4, args.warmup)):  # includes the sampler's generation-pool growth
                 step()
             torch.cuda.synchronize(dev)
             if world > 1:
@@ -302,7 +302,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--sharded-steps", type=int, default=3,
                     help="N > 1 only: steps of the dataset-sharded (all-to-all) variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -751,7 +751,7 @@ int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
   if (s->h_call_cap[r] < bytes) {
     if (s->h_call[r]) cudaFreeHost(s->h_call[r]);
     s->h_call[r] = nullptr;
-    CK(cudaHostAlloc(&s->h_call[r], bytes * 2, cudaHostAllocDefault), "sbs pinned");
+    CK(cudaHostAlloc(&s->h_call[r], bytes * 2 + 16, cudaHostAllocMapped | cudaHostAllocPortable), "sbs pinned");
     s->h_call_cap[r] = bytes * 2;
   }
   if (s->call_cap < bytes) {
@@ -764,7 +764,13 @@ int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
     s->call_cap = bytes * 2;
   }
   memcpy(s->h_call[r], pk.buf.data(), pk.buf.size());
-  CK(cudaMemcpyAsync(s->d_call, s->h_call[r], bytes, cudaMemcpyHostToDevice, st), "sbs upload");
+  // A kernel pulls the block over PCIe from the mapped pinned slot instead of
+  // a cudaMemcpyAsync: an H2D copy would queue on the copy engine behind any
+  // bulk upload in flight (the e2e leg streams a 153.6 MB dataset per step)
+  // and stall the draws for milliseconds.
+  void* src = nullptr;
+  CK(cudaHostGetDevicePointer(&src, s->h_call[r], 0), "sbs mapped slot");
+  CK(launch_copy_in(src, s->d_call, bytes, st, &s->ctx->launches), "sbs upload");
   CK(cudaEventRecord(s->uploaded[r], st), "sbs upload");
   return OPTB_OK;
 }

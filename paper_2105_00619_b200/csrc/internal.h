@@ -72,6 +72,10 @@ cudaError_t launch_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uin
                          uint8_t* out, uint64_t row_stride, cudaStream_t s, int num_sms,
                          uint64_t* launches);
 
+// dst[0, bytes) = src[0, bytes) by a kernel (src: mapped pinned host memory;
+// both 16-byte aligned, readable / writable up to bytes rounded up to 16).
+cudaError_t launch_copy_in(const void* src, void* dst, size_t bytes, cudaStream_t s, uint64_t* launches);
+
 // SBS launchers (sbs.cu).
 cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
                                uint64_t* class_offsets, int64_t* members, uint32_t* scratch,

@@ -550,4 +550,21 @@ cudaError_t launch_sbs_gather(const SbsGatherArgs& a, int64_t* examples, int32_t
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void k_copy_in(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t n16) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+}  // namespace
+
+cudaError_t launch_copy_in(const void* src, void* dst, size_t bytes, cudaStream_t s, uint64_t* launches) {
+  const uint64_t n16 = (bytes + 15) / 16;
+  const uint64_t blocks = (n16 + 255) / 256;
+  k_copy_in<<<static_cast<unsigned>(blocks < 64 ? blocks : 64), 256, 0, s>>>(static_cast<const uint4*>(src),
+                                                                             static_cast<uint4*>(dst), n16);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 }  // namespace optb_b200

@@ -1,6 +1,6 @@
 """Run one codec configuration a few times (for ncu captures of a single kernel pair).
 
-    python tools/kernel_probe.py MODE PER_CHUNK P BATCH N_BATCHES [OUT_DTYPE] [REPS]
+    python tools/kernel_probe.py MODE PER_CHUNK P BATCH N_BATCHES [OUT_DTYPE] [REPS] [fused]
 """
 import os
 import sys
@@ -21,9 +21,13 @@ def main():
     x = torch.randint(0, 256, (B * nb, P), dtype=torch.uint8, device="cuda")
     cont, offs = C.alloc_stream(L)
     out = torch.empty((B * nb, P), dtype=dt, device="cuda")
+    fused = len(sys.argv) > 8 and sys.argv[8] == "fused"
     for _ in range(reps):
-        C.encode_dev(L, x, cont, offs)
-        C.decode_dev(L, cont, out, offsets=offs, scale=1 / 255)
+        if fused:
+            C.roundtrip_dev(L, x, cont, out, offsets=offs, scale=1 / 255)
+        else:
+            C.encode_dev(L, x, cont, offs)
+            C.decode_dev(L, cont, out, offsets=offs, scale=1 / 255)
     C.sync()
     torch.cuda.synchronize()
 
