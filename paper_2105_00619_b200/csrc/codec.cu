@@ -193,56 +193,67 @@ __device__ __forceinline__ double pow256(int i) {
 }
 
 // ------------------------------------------------------------------ epilogue
+// y = RN(float(q) * s) (nn.cpp:186), then RN(y + b) with a per-class bias.
+// Fast form for 0 < s < 2^100: PRMT puts the byte q under the exponent of
+// 2^23 (a = 2^23 + q, exact), and one FFMA gives RN(a*s - 2^23*s) = RN(q*s)
+// because the product is exact inside the FMA and 2^23*s is an exact float;
+// so 2 full-rate ops per pixel instead of an extract + I2F + FMUL.  Other
+// scales (negative, zero, huge, non-finite) take the plain FMUL, which also
+// keeps -0.0 for q = 0 and NaN / Inf exactly as the reference.
+struct PxScale {
+  float s, ms, b;
+  bool fast, affine;
+};
+__device__ __forceinline__ PxScale px_scale(float s, float b, bool affine) {
+  PxScale c;
+  c.s = s;
+  c.b = b;
+  c.affine = affine;
+  c.fast = s > 0.0f && s < 0x1p100f;
+  c.ms = -__fmul_rn(s, 0x1p23f);
+  return c;
+}
+template <bool FAST>
+__device__ __forceinline__ float px_value(uint32_t w, int k, const PxScale& c) {
+  float y;
+  if constexpr (FAST) {
+    y = __fmaf_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | static_cast<uint32_t>(k))), c.s, c.ms);
+  } else {
+    y = __fmul_rn(static_cast<float>((w >> (8 * k)) & 0xffu), c.s);
+  }
+  return c.affine ? __fadd_rn(y, c.b) : y;
+}
+
 struct Out4 {
-  // store 4 consecutive decoded pixels q (bytes of `q4`) of row `row` at `dst`
-  template <int O>
-  static __device__ __forceinline__ void put(void* dst, uint32_t q4, float s, float b, bool affine) {
+  // store 4 consecutive decoded pixels q (bytes of `q4`) at `dst`
+  template <int O, bool FAST>
+  static __device__ __forceinline__ void put(void* dst, uint32_t q4, const PxScale& c) {
     float y[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float v = __fmul_rn(static_cast<float>((q4 >> (8 * k)) & 0xffu), s);
-      y[k] = affine ? __fadd_rn(v, b) : v;
-    }
+    for (int k = 0; k < 4; ++k) y[k] = px_value<FAST>(q4, k, c);
     if constexpr (O == OPTB_OUT_F32) {
       float4 f = make_float4(y[0], y[1], y[2], y[3]);
       stg16(dst, *reinterpret_cast<uint4*>(&f));
     } else if constexpr (O == OPTB_OUT_F16) {
-      const __half h0 = __float2half_rn(y[0]), h1 = __float2half_rn(y[1]);
-      const __half h2 = __float2half_rn(y[2]), h3 = __float2half_rn(y[3]);
-      uint2 u;
-      u.x = static_cast<uint32_t>(__half_as_ushort(h0)) |
-            (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-      u.y = static_cast<uint32_t>(__half_as_ushort(h2)) |
-            (static_cast<uint32_t>(__half_as_ushort(h3)) << 16);
-      stg8(dst, u);
+      const __half2 h0 = __floats2half2_rn(y[0], y[1]), h1 = __floats2half2_rn(y[2], y[3]);
+      stg8(dst, make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1)));
     } else {
-      const __nv_bfloat16 h0 = __float2bfloat16_rn(y[0]), h1 = __float2bfloat16_rn(y[1]);
-      const __nv_bfloat16 h2 = __float2bfloat16_rn(y[2]), h3 = __float2bfloat16_rn(y[3]);
-      uint2 u;
-      u.x = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
-            (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
-      u.y = static_cast<uint32_t>(__bfloat16_as_ushort(h2)) |
-            (static_cast<uint32_t>(__bfloat16_as_ushort(h3)) << 16);
-      stg8(dst, u);
+      const __nv_bfloat162 h0 = __floats2bfloat162_rn(y[0], y[1]), h1 = __floats2bfloat162_rn(y[2], y[3]);
+      stg8(dst, make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1)));
     }
   }
 };
 
 // 8 consecutive decoded pixels -> 8 binary16 / bfloat16 values, one 128-bit store.
 struct Out8 {
-  template <int O>
-  static __device__ __forceinline__ void put(void* dst, uint2 q8, float s, float b, bool affine) {
+  template <int O, bool FAST>
+  static __device__ __forceinline__ void put(void* dst, uint2 q8, const PxScale& c) {
     uint32_t w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t src = k < 2 ? q8.x : q8.y;
-      const int sh = 16 * (k & 1);
-      float y0 = __fmul_rn(static_cast<float>((src >> sh) & 0xffu), s);
-      float y1 = __fmul_rn(static_cast<float>((src >> (sh + 8)) & 0xffu), s);
-      if (affine) {
-        y0 = __fadd_rn(y0, b);
-        y1 = __fadd_rn(y1, b);
-      }
+      const int sh = 2 * (k & 1);
+      const float y0 = px_value<FAST>(src, sh, c), y1 = px_value<FAST>(src, sh + 1, c);
       if constexpr (O == OPTB_OUT_F16) {
         const __half2 h = __floats2half2_rn(y0, y1);
         w[k] = *reinterpret_cast<const uint32_t*>(&h);
@@ -887,22 +898,47 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
         const uint64_t r0L = (static_cast<uint64_t>(r0hi) << 32) | r0lo;
         const uint64_t gL = (static_cast<uint64_t>(ghi) << 32) | glo;
         const int sub = PX * (lane % LPS);
-        const uint64_t px = gL * 16 + sub;
+        uint8_t* dst = static_cast<uint8_t*>(out) + (r0L * ostride + gL * 16 + sub) * ES;
+        const uint64_t dstep = ostride * ES;
+        const uint8_t* src = slot + L * 16 + sub;
+        auto put_row = [&](uint8_t* d, int i, const PxScale& sc, auto fast) {
+          constexpr bool F = decltype(fast)::value;
+          if constexpr (PX == 4) {
+            Out4::put<O, F>(d, *reinterpret_cast<const uint32_t*>(src + i * 512), sc);
+          } else {
+            Out8::put<O, F>(d, *reinterpret_cast<const uint2*>(src + i * 512), sc);
+          }
+        };
+        if (!e.class_scale) {  // one scale for every row (the runner's kPixelScale)
+          const PxScale sc = px_scale(e.scale, 0.0f, false);
+          if (sc.fast) {
 #pragma unroll
-        for (int i = 0; i < S::NI; ++i) {
-          if (i < static_cast<int>(nL)) {
-            const uint64_t row = r0L + i;
-            float s, b;
-            bool aff;
-            row_affine(e, row, s, b, aff);
-            uint8_t* dst = static_cast<uint8_t*>(out) + (row * ostride + px) * ES;
-            if constexpr (PX == 4) {
-              const uint32_t q4 = *reinterpret_cast<const uint32_t*>(slot + i * 512 + L * 16 + sub);
-              Out4::put<O>(dst, q4, s, b, aff);
-            } else {
-              const uint2 q8 = *reinterpret_cast<const uint2*>(slot + i * 512 + L * 16 + sub);
-              Out8::put<O>(dst, q8, s, b, aff);
+            for (int i = 0; i < S::NI; ++i) {
+              if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::true_type{});
+              dst += dstep;
             }
+          } else {
+#pragma unroll
+            for (int i = 0; i < S::NI; ++i) {
+              if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::false_type{});
+              dst += dstep;
+            }
+          }
+        } else {  // per-class (scale, bias) tables indexed by the row's class
+#pragma unroll
+          for (int i = 0; i < S::NI; ++i) {
+            if (i < static_cast<int>(nL)) {
+              float s, b;
+              bool aff;
+              row_affine(e, r0L + i, s, b, aff);
+              const PxScale sc = px_scale(s, b, aff);
+              if (sc.fast) {
+                put_row(dst, i, sc, std::true_type{});
+              } else {
+                put_row(dst, i, sc, std::false_type{});
+              }
+            }
+            dst += dstep;
           }
         }
       }

@@ -279,6 +279,43 @@ def test_float_epilogue_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype):
     assert np.array_equal(got, ref.view(got.dtype))
 
 
+@pytest.mark.parametrize("dtype", ["float32", "float16", "bfloat16"])
+def test_epilogue_scale_edges_vs_oracle(pkg, oracle_mod, torch_cuda, dtype):
+    """The float epilogue's fast form (FFMA identity for 0 < s < 2^100) and its
+    plain-FMUL fallback agree bit for bit with the reference product on edge
+    scales: negative, +-0, subnormal, overflowing, the 2^100 boundary; also
+    per-class tables mixing both forms."""
+    torch, C, O = torch_cuda, pkg.codec, oracle_mod
+    rng = np.random.default_rng(17)
+    P, B, nb = 768, 32, 2
+    L, cont, offs, rc, ro = _stream_case(pkg, torch, O, 1, 16, P, B, nb, rng)
+    dt = getattr(torch, dtype)
+    kind = {"float32": O.F32, "float16": O.F16, "bfloat16": O.BF16}[dtype]
+    f32 = lambda v: float(np.float32(v))  # noqa: E731
+    scales = [f32(1 / 255), -f32(1 / 255), 0.0, -0.0, f32(1e-42), f32(3e38), f32(2.0 ** 100),
+              float(np.nextafter(np.float32(2.0 ** 100), np.float32(0))), f32(0.75), f32(1.0)]
+    for sc in scales:
+        out = torch.empty((B * nb, P), dtype=dt, device="cuda")
+        C.decode_dev(L, cont, out, scale=sc)
+        C.sync()
+        want = O.decode_stream(rc, ro, 1, 16, P, B, nb, out_dtype=kind, scale=sc)
+        got = out.cpu()
+        got = got.numpy().view(np.uint32) if dtype == "float32" else got.view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, want.view(got.dtype)), sc
+    row_class = rng.integers(0, len(scales), size=B * nb).astype(np.int32)
+    cs = np.array(scales, np.float32)
+    cb = rng.uniform(-2, 2, len(scales)).astype(np.float32)
+    out = torch.empty((B * nb, P), dtype=dt, device="cuda")
+    C.decode_dev(L, cont, out, class_scale=torch.from_numpy(cs).cuda(), class_bias=torch.from_numpy(cb).cuda(),
+                 row_class=torch.from_numpy(row_class).cuda())
+    C.sync()
+    want = O.decode_stream(rc, ro, 1, 16, P, B, nb, out_dtype=kind, scale=1.0, class_scale=cs, class_bias=cb,
+                           row_class=row_class)
+    got = out.cpu()
+    got = got.numpy().view(np.uint32) if dtype == "float32" else got.view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, want.view(got.dtype))
+
+
 def test_per_class_epilogue(pkg, oracle_mod, torch_cuda):
     """Per-class preprocessing table (the GPU form of sampler.hpp:39-40's hook):
     identity table == plain epilogue; random table == oracle."""
