@@ -34,6 +34,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <type_traits>
 
 #include "internal.h"
@@ -1222,12 +1225,8 @@ template <int MODE, bool PTRS>
 cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
                       uint64_t* launches) {
   const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_encode_vec<MODE, PTRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_encode_vec<MODE, PTRS>), static_cast<int>(smem));
+  if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(k_encode_vec<MODE, PTRS>, kThreads, smem, sms, items);
   k_encode_vec<MODE, PTRS><<<grid, kThreads, smem, s>>>(g, rs, static_cast<uint8_t*>(cont), offs);
@@ -1286,12 +1285,8 @@ cudaError_t dec_vec_launch(const CUtensorMap& cm, const Geom& g, const void* con
                            const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   const size_t smem = TMA ? static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA + 1024
                           : static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::RAW;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_decode_vec<MODE, O, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_decode_vec<MODE, O, TMA>), static_cast<int>(smem));
+  if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(k_decode_vec<MODE, O, TMA>, kThreads, smem, sms, items);
   k_decode_vec<MODE, O, TMA><<<grid, kThreads, smem, s>>>(cm, g, static_cast<const uint8_t*>(cont), offs, e, out,
@@ -1318,12 +1313,8 @@ cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void*
   constexpr size_t enc = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
   constexpr size_t dec = static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA;
   constexpr size_t smem = (enc > dec ? enc : dec) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_roundtrip_vec<MODE, O, PTRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr = true;
-  }
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_roundtrip_vec<MODE, O, PTRS>), static_cast<int>(smem));
+  if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(k_roundtrip_vec<MODE, O, PTRS>, kThreads, smem, sms, items);
   k_roundtrip_vec<MODE, O, PTRS><<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), e, out, err);
@@ -1461,6 +1452,20 @@ cudaError_t launch_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uin
   k_synth<<<grid, 256, 0, s>>>(seed, first_row, n_rows, P, out, row_stride);
   ++*launches;
   return cudaGetLastError();
+}
+
+cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(kernel, dev, bytes);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 }  // namespace optb_b200

@@ -11,6 +11,11 @@
 
 namespace optb_b200 {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size): attributes are per device context, and several contexts on
+// different devices may share one process.
+cudaError_t ensure_smem_attr(const void* kernel, int bytes);
+
 // Sets the calling thread's optb_last_error() text; returns `code`.
 int set_error_text(int code, const std::string& message);
 

@@ -522,11 +522,8 @@ cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t max_m
       use_smem = 0;
       smem = kJWin * sizeof(uint32_t);
     }
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_shuffle, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 8192);
-      attr = true;
-    }
+    const cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_shuffle), 200 * 1024 + 8192);
+    if (ae != cudaSuccess) return ae;
     k_shuffle<<<n_cls, 64, smem, s>>>(a, use_smem);
     ++*launches;
   }

@@ -5,7 +5,8 @@
     compute-sanitizer --tool synccheck python tools/sanitize_smoke.py
 
 Covers the vector and generic codec paths for all modes and output types,
-partial chunks, gathers, the range-error latch, the class index, the SBS
+partial chunks, gathers, the range-error latch, the fused round trip (TMA
+decode half) with index and row-address gathers, the class index, the SBS
 cursor (parallel Fisher-Yates and the forced serial redo), the pipeline,
 OPTB dump/load and the record loader.  Results are checked against the
 oracle so a sanitizer run is also a parity run.
@@ -53,6 +54,28 @@ def main():
                     C.sync()
                 except pkg.errors.FormatError:
                     pass
+    # fused round trip (TMA decode half), index and row-address gathers, all outputs
+    for mode in (0, 1, 2):
+        P, B, nb = 768, 40, 2
+        pc = C.capacity(mode)
+        ds = rng.integers(0, 256, (64, P), dtype=np.uint8)
+        ds_d = torch.from_numpy(ds).to(dev)
+        idx = rng.integers(0, 64, B * nb).astype(np.int64)
+        idx_d = torch.from_numpy(idx).to(dev)
+        L = C.layout(mode, pc, P, B, nb)
+        rc, ro = O.encode_stream(ds, idx, mode, pc, B, nb)
+        ptrs = C.shard_row_ptrs_dev(idx_d, torch.tensor([ds_d.data_ptr()], dtype=torch.int64, device=dev), 64, P)
+        for dt in (torch.uint8, torch.float32, torch.bfloat16):
+            for rows_api in (False, True):
+                cont, offs = C.alloc_stream(L)
+                out = torch.empty((B * nb, P), dtype=dt, device=dev)
+                if rows_api:
+                    C.roundtrip_rows_dev(L, ptrs, cont, out, offsets=offs, scale=1 / 255)
+                else:
+                    C.roundtrip_dev(L, ds_d, cont, out, offsets=offs, row_index=idx_d, scale=1 / 255)
+                C.sync()
+                assert np.array_equal(cont.cpu().numpy()[: rc.size], rc)
+                n_checks += 1
     labels = (np.arange(3000) % 7).astype(np.int32)
     offs_d, mem_d = S.class_index_dev(labels, 7)
     p = S.plan([1 / 7] * 7, 21, 5)
