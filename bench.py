@@ -212,56 +212,55 @@ def run_reference(args):
     return 0
 
 def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, world, rows, images_per_step, red_dev):
-    """End-to-end steps through the public API with host buffers (see main)."""
+    """End-to-end steps with host buffers in and out (see main).  Two legs:
+    optb_pipeline_step_host -- ONE C-ABI call per step: the epoch's pinned host
+    dataset is uploaded into one of two device buffers (copy engine), the step
+    runs, the decoded rows are downloaded into pinned host memory (second copy
+    engine); consecutive calls overlap both PCIe directions and the kernels --
+    and a zero-copy leg in which the gather kernel reads the drawn rows
+    straight from pinned host memory."""
     out_shape = (rows, P)
     ds_host = ds.cpu().pin_memory()
-    h2d = copy_in = torch.cuda.Stream(dev)
     d2h = torch.cuda.Stream(dev)
     plan2 = S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED)
     results = []
     for zero_copy in (False, True):
         cur2 = S.BatchCursor.from_device_index(plan2, offs, mem, device=dev.index)
-        ds_devs = [] if zero_copy else [torch.empty_like(ds) for _ in range(2)]
-        pipe2 = Pipeline(cur2, ds_host if zero_copy else ds_devs[0], MODE, BATCH, BATCHES_PER_STEP,
+        pipe2 = Pipeline(cur2, ds_host if zero_copy else ds, MODE, BATCH, BATCHES_PER_STEP,
                          per_chunk=PER_CHUNK, shard=rank, n_shards=world, device=dev.index,
                          steps_per_draw=args.steps_per_draw)
         outs = [torch.empty(out_shape, dtype=torch.uint8, device=dev) for _ in range(2)]
         out_hosts = [torch.empty(out_shape, dtype=torch.uint8).pin_memory() for _ in range(2)]
         ev = lambda: torch.cuda.Event()  # noqa: E731
-        up_done, enc_done, dec_done, down_done = [ev(), ev()], [ev(), ev()], [ev(), ev()], [ev(), ev()]
+        dec_done, down_done = [ev(), ev()], [ev(), ev()]
         k_state = [0]
-
-        def upload(k):
-            b = k % 2
-            if k >= 2:
-                copy_in.wait_event(enc_done[b])  # step k-2 finished reading this buffer
-            with torch.cuda.stream(copy_in):
-                ds_devs[b].copy_(ds_host, non_blocking=True)
-            up_done[b].record(copy_in)
 
         def step():
             k = k_state[0]
             b = k % 2
             if not zero_copy:
-                if k == 0:
-                    upload(0)
-                upload(k + 1)  # the next step's inputs move while this one computes
-                stream.wait_event(up_done[b])
-                pipe2.set_dataset(ds_devs[b])
-            if k >= 2:
-                stream.wait_event(down_done[b])
-            pipe2.step(outs[b], stream)
-            enc_done[b].record(stream)
-            dec_done[b].record(stream)
-            d2h.wait_event(dec_done[b])
-            with torch.cuda.stream(d2h):
-                out_hosts[b].copy_(outs[b], non_blocking=True)
-            down_done[b].record(d2h)
+                pipe2.step_host(ds_host, out_hosts[b], stream)
+            else:
+                if k >= 2:
+                    stream.wait_event(down_done[b])
+                pipe2.step(outs[b], stream)
+                dec_done[b].record(stream)
+                d2h.wait_event(dec_done[b])
+                with torch.cuda.stream(d2h):
+                    out_hosts[b].copy_(outs[b], non_blocking=True)
+                down_done[b].record(d2h)
             k_state[0] += 1
+
+        def wait_all():
+            if not zero_copy:
+                pipe2.host_wait(stream)
+            else:
+                stream.wait_event(down_done[(k_state[0] - 1) % 2])
 
         with torch.cuda.stream(stream):
             for _ in range(max(4, args.warmup)):  # includes the sampler's generation-pool growth
                 step()
+            wait_all()
             torch.cuda.synchronize(dev)
             if world > 1:
                 dist.barrier()
@@ -269,7 +268,7 @@ def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, wo
             e0.record(stream)
             for _ in range(args.e2e_steps):
                 step()
-            stream.wait_event(down_done[(k_state[0] - 1) % 2])
+            wait_all()
             e1.record(stream)
             e1.synchronize()
             torch.cuda.synchronize(dev)
@@ -289,9 +288,10 @@ def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, wo
                         "ms_per_step": round(ms, 3), "check": ok,
                         "path": ("pinned host dataset read zero-copy by the gather-encode kernel -> decode -> "
                                  "D2H of the decoded rows (copy stream, double-buffered)") if zero_copy else
-                                ("bulk H2D of the epoch's pinned host dataset into one of two device buffers "
-                                 "(copy engine, overlapping the previous step) -> optb_pipeline_step (SBS draws, "
-                                 "gather-encode, decode) -> D2H of the decoded rows to pinned host (copy stream)")})
+                                ("optb_pipeline_step_host, one C-ABI call per step: bulk H2D of the epoch's pinned "
+                                 "host dataset into one of two device buffers (copy engine) -> SBS draws + fused "
+                                 "gather-encode-decode -> D2H of the decoded rows to pinned host (second copy "
+                                 "engine); consecutive steps overlap both PCIe directions")})
     return results[0], results[1]
 
 
@@ -549,7 +549,7 @@ def main():
                        "timing": "host wall clock around synchronised steps (the exchange is host-driven)"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU baseline runs at N = 1 only
         threads = os.cpu_count() or 1
         v, kind, sample, used = reference_rate(max(threads * 2, 8), threads, 3)
         cpu = {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": kind, "sample": sample}

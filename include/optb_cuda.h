@@ -324,6 +324,19 @@ int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** e
                         const int32_t** classes);
 /* The pipeline's container planes (valid for the last enqueued step). */
 const void* optb_pipeline_containers(const optb_pipeline* p);
+/* The same step on host buffers (the E-D path for a dataset in host memory):
+ * uploads dataset_host ([n_rows][row_stride] u8, pinned for overlap) into one
+ * of two internal device buffers on a copy stream, runs optb_pipeline_step
+ * on `stream` into an internal device buffer, and copies the decoded rows to
+ * out_host (layout as optb_pipeline_step's `out`) on a second copy stream.
+ * Asynchronous: consecutive calls overlap the upload of step k+1, the kernels
+ * and the download of step k.  out_host is complete after
+ * optb_pipeline_host_wait. */
+int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint64_t n_rows,
+                            uint64_t row_stride, void* out_host, void* stream);
+/* Wait for every download enqueued by optb_pipeline_step_host: on the host
+ * (stream NULL), or by making `stream` wait for the last one. */
+int optb_pipeline_host_wait(optb_pipeline* p, void* stream);
 /* Device-timed durations (ms) of a completed step (last 64 steps): its SBS
  * draws (side stream), its gather-encode and its decode (for a fused
  * round-trip step: the whole launch in enc_ms and 0 in dec_ms). */

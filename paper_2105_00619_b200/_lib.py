@@ -112,6 +112,8 @@ SIGNATURES = {
     "optb_pipeline_create":(ct.c_int, [vp, ct.POINTER(PipelineDesc), ct.POINTER(vp)]),
     "optb_pipeline_step": (ct.c_int, [vp, vp, vp]),
     "optb_pipeline_set_dataset": (ct.c_int, [vp, vp, ct.c_uint64]),
+    "optb_pipeline_step_host": (ct.c_int, [vp, vp, ct.c_uint64, ct.c_uint64, vp, vp]),
+    "optb_pipeline_host_wait": (ct.c_int, [vp, vp]),
     "optb_pipeline_draws": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(vp), ct.POINTER(vp)]),
     "optb_pipeline_containers": (vp, [vp]),
     "optb_pipeline_timings": (ct.c_int, [vp, ct.c_uint64, fp, fp, fp]),

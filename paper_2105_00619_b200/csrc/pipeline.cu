@@ -14,6 +14,11 @@
 // Reference invariants kept: at most two live draw buffers (pipeline.hpp:19-20),
 // in-order delivery, and errors surfacing before the affected step is consumed
 // (device-side format errors latch in the context, optb_ctx_sync).
+// optb_pipeline_step_host is the same step on HOST buffers: the epoch's
+// dataset is uploaded into one of two device buffers on a copy stream (while
+// the previous step computes and downloads), the step runs, and the decoded
+// rows are copied back on a second copy stream -- both PCIe directions and
+// the kernels overlap across consecutive calls.
 // Built only on the public C ABI (include/optb_cuda.h).
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -41,6 +46,16 @@ struct optb_pipeline {
   uint64_t step = 0;   // next step to deliver
   uint64_t calls = 0;  // SBS calls enqueued
   bool timing = false;
+  // host leg (optb_pipeline_step_host): double-buffered device copies of the
+  // host dataset and of the decoded rows, with their own copy streams
+  struct Host {
+    cudaStream_t up = nullptr, down = nullptr;
+    uint8_t* ds[2] = {};
+    uint8_t* out[2] = {};
+    uint64_t ds_cap = 0, out_cap = 0;
+    cudaEvent_t up_done[2] = {}, used[2] = {}, down_done[2] = {};
+    uint64_t k = 0;  // host steps enqueued
+  } host;
 };
 
 namespace {
@@ -135,7 +150,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
     if (p->timing) cudaEventRecord(p->t_e1[r], s);
     if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
   }
-  if (p->timing) cudaEventRecord(p->t_d1[r], s);
+  if (p->timing && p->d.split_kernels) cudaEventRecord(p->t_d1[r], s);  // fused: the launch ends at t_e1
   ++p->step;
   return OPTB_OK;
 }
@@ -165,20 +180,117 @@ int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, 
   if (!p || !p->timing || step >= p->step || step + kTimingRing <= p->step) return OPTB_ERR_ARG;
   const int r = static_cast<int>(step % kTimingRing);
   const int rc = static_cast<int>((step / p->spd) % kTimingRing);
-  if (cudaEventSynchronize(p->t_d1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  cudaEvent_t last = p->d.split_kernels ? p->t_d1[r] : p->t_e1[r];
+  if (cudaEventSynchronize(last) != cudaSuccess) return OPTB_ERR_CUDA;
   if (sbs_ms) {  // the SBS call that produced this step's draws, per step
     if (cudaEventElapsedTime(sbs_ms, p->t_s0[rc], p->t_s1[rc]) != cudaSuccess) return OPTB_ERR_CUDA;
     *sbs_ms /= static_cast<float>(p->spd);
   }
   if (enc_ms && cudaEventElapsedTime(enc_ms, p->t_e0[r], p->t_e1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
-  if (dec_ms && cudaEventElapsedTime(dec_ms, p->t_e1[r], p->t_d1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (dec_ms) {
+    if (!p->d.split_kernels) {
+      *dec_ms = 0.0f;  // one fused launch: all of it is in enc_ms
+    } else if (cudaEventElapsedTime(dec_ms, p->t_e1[r], p->t_d1[r]) != cudaSuccess) {
+      return OPTB_ERR_CUDA;
+    }
+  }
   return OPTB_OK;
+}
+
+int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint64_t n_rows, uint64_t row_stride,
+                            void* out_host, void* stream) {
+  if (!p || !dataset_host || !out_host || !n_rows) return OPTB_ERR_ARG;
+  if (row_stride == 0) row_stride = p->d.layout.pixels;
+  if (row_stride < p->d.layout.pixels) return OPTB_ERR_ARG;
+  auto& h = p->host;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t es = p->d.epilogue.out_dtype == OPTB_OUT_U8 ? 1 : p->d.epilogue.out_dtype == OPTB_OUT_F32 ? 4 : 2;
+  const uint64_t ors = p->d.epilogue.out_row_stride ? p->d.epilogue.out_row_stride : p->d.layout.pixels;
+  const uint64_t ds_bytes = n_rows * row_stride, out_bytes = p->rows * ors * es;
+  if (!h.up) {
+    bool ok = cudaStreamCreateWithFlags(&h.up, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&h.down, cudaStreamNonBlocking) == cudaSuccess;
+    for (int b = 0; b < 2 && ok; ++b)
+      ok = cudaEventCreateWithFlags(&h.up_done[b], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h.used[b], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h.down_done[b], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) return OPTB_ERR_CUDA;
+  }
+  if (h.ds_cap < ds_bytes || h.out_cap < out_bytes) {  // (re)size: drain the leg first
+    if (cudaStreamSynchronize(h.up) != cudaSuccess || cudaStreamSynchronize(h.down) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return OPTB_ERR_CUDA;
+    for (int b = 0; b < 2; ++b) {
+      if (h.ds_cap < ds_bytes) {
+        if (h.ds[b]) cudaFree(h.ds[b]);
+        h.ds[b] = nullptr;
+        if (cudaMalloc(&h.ds[b], ds_bytes) != cudaSuccess) return OPTB_ERR_CUDA;
+      }
+      if (h.out_cap < out_bytes) {
+        if (h.out[b]) cudaFree(h.out[b]);
+        h.out[b] = nullptr;
+        if (cudaMalloc(&h.out[b], out_bytes) != cudaSuccess) return OPTB_ERR_CUDA;
+      }
+    }
+    h.ds_cap = h.ds_cap < ds_bytes ? ds_bytes : h.ds_cap;
+    h.out_cap = h.out_cap < out_bytes ? out_bytes : h.out_cap;
+    h.k = 0;  // fresh buffers: nothing in flight to wait for
+  }
+  const int b = static_cast<int>(h.k % 2);
+  // H2D of this step's dataset once step k-2 no longer reads buffer b; it
+  // runs on the copy engine while step k-1 computes and copies out
+  if (h.k >= 2 && cudaStreamWaitEvent(h.up, h.used[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (cudaMemcpyAsync(h.ds[b], dataset_host, ds_bytes, cudaMemcpyHostToDevice, h.up) != cudaSuccess ||
+      cudaEventRecord(h.up_done[b], h.up) != cudaSuccess || cudaStreamWaitEvent(s, h.up_done[b], 0) != cudaSuccess)
+    return OPTB_ERR_CUDA;
+  if (h.k >= 2 && cudaStreamWaitEvent(s, h.down_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  const uint8_t* prev_ds = p->d.dataset;
+  const uint64_t prev_stride = p->d.row_stride;
+  p->d.dataset = h.ds[b];
+  p->d.row_stride = row_stride;
+  int st = optb_pipeline_step(p, h.out[b], stream);
+  p->d.dataset = prev_ds;
+  p->d.row_stride = prev_stride;
+  if (st) return st;
+  if (cudaEventRecord(h.used[b], s) != cudaSuccess || cudaStreamWaitEvent(h.down, h.used[b], 0) != cudaSuccess ||
+      cudaMemcpyAsync(out_host, h.out[b], out_bytes, cudaMemcpyDeviceToHost, h.down) != cudaSuccess ||
+      cudaEventRecord(h.down_done[b], h.down) != cudaSuccess)
+    return OPTB_ERR_CUDA;
+  ++h.k;
+  return OPTB_OK;
+}
+
+int optb_pipeline_host_wait(optb_pipeline* p, void* stream) {
+  if (!p) return OPTB_ERR_ARG;
+  auto& h = p->host;
+  if (!h.up || h.k == 0) return OPTB_OK;
+  if (!stream) {  // host wait: every upload and download enqueued so far
+    if (cudaStreamSynchronize(h.up) != cudaSuccess || cudaStreamSynchronize(h.down) != cudaSuccess)
+      return OPTB_ERR_CUDA;
+    return OPTB_OK;
+  }
+  // device wait: the last download (it follows every earlier step's work)
+  const int b = static_cast<int>((h.k - 1) % 2);
+  return cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), h.down_done[b], 0) == cudaSuccess ? OPTB_OK
+                                                                                                : OPTB_ERR_CUDA;
 }
 
 void optb_pipeline_destroy(optb_pipeline* p) {
   if (!p) return;
   if (p->side) cudaStreamSynchronize(p->side);
   cudaDeviceSynchronize();
+  {
+    auto& h = p->host;
+    for (int b = 0; b < 2; ++b) {
+      if (h.ds[b]) cudaFree(h.ds[b]);
+      if (h.out[b]) cudaFree(h.out[b]);
+      if (h.up_done[b]) cudaEventDestroy(h.up_done[b]);
+      if (h.used[b]) cudaEventDestroy(h.used[b]);
+      if (h.down_done[b]) cudaEventDestroy(h.down_done[b]);
+    }
+    if (h.up) cudaStreamDestroy(h.up);
+    if (h.down) cudaStreamDestroy(h.down);
+  }
   for (int b = 0; b < 2; ++b) {
     if (p->ex[b]) cudaFree(p->ex[b]);
     if (p->cls[b]) cudaFree(p->cls[b]);

@@ -56,6 +56,25 @@ class Pipeline:
         check(lib.optb_pipeline_step(self._h, ct.c_void_p(out.data_ptr()), ct.c_void_p(stream.cuda_stream)))
         self.steps += 1
 
+    def step_host(self, dataset_host, out_host, stream=None):
+        """The step on host buffers (optb_pipeline_step_host): ``dataset_host``
+        ([N, >=P] u8 CPU tensor, pinned for overlap) is uploaded, the step
+        runs, and the decoded rows land in ``out_host`` (CPU tensor shaped
+        like ``step``'s ``out``) -- asynchronously; see host_wait()."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self._keep = self._keep[:4] + (dataset_host, out_host)
+        check(lib.optb_pipeline_step_host(self._h, ct.c_void_p(dataset_host.data_ptr()), dataset_host.shape[0],
+                                          dataset_host.stride(0), ct.c_void_p(out_host.data_ptr()),
+                                          ct.c_void_p(stream.cuda_stream)))
+        self.steps += 1
+
+    def host_wait(self, stream=None):
+        """Every step_host download has landed (stream None: block the host),
+        or `stream` waits for them (device-side)."""
+        check(lib.optb_pipeline_host_wait(self._h, None if stream is None else ct.c_void_p(stream.cuda_stream)))
+
     def set_dataset(self, dataset):
         """Rows for subsequent steps come from `dataset` (same shape)."""
         self._keep = self._keep + (dataset,)

@@ -76,3 +76,58 @@ def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda):
             want = O.decode_stream(cont, None, 1, 16, P, B, nb, out_dtype=O.F32, scale=1.0,
                                    class_scale=cs.cpu().numpy(), class_bias=cb.cpu().numpy(), row_class=c)
             assert np.array_equal(outs[r][step].cpu().numpy().view(np.uint32), want.view(np.uint32)), (step, r)
+
+
+
+def test_c2_full_size_fused_pipeline(pkg, oracle_mod, torch_cuda):
+    """The bench workload at full size (C2: 50 000 x 32x32x3, 100 classes,
+    B = 512, 97 batches per step, exact128, fused launch): for three steps the
+    decoded rows are exactly the dataset rows the oracle cursor draws
+    (exact128 at capacity is lossless), so draws and codec both match."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    S = pkg.sampler
+    N, K, B, nb, P = 50000, 100, 512, 97, 3072
+    labels = (np.arange(N) % K).astype(np.int32)
+    ds = torch.randint(0, 256, (N, P), dtype=torch.uint8, device="cuda")
+    offs, mem = S.class_index_dev(torch.from_numpy(labels).cuda(), K)
+    cur = S.BatchCursor.from_device_index(S.plan([1.0 / K] * K, B, 1234), offs, mem)
+    pipe = Pipeline(cur, ds, 1, B, nb, per_chunk=16, steps_per_draw=2)
+    assert pipe.fused
+    ro, rm = O.class_index(labels, K)
+    ref = O.Cursor(O.sbs_plan([1.0 / K] * K, B), ro, rm, B, 1234)
+    out = torch.empty((B * nb, P), dtype=torch.uint8, device="cuda")
+    for step in range(3):
+        pipe.step(out)
+        pkg.codec.sync()
+        want, _ = ref.next(nb)
+        assert torch.equal(out, ds[torch.from_numpy(want).cuda()]), step
+    pipe.close()
+
+
+@pytest.mark.parametrize("dtype", ["uint8", "bfloat16"])
+def test_pipeline_step_host_vs_oracle(pkg, oracle_mod, torch_cuda, dtype):
+    """optb_pipeline_step_host: host dataset in, host rows out, one C-ABI call
+    per step (uploads and downloads on the library's copy streams) == the
+    oracle's decode of the reference-stream draws, for every step."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P = 64, 5, 768
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    ds_host = torch.from_numpy(ds).pin_memory()
+    dt = getattr(torch, dtype)
+    pipe = Pipeline(cur, ds_host.cuda(), 1, B, nb, per_chunk=16, out_dtype=dt, scale=SCALE, steps_per_draw=2)
+    outs = [torch.empty((B * nb, P), dtype=dt).pin_memory() for _ in range(5)]
+    for o in outs:
+        pipe.step_host(ds_host, o)
+    pipe.host_wait()
+    pkg.codec.sync()
+    kind = {"uint8": O.U8, "bfloat16": O.BF16}[dtype]
+    for step in range(5):
+        ex, _ = ref.next(nb)
+        cont, offs_ = O.encode_stream(ds, ex, 1, 16, B, nb)
+        want = O.decode_stream(cont, offs_, 1, 16, P, B, nb, out_dtype=kind, scale=SCALE)
+        got = outs[step] if dtype == "uint8" else outs[step].view(torch.int16)
+        assert np.array_equal(got.numpy().view(want.dtype), want), step
+    pipe.close()
