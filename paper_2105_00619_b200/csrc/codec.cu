@@ -476,17 +476,27 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       const ChunkPos c = walk_chunk(g, wf);
       pend_n = c.n;
       pend_gi = wf.gi;
+      // uniform source choice outside the unrolled loop, predicated loads
+      // inside it (no per-row branches)
+      if constexpr (PTRS) {
+        const unsigned long long* rp = reinterpret_cast<const unsigned long long*>(src.ptrs) + c.r0;
 #pragma unroll
-      for (int i = 0; i < S::NI; ++i) {
-        const uint64_t r = c.r0 + i;
-        if constexpr (PTRS) {
-          rows[i] = (i < static_cast<int>(c.n)) ? __ldg(reinterpret_cast<const unsigned long long*>(src.ptrs) + r)
-                                                : 0ull;
-        } else {
-          rows[i] = (i < static_cast<int>(c.n))
-                        ? static_cast<uint32_t>(row_index ? __ldg(row_index + r) : static_cast<int64_t>(r))
-                        : 0u;
+        for (int i = 0; i < S::NI; ++i) {
+          RowT v = 0;
+          if (i < static_cast<int>(c.n)) v = __ldg(rp + i);
+          rows[i] = v;
         }
+      } else if (row_index) {
+        const int64_t* rp = row_index + c.r0;
+#pragma unroll
+        for (int i = 0; i < S::NI; ++i) {
+          RowT v = 0;
+          if (i < static_cast<int>(c.n)) v = static_cast<uint32_t>(__ldg(rp + i));
+          rows[i] = v;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < S::NI; ++i) rows[i] = static_cast<RowT>(c.r0 + i);  // used only for i < n
       }
     }
     walk_advance(wf, step, g, G);
@@ -634,8 +644,8 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
 // ------------------------------------------------------------------ K2 / K4
 // Decode.  Container words (and, lossless, the tile's parity bits) arrive in
 // a warp-private ring slot, either by cp.async straight into the XOR-swizzled
-// slot (any mode) or, for the exact and f64 modes, as ONE 2D TMA tensor load
-// per tile (the tile's 512*WC contiguous bytes as a [rows][128 B] box with the
+// slot or as ONE 2D TMA tensor load per tile (parity bits by cp.async next to
+// it) (the tile's 512*WC contiguous bytes as a [rows][128 B] box with the
 // hardware's 128-byte swizzle, completion on a per-stage mbarrier).  Each
 // pixel's word is range checked, lossless fields are expanded back to byte
 // lanes, the 16x16 transpose gives 16 pixels of every image per lane,
@@ -671,7 +681,6 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
   constexpr int SLOT = TMA ? DecSlot<MODE>::TMA : DecSlot<MODE>::RAW;
-  static_assert(!TMA || !S::OFFS, "TMA decode covers the exact and f64 modes");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* ring = smem_base + warp * kStages * SLOT;
   uint64_t* bar = bars + warp * kStages;
@@ -735,7 +744,7 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
         }
       }
     }
-    if constexpr (!TMA) cp_async_commit();
+    if constexpr (!TMA || S::OFFS) cp_async_commit();  // words (cp.async path) / parity bits
     if constexpr (S::OFFS) walk_advance(wi, step, g, G);
   };
 
@@ -745,9 +754,8 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
   uint32_t phase = 0;
   for (uint64_t base = first; base < items; base += stride) {
     issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
-    if constexpr (TMA) {
-      mbar_wait(bar + stage, phase);
-    } else {
+    if constexpr (TMA) mbar_wait(bar + stage, phase);
+    if constexpr (!TMA || S::OFFS) {
       cp_async_wait<kStages - 1>();
       __syncwarp();
     }
@@ -954,7 +962,7 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
       phase ^= 1u;
     }
   }
-  if constexpr (!TMA) cp_async_wait<0>();
+  if constexpr (!TMA || S::OFFS) cp_async_wait<0>();
 }
 
 template <int MODE, int O, bool TMA>
@@ -1299,10 +1307,8 @@ template <int MODE, int O>
 cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
                     DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   CUtensorMap cm;
-  if constexpr (!VecMode<MODE>::OFFS) {
-    if (tma_decode_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
-      return dec_vec_launch<MODE, O, true>(cm, g, cont, offs, e, out, err, s, sms, launches);
-  }
+  if (tma_decode_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
+    return dec_vec_launch<MODE, O, true>(cm, g, cont, offs, e, out, err, s, sms, launches);
   memset(&cm, 0, sizeof cm);
   return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
