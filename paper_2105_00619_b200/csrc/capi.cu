@@ -384,7 +384,7 @@ int roundtrip(optb_ctx* c, const optb_layout* L, const RowSrc& rs, void* contain
   if (ep.row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "decode: out_row_stride < pixels");
   const Geom g = make_geom(L);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_roundtrip(g, rs, containers, ep, out, c->d_err, s, c->sms, &c->launches);
+  cudaError_t e = launch_roundtrip(g, rs, containers, offsets, ep, out, c->d_err, s, c->sms, &c->launches);
   if (e == cudaErrorNotSupported) {
     e = launch_encode(g, rs, containers, offsets, s, c->sms, &c->launches);
     if (e != cudaSuccess) return cuda_err(e, "encode launch");

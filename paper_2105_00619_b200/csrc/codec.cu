@@ -447,16 +447,20 @@ __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> byte
 // PTRS: stream row r is read from the absolute address src.ptrs[r] (this
 // GPU's HBM, a peer GPU's HBM over NVLink, mapped pinned host memory) instead
 // of src.images + src.index[r] * src.stride.
+// warp_region: bytes of shared memory per warp (its ring), >= kStages * slot;
+// the fused kernel gives both bodies the same per-warp region so that a warp
+// in one phase never touches another warp's ring in the other phase.
 template <int MODE, bool PTRS>
 __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
-                                            uint8_t* __restrict__ offsets, uint8_t* smem_base) {
+                                            uint8_t* __restrict__ offsets, uint8_t* smem_base,
+                                            uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT) {
   const uint8_t* __restrict__ images = src.images;
   const uint64_t row_stride = src.stride;
   const int64_t* __restrict__ row_index = src.index;
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_base + warp * kStages * S::ENC_SLOT;
+  uint8_t* ring = smem_base + warp * warp_region;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
@@ -677,12 +681,12 @@ template <int MODE, int O, bool TMA>
 __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom& g, const uint8_t* __restrict__ cont,
                                             const uint8_t* __restrict__ offsets, const Epi& e,
                                             void* __restrict__ out, DevError* err, uint8_t* smem_base,
-                                            uint64_t* bars) {
+                                            uint64_t* bars, uint32_t warp_region = 0) {
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
   constexpr int SLOT = TMA ? DecSlot<MODE>::TMA : DecSlot<MODE>::RAW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_base + warp * kStages * SLOT;
+  uint8_t* ring = smem_base + warp * (warp_region ? warp_region : kStages * SLOT);
   uint64_t* bar = bars + warp * kStages;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
@@ -697,6 +701,7 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
   }
 
   const WalkStep step = walk_step(g, G, stride);
+  const bool bulk_parity = S::OFFS && g.P % 512 == 0;
   Walk wi = walk_at(g, G, first + lane);  // next tile to issue (parity planes)
   Walk wc = wi;                           // the tile being decoded
   auto issue = [&](uint64_t base, int stage) {
@@ -723,6 +728,21 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
         }
       }
       if constexpr (S::OFFS) {
+        if (bulk_parity) {
+          // P % 512 == 0: the tile lies in one chunk and image i's 512 parity
+          // bits are 64 contiguous, 64-aligned bytes of the plane -- four
+          // 16-byte cp.async.cg per image (L2, never a stale L1 line: the
+          // fused round trip reads back bits this warp just wrote)
+          const uint64_t k = wi.k, gi0 = wi.gi - lane;
+          const uint32_t n = walk_chunk(g, wi).n;
+          const uint8_t* plane = offsets + k * g.ostride + 2 * gi0;
+#pragma unroll
+          for (int j = lane; j < 4 * S::NI; j += 32) {
+            const int i = j >> 2, part = j & 3;
+            if (i < static_cast<int>(n))
+              cp_async16(slot + S::WORDS_B + i * 64 + part * 16, plane + (static_cast<uint64_t>(i) * g.P) / 8 + part * 16);
+          }
+        } else {
         // parity bits of lane pairs (4 bytes, 4-aligned as P % 32 == 0)
         const uint64_t t = wi.t;
         if ((lane & 1) == 0 && t < items) {
@@ -741,6 +761,7 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
               }
             }
           }
+        }
         }
       }
     }
@@ -984,20 +1005,29 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
 // No warp reads another warp's containers, so no grid-wide barrier is needed;
 // the kernel saves one launch's ramp-up and tail.  Exact and f64 modes (the
 // decode half reads each tile with one TMA tensor load).
+// Per-warp shared-memory region of the fused kernel: room for either ring,
+// 1024-aligned so every TMA slot stays 1024-aligned.
+template <int MODE>
+struct RtRegion {
+  static constexpr uint32_t ENC = kStages * VecMode<MODE>::ENC_SLOT;
+  static constexpr uint32_t DEC = kStages * DecSlot<MODE>::TMA;
+  static constexpr uint32_t BYTES = ((ENC > DEC ? ENC : DEC) + 1023) / 1024 * 1024;
+};
+
 template <int MODE, int O, bool PTRS>
 __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont, Epi e,
-                    void* __restrict__ out, DevError* err) {
+    k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
+                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bars[kWarps * kStages];
   uint8_t* base = align1024(smem_raw);
-  encode_body<MODE, PTRS>(g, src, cont, nullptr, base);
+  encode_body<MODE, PTRS>(g, src, cont, offsets, base, RtRegion<MODE>::BYTES);
   // this warp's container stores (generic proxy) before its TMA reads of
   // them, and its staging writes before the TMA fills of the same slots
   fence_proxy_async_global();
   fence_proxy_async_smem();
   __syncwarp();
-  decode_body<MODE, O, true>(&cmap, g, cont, nullptr, e, out, err, base, bars);
+  decode_body<MODE, O, true>(&cmap, g, cont, offsets, e, out, err, base, bars, RtRegion<MODE>::BYTES);
 }
 
 // ------------------------------------------------------------------ generic
@@ -1314,36 +1344,35 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
 }
 
 template <int MODE, int O, bool PTRS>
-cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, const Epi& e, void* out,
-                   DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  constexpr size_t enc = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
-  constexpr size_t dec = static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA;
-  constexpr size_t smem = (enc > dec ? enc : dec) + 1024;
+cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, const Epi& e,
+                   void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  constexpr size_t smem = static_cast<size_t>(kWarps) * RtRegion<MODE>::BYTES + 1024;
   cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_roundtrip_vec<MODE, O, PTRS>), static_cast<int>(smem));
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(k_roundtrip_vec<MODE, O, PTRS>, kThreads, smem, sms, items);
-  k_roundtrip_vec<MODE, O, PTRS><<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), e, out, err);
+  k_roundtrip_vec<MODE, O, PTRS><<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out,
+                                                              err);
   ++*launches;
   return cudaGetLastError();
 }
 
 template <int MODE, bool PTRS>
-cudaError_t rt_vec_out(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, const Epi& e, void* out,
-                       DevError* err, cudaStream_t s, int sms, uint64_t* l) {
+cudaError_t rt_vec_out(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
+                       const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* l) {
   switch (e.dtype) {
-    case OPTB_OUT_U8: return rt_vec<MODE, OPTB_OUT_U8, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
-    case OPTB_OUT_F32: return rt_vec<MODE, OPTB_OUT_F32, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
-    case OPTB_OUT_F16: return rt_vec<MODE, OPTB_OUT_F16, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
-    default: return rt_vec<MODE, OPTB_OUT_BF16, PTRS>(cm, g, rs, cont, e, out, err, s, sms, l);
+    case OPTB_OUT_U8: return rt_vec<MODE, OPTB_OUT_U8, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
+    case OPTB_OUT_F32: return rt_vec<MODE, OPTB_OUT_F32, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
+    case OPTB_OUT_F16: return rt_vec<MODE, OPTB_OUT_F16, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
+    default: return rt_vec<MODE, OPTB_OUT_BF16, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
   }
 }
 
 template <int MODE>
-cudaError_t rt_vec_any(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, const Epi& e, void* out,
-                       DevError* err, cudaStream_t s, int sms, uint64_t* l) {
-  if (rs.ptrs) return rt_vec_out<MODE, true>(cm, g, rs, cont, e, out, err, s, sms, l);
-  return rt_vec_out<MODE, false>(cm, g, rs, cont, e, out, err, s, sms, l);
+cudaError_t rt_vec_any(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
+                       const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* l) {
+  if (rs.ptrs) return rt_vec_out<MODE, true>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
+  return rt_vec_out<MODE, false>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
 }
 
 template <int MODE>
@@ -1432,21 +1461,30 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
   }
 }
 
-cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rs, void* containers, const Epi& e, void* out,
-                             DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rs, void* containers, uint8_t* offsets, const Epi& e,
+                             void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
   const bool vec = vec_ok(g) && rows_vec_ok(rs) && aligned16(containers) && aligned16(out) &&
                    (e.row_stride * es) % 16 == 0;
-  const bool tma_mode = g.mode == OPTB_EXACT64 || g.mode == OPTB_EXACT128 || g.mode == OPTB_F64;
+  // lossless: the decode half stages parity bits with 16-byte L2 copies, which
+  // needs whole tiles per chunk (P % 512) and a 16-byte aligned plane
+  const bool lossless = g.mode == OPTB_LOSSLESS64 || g.mode == OPTB_LOSSLESS128;
+  const bool fusable = !lossless || (g.P % 512 == 0 && aligned16(offsets));
   CUtensorMap cm;
-  if (!vec || !tma_mode || !tma_decode_enabled() || !container_map(&cm, containers, g.chunks * g.P * g.wc, g.wc))
+  if (!vec || !fusable || !tma_decode_enabled() ||
+      !container_map(&cm, containers, g.chunks * g.P * g.wc, g.wc))
     return cudaErrorNotSupported;  // caller: separate encode + decode launches
   switch (g.mode) {
-    case OPTB_EXACT64: return rt_vec_any<OPTB_EXACT64>(cm, g, rs, containers, e, out, err, s, sms, launches);
-    case OPTB_EXACT128: return rt_vec_any<OPTB_EXACT128>(cm, g, rs, containers, e, out, err, s, sms, launches);
+    case OPTB_EXACT64: return rt_vec_any<OPTB_EXACT64>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_EXACT128: return rt_vec_any<OPTB_EXACT128>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_LOSSLESS64:
+      return rt_vec_any<OPTB_LOSSLESS64>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_LOSSLESS128:
+      return rt_vec_any<OPTB_LOSSLESS128>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
     default:
-      if (g.per_chunk <= 8) return rt_vec_any<kF64Narrow>(cm, g, rs, containers, e, out, err, s, sms, launches);
-      return rt_vec_any<OPTB_F64>(cm, g, rs, containers, e, out, err, s, sms, launches);
+      if (g.per_chunk <= 8)
+        return rt_vec_any<kF64Narrow>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+      return rt_vec_any<OPTB_F64>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
   }
 }
 

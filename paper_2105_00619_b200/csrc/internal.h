@@ -69,10 +69,11 @@ cudaError_t launch_encode(const Geom& g, const RowSrc& rows, void* containers, u
 cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* offsets,
                           const Epi& e, void* out, DevError* err, cudaStream_t s, int num_sms,
                           uint64_t* launches);
-// Encode + decode of the same stream in one launch (exact / f64 vector path);
+// Encode + decode of the same stream in one launch (vector path; lossless
+// modes need P % 512 == 0);
 // cudaErrorNotSupported when the geometry needs the separate launches.
-cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rows, void* containers, const Epi& e, void* out,
-                             DevError* err, cudaStream_t s, int num_sms, uint64_t* launches);
+cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rows, void* containers, uint8_t* offsets, const Epi& e,
+                             void* out, DevError* err, cudaStream_t s, int num_sms, uint64_t* launches);
 cudaError_t launch_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uint64_t P,
                          uint8_t* out, uint64_t row_stride, cudaStream_t s, int num_sms,
                          uint64_t* launches);

@@ -43,10 +43,10 @@ class Pipeline:
                             n_shards, E, 1 if record_timings else 0, steps_per_draw, 1 if split_kernels else 0)
         self._h = ct.c_void_p()
         check(lib.optb_pipeline_create(_lib.context(device), ct.byref(desc), ct.byref(self._h)))
-        # one fused launch per step (optb_roundtrip_dev) for the exact / f64
-        # modes on the vector path; the library falls back to two launches
-        self.fused = (not split_kernels and int(mode) in (0, 1, 2) and P % 16 == 0 and dataset.stride(0) % 16 == 0
-                      and dataset.data_ptr() % 16 == 0)
+        # one fused launch per step (optb_roundtrip_dev) on the vector path
+        # (lossless: P % 512 == 0); the library falls back to two launches
+        self.fused = (not split_kernels and P % 16 == 0 and dataset.stride(0) % 16 == 0
+                      and dataset.data_ptr() % 16 == 0 and (int(mode) in (0, 1, 2) or P % 512 == 0))
         self.steps = 0
 
     def step(self, out, stream=None):

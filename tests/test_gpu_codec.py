@@ -210,7 +210,10 @@ def test_stream_parity_vs_oracle(pkg, oracle_mod, torch_cuda, mode, per_chunk, P
     (2, 6, 3072, 256, 1),      # f64 narrow (fused)
     (2, 16, 3072, 64, 2),      # f64 lossy (fused, 16-image variant)
     (1, 16, 768, 1000, 1),     # items not a multiple of the warp tile
-    (3, 9, 3072, 512, 1),      # lossless: separate launches
+    (3, 9, 3072, 512, 1),      # lossless64 fused (P % 512 == 0)
+    (4, 18, 3072, 100, 2),     # lossless128 fused, partial chunks
+    (4, 11, 1024, 50, 2),      # lossless128 fused, per_chunk < capacity
+    (3, 9, 768, 64, 2),        # lossless, P % 512 != 0: separate launches
     (1, 16, 108, 40, 2),       # generic path: separate launches
 ])
 @pytest.mark.parametrize("dtype", ["uint8", "float32", "bfloat16"])
@@ -242,11 +245,11 @@ def test_roundtrip_dev_vs_oracle(pkg, oracle_mod, torch_cuda, mode, per_chunk, P
 
 
 def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
-    """The exact / f64 vector geometries take the fused single launch."""
+    """Vector geometries take the fused single launch (lossless with P % 512 == 0)."""
     torch, C = torch_cuda, pkg.codec
     P, B, nb = 3072, 512, 2
     ds = torch.randint(0, 256, (B * nb, P), dtype=torch.uint8, device="cuda")
-    for mode, pc, launches in ((1, 16, 1), (0, 8, 1), (2, 6, 1), (3, 9, 2)):
+    for mode, pc, launches in ((1, 16, 1), (0, 8, 1), (2, 6, 1), (3, 9, 1), (4, 18, 1)):
         L = C.layout(mode, pc, P, B, nb)
         cont, offs = C.alloc_stream(L)
         out = torch.empty((B * nb, P), dtype=torch.uint8, device="cuda")
@@ -257,6 +260,33 @@ def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
         assert pkg._lib.launches(0) - n0 == launches, mode
         if pc <= C.capacity(mode):
             assert torch.equal(out, ds)
+
+
+@pytest.mark.parametrize("mode,pc", [(3, 9), (4, 18), (2, 6), (0, 8), (1, 16)])
+def test_roundtrip_dev_full_size_properties(pkg, torch_cuda, mode, pc):
+    """C3-sized streams (65 536 CIFAR images, > L2): the fused launch's
+    containers and parity planes equal optb_encode_dev's, and the decoded rows
+    are the gathered rows (lossless at capacity) -- with every warp in either
+    phase at once, so the phases' shared-memory rings must not overlap."""
+    torch, C = torch_cuda, pkg.codec
+    P, B, nb = 3072, 4096, 16
+    rows = B * nb
+    ds = torch.randint(0, 256, (rows, P), dtype=torch.uint8, device="cuda")
+    idx = torch.randperm(rows, device="cuda")
+    L = C.layout(mode, pc, P, B, nb)
+    cont, offs = C.alloc_stream(L)
+    out = torch.empty((rows, P), dtype=torch.uint8, device="cuda")
+    C.roundtrip_dev(L, ds, cont, out, offsets=offs, row_index=idx)
+    C.sync()
+    assert torch.equal(out, ds[idx])
+    cont2, offs2 = C.alloc_stream(L)
+    C.encode_dev(L, ds, cont2, offs2, row_index=idx)
+    C.sync()
+    nbytes = C.container_bytes(L)
+    assert torch.equal(cont[:nbytes], cont2[:nbytes])
+    if offs is not None:
+        ob = C.offsets_bytes(L)
+        assert torch.equal(offs[:ob], offs2[:ob])
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])

@@ -88,7 +88,7 @@ def main():
              "encode_frac": round(enc_b / t_enc / 1e9 / pk, 3), "decode_frac": round(dec_b / t_dec / 1e9 / pk, 3),
              "roundtrip_us": round(t_rt * 1e6, 1), "roundtrip_images_per_s": round(rows / t_rt, 1),
              "roundtrip_frac": round((enc_b + dec_b) / t_rt / 1e9 / pk, 3),
-             "roundtrip_fused": mode in (0, 1, 2) and P % 16 == 0}
+             "roundtrip_fused": P % 16 == 0 and (mode in (0, 1, 2) or P % 512 == 0)}
         res[name] = r
         del src, cont, out
 
