@@ -100,4 +100,5 @@ class Pipeline:
             self._h = None
 
     def __del__(self):
-        self.close()
+        if lib is not None:  # module globals may already be gone at interpreter exit
+            self.close()

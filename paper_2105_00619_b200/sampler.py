@@ -178,6 +178,6 @@ class BatchCursor:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None and getattr(lib, "optb_sbs_destroy", None) is not None:  # not at interpreter exit
             lib.optb_sbs_destroy(h)
-            self._h = None
+        self._h = None
