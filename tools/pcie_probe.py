@@ -51,6 +51,7 @@ def measure(torch, nbytes, reps=8):
     d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    extra = []
 
     def timed(fn):
         fn()
@@ -59,8 +60,8 @@ def measure(torch, nbytes, reps=8):
         e0.record()
         for _ in range(reps):
             fn()
-        torch.cuda.current_stream().wait_stream(s1)
-        torch.cuda.current_stream().wait_stream(s2)
+        for st in [s1, s2] + extra:
+            torch.cuda.current_stream().wait_stream(st)
         e1.record()
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
@@ -77,8 +78,29 @@ def measure(torch, nbytes, reps=8):
         h2d()
         d2h()
 
+    s3, s4 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    extra += [s3, s4]
+    half = nbytes // 2
+
+    def h2d_split():  # the same upload as two halves on two streams (two DMA queues)
+        with torch.cuda.stream(s1):
+            d_a[:half].copy_(h_in[:half], non_blocking=True)
+        with torch.cuda.stream(s3):
+            d_a[half:].copy_(h_in[half:], non_blocking=True)
+
+    def d2h_split():
+        with torch.cuda.stream(s2):
+            h_out[:half].copy_(d_b[:half], non_blocking=True)
+        with torch.cuda.stream(s4):
+            h_out[half:].copy_(d_b[half:], non_blocking=True)
+
+    def both_split():
+        h2d_split()
+        d2h_split()
+
     res = {}
-    for name, fn, mult in (("h2d", h2d, 1), ("d2h", d2h, 1), ("bidir", both, 2)):
+    for name, fn, mult in (("h2d", h2d, 1), ("d2h", d2h, 1), ("bidir", both, 2), ("h2d_2q", h2d_split, 1),
+                           ("d2h_2q", d2h_split, 1), ("bidir_2q", both_split, 2)):
         ms = timed(fn)
         res[name + "_gbs"] = round(mult * nbytes / ms / 1e6, 1)
     return res
