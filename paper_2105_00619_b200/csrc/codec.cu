@@ -1014,8 +1014,15 @@ struct RtRegion {
   static constexpr uint32_t BYTES = ((ENC > DEC ? ENC : DEC) + 1023) / 1024 * 1024;
 };
 
+// At most OPTB_RT_MAXREG registers per thread (no spills at 184): with 8
+// warps that leaves ~18 K registers per SM, so the SBS kernels of the next
+// draw call (side stream) co-reside with the persistent round trip instead of
+// waiting for its CTAs to retire.
+#ifndef OPTB_RT_MAXREG
+#define OPTB_RT_MAXREG 184
+#endif
 template <int MODE, int O, bool PTRS>
-__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+__global__ void __maxnreg__(OPTB_RT_MAXREG)
     k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                     uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
