@@ -24,10 +24,20 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <string>
+
+#include "internal.h"
 #include "optb_cuda.h"
 
 namespace {
 constexpr int kTimingRing = 64;
+
+// every failure sets optb_last_error() (the cause of a CUDA failure included)
+int arg_fail(const char* what) { return optb_b200::set_error_text(OPTB_ERR_ARG, std::string("pipeline: ") + what); }
+int cuda_fail(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  return optb_b200::set_error_text(OPTB_ERR_CUDA, std::string("pipeline: ") + what + ": " + cudaGetErrorString(e));
+}
 }
 
 struct optb_pipeline {
@@ -63,14 +73,14 @@ namespace {
 int enqueue_draws(optb_pipeline* p) {
   const uint64_t c = p->calls;
   const int b = static_cast<int>(c % 2);
-  if (c >= 2 && cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (c >= 2 && cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess) return cuda_fail("stream wait");
   const int r = static_cast<int>(c % kTimingRing);
   if (p->timing) cudaEventRecord(p->t_s0[r], p->side);
   const uint64_t n = p->d.layout.n_batches * p->d.n_shards * p->spd;
   int st = optb_sbs_next_dev(p->d.sbs, n, p->d.shard, p->d.n_shards, p->ex[b], p->cls[b], p->side);
   if (st) return st;
   if (p->timing) cudaEventRecord(p->t_s1[r], p->side);
-  if (cudaEventRecord(p->sbs_done[b], p->side) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (cudaEventRecord(p->sbs_done[b], p->side) != cudaSuccess) return cuda_fail("event record");
   ++p->calls;
   return OPTB_OK;
 }
@@ -80,11 +90,11 @@ int enqueue_draws(optb_pipeline* p) {
 extern "C" {
 
 int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeline** out) {
-  if (!ctx || !d || !out || !d->sbs || !d->dataset) return OPTB_ERR_ARG;
+  if (!ctx || !d || !out || !d->sbs || !d->dataset) return arg_fail("create: null ctx, descriptor, sampler or dataset");
   *out = nullptr;
   int st = optb_layout_check(&d->layout);
   if (st) return st;
-  if (d->n_shards == 0 || d->shard >= d->n_shards) return OPTB_ERR_ARG;
+  if (d->n_shards == 0 || d->shard >= d->n_shards) return arg_fail("create: shard must be < n_shards");
   auto* p = new optb_pipeline();
   p->ctx = ctx;
   p->d = *d;
@@ -108,7 +118,7 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
   }
   if (!ok) {
     optb_pipeline_destroy(p);
-    return OPTB_ERR_CUDA;
+    return cuda_fail("CUDA call failed");
   }
   st = enqueue_draws(p);  // the first call's draws start right away
   if (st) {
@@ -120,7 +130,7 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
 }
 
 int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
-  if (!p || !out) return OPTB_ERR_ARG;
+  if (!p || !out) return arg_fail("step: null pipeline or output");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t k = p->step;
   const uint64_t call = k / p->spd, sub = k % p->spd;
@@ -130,7 +140,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   if (sub == 0) {
     st = enqueue_draws(p);  // the next call's draws overlap this call's steps
     if (st) return st;
-    if (cudaStreamWaitEvent(s, p->sbs_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+    if (cudaStreamWaitEvent(s, p->sbs_done[b], 0) != cudaSuccess) return cuda_fail("stream wait");
   }
   optb_epilogue e = p->d.epilogue;
   if (e.class_scale && !e.row_class) e.row_class = p->cls[b] + sub * p->rows;
@@ -140,7 +150,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
                          p->cont, p->offs, s);
     if (st) return st;
     if (p->timing) cudaEventRecord(p->t_e1[r], s);
-    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
+    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
     st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
     if (st) return st;
   } else {
@@ -148,7 +158,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
                             p->cont, p->offs, &e, out, s);
     if (st) return st;
     if (p->timing) cudaEventRecord(p->t_e1[r], s);
-    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return OPTB_ERR_CUDA;
+    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
   }
   if (p->timing && p->d.split_kernels) cudaEventRecord(p->t_d1[r], s);  // fused: the launch ends at t_e1
   ++p->step;
@@ -156,7 +166,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
 }
 
 int optb_pipeline_set_dataset(optb_pipeline* p, const uint8_t* dataset, uint64_t row_stride) {
-  if (!p || !dataset) return OPTB_ERR_ARG;
+  if (!p || !dataset) return arg_fail("set_dataset: null pipeline or dataset");
   p->d.dataset = dataset;
   p->d.row_stride = row_stride;
   return OPTB_OK;
@@ -164,9 +174,9 @@ int optb_pipeline_set_dataset(optb_pipeline* p, const uint8_t* dataset, uint64_t
 
 int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
                         const int32_t** classes) {
-  if (!p || step >= p->calls * p->spd) return OPTB_ERR_ARG;
+  if (!p || step >= p->calls * p->spd) return arg_fail("draws: step not drawn yet");
   const uint64_t call = step / p->spd;
-  if (call + 2 < p->calls) return OPTB_ERR_ARG;  // buffer already reused
+  if (call + 2 < p->calls) return arg_fail("draws: step's draw buffer already reused");
   const uint64_t sub = step % p->spd;
   if (examples) *examples = p->ex[call % 2] + sub * p->rows;
   if (classes) *classes = p->cls[call % 2] + sub * p->rows;
@@ -177,21 +187,22 @@ const void* optb_pipeline_containers(const optb_pipeline* p) { return p ? p->con
 
 int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, float* enc_ms,
                           float* dec_ms) {
-  if (!p || !p->timing || step >= p->step || step + kTimingRing <= p->step) return OPTB_ERR_ARG;
+  if (!p || !p->timing || step >= p->step || step + kTimingRing <= p->step)
+    return arg_fail("timings: not recorded for that step (record_timings, last 64 steps)");
   const int r = static_cast<int>(step % kTimingRing);
   const int rc = static_cast<int>((step / p->spd) % kTimingRing);
   cudaEvent_t last = p->d.split_kernels ? p->t_d1[r] : p->t_e1[r];
-  if (cudaEventSynchronize(last) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (cudaEventSynchronize(last) != cudaSuccess) return cuda_fail("synchronize");
   if (sbs_ms) {  // the SBS call that produced this step's draws, per step
-    if (cudaEventElapsedTime(sbs_ms, p->t_s0[rc], p->t_s1[rc]) != cudaSuccess) return OPTB_ERR_CUDA;
+    if (cudaEventElapsedTime(sbs_ms, p->t_s0[rc], p->t_s1[rc]) != cudaSuccess) return cuda_fail("event timing");
     *sbs_ms /= static_cast<float>(p->spd);
   }
-  if (enc_ms && cudaEventElapsedTime(enc_ms, p->t_e0[r], p->t_e1[r]) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (enc_ms && cudaEventElapsedTime(enc_ms, p->t_e0[r], p->t_e1[r]) != cudaSuccess) return cuda_fail("event timing");
   if (dec_ms) {
     if (!p->d.split_kernels) {
       *dec_ms = 0.0f;  // one fused launch: all of it is in enc_ms
     } else if (cudaEventElapsedTime(dec_ms, p->t_e1[r], p->t_d1[r]) != cudaSuccess) {
-      return OPTB_ERR_CUDA;
+      return cuda_fail("CUDA call failed");
     }
   }
   return OPTB_OK;
@@ -199,9 +210,9 @@ int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, 
 
 int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint64_t n_rows, uint64_t row_stride,
                             void* out_host, void* stream) {
-  if (!p || !dataset_host || !out_host || !n_rows) return OPTB_ERR_ARG;
+  if (!p || !dataset_host || !out_host || !n_rows) return arg_fail("step_host: null buffer or empty dataset");
   if (row_stride == 0) row_stride = p->d.layout.pixels;
-  if (row_stride < p->d.layout.pixels) return OPTB_ERR_ARG;
+  if (row_stride < p->d.layout.pixels) return arg_fail("step_host: row_stride < pixels");
   auto& h = p->host;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t es = p->d.epilogue.out_dtype == OPTB_OUT_U8 ? 1 : p->d.epilogue.out_dtype == OPTB_OUT_F32 ? 4 : 2;
@@ -214,22 +225,22 @@ int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint6
       ok = cudaEventCreateWithFlags(&h.up_done[b], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&h.used[b], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&h.down_done[b], cudaEventDisableTiming) == cudaSuccess;
-    if (!ok) return OPTB_ERR_CUDA;
+    if (!ok) return cuda_fail("CUDA call failed");
   }
   if (h.ds_cap < ds_bytes || h.out_cap < out_bytes) {  // (re)size: drain the leg first
     if (cudaStreamSynchronize(h.up) != cudaSuccess || cudaStreamSynchronize(h.down) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
-      return OPTB_ERR_CUDA;
+      return cuda_fail("CUDA call failed");
     for (int b = 0; b < 2; ++b) {
       if (h.ds_cap < ds_bytes) {
         if (h.ds[b]) cudaFree(h.ds[b]);
         h.ds[b] = nullptr;
-        if (cudaMalloc(&h.ds[b], ds_bytes) != cudaSuccess) return OPTB_ERR_CUDA;
+        if (cudaMalloc(&h.ds[b], ds_bytes) != cudaSuccess) return cuda_fail("device allocation");
       }
       if (h.out_cap < out_bytes) {
         if (h.out[b]) cudaFree(h.out[b]);
         h.out[b] = nullptr;
-        if (cudaMalloc(&h.out[b], out_bytes) != cudaSuccess) return OPTB_ERR_CUDA;
+        if (cudaMalloc(&h.out[b], out_bytes) != cudaSuccess) return cuda_fail("device allocation");
       }
     }
     h.ds_cap = h.ds_cap < ds_bytes ? ds_bytes : h.ds_cap;
@@ -239,11 +250,11 @@ int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint6
   const int b = static_cast<int>(h.k % 2);
   // H2D of this step's dataset once step k-2 no longer reads buffer b; it
   // runs on the copy engine while step k-1 computes and copies out
-  if (h.k >= 2 && cudaStreamWaitEvent(h.up, h.used[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+  if (h.k >= 2 && cudaStreamWaitEvent(h.up, h.used[b], 0) != cudaSuccess) return cuda_fail("stream wait");
   if (cudaMemcpyAsync(h.ds[b], dataset_host, ds_bytes, cudaMemcpyHostToDevice, h.up) != cudaSuccess ||
       cudaEventRecord(h.up_done[b], h.up) != cudaSuccess || cudaStreamWaitEvent(s, h.up_done[b], 0) != cudaSuccess)
-    return OPTB_ERR_CUDA;
-  if (h.k >= 2 && cudaStreamWaitEvent(s, h.down_done[b], 0) != cudaSuccess) return OPTB_ERR_CUDA;
+    return cuda_fail("CUDA call failed");
+  if (h.k >= 2 && cudaStreamWaitEvent(s, h.down_done[b], 0) != cudaSuccess) return cuda_fail("stream wait");
   const uint8_t* prev_ds = p->d.dataset;
   const uint64_t prev_stride = p->d.row_stride;
   p->d.dataset = h.ds[b];
@@ -255,18 +266,18 @@ int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint6
   if (cudaEventRecord(h.used[b], s) != cudaSuccess || cudaStreamWaitEvent(h.down, h.used[b], 0) != cudaSuccess ||
       cudaMemcpyAsync(out_host, h.out[b], out_bytes, cudaMemcpyDeviceToHost, h.down) != cudaSuccess ||
       cudaEventRecord(h.down_done[b], h.down) != cudaSuccess)
-    return OPTB_ERR_CUDA;
+    return cuda_fail("CUDA call failed");
   ++h.k;
   return OPTB_OK;
 }
 
 int optb_pipeline_host_wait(optb_pipeline* p, void* stream) {
-  if (!p) return OPTB_ERR_ARG;
+  if (!p) return arg_fail("null pipeline");
   auto& h = p->host;
   if (!h.up || h.k == 0) return OPTB_OK;
   if (!stream) {  // host wait: every upload and download enqueued so far
     if (cudaStreamSynchronize(h.up) != cudaSuccess || cudaStreamSynchronize(h.down) != cudaSuccess)
-      return OPTB_ERR_CUDA;
+      return cuda_fail("CUDA call failed");
     return OPTB_OK;
   }
   // device wait: the last download (it follows every earlier step's work)
