@@ -710,6 +710,13 @@ struct optb_sbs {
   int64_t* d_pool = nullptr;  // [N current permutations][generation area]
   uint64_t pool_cap = 0;      // elements
   unsigned long long* d_chain = nullptr;
+  // host mirror of the chain state after every enqueued call (the seeds of a
+  // call's events are walked here, one mix each); a device-side serial redo
+  // that ends elsewhere bumps *diverged_h and the next call resyncs
+  uint64_t host_chain = 0;
+  unsigned int* diverged_h = nullptr;  // mapped pinned counter
+  unsigned int* diverged_d = nullptr;
+  unsigned int diverged_seen = 0;
   uint8_t* d_static = nullptr;  // counts[C] prefix[C+1] size[C] row_cls[B]
   uint8_t* d_call = nullptr;    // per-call block (stream ordered reuse)
   size_t call_cap = 0;
@@ -725,6 +732,13 @@ struct optb_sbs {
 };
 
 namespace {
+
+// SplitMix64 finaliser (rng.hpp:16-21), host side.
+uint64_t host_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
 
 // Packs per-call arrays into one 16-byte aligned block.
 struct Packer {
@@ -843,8 +857,25 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
     gen_base->assign(C, 0);
     for (uint64_t c = 0; c < C; ++c) (*gen_base)[c] = per[c].empty() ? s->off[c] : base[c];
   }
+  // the chain seeds of this call's events, walked on the host from its mirror
+  // of the device state (resynced first if a serial redo diverged from it)
+  if (*reinterpret_cast<volatile unsigned int*>(s->diverged_h) != s->diverged_seen) {
+    CK(cudaDeviceSynchronize(), "sbs resync");
+    unsigned long long dev_chain = 0;
+    CK(cudaMemcpy(&dev_chain, s->d_chain, 8, cudaMemcpyDeviceToHost), "sbs resync");
+    s->host_chain = dev_chain;
+    s->diverged_seen = *reinterpret_cast<volatile unsigned int*>(s->diverged_h);
+  }
+  std::vector<uint64_t> seeds(std::max<uint64_t>(E, 1), 0);
+  const uint64_t expect_start = s->host_chain;
+  uint64_t chain = expect_start;
+  for (uint64_t e = 0; e < E; ++e) {  // K = m-1 draws + next_u64 (sampler.cpp:84-88), one mix
+    seeds[e] = chain;
+    chain = host_mix64(chain + (evs[e].m >= 2 ? static_cast<uint64_t>(evs[e].m) : 1ull) * 0x9e3779b97f4a7c15ull);
+  }
+  s->host_chain = chain;
   const size_t o_ev = pk.put(evs.data(), E);
-  const size_t o_seeds = pk.reserve(std::max<uint64_t>(E, 1) * sizeof(uint64_t));
+  const size_t o_seeds = pk.put(seeds.data(), seeds.size());
   const size_t o_flag = pk.reserve(16);
   const size_t o_begin = pk.put(begin.data(), begin.size());
   const size_t o_list = pk.put(list.data(), list.size());
@@ -868,7 +899,10 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
   a.flag = reinterpret_cast<uint32_t*>(d + o_flag);
   a.chain = s->d_chain;
   a.pool = s->d_pool;
-  cudaError_t e = launch_sbs_events(a, static_cast<uint32_t>(ccopy.size()),
+  a.expect_start = expect_start;
+  a.expect_final = chain;
+  a.diverged = s->diverged_d;
+  cudaError_t e = launch_sbs_events(a, static_cast<uint32_t>(ccopy.size()), static_cast<uint32_t>(list.size()),
                                     s->small_ids ? s->max_m : 0xffffffffu, s->force_serial, st,
                                     &s->ctx->launches);
   if (e != cudaSuccess) return cuda_err(e, "sbs events");
@@ -1012,6 +1046,10 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
       return fail(cuda_err(cudaGetLastError(), "sbs event"));
   if (cudaMalloc(&s->d_chain, sizeof(unsigned long long)) != cudaSuccess)
     return fail(cuda_err(cudaGetLastError(), "sbs chain"));
+  if (cudaHostAlloc(&s->diverged_h, 16, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->diverged_d), s->diverged_h, 0) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs mapped counter"));
+  *s->diverged_h = 0;
   int rc = ensure_pool(s, std::max<uint64_t>(s->N, 1), st);
   if (rc) return fail(rc);
   if (s->N) {
@@ -1043,6 +1081,7 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
   const unsigned long long seed64 = seed;
   if (cudaMemcpy(s->d_chain, &seed64, 8, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(cuda_err(cudaGetLastError(), "sbs seed"));
+  s->host_chain = seed64;
   // constructor: reshuffle every class in class order (sampler.cpp:73-81),
   // including empty and single-example classes (they still consume a draw)
   std::vector<EvKey> keys(C);
@@ -1061,6 +1100,7 @@ void optb_sbs_destroy(optb_sbs* s) {
   cudaDeviceSynchronize();
   if (s->d_pool) cudaFree(s->d_pool);
   if (s->d_chain) cudaFree(s->d_chain);
+  if (s->diverged_h) cudaFreeHost(s->diverged_h);
   if (s->d_static) cudaFree(s->d_static);
   if (s->d_call) cudaFree(s->d_call);
   for (int r = 0; r < optb_sbs::kRing; ++r) {

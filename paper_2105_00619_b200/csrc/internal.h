@@ -105,15 +105,23 @@ struct ChainArgs {
   const uint32_t* cls_list;   // event ids of each reshuffling class, generation order
   const uint64_t* cls_copy;   // pool offset receiving the class's pre-call permutation
   const uint64_t* cls_final;  // pool offset of the class's current permutation
-  uint64_t* seeds;            // [E] chain state at the start of each event
+  uint64_t* seeds;            // [E] chain state at the start of each event (host-computed)
   uint32_t* flag;             // [1] rejection seen (forces the exact serial redo)
   unsigned long long* chain;  // chain state before the first event; advanced in place
   int64_t* pool;
+  // The host walks the chain (one mix per event, no rejection assumed) from
+  // its mirror of the chain state; the kernels use its seeds only if the
+  // device state equals expect_start and no draw is rejected, otherwise the
+  // call is redone serially from the device state (the authority).
+  uint64_t expect_start, expect_final;
+  unsigned int* diverged;     // mapped host counter: serial redos that moved the chain off the host's walk
 };
 
-// k_shuffle (one CTA per reshuffling class) + k_chain_finish (chain advance,
-// or the exact serial redo after a rejection / when forced).
-cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t max_m, int force,
+// k_fy_gen (one CTA per reshuffle event) + k_compose (one CTA per reshuffling
+// class), or k_shuffle (one CTA per class, large classes), then k_chain_finish
+// (chain advance, or the exact serial redo after a rejection / when forced).
+// n_gen = reshuffle events with m >= 2 (the length of cls_list).
+cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m, int force,
                               cudaStream_t s, uint64_t* launches);
 
 struct SbsGatherArgs {

@@ -156,49 +156,17 @@ __global__ void k_ci_label_value(const int32_t* labels, uint64_t C, DevError* er
 }
 
 // ------------------------------------------------------------------ K9
-// One CTA per class that reshuffles in this call (m >= 2).  Thread 0 walks the
-// whole event list once assuming no rejection (one mix per event) and records
-// the start state of this class's events; then, per event in generation
-// order, the lanes compute every draw x_k = mix(s + k*gamma), check it against
+// One CTA per class that reshuffles in this call (m >= 2).  The start state
+// of every event comes from the host's walk of the chain (ChainArgs::seeds,
+// valid when the device chain equals expect_start -- checked first); then,
+// per event in generation order, the lanes compute every draw
+// x_k = mix(s + k*gamma), check it against
 // next_below's bound (rng.hpp:29-35) and turn it into the swap target
 // j = x mod i; thread 0 applies the swaps in shared memory.  A rejected draw
 // sets calls->flag and the class stops; k_chain_finish then redoes the whole
 // call exactly (serially).  The permutation lives in shared memory as u32 when
 // it fits (host guarantees ids < 2^32 then), else in the generation pool.
 constexpr int kJWin = 2048;
-constexpr int kWalk = 1024;
-
-// Called by every thread of a block.  Thread 0 walks the event list assuming
-// no rejection (one mix per event: K = m-1, or 0 for m <= 1); the list is
-// staged into shared memory chunk by chunk by the whole block first, so the
-// serial walk never waits on a global load (it runs next to bandwidth-bound
-// encode/decode kernels).  Optionally records the start state of `cls`'s
-// events in a.seeds.  Returns the chain state after the last event.
-__device__ uint64_t chain_walk(const ChainArgs& a, uint32_t cls, bool want_seeds) {
-  __shared__ uint2 evs[kWalk];
-  __shared__ uint64_t s_sh;
-  if (threadIdx.x == 0) s_sh = *a.chain;
-  for (uint64_t base = 0; base < a.E; base += kWalk) {
-    const uint32_t cnt = static_cast<uint32_t>(a.E - base < kWalk ? a.E - base : kWalk);
-    __syncthreads();
-    for (uint32_t x = threadIdx.x; x < cnt; x += blockDim.x) {
-      const SbsEvent ev = a.ev[base + x];
-      evs[x] = make_uint2(ev.cls, ev.m);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t s = s_sh;
-      for (uint32_t x = 0; x < cnt; ++x) {
-        const uint2 ev = evs[x];
-        if (want_seeds && ev.x == cls) a.seeds[base + x] = s;
-        s = mix64(s + (ev.y >= 2 ? static_cast<uint64_t>(ev.y) : 1ull) * kGamma);
-      }
-      s_sh = s;
-    }
-  }
-  __syncthreads();
-  return s_sh;
-}
 
 __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
   extern __shared__ uint32_t sh[];
@@ -206,8 +174,7 @@ __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
   uint32_t* perm = sh + kJWin;  // m entries (smem path)
   const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
   const SbsEvent first = a.ev[a.cls_list[b]];
-  const uint32_t cls = first.cls, m = first.m;
-  chain_walk(a, cls, true);  // this class's event start states -> a.seeds
+  const uint32_t m = first.m;
   const uint64_t copy_to = a.cls_copy[blockIdx.x];
   if (use_smem) {
     for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) {
@@ -219,6 +186,12 @@ __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
     for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) a.pool[copy_to + x] = a.pool[first.src + x];
   }
   __syncthreads();
+  // the host's seeds hold only if the device chain is where the host assumed;
+  // otherwise k_chain_finish redoes the call from the pre-call copies above
+  if (*a.chain != a.expect_start) {
+    if (threadIdx.x == 0) atomicExch(a.flag, 1u);
+    return;
+  }
   uint64_t cur_src = copy_to;
   for (uint32_t q = b; q < end; ++q) {
     const uint32_t e = a.cls_list[q];
@@ -318,79 +291,106 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
   return before + x - v;
 }
 
-__global__ void __launch_bounds__(kParThreads) k_shuffle_par(ChainArgs a) {
+// ------------------------------------------------------------------ K9a / K9b
+// The generations of a class in one call are a chain perm_j = FY_j(perm_j-1),
+// but FY's swap targets depend only on the draws, so FY_j(A)[p] = A[pi_j[p]]
+// with pi_j = FY_j(identity).  K9a computes every pi_j of the call at once --
+// one CTA per reshuffle event, the parallel Fisher-Yates above on the
+// identity -- and K9b composes them per class, perm_j[p] = perm_j-1[pi_j[p]],
+// a shared-memory gather per generation.  The call's critical path is one
+// parallel Fisher-Yates plus one gather per generation, instead of one
+// Fisher-Yates per generation: it stays flat when a rank draws the batches
+// of all N ranks per step (N-GPU runs).
+__global__ void __launch_bounds__(kParThreads) k_fy_gen(ChainArgs a) {
   extern __shared__ uint32_t sh[];
   __shared__ uint32_t warp_tot[kParThreads / 32];
-  const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
-  const SbsEvent first = a.ev[a.cls_list[b]];
-  const uint32_t cls = first.cls, m = first.m;
+  if (*a.chain != a.expect_start) return;  // stale host seeds: K9b flags, K8 redoes serially
+  const uint32_t e = a.cls_list[blockIdx.x];
+  const SbsEvent E = a.ev[e];
+  const uint32_t m = E.m;
   uint32_t* js = sh;               // [m + 1]  swap target of step i (i = 2..m)
   uint32_t* off = js + (m + 1);    // [m + 1]  bucket starts, then ends
   uint32_t* bk = off + (m + 1);    // [m]      steps bucketed by target
-  uint32_t* pa = bk + m;           // [m]      input permutation
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(pa + m);  // [m] bucket sizes
-  chain_walk(a, cls, true);
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(bk + m);  // [m] bucket sizes
+  const uint64_t s = a.seeds[e];
+  const uint32_t per = (m + kParThreads - 1) / kParThreads;
+  const uint32_t lo = min(m, threadIdx.x * per), hi = min(m, lo + per);
+  bool rej = false;
+  for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) cnt[x] = 0;
+  __syncthreads();
+  for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) {
+    const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
+    rej |= rejected(x, i);
+    const uint32_t j = static_cast<uint32_t>(x % i);
+    js[i] = j;
+    atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
+  }
+  if (__syncthreads_or(rej)) {
+    if (threadIdx.x == 0) atomicExch(a.flag, 1u);
+    return;  // k_chain_finish redoes this call serially
+  }
+  uint32_t local = 0;
+  for (uint32_t x = lo; x < hi; ++x) local += cnt[x];
+  uint32_t run = block_exclusive_scan(local, warp_tot);
+  for (uint32_t x = lo; x < hi; ++x) {
+    off[x] = run;
+    run += cnt[x];
+  }
+  __syncthreads();
+  for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) bk[atomicAdd(&off[js[i]], 1u)] = i;
+  __syncthreads();  // off[x] now holds the end of bucket x
+  int64_t* gout = a.pool + E.slot;
+  for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+    uint32_t x = p >= 1 ? js[p + 1] : 0u;
+    uint32_t k = p >= 1 ? p + 2 : 2u;
+    for (;;) {
+      const uint32_t hi_b = off[x], lo_b = hi_b - cnt[x];
+      uint32_t best = 0xffffffffu;
+      for (uint32_t t = lo_b; t < hi_b; ++t) {
+        const uint32_t st = bk[t];
+        if (st >= k && st < best) best = st;
+      }
+      if (best == 0xffffffffu) break;
+      x = best - 1;
+      k = best + 1;
+    }
+    gout[p] = x;  // pi[p]: the input position that lands at p
+  }
+}
+
+__global__ void __launch_bounds__(kParThreads) k_compose(ChainArgs a) {
+  extern __shared__ uint32_t sh[];
+  const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
+  const SbsEvent first = a.ev[a.cls_list[b]];
+  const uint32_t m = first.m;
+  uint32_t* prev = sh;
+  uint32_t* next = sh + m;
   const uint64_t copy_to = a.cls_copy[blockIdx.x];
   for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) {
     const int64_t v = a.pool[first.src + x];
-    pa[x] = static_cast<uint32_t>(v);
-    a.pool[copy_to + x] = v;
+    prev[x] = static_cast<uint32_t>(v);
+    a.pool[copy_to + x] = v;  // pre-call copy: the input of a serial redo
   }
   __syncthreads();
-  // per-thread contiguous ranges for the scan
-  const uint32_t per = (m + kParThreads - 1) / kParThreads;
-  const uint32_t lo = min(m, threadIdx.x * per), hi = min(m, lo + per);
+  if (*a.chain != a.expect_start) {
+    if (threadIdx.x == 0) atomicExch(a.flag, 1u);
+    return;
+  }
+  if (*reinterpret_cast<volatile uint32_t*>(a.flag)) return;  // a rejection: K8 redoes the call
   for (uint32_t q = b; q < end; ++q) {
-    const uint32_t e = a.cls_list[q];
-    const SbsEvent E = a.ev[e];
-    const uint64_t s = a.seeds[e];
-    bool rej = false;
-    for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) cnt[x] = 0;
-    __syncthreads();
-    for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) {
-      const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
-      rej |= rejected(x, i);
-      const uint32_t j = static_cast<uint32_t>(x % i);
-      js[i] = j;
-      atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
-    }
-    if (__syncthreads_or(rej)) {
-      if (threadIdx.x == 0) atomicExch(a.flag, 1u);
-      return;  // k_chain_finish redoes this call serially
-    }
-    uint32_t local = 0;
-    for (uint32_t x = lo; x < hi; ++x) local += cnt[x];
-    uint32_t run = block_exclusive_scan(local, warp_tot);
-    for (uint32_t x = lo; x < hi; ++x) {
-      off[x] = run;
-      run += cnt[x];
-    }
-    __syncthreads();
-    for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) bk[atomicAdd(&off[js[i]], 1u)] = i;
-    __syncthreads();  // off[x] now holds the end of bucket x
-    int64_t* gout = a.pool + E.slot;
+    int64_t* g = a.pool + a.ev[a.cls_list[q]].slot;
     for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
-      uint32_t x = p >= 1 ? js[p + 1] : 0u;
-      uint32_t k = p >= 1 ? p + 2 : 2u;
-      for (;;) {
-        const uint32_t hi_b = off[x], lo_b = hi_b - cnt[x];
-        uint32_t best = 0xffffffffu;
-        for (uint32_t t = lo_b; t < hi_b; ++t) {
-          const uint32_t st = bk[t];
-          if (st >= k && st < best) best = st;
-        }
-        if (best == 0xffffffffu) break;
-        x = best - 1;
-        k = best + 1;
-      }
-      gout[p] = pa[x];
+      const uint32_t v = prev[static_cast<uint32_t>(g[p])];
+      next[p] = v;
+      g[p] = v;
     }
     __syncthreads();
-    for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) pa[x] = static_cast<uint32_t>(gout[x]);
-    __syncthreads();
+    uint32_t* t = prev;
+    prev = next;
+    next = t;
   }
   const uint64_t final_to = a.cls_final[blockIdx.x];
-  for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) a.pool[final_to + x] = pa[x];
+  for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) a.pool[final_to + x] = prev[x];
 }
 
 // ------------------------------------------------------------------ K8
@@ -401,9 +401,8 @@ __global__ void __launch_bounds__(kParThreads) k_shuffle_par(ChainArgs a) {
 // generation pool starting from each class's pre-call copy, then write back
 // the newest generations.
 __global__ void k_chain_finish(ChainArgs a, uint32_t n_cls, int force) {
-  if (!force && *a.flag == 0u) {
-    const uint64_t s = chain_walk(a, 0xffffffffu, false);
-    if (threadIdx.x == 0) *a.chain = s;
+  if (!force && *a.flag == 0u && *a.chain == a.expect_start) {
+    if (threadIdx.x == 0) *a.chain = a.expect_final;  // the host's walk held
     return;
   }
   if (threadIdx.x != 0) return;
@@ -442,6 +441,10 @@ __global__ void k_chain_finish(ChainArgs a, uint32_t n_cls, int force) {
     const uint32_t last = a.cls_list[a.cls_begin[q + 1] - 1];
     const SbsEvent ev = a.ev[last];
     for (uint32_t x = 0; x < ev.m; ++x) a.pool[a.cls_final[q] + x] = a.pool[ev.slot + x];
+  }
+  if (s != a.expect_final && a.diverged) {  // the host must resync its chain mirror
+    *reinterpret_cast<volatile unsigned int*>(a.diverged) += 1u;
+    __threadfence_system();
   }
   *a.chain = s;
   *a.flag = 0u;
@@ -504,17 +507,17 @@ cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
 }
 
 
-cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t max_m, int force,
+cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m, int force,
                               cudaStream_t s, uint64_t* launches) {
   if (n_cls > 0 && max_m != 0xffffffffu && max_m <= kParMaxM) {
-    static bool par_attr = false;
-    if (!par_attr) {
-      cudaFuncSetAttribute(k_shuffle_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(par_smem_bytes(kParMaxM)));
-      par_attr = true;
-    }
-    k_shuffle_par<<<n_cls, kParThreads, par_smem_bytes(max_m), s>>>(a);
-    ++*launches;
+    cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_fy_gen),
+                                      static_cast<int>(par_smem_bytes(kParMaxM)));
+    if (ae != cudaSuccess) return ae;
+    ae = ensure_smem_attr(reinterpret_cast<const void*>(k_compose), static_cast<int>(8 * kParMaxM));
+    if (ae != cudaSuccess) return ae;
+    k_fy_gen<<<n_gen, kParThreads, par_smem_bytes(max_m), s>>>(a);
+    k_compose<<<n_cls, kParThreads, 8 * static_cast<size_t>(max_m), s>>>(a);
+    *launches += 2;
   } else if (n_cls > 0) {
     size_t smem = (kJWin + static_cast<size_t>(max_m)) * sizeof(uint32_t);
     int use_smem = 1;

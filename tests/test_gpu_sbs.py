@@ -194,3 +194,36 @@ def test_c5_scale_stream_vs_oracle(pkg, oracle_mod, torch_cuda):
     oc = O.Cursor(O.sbs_plan([0.01] * 100, 512), ro, rm, 512, 1234)
     rex, _ = oc.next(64)
     assert np.array_equal(ex.cpu().numpy(), rex)
+
+
+@pytest.mark.parametrize("case", ["rej_a", "rej_b"])
+def test_rejection_with_calls_in_flight(golden, pkg, torch_cuda, case):
+    """Device draws enqueued back to back with no host synchronisation: when a
+    call hits a rejection, the calls already enqueued behind it were planned
+    from the host's (now stale) chain walk -- the device detects the mismatch
+    and redoes them serially from its own chain state, and the host resyncs
+    its mirror once it sees the divergence.  The stream equals the reference's."""
+    torch = torch_cuda
+    meta, arrays = golden
+    a = arrays["sbs"]
+    g = meta["sbs"][case]
+    S = pkg.sampler
+    o = g["class_offsets"]
+    m = a["rej_a_members"].tolist()
+    by_class = [m[o[c]:o[c + 1]] for c in range(3)]
+    want = a[f"{case}_examples"]
+    cur = S.BatchCursor(S.plan(g["weights"], g["batch"], g["seed"]), S.ClassIndex(by_class))
+    outs, drawn = [], 0
+    while drawn + 2 <= g["batches"]:
+        ex, _ = cur.next_dev(2)
+        outs.append(ex.clone())
+        drawn += 2
+    torch.cuda.synchronize()
+    got = torch.cat(outs).cpu().numpy()
+    assert np.array_equal(got, want[: got.size])
+    # and the cursor keeps going correctly afterwards
+    rest = g["batches"] - drawn
+    if rest:
+        ex, _ = cur.next_dev(rest)
+        torch.cuda.synchronize()
+        assert np.array_equal(ex.cpu().numpy(), want[got.size: got.size + ex.numel()])
