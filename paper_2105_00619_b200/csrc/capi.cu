@@ -902,8 +902,11 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
   a.expect_start = expect_start;
   a.expect_final = chain;
   a.diverged = s->diverged_d;
+  uint64_t max_gen_words = 0;
+  for (uint64_t c = 0; c < C; ++c)
+    if (!per[c].empty()) max_gen_words = std::max<uint64_t>(max_gen_words, per[c].size() * s->m[c]);
   cudaError_t e = launch_sbs_events(a, static_cast<uint32_t>(ccopy.size()), static_cast<uint32_t>(list.size()),
-                                    s->small_ids ? s->max_m : 0xffffffffu, s->force_serial, st,
+                                    s->small_ids ? s->max_m : 0xffffffffu, max_gen_words, s->force_serial, st,
                                     &s->ctx->launches);
   if (e != cudaSuccess) return cuda_err(e, "sbs events");
   if (s->prof) cudaEventRecord(s->pe[2], st);
@@ -1150,22 +1153,28 @@ int optb_sbs_next_dev(optb_sbs* s, uint64_t n, uint32_t shard, uint32_t n_shards
   const uint64_t C = s->C;
   // Lazy reshuffles (sampler.cpp:97): class c's draw D (counted from the
   // constructor) starts generation D / m_c when D % m_c == 0 and D > 0.
-  std::vector<EvKey> keys;
+  // Chain order is (batch, class, generation).  Classes are enumerated in
+  // order and each class's generations in order, so a stable counting sort
+  // by batch gives the whole order in O(events + batches) (N-GPU runs plan
+  // N x 97 batches per step here; a comparison sort dominated the host time).
+  std::vector<EvKey> gen_order;
   std::vector<uint64_t> ev_count(C, 0);
+  const uint64_t beta0 = s->batches, n_beta = n + 1;
+  std::vector<uint32_t> at(n_beta + 1, 0);
   for (uint64_t c = 0; c < C; ++c) {
     const uint64_t cnt = s->counts[c], mm = s->m[c];
     if (cnt == 0 || mm == 0) continue;
     const uint64_t D1 = (s->batches + n) * cnt;
     for (uint64_t g = s->gen[c] + 1; g * mm < D1; ++g) {
-      keys.push_back({(g * mm) / cnt, c, g, g - s->gen[c]});
+      const uint64_t beta = (g * mm) / cnt;
+      gen_order.push_back({beta, c, g, g - s->gen[c]});
+      ++at[beta - beta0 + 1];
       ++ev_count[c];
     }
   }
-  std::sort(keys.begin(), keys.end(), [](const EvKey& a, const EvKey& b) {
-    if (a.beta != b.beta) return a.beta < b.beta;
-    if (a.cls != b.cls) return a.cls < b.cls;
-    return a.g < b.g;
-  });
+  for (uint64_t b = 0; b < n_beta; ++b) at[b + 1] += at[b];
+  std::vector<EvKey> keys(gen_order.size());
+  for (const EvKey& k : gen_order) keys[at[k.beta - beta0]++] = k;
   // gather tables: drawn_before, generation at pool slot 0, its offset, stride
   std::vector<uint64_t> ga(4 * C);
   for (uint64_t c = 0; c < C; ++c) {

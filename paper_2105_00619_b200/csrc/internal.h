@@ -120,9 +120,10 @@ struct ChainArgs {
 // k_fy_gen (one CTA per reshuffle event) + k_compose (one CTA per reshuffling
 // class), or k_shuffle (one CTA per class, large classes), then k_chain_finish
 // (chain advance, or the exact serial redo after a rejection / when forced).
-// n_gen = reshuffle events with m >= 2 (the length of cls_list).
-cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m, int force,
-                              cudaStream_t s, uint64_t* launches);
+// n_gen = reshuffle events with m >= 2 (the length of cls_list);
+// max_gen_words = max over reshuffling classes of (its events) x m.
+cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m,
+                              uint64_t max_gen_words, int force, cudaStream_t s, uint64_t* launches);
 
 struct SbsGatherArgs {
   const uint32_t* row_cls;       // [B] class of each batch row (class-major)

@@ -358,13 +358,91 @@ __global__ void __launch_bounds__(kParThreads) k_fy_gen(ChainArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(kParThreads) k_compose(ChainArgs a) {
+// K9a for small classes: one WARP per reshuffle event (kFyWarps events per
+// CTA), warp-synchronous -- many more events in flight next to the
+// persistent codec kernel than with a CTA each.  Same algorithm as k_fy_gen.
+constexpr int kFyWarps = 2;
+constexpr uint32_t kFyWarpMaxM = 1536;
+__host__ __device__ inline size_t fy_warp_smem_bytes(uint32_t m) { return kFyWarps * (4ull * (3ull * m + 2) + 2ull * (m + 2) + 16); }
+
+__global__ void __launch_bounds__(kFyWarps * 32) k_fy_gen_warp(ChainArgs a, uint32_t n_gen, uint32_t max_m) {
+  extern __shared__ uint32_t sh[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t q = blockIdx.x * kFyWarps + w;
+  if (q >= n_gen || *a.chain != a.expect_start) return;
+  const uint32_t e = a.cls_list[q];
+  const SbsEvent E = a.ev[e];
+  const uint32_t m = E.m;
+  const size_t words = (fy_warp_smem_bytes(max_m) / kFyWarps) / 4;
+  uint32_t* js = sh + w * words;   // [m + 1]
+  uint32_t* off = js + (m + 1);    // [m + 1]
+  uint32_t* bk = off + (m + 1);    // [m]
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(bk + m);  // [m]
+  const uint64_t s = a.seeds[e];
+  for (uint32_t x = lane; x < (m + 1) / 2; x += 32) reinterpret_cast<uint32_t*>(cnt)[x] = 0;
+  __syncwarp();
+  bool rej = false;
+  for (uint32_t i = 2 + lane; i <= m; i += 32) {
+    const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
+    rej |= rejected(x, i);
+    const uint32_t j = static_cast<uint32_t>(x % i);
+    js[i] = j;
+    atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
+  }
+  if (__any_sync(0xffffffffu, rej)) {
+    if (lane == 0) atomicExch(a.flag, 1u);
+    return;  // k_chain_finish redoes this call serially
+  }
+  __syncwarp();
+  // exclusive scan of the bucket sizes: contiguous ranges per lane
+  const uint32_t per = (m + 31) / 32;
+  const uint32_t lo = min(m, lane * per), hi = min(m, lo + per);
+  uint32_t local = 0;
+  for (uint32_t x = lo; x < hi; ++x) local += cnt[x];
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t run = incl - local;
+  for (uint32_t x = lo; x < hi; ++x) {
+    off[x] = run;
+    run += cnt[x];
+  }
+  __syncwarp();
+  for (uint32_t i = 2 + lane; i <= m; i += 32) bk[atomicAdd(&off[js[i]], 1u)] = i;
+  __syncwarp();  // off[x] now holds the end of bucket x
+  int64_t* gout = a.pool + E.slot;
+  for (uint32_t p = lane; p < m; p += 32) {
+    uint32_t x = p >= 1 ? js[p + 1] : 0u;
+    uint32_t k = p >= 1 ? p + 2 : 2u;
+    for (;;) {
+      const uint32_t hi_b = off[x], lo_b = hi_b - cnt[x];
+      uint32_t best = 0xffffffffu;
+      for (uint32_t t = lo_b; t < hi_b; ++t) {
+        const uint32_t st = bk[t];
+        if (st >= k && st < best) best = st;
+      }
+      if (best == 0xffffffffu) break;
+      x = best - 1;
+      k = best + 1;
+    }
+    gout[p] = x;
+  }
+}
+
+// prefetch != 0: the class's generations fit in shared memory after the two
+// permutation buffers, and are all loaded in one sweep (every load in flight
+// at once) before the composition, which then runs from shared memory only.
+__global__ void __launch_bounds__(kParThreads) k_compose(ChainArgs a, int prefetch) {
   extern __shared__ uint32_t sh[];
   const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
   const SbsEvent first = a.ev[a.cls_list[b]];
   const uint32_t m = first.m;
   uint32_t* prev = sh;
   uint32_t* next = sh + m;
+  uint32_t* pis = sh + 2 * m;  // [gens][m] when prefetching
   const uint64_t copy_to = a.cls_copy[blockIdx.x];
   for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) {
     const int64_t v = a.pool[first.src + x];
@@ -377,17 +455,38 @@ __global__ void __launch_bounds__(kParThreads) k_compose(ChainArgs a) {
     return;
   }
   if (*reinterpret_cast<volatile uint32_t*>(a.flag)) return;  // a rejection: K8 redoes the call
-  for (uint32_t q = b; q < end; ++q) {
-    int64_t* g = a.pool + a.ev[a.cls_list[q]].slot;
-    for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
-      const uint32_t v = prev[static_cast<uint32_t>(g[p])];
-      next[p] = v;
-      g[p] = v;
+  if (prefetch) {
+    const uint32_t gens = end - b;
+    for (uint32_t x = threadIdx.x; x < gens * m; x += blockDim.x) {
+      const uint32_t q = x / m, p = x - q * m;
+      pis[x] = static_cast<uint32_t>(a.pool[a.ev[a.cls_list[b + q]].slot + p]);
     }
     __syncthreads();
-    uint32_t* t = prev;
-    prev = next;
-    next = t;
+    for (uint32_t q = 0; q < gens; ++q) {
+      int64_t* g = a.pool + a.ev[a.cls_list[b + q]].slot;
+      for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+        const uint32_t v = prev[pis[q * m + p]];
+        next[p] = v;
+        g[p] = v;
+      }
+      __syncthreads();
+      uint32_t* t = prev;
+      prev = next;
+      next = t;
+    }
+  } else {
+    for (uint32_t q = b; q < end; ++q) {
+      int64_t* g = a.pool + a.ev[a.cls_list[q]].slot;
+      for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+        const uint32_t v = prev[static_cast<uint32_t>(g[p])];
+        next[p] = v;
+        g[p] = v;
+      }
+      __syncthreads();
+      uint32_t* t = prev;
+      prev = next;
+      next = t;
+    }
   }
   const uint64_t final_to = a.cls_final[blockIdx.x];
   for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) a.pool[final_to + x] = prev[x];
@@ -507,16 +606,28 @@ cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
 }
 
 
-cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m, int force,
-                              cudaStream_t s, uint64_t* launches) {
+cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m,
+                              uint64_t max_gen_words, int force, cudaStream_t s, uint64_t* launches) {
   if (n_cls > 0 && max_m != 0xffffffffu && max_m <= kParMaxM) {
     cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_fy_gen),
                                       static_cast<int>(par_smem_bytes(kParMaxM)));
     if (ae != cudaSuccess) return ae;
-    ae = ensure_smem_attr(reinterpret_cast<const void*>(k_compose), static_cast<int>(8 * kParMaxM));
+    // prefetch the generations into shared memory when the largest class's
+    // (gens x m) words fit in 64 KB beside the two permutation buffers
+    const size_t pref = static_cast<size_t>(max_gen_words) * 4 <= 64 * 1024 ? static_cast<size_t>(max_gen_words) * 4 : 0;
+    const size_t csmem = 8 * static_cast<size_t>(max_m) + pref;
+    ae = ensure_smem_attr(reinterpret_cast<const void*>(k_compose), static_cast<int>(8 * kParMaxM + 64 * 1024));
     if (ae != cudaSuccess) return ae;
-    k_fy_gen<<<n_gen, kParThreads, par_smem_bytes(max_m), s>>>(a);
-    k_compose<<<n_cls, kParThreads, 8 * static_cast<size_t>(max_m), s>>>(a);
+    if (max_m <= kFyWarpMaxM) {
+      ae = ensure_smem_attr(reinterpret_cast<const void*>(k_fy_gen_warp),
+                            static_cast<int>(fy_warp_smem_bytes(kFyWarpMaxM)));
+      if (ae != cudaSuccess) return ae;
+      k_fy_gen_warp<<<(n_gen + kFyWarps - 1) / kFyWarps, kFyWarps * 32, fy_warp_smem_bytes(max_m), s>>>(a, n_gen,
+                                                                                                      max_m);
+    } else {
+      k_fy_gen<<<n_gen, kParThreads, par_smem_bytes(max_m), s>>>(a);
+    }
+    k_compose<<<n_cls, kParThreads, csmem, s>>>(a, pref ? 1 : 0);
     *launches += 2;
   } else if (n_cls > 0) {
     size_t smem = (kJWin + static_cast<size_t>(max_m)) * sizeof(uint32_t);
