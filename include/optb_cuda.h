@@ -319,7 +319,9 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream);
 /* Rows for subsequent steps come from `dataset` (e.g. a double-buffered
  * device copy of a host dataset refreshed by the caller every step). */
 int optb_pipeline_set_dataset(optb_pipeline* p, const uint8_t* dataset, uint64_t row_stride);
-/* Device draws (examples, classes) of a step still buffered (the last two). */
+/* Device draws (examples, classes) of a step still buffered (the last two
+ * sampler calls; three when n_shards >= 4, where the sampler runs two calls
+ * ahead). */
 int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** examples,
                         const int32_t** classes);
 /* The pipeline's container planes (valid for the last enqueued step). */

@@ -46,11 +46,16 @@ struct optb_pipeline {
   uint32_t spd = 1;       // steps per SBS call
   uint64_t rows = 0;      // rows per step
   cudaStream_t side = nullptr;
-  int64_t* ex[2] = {};
-  int32_t* cls[2] = {};
+  // draw buffers: nbuf - 1 sampler calls run ahead of the step being
+  // computed (1 normally; 2 when every rank draws the stream of >= 4 ranks,
+  // whose sampler work no longer fits in one call's worth of steps)
+  static constexpr int kMaxBufs = 3;
+  int nbuf = 2;
+  int64_t* ex[kMaxBufs] = {};
+  int32_t* cls[kMaxBufs] = {};
   void* cont = nullptr;
   uint8_t* offs = nullptr;
-  cudaEvent_t sbs_done[2] = {}, enc_done[2] = {};
+  cudaEvent_t sbs_done[kMaxBufs] = {}, enc_done[kMaxBufs] = {};
   cudaEvent_t t_s0[kTimingRing] = {}, t_s1[kTimingRing] = {}, t_e0[kTimingRing] = {},
               t_e1[kTimingRing] = {}, t_d1[kTimingRing] = {};
   uint64_t step = 0;   // next step to deliver
@@ -72,8 +77,9 @@ namespace {
 
 int enqueue_draws(optb_pipeline* p) {
   const uint64_t c = p->calls;
-  const int b = static_cast<int>(c % 2);
-  if (c >= 2 && cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess) return cuda_fail("stream wait");
+  const int b = static_cast<int>(c % p->nbuf);
+  if (c >= static_cast<uint64_t>(p->nbuf) && cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess)
+    return cuda_fail("stream wait");
   const int r = static_cast<int>(c % kTimingRing);
   if (p->timing) cudaEventRecord(p->t_s0[r], p->side);
   const uint64_t n = p->d.layout.n_batches * p->d.n_shards * p->spd;
@@ -101,8 +107,9 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
   p->spd = d->steps_per_draw ? d->steps_per_draw : 1;
   p->timing = d->record_timings != 0;
   p->rows = optb_layout_rows(&d->layout);
+  p->nbuf = d->n_shards >= 4 ? 3 : 2;
   bool ok = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) == cudaSuccess;
-  for (int b = 0; b < 2 && ok; ++b) {
+  for (int b = 0; b < p->nbuf && ok; ++b) {
     ok = cudaMalloc(&p->ex[b], p->rows * p->spd * sizeof(int64_t)) == cudaSuccess &&
          cudaMalloc(&p->cls[b], p->rows * p->spd * sizeof(int32_t)) == cudaSuccess &&
          cudaEventCreateWithFlags(&p->sbs_done[b], cudaEventDisableTiming) == cudaSuccess &&
@@ -120,10 +127,12 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
     optb_pipeline_destroy(p);
     return cuda_fail("CUDA call failed");
   }
-  st = enqueue_draws(p);  // the first call's draws start right away
-  if (st) {
-    optb_pipeline_destroy(p);
-    return st;
+  for (int c = 0; c + 1 < p->nbuf; ++c) {  // the first calls' draws start right away
+    st = enqueue_draws(p);
+    if (st) {
+      optb_pipeline_destroy(p);
+      return st;
+    }
   }
   *out = p;
   return OPTB_OK;
@@ -134,7 +143,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t k = p->step;
   const uint64_t call = k / p->spd, sub = k % p->spd;
-  const int b = static_cast<int>(call % 2);
+  const int b = static_cast<int>(call % p->nbuf);
   const int r = static_cast<int>(k % kTimingRing);
   int st;
   if (sub == 0) {
@@ -176,10 +185,10 @@ int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** e
                         const int32_t** classes) {
   if (!p || step >= p->calls * p->spd) return arg_fail("draws: step not drawn yet");
   const uint64_t call = step / p->spd;
-  if (call + 2 < p->calls) return arg_fail("draws: step's draw buffer already reused");
+  if (call + static_cast<uint64_t>(p->nbuf) < p->calls) return arg_fail("draws: step's draw buffer already reused");
   const uint64_t sub = step % p->spd;
-  if (examples) *examples = p->ex[call % 2] + sub * p->rows;
-  if (classes) *classes = p->cls[call % 2] + sub * p->rows;
+  if (examples) *examples = p->ex[call % p->nbuf] + sub * p->rows;
+  if (classes) *classes = p->cls[call % p->nbuf] + sub * p->rows;
   return OPTB_OK;
 }
 
@@ -302,7 +311,7 @@ void optb_pipeline_destroy(optb_pipeline* p) {
     if (h.up) cudaStreamDestroy(h.up);
     if (h.down) cudaStreamDestroy(h.down);
   }
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < p->kMaxBufs; ++b) {
     if (p->ex[b]) cudaFree(p->ex[b]);
     if (p->cls[b]) cudaFree(p->cls[b]);
     if (p->sbs_done[b]) cudaEventDestroy(p->sbs_done[b]);

@@ -47,11 +47,12 @@ def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype, spd,
     pipe.close()
 
 
-def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda):
+@pytest.mark.parametrize("G", [2, 4])  # 4 shards: three draw buffers, two calls ahead
+def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda, G):
     torch, O = torch_cuda, oracle_mod
     from paper_2105_00619_b200.pipeline import Pipeline
     S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
-    B, nb, P, G = 64, 3, 768, 2
+    B, nb, P = 64, 3, 768
     ds_d = torch.from_numpy(ds).cuda()
     cs = torch.linspace(0.001, 0.01, 10, device="cuda")
     cb = torch.linspace(-1, 1, 10, device="cuda")
@@ -61,13 +62,13 @@ def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda):
         pipe = Pipeline(cur, ds_d, 1, B, nb, shard=r, n_shards=G, out_dtype=torch.float32, class_scale=cs,
                         class_bias=cb)
         outs[r] = []
-        for _ in range(2):
+        for _ in range(3):
             o = torch.empty((B * nb, P), dtype=torch.float32, device="cuda")
             pipe.step(o)
             outs[r].append(o)
         pkg.codec.sync()
         pipe.close()
-    for step in range(2):
+    for step in range(3):
         ex, cl = ref.next(nb * G)
         ex, cl = ex.reshape(nb * G, B), cl.reshape(nb * G, B)
         for r in range(G):
