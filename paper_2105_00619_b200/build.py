@@ -27,7 +27,8 @@ CUDA_LIB = "/usr/local/cuda/lib64"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
               "--expt-relaxed-constexpr", "-diag-suppress", "177", "-I" + INCLUDE]
-CUDA_SOURCES = ["codec.cu", "sbs.cu", "capi.cu", "pipeline.cu", "io.cu", "peer.cu"]
+CUDA_SOURCES = ["codec.cu"] + [f"codec_v{v}.cu" for v in range(6)] + ["sbs.cu", "capi.cu", "pipeline.cu", "io.cu",
+                                                                      "peer.cu"]
 CUDA_LIB_NAME = os.path.join(PKG, "liboptb_cuda.so")
 SHIM_LIB_NAME = os.path.join(PKG, "liboptb_shim.so")
 SHIM_SOURCES = ["codec.cpp", "sampler.cpp", "nn.cpp"]
@@ -49,7 +50,8 @@ def _stale(target, sources):
 
 def build_cuda(force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, "internal.h"), os.path.join(INCLUDE, "optb_cuda.h")]
+    headers = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "codec_impl.cuh"),
+               os.path.join(INCLUDE, "optb_cuda.h")]
     objs = []
     jobs = []
     for src in CUDA_SOURCES:
@@ -58,7 +60,7 @@ def build_cuda(force: bool = False) -> str:
         objs.append(o)
         if force or _stale(o, [s] + headers):
             jobs.append([NVCC] + ARCH + NVCC_FLAGS + ["-c", s, "-o", o])
-    with cf.ThreadPoolExecutor(max_workers=len(CUDA_SOURCES)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=min(len(CUDA_SOURCES), os.cpu_count() or 4)) as ex:
         list(ex.map(_run, jobs))
     if force or _stale(CUDA_LIB_NAME, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", CUDA_LIB_NAME] + objs + ["-cudart", "static"])

@@ -1,1210 +1,10 @@
-// codec.cu -- sm_100a encode / decode kernels for the optb container modes.
-//
-// Reference semantics (file:line under /root/reference/proj):
-//   encode  codec.cpp:106-146   decode  codec.cpp:148-208
-//   gather  dataset.cpp:16-22 + runner.cpp:77-90 (chunking of a batch)
-//   float epilogue  nn.cpp:183-189 (float(q)*scale), fp16 store nn.cpp:235 ->
-//   tensor.cpp:12-51 (RNE; __float2half_rn is bit-identical on q*scale values,
-//   SURVEY App. B).
-//
-// Kernel families:
-//   k_encode_vec<MODE>    K1/K3/K5: gathered rows by cp.async into a 2-stage
-//                         warp-private smem ring, 16-pixel x 16-image register
-//                         byte transpose (PRMT), per-mode word build (exact
-//                         bytes, lossless 7-bit compaction + 16-bit parity
-//                         stores, f64 ordered binary64 adds), XOR-swizzled
-//                         staging, fully coalesced 128/64-bit container stores.
-//   k_decode_vec<MODE,O,TMA>  K2/K4/K6: container words by one 2D TMA tensor
-//                         load per tile (128-byte hardware swizzle, mbarrier
-//                         completion; exact / f64 modes) or by cp.async into
-//                         XOR-swizzled slots (+ lossless parity bits), per-mode
-//                         range check and unpack, transpose, u8 rows stored
-//                         directly or through a u8 tile with the fused
-//                         fp32/fp16/bf16 epilogue.
-//   k_roundtrip_vec<MODE,O>  K1+K2 in one persistent launch (optb_roundtrip_dev,
-//                         the E-D pipeline step): each warp encodes its tiles
-//                         into HBM, then decodes the same tiles back.
-//   k_{en,de}code_generic any P / stride / alignment: one pixel per lane,
-//                         warp ballots for the parity plane.
-#include <cuda.h>
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
-#include <cuda_runtime.h>
-#include <stdint.h>
-#include <stdlib.h>
-#include <string.h>
-
-#include <mutex>
-#include <set>
-#include <tuple>
-#include <type_traits>
-
-#include "internal.h"
+// codec.cu -- dispatch of the optb codec kernels (the kernels themselves are in
+// codec_impl.cuh, instantiated per mode variant by codec_v<N>.cu), the
+// synthetic-data kernel, and the shared launch helpers.
+#include "codec_impl.cuh"
 
 namespace optb_b200 {
 namespace {
-
-#ifndef OPTB_VEC_WARPS
-#define OPTB_VEC_WARPS 8
-#endif
-#ifndef OPTB_VEC_STAGES
-#define OPTB_VEC_STAGES 2
-#endif
-constexpr int kWarps = OPTB_VEC_WARPS;  // warps per CTA for the vector kernels
-constexpr int kThreads = kWarps * 32;
-
-__device__ __forceinline__ uint4 ldg16(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint2 ldg8(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void stg16(void* p, uint4 v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ void stg8(void* p, uint2 v) {
-  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
-}
-
-// 4x4 byte transpose of rows a0..a3 (row r's byte c -> row c's byte r).
-__device__ __forceinline__ void t4x4(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
-  const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a0, a1, 0x7362);
-  const uint32_t t2 = __byte_perm(a2, a3, 0x5140), t3 = __byte_perm(a2, a3, 0x7362);
-  a0 = __byte_perm(t0, t2, 0x5410);
-  a1 = __byte_perm(t0, t2, 0x7632);
-  a2 = __byte_perm(t1, t3, 0x5410);
-  a3 = __byte_perm(t1, t3, 0x7632);
-}
-
-// 16x16 byte transpose, m[r][q] holds bytes 4q..4q+3 of row r.  ROWS / COLS
-// bound the live part (rows >= ROWS are zero, columns >= COLS are unused):
-// exact64 uses 8 of the 16 image columns / rows.
-template <int ROWS, int COLS>
-__device__ __forceinline__ void transpose16(uint32_t (&m)[16][4]) {
-  uint32_t t[16][4];
-#pragma unroll
-  for (int R = 0; R < 4; ++R) {
-#pragma unroll
-    for (int Q = 0; Q < 4; ++Q) {
-      if (4 * Q >= COLS) continue;
-      uint32_t a0 = 4 * R + 0 < ROWS ? m[4 * R + 0][Q] : 0u;
-      uint32_t a1 = 4 * R + 1 < ROWS ? m[4 * R + 1][Q] : 0u;
-      uint32_t a2 = 4 * R + 2 < ROWS ? m[4 * R + 2][Q] : 0u;
-      uint32_t a3 = 4 * R + 3 < ROWS ? m[4 * R + 3][Q] : 0u;
-      t4x4(a0, a1, a2, a3);
-      t[4 * Q + 0][R] = a0;
-      t[4 * Q + 1][R] = a1;
-      t[4 * Q + 2][R] = a2;
-      t[4 * Q + 3][R] = a3;
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 16; ++r)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) m[r][q] = (r < COLS) ? t[r][q] : 0u;
-}
-
-struct ChunkPos {
-  uint64_t r0;  // first stream row of the chunk
-  uint32_t n;   // images in the chunk
-};
-
-__device__ __forceinline__ ChunkPos chunk_pos(const Geom& g, uint64_t k) {
-  const uint64_t b = k / g.cpb;
-  const uint32_t j = static_cast<uint32_t>(k - b * g.cpb);
-  const uint64_t first = static_cast<uint64_t>(j) * g.per_chunk;
-  const uint64_t left = g.B - first;
-  ChunkPos c;
-  c.r0 = b * g.B + first;
-  c.n = left < g.per_chunk ? static_cast<uint32_t>(left) : g.per_chunk;
-  return c;
-}
-
-// A lane's work item t = k*G + gi (chunk k = b*cpb + j, G = items per chunk)
-// along its grid-stride sequence.  The hot loops advance it with adds and
-// compares only; the 64-bit divisions happen once, at kernel start.
-struct Walk {
-  uint64_t t, k, gi, b;
-  uint32_t j;
-};
-struct WalkStep {
-  uint64_t dt, dk, dgi, db;
-  uint32_t dj;
-};
-__device__ __forceinline__ Walk walk_at(const Geom& g, uint64_t G, uint64_t t) {
-  Walk w;
-  w.t = t;
-  w.k = t / G;
-  w.gi = t - w.k * G;
-  w.b = w.k / g.cpb;
-  w.j = static_cast<uint32_t>(w.k - w.b * g.cpb);
-  return w;
-}
-__device__ __forceinline__ WalkStep walk_step(const Geom& g, uint64_t G, uint64_t dt) {
-  WalkStep s;
-  s.dt = dt;
-  s.dk = dt / G;
-  s.dgi = dt - s.dk * G;
-  s.db = s.dk / g.cpb;
-  s.dj = static_cast<uint32_t>(s.dk - s.db * g.cpb);
-  return s;
-}
-__device__ __forceinline__ void walk_advance(Walk& w, const WalkStep& s, const Geom& g, uint64_t G) {
-  w.t += s.dt;
-  w.gi += s.dgi;
-  w.k += s.dk;
-  w.b += s.db;
-  w.j += s.dj;
-  if (w.gi >= G) {  // gi, dgi < G: at most one carry
-    w.gi -= G;
-    ++w.k;
-    ++w.j;
-  }
-  if (w.j >= g.cpb) {  // j, dj < cpb, carry <= 1: at most one wrap
-    w.j -= g.cpb;
-    ++w.b;
-  }
-}
-__device__ __forceinline__ ChunkPos walk_chunk(const Geom& g, const Walk& w) {
-  const uint64_t first = static_cast<uint64_t>(w.j) * g.per_chunk;
-  const uint64_t left = g.B - first;
-  ChunkPos c;
-  c.r0 = w.b * g.B + first;
-  c.n = left < g.per_chunk ? static_cast<uint32_t>(left) : g.per_chunk;
-  return c;
-}
-
-__device__ __forceinline__ void latch_error(DevError* err, uint32_t kind, uint64_t chunk,
-                                            uint32_t n) {
-  atomicCAS(&err->kind, 0u, kind);
-  atomicMin(&err->key, static_cast<unsigned long long>((chunk << 8) | n));
-}
-
-// 256^i as an exact binary64 built from its exponent bits (0 <= i <= 16).
-__device__ __forceinline__ double pow256(int i) {
-  return __longlong_as_double(static_cast<long long>(1023 + 8 * i) << 52);
-}
-
-// ------------------------------------------------------------------ epilogue
-// y = RN(float(q) * s) (nn.cpp:186), then RN(y + b) with a per-class bias.
-// Fast form for 0 < s < 2^100: PRMT puts the byte q under the exponent of
-// 2^23 (a = 2^23 + q, exact), and one FFMA gives RN(a*s - 2^23*s) = RN(q*s)
-// because the product is exact inside the FMA and 2^23*s is an exact float;
-// so 2 full-rate ops per pixel instead of an extract + I2F + FMUL.  Other
-// scales (negative, zero, huge, non-finite) take the plain FMUL, which also
-// keeps -0.0 for q = 0 and NaN / Inf exactly as the reference.
-struct PxScale {
-  float s, ms, b;
-  bool fast, affine;
-};
-__device__ __forceinline__ PxScale px_scale(float s, float b, bool affine) {
-  PxScale c;
-  c.s = s;
-  c.b = b;
-  c.affine = affine;
-  c.fast = s > 0.0f && s < 0x1p100f;
-  c.ms = -__fmul_rn(s, 0x1p23f);
-  return c;
-}
-template <bool FAST>
-__device__ __forceinline__ float px_value(uint32_t w, int k, const PxScale& c) {
-  float y;
-  if constexpr (FAST) {
-    y = __fmaf_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650u | static_cast<uint32_t>(k))), c.s, c.ms);
-  } else {
-    y = __fmul_rn(static_cast<float>((w >> (8 * k)) & 0xffu), c.s);
-  }
-  return c.affine ? __fadd_rn(y, c.b) : y;
-}
-
-struct Out4 {
-  // store 4 consecutive decoded pixels q (bytes of `q4`) at `dst`
-  template <int O, bool FAST>
-  static __device__ __forceinline__ void put(void* dst, uint32_t q4, const PxScale& c) {
-    float y[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = px_value<FAST>(q4, k, c);
-    if constexpr (O == OPTB_OUT_F32) {
-      float4 f = make_float4(y[0], y[1], y[2], y[3]);
-      stg16(dst, *reinterpret_cast<uint4*>(&f));
-    } else if constexpr (O == OPTB_OUT_F16) {
-      const __half2 h0 = __floats2half2_rn(y[0], y[1]), h1 = __floats2half2_rn(y[2], y[3]);
-      stg8(dst, make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1)));
-    } else {
-      const __nv_bfloat162 h0 = __floats2bfloat162_rn(y[0], y[1]), h1 = __floats2bfloat162_rn(y[2], y[3]);
-      stg8(dst, make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1)));
-    }
-  }
-};
-
-// 8 consecutive decoded pixels -> 8 binary16 / bfloat16 values, one 128-bit store.
-struct Out8 {
-  template <int O, bool FAST>
-  static __device__ __forceinline__ void put(void* dst, uint2 q8, const PxScale& c) {
-    uint32_t w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t src = k < 2 ? q8.x : q8.y;
-      const int sh = 2 * (k & 1);
-      const float y0 = px_value<FAST>(src, sh, c), y1 = px_value<FAST>(src, sh + 1, c);
-      if constexpr (O == OPTB_OUT_F16) {
-        const __half2 h = __floats2half2_rn(y0, y1);
-        w[k] = *reinterpret_cast<const uint32_t*>(&h);
-      } else {
-        const __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
-        w[k] = *reinterpret_cast<const uint32_t*>(&h);
-      }
-    }
-    stg16(dst, make_uint4(w[0], w[1], w[2], w[3]));
-  }
-};
-
-template <int O>
-__device__ __forceinline__ void put1(void* out, uint64_t idx, uint32_t q, float s, float b,
-                                     bool affine) {
-  if constexpr (O == OPTB_OUT_U8) {
-    static_cast<uint8_t*>(out)[idx] = static_cast<uint8_t>(q);
-  } else {
-    const float v0 = __fmul_rn(static_cast<float>(q), s);
-    const float y = affine ? __fadd_rn(v0, b) : v0;
-    if constexpr (O == OPTB_OUT_F32) {
-      static_cast<float*>(out)[idx] = y;
-    } else if constexpr (O == OPTB_OUT_F16) {
-      static_cast<__half*>(out)[idx] = __float2half_rn(y);
-    } else {
-      static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(y);
-    }
-  }
-}
-
-__device__ __forceinline__ void row_affine(const Epi& e, uint64_t row, float& s, float& b,
-                                           bool& affine) {
-  s = e.scale;
-  b = 0.0f;
-  affine = false;
-  if (e.class_scale) {
-    const int32_t c = __ldg(e.row_class + row);
-    s = __ldg(e.class_scale + c);
-    if (e.class_bias) {
-      b = __ldg(e.class_bias + c);
-      affine = true;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ async copy
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// ------------------------------------------------------------------ TMA / mbarrier
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n OPTB_WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra OPTB_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
-      "r"(phase)
-      : "memory");
-}
-// 2D tensor-map tile load into shared memory, completing on mbarrier `b`
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-      "[%4];" ::"r"(smem_u32(dst)),
-      "l"(m), "r"(c0), "r"(c1), "r"(smem_u32(b))
-      : "memory");
-}
-// order this thread's generic-proxy accesses before later async-proxy (TMA) ones
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// Work items: 16 consecutive pixels of one chunk, linear in (chunk, group),
-// so a warp's 32 items cover 32*16*WC contiguous container bytes.  Each warp
-// runs a kStages-deep cp.async pipeline over its tiles (one tile = the warp's
-// 32 items) in a warp-private ring of shared-memory slots: the copies of the
-// next kStages-1 tiles are in flight while the current tile is transposed.
-// Requires P % 16 == 0 and 16-byte aligned rows / containers / outputs.
-constexpr int kStages = OPTB_VEC_STAGES;
-
-
-// ------------------------------------------------------------------ K1 / K3
-// Gather-encode for the exact and lossless modes.  Stage slot layout on
-// input: row i of the chunk, lane L's 16 pixels at i*512 + L*16
-// (conflict-free); after the register transpose the slot is reused as the
-// output tile, word p of lane L at (L*16 + (p ^ (L & SW)))*WC (conflict-free
-// both ways), then copied out with fully coalesced 128-bit (64-bit) stores.
-// Lossless (codec.cpp:125-135): each pixel's 7-bit fields (px >> 1) are
-// compacted from byte lanes with three mask/shift steps; the parity bits
-// (px & 1) of a lane's 16 pixels of image i are one 16-bit store at plane bit
-// i*P + 16*group (aligned: the vector path needs P % 32 == 0 in these modes).
-// kF64Narrow: Float64Faithful with at most 8 images per container (the
-// common case, capacity 6): half the staging and transpose work of the
-// 16-image (lossy) variant, two CTAs per SM.
-constexpr int kF64Narrow = 5;
-
-template <int MODE>
-struct VecMode {
-  static constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
-  static constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
-  static constexpr bool F64 = MODE == OPTB_F64 || MODE == kF64Narrow;
-  static constexpr int NI = (MODE == OPTB_EXACT64 || MODE == kF64Narrow) ? 8
-                            : (MODE == OPTB_EXACT128 || F64) ? 16
-                            : (MODE == OPTB_LOSSLESS64) ? 9 : 18;      // images per word
-  static constexpr int NT = NI < 16 ? NI : 16;                         // images in the 16x16 transpose
-  static constexpr int SW = (WC == 16) ? 7 : 15;                       // slot XOR swizzle mask
-  static constexpr int ROWS_B = NI * 512;                              // staged input rows
-  static constexpr int WORDS_B = 512 * WC;                             // container words of a tile
-  static constexpr int PAR_B = OFFS ? NI * 64 : 0;                     // staged parity bits (decode)
-  static constexpr int ENC_SLOT = ROWS_B > WORDS_B ? ROWS_B : WORDS_B;
-  static constexpr int DEC_SLOT = (WORDS_B + PAR_B) > ROWS_B ? (WORDS_B + PAR_B) : ROWS_B;
-  static constexpr int MIN_BLOCKS = (WC == 16 || NI == 16) ? 1 : 2;
-};
-
-// Float64Faithful peel of one container value into 16 image bytes
-// (codec.cpp:171-175: q = fmod(acc, 256), acc = (acc - q) / 256, pixel =
-// (u8)q), without fmod:
-//  * 0 <= acc < 2^64: the peel is exactly the integer peel of trunc(acc) --
-//    fmod keeps acc's fraction in q, (u8)q drops it, (acc - q)/256 is
-//    trunc(acc/256);
-//  * acc >= 2^64: acc is a multiple of 2^12, so q = 0 and acc/256 is exact;
-//  * +inf / NaN: q is NaN -> pixel 0 (the reference's x86 conversion), and
-//    acc stays non-finite; the acc >= 2^64 branch yields the same bytes.
-__device__ __forceinline__ void f64_peel16(double acc, uint32_t (&b)[4]) {
-  b[0] = b[1] = b[2] = b[3] = 0u;
-  bool small = acc < 0x1.0p64;
-  uint64_t iacc = small ? static_cast<uint64_t>(acc) : 0ull;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    uint32_t q = 0u;
-    if (small) {
-      q = static_cast<uint32_t>(iacc & 0xffull);
-      iacc >>= 8;
-    } else {
-      acc = __dmul_rn(acc, 0x1.0p-8);
-      small = acc < 0x1.0p64;
-      if (small) iacc = static_cast<uint64_t>(acc);
-    }
-    b[i >> 2] |= q << (8 * (i & 3));
-  }
-}
-
-// Out-of-line so the rare lossy >= 2^64 case does not bloat the unrolled
-// per-pixel loops of the decode kernel.
-__device__ __noinline__ uint4 f64_peel_big(double acc) {
-  uint32_t t[4];
-  f64_peel16(acc, t);
-  return make_uint4(t[0], t[1], t[2], t[3]);
-}
-
-__device__ __forceinline__ uint64_t compact7(uint64_t x) {  // 8 byte lanes -> 8 x 7-bit fields
-  x = (x & 0x007F007F007F007Full) | ((x & 0x7F007F007F007F00ull) >> 1);
-  x = (x & 0x00003FFF00003FFFull) | ((x & 0x3FFF00003FFF0000ull) >> 2);
-  return (x & 0x000000000FFFFFFFull) | ((x & 0x0FFFFFFF00000000ull) >> 4);
-}
-__device__ __forceinline__ uint64_t expand7(uint64_t x) {  // inverse of compact7
-  x = (x & 0x0FFFFFFFull) | ((x << 4) & 0x0FFFFFFF00000000ull);
-  x = (x & 0x00003FFF00003FFFull) | ((x << 2) & 0x3FFF00003FFF0000ull);
-  return (x & 0x007F007F007F007Full) | ((x << 1) & 0x7F007F007F007F00ull);
-}
-__device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> bytes' LSBs
-  return (b * 0x00204081u) & 0x01010101u;
-}
-
-// PTRS: stream row r is read from the absolute address src.ptrs[r] (this
-// GPU's HBM, a peer GPU's HBM over NVLink, mapped pinned host memory) instead
-// of src.images + src.index[r] * src.stride.
-// warp_region: bytes of shared memory per warp (its ring), >= kStages * slot;
-// the fused kernel gives both bodies the same per-warp region so that a warp
-// in one phase never touches another warp's ring in the other phase.
-template <int MODE, bool PTRS>
-__device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
-                                            uint8_t* __restrict__ offsets, uint8_t* smem_base,
-                                            uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT) {
-  const uint8_t* __restrict__ images = src.images;
-  const uint64_t row_stride = src.stride;
-  const int64_t* __restrict__ row_index = src.index;
-  using S = VecMode<MODE>;
-  constexpr int WC = S::WC;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_base + warp * warp_region;
-  const uint64_t G = g.P / 16;
-  const uint64_t items = g.chunks * G;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
-  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
-
-  const WalkStep step = walk_step(g, G, stride);
-  // Dataset row ids of a tile are fetched one stage before its copies are
-  // issued, so the dependent index loads never stall the pipeline.
-  Walk wf = walk_at(g, G, first + lane);  // next tile to fetch row ids for
-  using RowT = typename std::conditional<PTRS, uint64_t, uint32_t>::type;
-  RowT rows[S::NI];
-  uint64_t pend_gi = 0;  // group and image count of the fetched tile
-  uint32_t pend_n = 0;
-  auto fetch_rows = [&]() {
-    pend_n = 0;
-    if (wf.t < items) {
-      const ChunkPos c = walk_chunk(g, wf);
-      pend_n = c.n;
-      pend_gi = wf.gi;
-      // uniform source choice outside the unrolled loop, predicated loads
-      // inside it (no per-row branches)
-      if constexpr (PTRS) {
-        const unsigned long long* rp = reinterpret_cast<const unsigned long long*>(src.ptrs) + c.r0;
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i) {
-          RowT v = 0;
-          if (i < static_cast<int>(c.n)) v = __ldg(rp + i);
-          rows[i] = v;
-        }
-      } else if (row_index) {
-        const int64_t* rp = row_index + c.r0;
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i) {
-          RowT v = 0;
-          if (i < static_cast<int>(c.n)) v = static_cast<uint32_t>(__ldg(rp + i));
-          rows[i] = v;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i) rows[i] = static_cast<RowT>(c.r0 + i);  // used only for i < n
-      }
-    }
-    walk_advance(wf, step, g, G);
-  };
-  auto issue = [&](int stage) {
-    uint8_t* slot = ring + stage * S::ENC_SLOT;
-#pragma unroll
-    for (int i = 0; i < S::NI; ++i) {
-      if (i < static_cast<int>(pend_n)) {
-        const uint8_t* row = PTRS ? reinterpret_cast<const uint8_t*>(static_cast<uintptr_t>(rows[i]))
-                                  : images + static_cast<uint64_t>(rows[i]) * row_stride;
-        cp_async16(slot + i * 512 + lane * 16, row + pend_gi * 16);
-      }
-    }
-    cp_async_commit();
-  };
-
-#pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    fetch_rows();
-    issue(s);
-  }
-  fetch_rows();
-  int stage = 0;
-  Walk wc = walk_at(g, G, first + lane);  // the tile being transposed
-  for (uint64_t base = first; base < items; base += stride) {
-    issue((stage + kStages - 1) % kStages);
-    fetch_rows();  // consumed by the next iteration's issue
-    cp_async_wait<kStages - 1>();
-    __syncwarp();
-    uint8_t* slot = ring + stage * S::ENC_SLOT;
-    const uint64_t t = wc.t;
-    uint32_t n = 0;
-    const uint64_t k = wc.k, gi = wc.gi;
-    if (t < items) n = walk_chunk(g, wc).n;
-    walk_advance(wc, step, g, G);
-    uint32_t m[16][4];
-    uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};  // images 16, 17 (lossless128)
-#pragma unroll
-    for (int i = 0; i < S::NI; ++i) {
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (i < static_cast<int>(n)) v = *reinterpret_cast<const uint4*>(slot + i * 512 + lane * 16);
-      if constexpr (S::OFFS) {
-        // parity bits of 16 pixels at plane bit i*P + 16*gi (codec.cpp:132-133);
-        // images in [n, per_chunk) (partial chunk) write zeros so the padded
-        // plane is deterministic; the plane holds per_chunk images
-        if (t < items && i < static_cast<int>(g.per_chunk)) {
-          const uint32_t bits = (((v.x & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) |
-                                ((((v.y & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 4) |
-                                ((((v.z & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 8) |
-                                ((((v.w & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 12);
-          *reinterpret_cast<uint16_t*>(offsets + k * g.ostride + (static_cast<uint64_t>(i) * g.P) / 8 + 2 * gi) =
-              static_cast<uint16_t>(bits);
-        }
-      }
-      if (i < 16) {
-        m[i][0] = v.x;
-        m[i][1] = v.y;
-        m[i][2] = v.z;
-        m[i][3] = v.w;
-      } else if (i == 16) {
-        x16[0] = v.x; x16[1] = v.y; x16[2] = v.z; x16[3] = v.w;
-      } else {
-        x17[0] = v.x; x17[1] = v.y; x17[2] = v.z; x17[3] = v.w;
-      }
-    }
-    if constexpr (S::OFFS) {
-      if (t < items && gi == 0) {  // zero the plane's stride padding once per chunk
-        for (uint64_t b = (static_cast<uint64_t>(g.per_chunk) * g.P) / 8; b < g.ostride; b += 4)
-          *reinterpret_cast<uint32_t*>(offsets + k * g.ostride + b) = 0u;
-      }
-    }
-    transpose16<S::NT, 16>(m);  // m[p] = bytes of images 0..15 at pixel p
-    __syncwarp();
-#pragma unroll
-    for (int p = 0; p < 16; ++p) {
-      const int sl = p ^ (lane & S::SW);
-      if constexpr (S::F64) {
-        // acc += px_i * 256^i in binary64, i ascending (codec.cpp:116-120); the
-        // products are exact, the adds round in the reference's order
-        double acc = 0.0;
-        if (n <= 6u) {
-          // every partial sum is an integer < 2^48: exact, so the ordered sum
-          // is the packed integer itself (one conversion instead of 2n ops)
-          const uint64_t word = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
-          acc = static_cast<double>(word & ((1ull << (8 * n)) - 1ull));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i < static_cast<int>(n))
-              acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
-                                             pow256(i)));
-        }
-        *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
-      } else if constexpr (S::OFFS) {
-        const uint64_t lo8 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];  // images 0..7
-        const uint64_t lo = compact7((lo8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
-        if constexpr (WC == 8) {  // lossless64: fields 0..7 + image 8's field at bit 56
-          const uint64_t f8 = (m[p][2] & 0xFFu) >> 1;
-          *reinterpret_cast<uint64_t*>(slot + (lane * 16 + sl) * 8) = lo | (f8 << 56);
-        } else {  // lossless128: fields 0..15, images 16/17 at bits 112/119
-          const uint64_t hi8 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
-          const uint64_t hi = compact7((hi8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
-          const uint64_t f16 = ((x16[p >> 2] >> (8 * (p & 3))) & 0xFFu) >> 1;
-          const uint64_t f17 = ((x17[p >> 2] >> (8 * (p & 3))) & 0xFFu) >> 1;
-          const uint64_t w0 = lo | (hi << 56);
-          const uint64_t w1 = (hi >> 8) | (f16 << 48) | (f17 << 55);
-          *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) =
-              make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1),
-                         static_cast<uint32_t>(w1 >> 32));
-        }
-      } else if constexpr (WC == 16) {
-        *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
-      } else {
-        *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) = make_uint2(m[p][0], m[p][1]);
-      }
-    }
-    __syncwarp();
-    uint8_t* dst = cont + base * 16 * WC;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int W = q * 32 + lane, L = W >> 4, p = W & 15;
-      if (base + L < items) {
-        const int sl = p ^ (L & S::SW);
-        if constexpr (WC == 16) {
-          stg16(dst + W * 16, *reinterpret_cast<const uint4*>(slot + (L * 16 + sl) * 16));
-        } else {
-          stg8(dst + W * 8, *reinterpret_cast<const uint2*>(slot + (L * 16 + sl) * 8));
-        }
-      }
-    }
-    __syncwarp();
-    stage = (stage + 1) % kStages;
-  }
-  cp_async_wait<0>();
-}
-
-template <int MODE, bool PTRS>
-__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_encode_vec(Geom g, RowSrc src, uint8_t* __restrict__ cont, uint8_t* __restrict__ offsets) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  encode_body<MODE, PTRS>(g, src, cont, offsets, smem_raw);
-}
-
-// ------------------------------------------------------------------ K2 / K4
-// Decode.  Container words (and, lossless, the tile's parity bits) arrive in
-// a warp-private ring slot, either by cp.async straight into the XOR-swizzled
-// slot or as ONE 2D TMA tensor load per tile (parity bits by cp.async next to
-// it) (the tile's 512*WC contiguous bytes as a [rows][128 B] box with the
-// hardware's 128-byte swizzle, completion on a per-stage mbarrier).  Each
-// pixel's word is range checked, lossless fields are expanded back to byte
-// lanes, the 16x16 transpose gives 16 pixels of every image per lane,
-// lossless rows get (field << 1) | parity; u8 rows are stored directly (each
-// warp instruction writes 512 contiguous bytes of one row); float outputs go
-// through a u8 tile in the same slot so that the epilogue stores are
-// coalesced too.
-//
-// TMA slot layout (SWIZZLE_128B, slot 1024-byte aligned): byte b of the tile
-// sits at row r = b / 128, 16-byte chunk c = (b % 128) / 16, stored at
-// r*128 + ((c ^ (r & 7)) << 4) + b % 16.  Lane L's word p is tile byte
-// (16L + p) * WC.  The read order below keeps the 8 lanes of each
-// quarter-warp on 8 distinct chunks (conflict-free):
-//   WC = 16: r = 2L + p/8, c = p%8; at step j lane L reads p = j and j+8,
-//            lanes with L & 4 the high half first;
-//   WC = 8 : r = L, c = p/2; at step c lane L reads words 2c, 2c+1.
-template <int MODE>
-struct DecSlot {
-  static constexpr int RAW = VecMode<MODE>::DEC_SLOT;
-  static constexpr int TMA = (RAW + 1023) / 1024 * 1024;
-};
-
-__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  const uint32_t a = smem_u32(p);
-  return p + (((a + 1023u) & ~1023u) - a);
-}
-
-template <int MODE, int O, bool TMA>
-__device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom& g, const uint8_t* __restrict__ cont,
-                                            const uint8_t* __restrict__ offsets, const Epi& e,
-                                            void* __restrict__ out, DevError* err, uint8_t* smem_base,
-                                            uint64_t* bars, uint32_t warp_region = 0) {
-  using S = VecMode<MODE>;
-  constexpr int WC = S::WC;
-  constexpr int SLOT = TMA ? DecSlot<MODE>::TMA : DecSlot<MODE>::RAW;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_base + warp * (warp_region ? warp_region : kStages * SLOT);
-  uint64_t* bar = bars + warp * kStages;
-  const uint64_t G = g.P / 16;
-  const uint64_t items = g.chunks * G;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
-  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
-  const uint64_t ostride = e.row_stride;
-  if constexpr (TMA) {
-    if (lane == 0)
-      for (int st = 0; st < kStages; ++st) mbar_init(bar + st, 1);
-    fence_mbar_init();
-    __syncwarp();
-  }
-
-  const WalkStep step = walk_step(g, G, stride);
-  const bool bulk_parity = S::OFFS && g.P % 512 == 0;
-  Walk wi = walk_at(g, G, first + lane);  // next tile to issue (parity planes)
-  Walk wc = wi;                           // the tile being decoded
-  auto issue = [&](uint64_t base, int stage) {
-    if (base < items) {
-      uint8_t* slot = ring + stage * SLOT;
-      if constexpr (TMA) {
-        if (lane == 0) {
-          mbar_expect_tx(bar + stage, 512 * WC);
-          tma_load_2d(slot, cmap, 0, static_cast<int>((base * 16 * WC) >> 7), bar + stage);
-        }
-      } else {
-        const uint8_t* src = cont + base * 16 * WC;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int W = q * 32 + lane, L = W >> 4, p = W & 15;
-          if (base + L < items) {
-            const int sl = p ^ (L & S::SW);
-            if constexpr (WC == 16) {
-              cp_async16(slot + (L * 16 + sl) * 16, src + W * 16);
-            } else {
-              cp_async8(slot + (L * 16 + sl) * 8, src + W * 8);
-            }
-          }
-        }
-      }
-      if constexpr (S::OFFS) {
-        if (bulk_parity) {
-          // P % 512 == 0: the tile lies in one chunk and image i's 512 parity
-          // bits are 64 contiguous, 64-aligned bytes of the plane -- four
-          // 16-byte cp.async.cg per image (L2, never a stale L1 line: the
-          // fused round trip reads back bits this warp just wrote)
-          const uint64_t k = wi.k, gi0 = wi.gi - lane;
-          const uint32_t n = walk_chunk(g, wi).n;
-          const uint8_t* plane = offsets + k * g.ostride + 2 * gi0;
-#pragma unroll
-          for (int j = lane; j < 4 * S::NI; j += 32) {
-            const int i = j >> 2, part = j & 3;
-            if (i < static_cast<int>(n))
-              cp_async16(slot + S::WORDS_B + i * 64 + part * 16, plane + (static_cast<uint64_t>(i) * g.P) / 8 + part * 16);
-          }
-        } else {
-        // parity bits of lane pairs (4 bytes, 4-aligned as P % 32 == 0)
-        const uint64_t t = wi.t;
-        if ((lane & 1) == 0 && t < items) {
-          const uint64_t k = wi.k, gi = wi.gi;
-          const uint32_t n = walk_chunk(g, wi).n;
-          const bool pair = (t + 1 < items) && (gi + 1 < G);
-#pragma unroll
-          for (int i = 0; i < S::NI; ++i) {
-            if (i < static_cast<int>(n)) {
-              const uint8_t* ps = offsets + k * g.ostride + (static_cast<uint64_t>(i) * g.P) / 8 + 2 * gi;
-              uint8_t* pd = slot + S::WORDS_B + i * 64 + lane * 2;
-              if (pair) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(pd)), "l"(ps) : "memory");
-              } else {
-                *reinterpret_cast<uint16_t*>(pd) = *reinterpret_cast<const uint16_t*>(ps);
-              }
-            }
-          }
-        }
-        }
-      }
-    }
-    if constexpr (!TMA || S::OFFS) cp_async_commit();  // words (cp.async path) / parity bits
-    if constexpr (S::OFFS) walk_advance(wi, step, g, G);
-  };
-
-#pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue(first + s * stride, s);
-  int stage = 0;
-  uint32_t phase = 0;
-  for (uint64_t base = first; base < items; base += stride) {
-    issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
-    if constexpr (TMA) mbar_wait(bar + stage, phase);
-    if constexpr (!TMA || S::OFFS) {
-      cp_async_wait<kStages - 1>();
-      __syncwarp();
-    }
-    uint8_t* slot = ring + stage * SLOT;
-    const bool valid = wc.t < items;
-    const uint64_t k = wc.k, gi = wc.gi;
-    ChunkPos c{0, 0};
-    if (valid) c = walk_chunk(g, wc);
-    walk_advance(wc, step, g, G);
-    // raw words: m[p] = word of pixel 16*gi + p (low 8 bytes in [0..1] for WC 8)
-    uint32_t m[16][4];
-    if constexpr (TMA && WC == 16) {
-      const bool hi = (lane >> 2) & 1;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int ra = 2 * lane + (hi ? 1 : 0), rb = 2 * lane + (hi ? 0 : 1);
-        const uint4 a = *reinterpret_cast<const uint4*>(slot + ra * 128 + ((j ^ (ra & 7)) << 4));
-        const uint4 b = *reinterpret_cast<const uint4*>(slot + rb * 128 + ((j ^ (rb & 7)) << 4));
-        m[j][0] = hi ? b.x : a.x;
-        m[j][1] = hi ? b.y : a.y;
-        m[j][2] = hi ? b.z : a.z;
-        m[j][3] = hi ? b.w : a.w;
-        m[j + 8][0] = hi ? a.x : b.x;
-        m[j + 8][1] = hi ? a.y : b.y;
-        m[j + 8][2] = hi ? a.z : b.z;
-        m[j + 8][3] = hi ? a.w : b.w;
-      }
-    } else if constexpr (TMA) {
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const uint4 v = *reinterpret_cast<const uint4*>(slot + lane * 128 + ((cc ^ (lane & 7)) << 4));
-        m[2 * cc][0] = v.x;
-        m[2 * cc][1] = v.y;
-        m[2 * cc + 1][0] = v.z;
-        m[2 * cc + 1][1] = v.w;
-        m[2 * cc][2] = m[2 * cc][3] = m[2 * cc + 1][2] = m[2 * cc + 1][3] = 0u;
-      }
-    } else {
-#pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        const int sl = p ^ (lane & S::SW);
-        if constexpr (WC == 16) {
-          const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
-          m[p][0] = v.x;
-          m[p][1] = v.y;
-          m[p][2] = v.z;
-          m[p][3] = v.w;
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
-          m[p][0] = v.x;
-          m[p][1] = v.y;
-          m[p][2] = m[p][3] = 0u;
-        }
-      }
-    }
-    uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
-    bool bad = false;
-#pragma unroll
-    for (int p = 0; p < 16; ++p) {
-      const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
-      const uint64_t w1 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
-      if constexpr (S::F64) {
-        // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
-        const double acc = __longlong_as_double(static_cast<long long>(w0));
-        bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
-        if (acc < 0x1.0p64) {  // common case: the peel is the integer's bytes
-          const uint64_t iacc = static_cast<uint64_t>(acc);
-          m[p][0] = static_cast<uint32_t>(iacc);
-          m[p][1] = static_cast<uint32_t>(iacc >> 32);
-          m[p][2] = m[p][3] = 0u;
-        } else {
-          const uint4 v = f64_peel_big(acc);
-          m[p][0] = v.x;
-          m[p][1] = v.y;
-          m[p][2] = v.z;
-          m[p][3] = v.w;
-        }
-      } else if constexpr (S::OFFS) {
-        // range check (codec.cpp:189-194): bits >= 7n must be zero
-        const unsigned used = 7u * c.n;
-        if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
-        else bad |= (w1 >> (used - 64u)) != 0;
-        const uint64_t lo = expand7(w0 & 0x00FFFFFFFFFFFFFFull);  // images 0..7
-        m[p][0] = static_cast<uint32_t>(lo);
-        m[p][1] = static_cast<uint32_t>(lo >> 32);
-        if constexpr (WC == 8) {
-          m[p][2] = static_cast<uint32_t>(w0 >> 56) & 0x7Fu;  // image 8
-          m[p][3] = 0u;
-        } else {
-          const uint64_t hi = expand7(((w0 >> 56) | (w1 << 8)) & 0x00FFFFFFFFFFFFFFull);  // images 8..15
-          m[p][2] = static_cast<uint32_t>(hi);
-          m[p][3] = static_cast<uint32_t>(hi >> 32);
-          x16[p >> 2] |= static_cast<uint32_t>((w1 >> 48) & 0x7Fu) << (8 * (p & 3));
-          x17[p >> 2] |= static_cast<uint32_t>((w1 >> 55) & 0x7Fu) << (8 * (p & 3));
-        }
-      }
-    }
-    transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (fields for lossless)
-    if (valid) {
-      if constexpr (!S::OFFS && !S::F64) {
-        // range check (codec.cpp:189-194): bytes of images >= n must be zero
-        uint32_t hi = 0;
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i)
-          if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
-        bad = hi != 0;
-      }
-      if (bad) latch_error(err, S::F64 ? kErrF64Range : kErrIntRange, g.chunk_base + k, c.n);
-    }
-    if constexpr (S::OFFS) {
-      // pixel = (field << 1) | parity (codec.cpp:196-201)
-#pragma unroll
-      for (int i = 0; i < S::NI; ++i) {
-        uint32_t bits = 0;
-        if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
-        uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) row[q] = (row[q] << 1) | nibble_lsbs((bits >> (4 * q)) & 0xFu);
-      }
-    }
-    auto row_vec = [&](int i) -> uint4 {
-      if (i < 16) return make_uint4(m[i < 16 ? i : 0][0], m[i < 16 ? i : 0][1], m[i < 16 ? i : 0][2], m[i < 16 ? i : 0][3]);
-      if (i == 16) return make_uint4(x16[0], x16[1], x16[2], x16[3]);
-      return make_uint4(x17[0], x17[1], x17[2], x17[3]);
-    };
-    if constexpr (O == OPTB_OUT_U8) {
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i)
-          if (i < static_cast<int>(c.n))
-            stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16, row_vec(i));
-      }
-    } else {
-      __syncwarp();  // all lanes done reading the slot
-      // u8 tile in the same slot: image i, lane L's 16 pixels at i*512 + L*16
-#pragma unroll
-      for (int i = 0; i < S::NI; ++i) *reinterpret_cast<uint4*>(slot + i * 512 + lane * 16) = row_vec(i);
-      __syncwarp();
-      // epilogue: every lane stores 16 bytes per row -- PX = 4 fp32 or 8 half
-      // pixels, starting at pixel PX*(lane % LPS) of source lane L's group
-      constexpr int ES = (O == OPTB_OUT_F32) ? 4 : 2;
-      constexpr int PX = 16 / ES, LPS = 16 / PX, ROUNDS = 32 / (32 / LPS);
-#pragma unroll
-      for (int cc = 0; cc < ROUNDS; ++cc) {
-        const int L = lane / LPS + (32 / LPS) * cc;
-        const uint32_t r0lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0), L);
-        const uint32_t r0hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0 >> 32), L);
-        const uint32_t nL = __shfl_sync(0xffffffffu, valid ? c.n : 0u, L);
-        const uint32_t glo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi), L);
-        const uint32_t ghi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi >> 32), L);
-        const uint64_t r0L = (static_cast<uint64_t>(r0hi) << 32) | r0lo;
-        const uint64_t gL = (static_cast<uint64_t>(ghi) << 32) | glo;
-        const int sub = PX * (lane % LPS);
-        uint8_t* dst = static_cast<uint8_t*>(out) + (r0L * ostride + gL * 16 + sub) * ES;
-        const uint64_t dstep = ostride * ES;
-        const uint8_t* src = slot + L * 16 + sub;
-        auto put_row = [&](uint8_t* d, int i, const PxScale& sc, auto fast) {
-          constexpr bool F = decltype(fast)::value;
-          if constexpr (PX == 4) {
-            Out4::put<O, F>(d, *reinterpret_cast<const uint32_t*>(src + i * 512), sc);
-          } else {
-            Out8::put<O, F>(d, *reinterpret_cast<const uint2*>(src + i * 512), sc);
-          }
-        };
-        if (!e.class_scale) {  // one scale for every row (the runner's kPixelScale)
-          const PxScale sc = px_scale(e.scale, 0.0f, false);
-          if (sc.fast) {
-#pragma unroll
-            for (int i = 0; i < S::NI; ++i) {
-              if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::true_type{});
-              dst += dstep;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < S::NI; ++i) {
-              if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::false_type{});
-              dst += dstep;
-            }
-          }
-        } else {  // per-class (scale, bias) tables indexed by the row's class
-#pragma unroll
-          for (int i = 0; i < S::NI; ++i) {
-            if (i < static_cast<int>(nL)) {
-              float s, b;
-              bool aff;
-              row_affine(e, r0L + i, s, b, aff);
-              const PxScale sc = px_scale(s, b, aff);
-              if (sc.fast) {
-                put_row(dst, i, sc, std::true_type{});
-              } else {
-                put_row(dst, i, sc, std::false_type{});
-              }
-            }
-            dst += dstep;
-          }
-        }
-      }
-      // the slot's next fill is an async-proxy (TMA) write
-      if constexpr (TMA) fence_proxy_async_smem();
-    }
-    __syncwarp();
-    if (++stage == kStages) {
-      stage = 0;
-      phase ^= 1u;
-    }
-  }
-  if constexpr (!TMA || S::OFFS) cp_async_wait<0>();
-}
-
-template <int MODE, int O, bool TMA>
-__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
-    k_decode_vec(const __grid_constant__ CUtensorMap cmap, Geom g, const uint8_t* __restrict__ cont,
-                 const uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  __shared__ uint64_t bars[TMA ? kWarps * kStages : 1];
-  decode_body<MODE, O, TMA>(&cmap, g, cont, offsets, e, out, err, TMA ? align1024(smem_raw) : smem_raw, bars);
-}
-
-// ------------------------------------------------------------------ K1+K2 fused
-// One step's round trip in one persistent launch (the E-D pipeline step,
-// pipeline.cpp:197-216 producer encode + runner.cpp:292-309 consumer decode):
-// every warp gather-encodes its tiles into the container stream in HBM, then
-// decodes the same tiles back -- in the order it wrote them, so by the time a
-// tile is read back the rest of the step's ~150 MB of traffic has gone
-// through L2 and the read is served by HBM like a separate decode launch.
-// No warp reads another warp's containers, so no grid-wide barrier is needed;
-// the kernel saves one launch's ramp-up and tail.  Exact and f64 modes (the
-// decode half reads each tile with one TMA tensor load).
-// Per-warp shared-memory region of the fused kernel: room for either ring,
-// 1024-aligned so every TMA slot stays 1024-aligned.
-template <int MODE>
-struct RtRegion {
-  static constexpr uint32_t ENC = kStages * VecMode<MODE>::ENC_SLOT;
-  static constexpr uint32_t DEC = kStages * DecSlot<MODE>::TMA;
-  static constexpr uint32_t BYTES = ((ENC > DEC ? ENC : DEC) + 1023) / 1024 * 1024;
-};
-
-// At most OPTB_RT_MAXREG registers per thread (no spills at 184): with 8
-// warps that leaves ~18 K registers per SM, so the SBS kernels of the next
-// draw call (side stream) co-reside with the persistent round trip instead of
-// waiting for its CTAs to retire.
-#ifndef OPTB_RT_MAXREG
-#define OPTB_RT_MAXREG 184
-#endif
-template <int MODE, int O, bool PTRS>
-__global__ void __maxnreg__(OPTB_RT_MAXREG)
-    k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
-                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  __shared__ uint64_t bars[kWarps * kStages];
-  uint8_t* base = align1024(smem_raw);
-  encode_body<MODE, PTRS>(g, src, cont, offsets, base, RtRegion<MODE>::BYTES);
-  // this warp's container stores (generic proxy) before its TMA reads of
-  // them, and its staging writes before the TMA fills of the same slots
-  fence_proxy_async_global();
-  fence_proxy_async_smem();
-  __syncwarp();
-  decode_body<MODE, O, true>(&cmap, g, cont, offsets, e, out, err, base, bars, RtRegion<MODE>::BYTES);
-}
-
-// ------------------------------------------------------------------ generic
-// One pixel per lane; any P, any alignment; all five modes.  Items are linear
-// in (chunk, pixel), so a warp's lanes are consecutive pixels of (at most two)
-// chunks.  Lossless parity bits are accumulated with warp ballots and written
-// with atomicOr into a zeroed plane (covers unaligned bit offsets).
-template <int MODE>
-__global__ void __launch_bounds__(256) k_encode_generic(Geom g, RowSrc rs, uint8_t* __restrict__ cont,
-                                                        uint8_t* __restrict__ offsets) {
-  constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
-  constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
-  constexpr int MAXN = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128) ? 16
-                       : (MODE == OPTB_F64) ? 16 : (MODE == OPTB_LOSSLESS64) ? 9 : 18;
-  const uint64_t items = g.chunks * g.P;
-  const int lane = threadIdx.x & 31;
-  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u);
-       t0 < items; t0 += gstride) {
-    const uint64_t t = t0 + lane;
-    const bool valid = t < items;
-    uint64_t k = 0, p = 0;
-    ChunkPos c{0, 0};
-    if (valid) {
-      k = t / g.P;
-      p = t - k * g.P;
-      c = chunk_pos(g, k);
-    }
-    unsigned __int128 acc = 0;
-    double dacc = 0.0;
-#pragma unroll
-    for (int i = 0; i < MAXN; ++i) {
-      uint32_t px = 0;
-      const bool has = valid && i < static_cast<int>(c.n);
-      if (has) {
-        const uint64_t r = c.r0 + i;
-        if (rs.ptrs) {
-          px = __ldg(reinterpret_cast<const uint8_t*>(static_cast<uintptr_t>(__ldg(
-                         reinterpret_cast<const unsigned long long*>(rs.ptrs) + r))) + p);
-        } else {
-          const uint64_t src = rs.index ? static_cast<uint64_t>(__ldg(rs.index + r)) : r;
-          px = __ldg(rs.images + src * rs.stride + p);
-        }
-        if constexpr (MODE == OPTB_F64) {
-          // codec.cpp:116-120: acc += px * 256^i in binary64, i ascending
-          dacc = __dadd_rn(dacc, __dmul_rn(static_cast<double>(px), pow256(i)));
-        } else if constexpr (OFFS) {
-          acc |= static_cast<unsigned __int128>(px >> 1) << (7 * i);
-        } else {
-          acc |= static_cast<unsigned __int128>(px) << (8 * i);
-        }
-      }
-      if constexpr (OFFS) {
-        // parity bit i*P + p of chunk k (codec.cpp:132-133)
-        const uint32_t bits = __ballot_sync(0xffffffffu, has && (px & 1u));
-        const uint32_t inchunk = __ballot_sync(0xffffffffu, has);
-        if (has) {
-          // the first lane of each same-chunk run writes that run's bits
-          const uint32_t same = __match_any_sync(inchunk, k);
-          const int lead = __ffs(same) - 1;
-          if (lane == lead) {
-            const uint32_t seg = (bits & same) >> lead;
-            if (seg) {
-              const uint64_t bit = static_cast<uint64_t>(i) * g.P + p;  // p of the leader
-              uint32_t* plane = reinterpret_cast<uint32_t*>(offsets + k * g.ostride);
-              const uint64_t w = bit >> 5;
-              const uint32_t sh = static_cast<uint32_t>(bit & 31);
-              atomicOr(plane + w, seg << sh);
-              if (sh && (seg >> (32 - sh))) atomicOr(plane + w + 1, seg >> (32 - sh));
-            }
-          }
-        }
-      }
-    }
-    if (valid) {
-      uint8_t* w = cont + t * WC;
-      if constexpr (MODE == OPTB_F64) {
-        *reinterpret_cast<double*>(w) = dacc;
-      } else if constexpr (WC == 8) {
-        *reinterpret_cast<uint64_t*>(w) = static_cast<uint64_t>(acc);
-      } else {
-        reinterpret_cast<uint64_t*>(w)[0] = static_cast<uint64_t>(acc);
-        reinterpret_cast<uint64_t*>(w)[1] = static_cast<uint64_t>(acc >> 64);
-      }
-    }
-  }
-}
-
-template <int MODE, int O>
-__global__ void __launch_bounds__(256) k_decode_generic(Geom g, const uint8_t* __restrict__ cont,
-                                                        const uint8_t* __restrict__ offsets, Epi e,
-                                                        void* __restrict__ out, DevError* err) {
-  constexpr bool OFFS = (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128);
-  constexpr int WC = (MODE == OPTB_EXACT128 || MODE == OPTB_LOSSLESS128) ? 16 : 8;
-  constexpr int MAXN = (MODE == OPTB_EXACT64) ? 8 : (MODE == OPTB_EXACT128) ? 16
-                       : (MODE == OPTB_F64) ? 16 : (MODE == OPTB_LOSSLESS64) ? 9 : 18;
-  constexpr unsigned PER = OFFS ? 7u : 8u;
-  const uint64_t items = g.chunks * g.P;
-  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < items;
-       t += gstride) {
-    const uint64_t k = t / g.P;
-    const uint64_t p = t - k * g.P;
-    const ChunkPos c = chunk_pos(g, k);
-    const uint8_t* w = cont + t * WC;
-    if constexpr (MODE == OPTB_F64) {
-      double acc = *reinterpret_cast<const double*>(w);
-      // codec.cpp:163-170
-      const bool check = c.n <= 6u;
-      const double limit = pow256(static_cast<int>(c.n));
-      if (!(acc >= 0.0) || (check && acc >= limit)) {
-        latch_error(err, kErrF64Range, g.chunk_base + k, c.n);
-        continue;
-      }
-      // codec.cpp:171-175 peels with q = fmod(acc, 256), acc = (acc - q) / 256.
-      // For 0 <= acc < 2^64 that is exactly the integer peel of trunc(acc):
-      // fmod keeps acc's fraction in q, (u8)q drops it, and (acc - q)/256 is
-      // trunc(acc/256).  Only lossy sums >= 2^64 (n >= 9) need fmod itself.
-      const bool small = acc < 0x1.0p64;
-      uint64_t iacc = small ? static_cast<uint64_t>(acc) : 0ull;
-#pragma unroll
-      for (int i = 0; i < MAXN; ++i) {
-        if (i < static_cast<int>(c.n)) {
-          double q;
-          if (small) {
-            q = static_cast<double>(iacc & 0xffull);
-            iacc >>= 8;
-          } else {
-            q = fmod(acc, 256.0);                          // exact
-            acc = __dmul_rn(__dsub_rn(acc, q), 0x1.0p-8);  // exact
-          }
-          const uint64_t row = c.r0 + i;
-          float s, b;
-          bool aff;
-          row_affine(e, row, s, b, aff);
-          put1<O>(out, row * e.row_stride + p, static_cast<uint32_t>(q), s, b, aff);
-        }
-      }
-    } else {
-      unsigned __int128 acc;
-      if constexpr (WC == 8) {
-        acc = *reinterpret_cast<const uint64_t*>(w);
-      } else {
-        acc = (static_cast<unsigned __int128>(reinterpret_cast<const uint64_t*>(w)[1]) << 64) |
-              reinterpret_cast<const uint64_t*>(w)[0];
-      }
-      const unsigned used = PER * c.n;
-      if (used < WC * 8u && (acc >> used) != 0) {  // codec.cpp:189-194
-        latch_error(err, kErrIntRange, g.chunk_base + k, c.n);
-        continue;
-      }
-      const uint8_t* plane = OFFS ? offsets + k * g.ostride : nullptr;
-#pragma unroll
-      for (int i = 0; i < MAXN; ++i) {
-        if (i < static_cast<int>(c.n)) {
-          uint32_t q = static_cast<uint32_t>(acc >> (PER * i)) & ((1u << PER) - 1u);
-          if constexpr (OFFS) {
-            const uint64_t bit = static_cast<uint64_t>(i) * g.P + p;
-            q = (q << 1) | ((__ldg(plane + (bit >> 3)) >> (bit & 7)) & 1u);
-          }
-          const uint64_t row = c.r0 + i;
-          float s, b;
-          bool aff;
-          row_affine(e, row, s, b, aff);
-          put1<O>(out, row * e.row_stride + p, q, s, b, aff);
-        }
-      }
-    }
-  }
-}
 
 // ------------------------------------------------------------------ synth
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -1230,188 +30,8 @@ __global__ void k_synth(uint64_t seed, uint64_t first_row, uint64_t n_rows, uint
   }
 }
 
-// ------------------------------------------------------------------ dispatch
-template <typename K>
-int grid_for(K kernel, int threads, size_t smem, int num_sms, uint64_t work_units) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t want = (work_units + threads - 1) / threads;
-  const uint64_t cap = static_cast<uint64_t>(per_sm) * num_sms;
-  return static_cast<int>(want < cap ? (want ? want : 1) : cap);
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-template <int MODE>
-cudaError_t enc_generic(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
-                        uint64_t* launches) {
-  if (MODE == OPTB_LOSSLESS64 || MODE == OPTB_LOSSLESS128) {
-    cudaError_t st = cudaMemsetAsync(offs, 0, g.chunks * g.ostride, s);
-    if (st != cudaSuccess) return st;
-  }
-  const int grid = grid_for(k_encode_generic<MODE>, 256, 0, sms, g.chunks * g.P);
-  k_encode_generic<MODE><<<grid, 256, 0, s>>>(g, rs, static_cast<uint8_t*>(cont), offs);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-template <int MODE, int O>
-cudaError_t dec_generic(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e,
-                        void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  const int grid = grid_for(k_decode_generic<MODE, O>, 256, 0, sms, g.chunks * g.P);
-  k_decode_generic<MODE, O><<<grid, 256, 0, s>>>(g, static_cast<const uint8_t*>(cont), offs, e,
-                                                 out, err);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-template <int MODE, bool PTRS>
-cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
-                      uint64_t* launches) {
-  const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
-  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_encode_vec<MODE, PTRS>), static_cast<int>(smem));
-  if (ae != cudaSuccess) return ae;
-  const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_encode_vec<MODE, PTRS>, kThreads, smem, sms, items);
-  k_encode_vec<MODE, PTRS><<<grid, kThreads, smem, s>>>(g, rs, static_cast<uint8_t*>(cont), offs);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-template <int MODE>
-cudaError_t enc_vec(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
-                    uint64_t* launches) {
-  if (rs.ptrs) return enc_vec_t<MODE, true>(g, rs, cont, offs, s, sms, launches);
-  return enc_vec_t<MODE, false>(g, rs, cont, offs, s, sms, launches);
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_tiled() {
-  static const EncodeTiledFn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return static_cast<EncodeTiledFn>(nullptr);
-    return reinterpret_cast<EncodeTiledFn>(f);
-  }();
-  return fn;
-}
-
-// The container stream as a [bytes/128][128] u8 tensor, box = one decode tile
-// (512 words = 512*WC bytes), 128-byte hardware swizzle (see decode_body).
-bool container_map(CUtensorMap* m, const void* cont, uint64_t bytes, int wc) {
-  const EncodeTiledFn fn = encode_tiled();
-  if (!fn || bytes % 128 || bytes / 128 > 0x7fffffffull) return false;
-  const cuuint64_t dims[2] = {128, bytes / 128};
-  const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(512 * wc / 128)};
-  const cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(cont), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// OPTB_DECODE_TMA=0 selects the cp.async decode (A/B measurements)
-bool tma_decode_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("OPTB_DECODE_TMA");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
-
-template <int MODE, int O, bool TMA>
-cudaError_t dec_vec_launch(const CUtensorMap& cm, const Geom& g, const void* cont, const uint8_t* offs,
-                           const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = TMA ? static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA + 1024
-                          : static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::RAW;
-  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_decode_vec<MODE, O, TMA>), static_cast<int>(smem));
-  if (ae != cudaSuccess) return ae;
-  const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_decode_vec<MODE, O, TMA>, kThreads, smem, sms, items);
-  k_decode_vec<MODE, O, TMA><<<grid, kThreads, smem, s>>>(cm, g, static_cast<const uint8_t*>(cont), offs, e, out,
-                                                          err);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-template <int MODE, int O>
-cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
-                    DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  CUtensorMap cm;
-  if (tma_decode_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
-    return dec_vec_launch<MODE, O, true>(cm, g, cont, offs, e, out, err, s, sms, launches);
-  memset(&cm, 0, sizeof cm);
-  return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
-}
-
-template <int MODE, int O, bool PTRS>
-cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, const Epi& e,
-                   void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  constexpr size_t smem = static_cast<size_t>(kWarps) * RtRegion<MODE>::BYTES + 1024;
-  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_roundtrip_vec<MODE, O, PTRS>), static_cast<int>(smem));
-  if (ae != cudaSuccess) return ae;
-  const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_roundtrip_vec<MODE, O, PTRS>, kThreads, smem, sms, items);
-  k_roundtrip_vec<MODE, O, PTRS><<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out,
-                                                              err);
-  ++*launches;
-  return cudaGetLastError();
-}
-
-template <int MODE, bool PTRS>
-cudaError_t rt_vec_out(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
-                       const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* l) {
-  switch (e.dtype) {
-    case OPTB_OUT_U8: return rt_vec<MODE, OPTB_OUT_U8, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
-    case OPTB_OUT_F32: return rt_vec<MODE, OPTB_OUT_F32, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
-    case OPTB_OUT_F16: return rt_vec<MODE, OPTB_OUT_F16, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
-    default: return rt_vec<MODE, OPTB_OUT_BF16, PTRS>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
-  }
-}
-
-template <int MODE>
-cudaError_t rt_vec_any(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
-                       const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* l) {
-  if (rs.ptrs) return rt_vec_out<MODE, true>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
-  return rt_vec_out<MODE, false>(cm, g, rs, cont, offs, e, out, err, s, sms, l);
-}
-
-template <int MODE>
-cudaError_t dec_generic_any(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e,
-                            void* out, DevError* err, cudaStream_t s, int sms, uint64_t* l) {
-  switch (e.dtype) {
-    case OPTB_OUT_U8: return dec_generic<MODE, OPTB_OUT_U8>(g, cont, offs, e, out, err, s, sms, l);
-    case OPTB_OUT_F32: return dec_generic<MODE, OPTB_OUT_F32>(g, cont, offs, e, out, err, s, sms, l);
-    case OPTB_OUT_F16: return dec_generic<MODE, OPTB_OUT_F16>(g, cont, offs, e, out, err, s, sms, l);
-    default: return dec_generic<MODE, OPTB_OUT_BF16>(g, cont, offs, e, out, err, s, sms, l);
-  }
-}
-
-template <int MODE>
-cudaError_t dec_vec_any(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
-                        DevError* err, cudaStream_t s, int sms, uint64_t* l) {
-  switch (e.dtype) {
-    case OPTB_OUT_U8: return dec_vec<MODE, OPTB_OUT_U8>(g, cont, offs, e, out, err, s, sms, l);
-    case OPTB_OUT_F32: return dec_vec<MODE, OPTB_OUT_F32>(g, cont, offs, e, out, err, s, sms, l);
-    case OPTB_OUT_F16: return dec_vec<MODE, OPTB_OUT_F16>(g, cont, offs, e, out, err, s, sms, l);
-    default: return dec_vec<MODE, OPTB_OUT_BF16>(g, cont, offs, e, out, err, s, sms, l);
-  }
-}
-
-// The vector kernels need 16-pixel groups (P % 16), 16-byte aligned rows and
-// planes; the lossless ones also 32-pixel aligned parity words (P % 32).
-bool vec_ok(const Geom& g) {
-  const bool lossless = g.mode == OPTB_LOSSLESS64 || g.mode == OPTB_LOSSLESS128;
-  return lossless ? g.P % 32 == 0 : g.P % 16 == 0;
-}
-
 }  // namespace
+
 
 // Row sources qualify for the vector path when every row is 16-byte aligned:
 // index mode checks base and stride, pointer mode trusts the caller's flag.
@@ -1423,22 +43,13 @@ cudaError_t launch_encode(const Geom& g, const RowSrc& rs, void* containers, uin
                           int sms, uint64_t* launches) {
   const bool vec = vec_ok(g) && rows_vec_ok(rs) && aligned16(containers);
   switch (g.mode) {
-    case OPTB_EXACT64:
-      if (vec) return enc_vec<OPTB_EXACT64>(g, rs, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_EXACT64>(g, rs, containers, offsets, s, sms, launches);
-    case OPTB_EXACT128:
-      if (vec) return enc_vec<OPTB_EXACT128>(g, rs, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_EXACT128>(g, rs, containers, offsets, s, sms, launches);
+    case OPTB_EXACT64: return encode_v0(g, rs, vec, containers, offsets, s, sms, launches);
+    case OPTB_EXACT128: return encode_v1(g, rs, vec, containers, offsets, s, sms, launches);
     case OPTB_F64:
-      if (vec && g.per_chunk <= 8) return enc_vec<kF64Narrow>(g, rs, containers, offsets, s, sms, launches);
-      if (vec) return enc_vec<OPTB_F64>(g, rs, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_F64>(g, rs, containers, offsets, s, sms, launches);
-    case OPTB_LOSSLESS64:
-      if (vec) return enc_vec<OPTB_LOSSLESS64>(g, rs, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_LOSSLESS64>(g, rs, containers, offsets, s, sms, launches);
-    default:
-      if (vec) return enc_vec<OPTB_LOSSLESS128>(g, rs, containers, offsets, s, sms, launches);
-      return enc_generic<OPTB_LOSSLESS128>(g, rs, containers, offsets, s, sms, launches);
+      if (vec && g.per_chunk <= 8) return encode_v5(g, rs, true, containers, offsets, s, sms, launches);
+      return encode_v2(g, rs, vec, containers, offsets, s, sms, launches);
+    case OPTB_LOSSLESS64: return encode_v3(g, rs, vec, containers, offsets, s, sms, launches);
+    default: return encode_v4(g, rs, vec, containers, offsets, s, sms, launches);
   }
 }
 
@@ -1448,23 +59,13 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
   const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
   const bool vec = vec_ok(g) && aligned16(containers) && aligned16(out) && (e.row_stride * es) % 16 == 0;
   switch (g.mode) {
-    case OPTB_EXACT64:
-      if (vec) return dec_vec_any<OPTB_EXACT64>(g, containers, offsets, e, out, err, s, sms, launches);
-      return dec_generic_any<OPTB_EXACT64>(g, containers, offsets, e, out, err, s, sms, launches);
-    case OPTB_EXACT128:
-      if (vec) return dec_vec_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
-      return dec_generic_any<OPTB_EXACT128>(g, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_EXACT64: return decode_v0(g, containers, offsets, e, vec, out, err, s, sms, launches);
+    case OPTB_EXACT128: return decode_v1(g, containers, offsets, e, vec, out, err, s, sms, launches);
     case OPTB_F64:
-      if (vec && g.per_chunk <= 8)
-        return dec_vec_any<kF64Narrow>(g, containers, offsets, e, out, err, s, sms, launches);
-      if (vec) return dec_vec_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
-      return dec_generic_any<OPTB_F64>(g, containers, offsets, e, out, err, s, sms, launches);
-    case OPTB_LOSSLESS64:
-      if (vec) return dec_vec_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms, launches);
-      return dec_generic_any<OPTB_LOSSLESS64>(g, containers, offsets, e, out, err, s, sms, launches);
-    default:
-      if (vec) return dec_vec_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms, launches);
-      return dec_generic_any<OPTB_LOSSLESS128>(g, containers, offsets, e, out, err, s, sms, launches);
+      if (vec && g.per_chunk <= 8) return decode_v5(g, containers, offsets, e, true, out, err, s, sms, launches);
+      return decode_v2(g, containers, offsets, e, vec, out, err, s, sms, launches);
+    case OPTB_LOSSLESS64: return decode_v3(g, containers, offsets, e, vec, out, err, s, sms, launches);
+    default: return decode_v4(g, containers, offsets, e, vec, out, err, s, sms, launches);
   }
 }
 
@@ -1482,16 +83,13 @@ cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rs, void* containers, 
       !container_map(&cm, containers, g.chunks * g.P * g.wc, g.wc))
     return cudaErrorNotSupported;  // caller: separate encode + decode launches
   switch (g.mode) {
-    case OPTB_EXACT64: return rt_vec_any<OPTB_EXACT64>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
-    case OPTB_EXACT128: return rt_vec_any<OPTB_EXACT128>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
-    case OPTB_LOSSLESS64:
-      return rt_vec_any<OPTB_LOSSLESS64>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
-    case OPTB_LOSSLESS128:
-      return rt_vec_any<OPTB_LOSSLESS128>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_EXACT64: return roundtrip_v0(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_EXACT128: return roundtrip_v1(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_LOSSLESS64: return roundtrip_v3(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+    case OPTB_LOSSLESS128: return roundtrip_v4(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
     default:
-      if (g.per_chunk <= 8)
-        return rt_vec_any<kF64Narrow>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
-      return rt_vec_any<OPTB_F64>(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+      if (g.per_chunk <= 8) return roundtrip_v5(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
+      return roundtrip_v2(cm, g, rs, containers, offsets, e, out, err, s, sms, launches);
   }
 }
 

@@ -9,10 +9,12 @@ FLAGS="-std=c++17 -O3 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr -diag-
 for v in "$@"; do
   w=${v%x*}; s=${v#*x}
   d=build/tune/$v; mkdir -p $d
-  nvcc $ARCH $FLAGS -DOPTB_VEC_WARPS=$w -DOPTB_VEC_STAGES=$s $EXTRA -c paper_2105_00619_b200/csrc/codec.cu -o $d/codec.o &
+  for f in codec codec_v0 codec_v1 codec_v2 codec_v3 codec_v4 codec_v5; do
+    nvcc $ARCH $FLAGS -DOPTB_VEC_WARPS=$w -DOPTB_VEC_STAGES=$s $EXTRA -c paper_2105_00619_b200/csrc/$f.cu -o $d/$f.o &
+  done
 done
 wait
 for v in "$@"; do
   d=build/tune/$v
-  nvcc $ARCH -shared -o $d/liboptb_cuda.so $d/codec.o build/sbs.o build/capi.o build/pipeline.o build/io.o build/peer.o -cudart static
+  nvcc $ARCH -shared -o $d/liboptb_cuda.so $d/codec*.o build/sbs.o build/capi.o build/pipeline.o build/io.o build/peer.o -cudart static
 done
