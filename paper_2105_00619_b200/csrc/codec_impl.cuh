@@ -1018,15 +1018,22 @@ struct RtRegion {
   static constexpr uint32_t BYTES = ((ENC > DEC ? ENC : DEC) + 1023) / 1024 * 1024;
 };
 
-// At most OPTB_RT_MAXREG registers per thread (no spills at 184): with 8
-// warps that leaves ~18 K registers per SM, so the SBS kernels of the next
-// draw call (side stream) co-reside with the persistent round trip instead of
-// waiting for its CTAs to retire.
+// Register budget: at most OPTB_RT_MAXREG per thread for one CTA per SM (no
+// spills at 184), which leaves ~18 K registers per SM for the SBS kernels of
+// the next draw call on the side stream; 128 for two CTAs per SM.  The
+// 16-byte-word variants always run one CTA per SM; the 8-byte ones two
+// (f64, lossless64: ALU-heavier), except exact64 with more than two images
+// per container, measured faster with one (ONE_CTA; configs_bench: C1 0.89 ->
+// 0.95 of peak, while n = 2 drops 0.95 -> 0.89 with one CTA).
 #ifndef OPTB_RT_MAXREG
 #define OPTB_RT_MAXREG 184
 #endif
-template <int MODE, int O, bool PTRS>
-__global__ void __maxnreg__(OPTB_RT_MAXREG)
+template <int MODE, bool ONE_CTA>
+struct RtRegs {
+  static constexpr int VALUE = (VecMode<MODE>::MIN_BLOCKS == 2 && !ONE_CTA) ? 128 : OPTB_RT_MAXREG;
+};
+template <int MODE, int O, bool PTRS, bool ONE_CTA = false>
+__global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_vec(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                     uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1330,18 +1337,27 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
   return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
 
+template <int MODE, int O, bool PTRS, bool ONE_CTA>
+cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, const Epi& e,
+                     void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  constexpr size_t smem = static_cast<size_t>(kWarps) * RtRegion<MODE>::BYTES + 1024;
+  auto kernel = k_roundtrip_vec<MODE, O, PTRS, ONE_CTA>;
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
+  if (ae != cudaSuccess) return ae;
+  const uint64_t items = g.chunks * (g.P / 16);
+  const int grid = grid_for(kernel, kThreads, smem, sms, items);
+  kernel<<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 template <int MODE, int O, bool PTRS>
 cudaError_t rt_vec(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, const Epi& e,
                    void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  constexpr size_t smem = static_cast<size_t>(kWarps) * RtRegion<MODE>::BYTES + 1024;
-  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_roundtrip_vec<MODE, O, PTRS>), static_cast<int>(smem));
-  if (ae != cudaSuccess) return ae;
-  const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_roundtrip_vec<MODE, O, PTRS>, kThreads, smem, sms, items);
-  k_roundtrip_vec<MODE, O, PTRS><<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out,
-                                                              err);
-  ++*launches;
-  return cudaGetLastError();
+  if constexpr (MODE == OPTB_EXACT64) {
+    if (g.per_chunk > 2) return rt_vec_t<MODE, O, PTRS, true>(cm, g, rs, cont, offs, e, out, err, s, sms, launches);
+  }
+  return rt_vec_t<MODE, O, PTRS, false>(cm, g, rs, cont, offs, e, out, err, s, sms, launches);
 }
 
 template <int MODE, bool PTRS>
