@@ -455,6 +455,10 @@ def main():
             e1.record(stream)
             e1.synchronize()
             sms_ = e0.elapsed_time(e1) / args.split_steps
+            if world > 1:
+                t = torch.tensor([sms_], device=red_dev)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
+                sms_ = float(t.item())
             tim5 = [pipe5.timings(k) for k in range(max(args.warmup, args.warmup + args.split_steps - 60),
                                                      args.warmup + args.split_steps)]
             pipe5.close()
@@ -504,6 +508,10 @@ def main():
             e1.record(stream)
             e1.synchronize()
             ms7 = e0.elapsed_time(e1) / args.split_steps
+            if world > 1:
+                t = torch.tensor([ms7], device=red_dev)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
+                ms7 = float(t.item())
             k7 = statistics.mean(pipe7.timings(k)[1] for k in range(max(args.warmup, args.warmup + args.split_steps
                                                                           - 60), args.warmup + args.split_steps))
             pipe7.close()
@@ -522,62 +530,72 @@ def main():
     if world > 1 and args.sharded_steps > 0:
         from paper_2105_00619_b200.sharded import PeerShardedGather, ShardedGather
         per = (N_EXAMPLES + world - 1) // world
+        # optional legs: a failure (e.g. peers not mappable when each process
+        # sees one GPU) is reported in the line instead of ending the run
         with torch.cuda.stream(stream):
             local_rows = ds[rank * per:(rank + 1) * per].clone()
-            cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                   device=local)
-            pg = PeerShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP,
-                                   device=local)
-            for _ in range(args.warmup):
-                pg.step(out, stream)
-            torch.cuda.synchronize(dev)
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.sharded_steps):
-                pg.step(out, stream)
-            e1.record(stream)
-            e1.synchronize()
-            pms = e0.elapsed_time(e1) / args.sharded_steps
-            # check the last step against the replicated dataset
-            cur6 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                   device=local)
-            for _ in range(args.warmup + args.sharded_steps):
-                ex6, _ = cur6.next_dev(BATCHES_PER_STEP * world, shard=rank, n_shards=world)
-            pok = bool(torch.equal(out, ds[ex6]))
-            remote = int(((ex6 // per) != rank).sum())
-            pg.close()
-            t = torch.tensor([pms], device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-            pms = float(t.item())
-        sharded = {"value": round(images_per_step / (pms / 1e3), 1), "unit": UNIT, "ms_per_step": round(pms, 3),
-                   "exchange": "peer memory: CUDA IPC-mapped shards read by the fused gather-encode-decode kernel "
-                               "(optb_roundtrip_rows_dev)" + (" -- ranks share one GPU (smoke run)" if oversub else
-                                                             " over NVLink / NVSwitch"),
-                   "rows_from_peers_per_step_rank0": remote, "bytes_from_peers_per_step_rank0": remote * P,
-                   "check": pok, "timing": "CUDA events on the launching stream, max over ranks"}
-        with torch.cuda.stream(stream):
-            cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                   device=local)
-            sg = ShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP, device=local,
-                               exchange="gloo" if oversub else "nccl")
-            sg.step(out)
-            torch.cuda.synchronize(dev)
-            dist.barrier()
-            t0 = time.perf_counter()
-            moved = 0
-            for _ in range(args.sharded_steps):
-                _, recv = sg.step(out)
-                moved += (sum(recv) - recv[rank]) * P
-            torch.cuda.synchronize(dev)
-            sms = (time.perf_counter() - t0) / args.sharded_steps * 1e3
-            t = torch.tensor([sms], device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-            sms = float(t.item())
-        sharded_a2a = {"value": round(images_per_step / (sms / 1e3), 1), "unit": UNIT, "ms_per_step": round(sms, 3),
-                       "exchange": "gloo (oversubscribed smoke run)" if oversub else "nccl all_to_all_single",
-                       "bytes_exchanged_per_step_rank0": int(moved / args.sharded_steps),
-                       "timing": "host wall clock around synchronised steps (the exchange is host-driven)"}
+        try:
+            with torch.cuda.stream(stream):
+                cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                       device=local)
+                pg = PeerShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP,
+                                       device=local)
+                for _ in range(args.warmup):
+                    pg.step(out, stream)
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(args.sharded_steps):
+                    pg.step(out, stream)
+                e1.record(stream)
+                e1.synchronize()
+                pms = e0.elapsed_time(e1) / args.sharded_steps
+                # check the last step against the replicated dataset
+                cur6 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                       device=local)
+                for _ in range(args.warmup + args.sharded_steps):
+                    ex6, _ = cur6.next_dev(BATCHES_PER_STEP * world, shard=rank, n_shards=world)
+                pok = bool(torch.equal(out, ds[ex6]))
+                remote = int(((ex6 // per) != rank).sum())
+                pg.close()
+                t = torch.tensor([pms], device=red_dev)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
+                pms = float(t.item())
+            sharded = {"value": round(images_per_step / (pms / 1e3), 1), "unit": UNIT, "ms_per_step": round(pms, 3),
+                       "exchange": "peer memory: CUDA IPC-mapped shards read by the fused gather-encode-decode kernel "
+                                   "(optb_roundtrip_rows_dev)" + (" -- ranks share one GPU (smoke run)" if oversub else
+                                                                 " over NVLink / NVSwitch"),
+                       "rows_from_peers_per_step_rank0": remote, "bytes_from_peers_per_step_rank0": remote * P,
+                       "check": pok, "timing": "CUDA events on the launching stream, max over ranks (sum when ranks share a GPU)"}
+        except Exception as ex:  # noqa: BLE001
+            sharded = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
+        try:
+            with torch.cuda.stream(stream):
+                cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                       device=local)
+                sg = ShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP, device=local,
+                                   exchange="gloo" if oversub else "nccl")
+                sg.step(out)
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+                t0 = time.perf_counter()
+                moved = 0
+                for _ in range(args.sharded_steps):
+                    _, recv = sg.step(out)
+                    moved += (sum(recv) - recv[rank]) * P
+                torch.cuda.synchronize(dev)
+                sms = (time.perf_counter() - t0) / args.sharded_steps * 1e3
+                t = torch.tensor([sms], device=red_dev)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
+                sms = float(t.item())
+            sharded_a2a = {"value": round(images_per_step / (sms / 1e3), 1), "unit": UNIT, "ms_per_step": round(sms, 3),
+                           "exchange": "gloo (oversubscribed smoke run)" if oversub else "nccl all_to_all_single",
+                           "bytes_exchanged_per_step_rank0": int(moved / args.sharded_steps),
+                           "timing": "host wall clock around synchronised steps (the exchange is host-driven)"}
+
+        except Exception as ex:  # noqa: BLE001
+            sharded_a2a = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU baseline runs at N = 1 only

@@ -151,14 +151,30 @@ class PeerShardedGather:
         if any(e[2] != self.stride for e in everyone):
             raise ValueError("PeerShardedGather: shards must share one row stride")
         bases, self._opened = [], []
-        for q, (h, o, _) in enumerate(everyone):
-            if q == rank:
-                bases.append(local_rows.data_ptr())
-                continue
-            p = ct.c_void_p()
-            check(lib.optb_ipc_open(device, (ct.c_uint8 * 64).from_buffer_copy(h), o, ct.byref(p)))
-            self._opened.append((p.value, o))
-            bases.append(p.value)
+        err = ""
+        try:
+            for q, (h, o, _) in enumerate(everyone):
+                if q == rank:
+                    bases.append(local_rows.data_ptr())
+                    continue
+                p = ct.c_void_p()
+                check(lib.optb_ipc_open(device, (ct.c_uint8 * 64).from_buffer_copy(h), o, ct.byref(p)))
+                self._opened.append((p.value, o))
+                bases.append(p.value)
+        except Exception as e:  # noqa: BLE001 -- decided collectively below
+            err = str(e)
+        # every rank must agree before anyone relies on the mappings (a rank
+        # that cannot map a peer, e.g. one GPU visible per process, must not
+        # leave the others waiting in a later collective)
+        nccl = dist.get_backend(group) == "nccl"
+        flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev if nccl else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            for p_, o_ in self._opened:
+                lib.optb_ipc_close(ct.c_void_p(p_), o_)
+            self._opened = None
+            raise RuntimeError("PeerShardedGather: peer shards could not be mapped on every rank"
+                               + (f" ({err})" if err else ""))
         self.aligned16 = all(b % 16 == 0 for b in bases) and self.stride % 16 == 0
         self.bases = torch.tensor(bases, dtype=torch.int64, device=dev)
         self.ptrs = torch.empty(max(self.rows, 1), dtype=torch.int64, device=dev)
