@@ -329,9 +329,13 @@ def main():
     rank, world, local = env_rank()
     n_dev = torch.cuda.device_count()
     # one process per GPU over NCCL; ranks > GPUs (a smoke run of the sharded
-    # path on one device) fall back to gloo for the barrier / max-over-ranks
-    oversub = world > n_dev
-    local = local % n_dev
+    # path on one device) fall back to gloo for the barrier / max-over-ranks.
+    # A launcher that gives every rank its own single visible GPU
+    # (CUDA_VISIBLE_DEVICES per rank) is one process per GPU too.
+    isolated = world > 1 and n_dev == 1 and os.environ.get("CUDA_VISIBLE_DEVICES", "").count(",") == 0 \
+        and os.environ.get("CUDA_VISIBLE_DEVICES", "") != "" and os.environ.get("OPTB_SHARED_GPU") is None
+    oversub = world > n_dev and not isolated
+    local = 0 if isolated else local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     red_dev = torch.device("cpu") if oversub else dev
