@@ -434,15 +434,32 @@ __device__ __noinline__ uint4 f64_peel_big(double acc) {
   return make_uint4(t[0], t[1], t[2], t[3]);
 }
 
-__device__ __forceinline__ uint64_t compact7(uint64_t x) {  // 8 byte lanes -> 8 x 7-bit fields
-  x = (x & 0x007F007F007F007Full) | ((x & 0x7F007F007F007F00ull) >> 1);
-  x = (x & 0x00003FFF00003FFFull) | ((x & 0x3FFF00003FFF0000ull) >> 2);
-  return (x & 0x000000000FFFFFFFull) | ((x & 0x0FFFFFFF00000000ull) >> 4);
+// 8 byte lanes (a = images 0..3, b = images 4..7 of one pixel) -> the 56-bit
+// word of their 7-bit fields px >> 1 (field i at bit 7i), as (low, high)
+// halves.  Two mask-and-merge stages per 32-bit half whose left shifts are
+// multiplies -- IMAD runs on the FMA pipe, while the integer pipe is what
+// bounds the lossless encoder -- then one merge of the halves:
+//   stage 1: (x & 0xFE00FE00) + (x & 0x00FE00FE) * 2  = field pairs    << 2
+//   stage 2: (y & 0xFFFC0000) + (y & 0x0000FFFC) * 4  = 28-bit groups  << 4
+__device__ __forceinline__ uint2 pack7x8(uint32_t a, uint32_t b) {
+  const uint32_t ga = (a & 0xFE00FE00u) + (a & 0x00FE00FEu) * 2u;
+  const uint32_t gb = (b & 0xFE00FE00u) + (b & 0x00FE00FEu) * 2u;
+  const uint32_t ha = (ga & 0xFFFC0000u) + (ga & 0x0000FFFCu) * 4u;
+  const uint32_t hb = (gb & 0xFFFC0000u) + (gb & 0x0000FFFCu) * 4u;
+  return make_uint2((ha >> 4) + hb * (1u << 24), hb >> 8);
 }
-__device__ __forceinline__ uint64_t expand7(uint64_t x) {  // inverse of compact7
-  x = (x & 0x0FFFFFFFull) | ((x << 4) & 0x0FFFFFFF00000000ull);
-  x = (x & 0x00003FFF00003FFFull) | ((x << 2) & 0x3FFF00003FFF0000ull);
-  return (x & 0x007F007F007F007Full) | ((x << 1) & 0x7F007F007F007F00ull);
+// Inverse of pack7x8 with the pixel's shift folded in: the 56-bit word of 8
+// fields (low, high halves) -> 8 byte lanes holding field << 1 (the pixel
+// without its parity bit); left shifts as multiplies (FMA pipe):
+//   28-bit groups -> 32-bit halves; (g & 0x3FFF) + (g & 0x0FFFC000) * 4;
+//   (h & 0x007F007F) * 2 + (h & 0x3F803F80) * 4.
+__device__ __forceinline__ uint2 unpack7x8_shl1(uint32_t lo, uint32_t hi) {
+  const uint32_t ga = lo & 0x0FFFFFFFu;
+  const uint32_t gb = __funnelshift_r(lo, hi, 28) & 0x0FFFFFFFu;
+  const uint32_t ha = (ga & 0x3FFFu) + (ga & 0x0FFFC000u) * 4u;
+  const uint32_t hb = (gb & 0x3FFFu) + (gb & 0x0FFFC000u) * 4u;
+  return make_uint2((ha & 0x007F007Fu) * 2u + (ha & 0x3F803F80u) * 4u,
+                    (hb & 0x007F007Fu) * 2u + (hb & 0x3F803F80u) * 4u);
 }
 __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> bytes' LSBs
   return (b * 0x00204081u) & 0x01010101u;
@@ -550,8 +567,9 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       if constexpr (S::OFFS) {
         // parity bits of 16 pixels at plane bit i*P + 16*gi (codec.cpp:132-133);
         // images in [n, per_chunk) (partial chunk) write zeros so the padded
-        // plane is deterministic; the plane holds per_chunk images
-        if (t < items && i < static_cast<int>(g.per_chunk)) {
+        // plane is deterministic; the plane holds per_chunk images.  Images
+        // 0..15 are done after the transpose (below); 16 and 17 here.
+        if (i >= 16 && t < items && i < static_cast<int>(g.per_chunk)) {
           const uint32_t bits = (((v.x & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) |
                                 ((((v.y & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 4) |
                                 ((((v.z & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << 8) |
@@ -578,6 +596,34 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       }
     }
     transpose16<S::NT, 16>(m);  // m[p] = bytes of images 0..15 at pixel p
+    if constexpr (S::OFFS) {
+      // parity planes of images 0..min(NI,16)-1 from the transposed bytes:
+      // lo[q] / hi[q] collect the low bits of pixels 0..7 / 8..15 of images
+      // 4q..4q+3 (bit p of byte k), the shifts as multiplies on the FMA pipe;
+      // one PRMT then yields image 4q+k's 16 bits
+      constexpr int NQ = (S::NT + 3) / 4;
+      uint32_t lo[NQ], hi[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        lo[q] = m[0][q] & 0x01010101u;
+        hi[q] = m[8][q] & 0x01010101u;
+#pragma unroll
+        for (int p = 1; p < 8; ++p) {
+          lo[q] += (m[p][q] & 0x01010101u) * (1u << p);
+          hi[q] += (m[p + 8][q] & 0x01010101u) * (1u << p);
+        }
+      }
+      if (t < items) {
+        uint8_t* plane = offsets + k * g.ostride + 2 * gi;
+#pragma unroll
+        for (int i = 0; i < S::NT; ++i) {
+          if (i < static_cast<int>(g.per_chunk)) {
+            const uint32_t bits = __byte_perm(lo[i >> 2], hi[i >> 2], (i & 3) | (((i & 3) + 4) << 4));
+            *reinterpret_cast<uint16_t*>(plane + (static_cast<uint64_t>(i) * g.P) / 8) = static_cast<uint16_t>(bits);
+          }
+        }
+      }
+    }
     __syncwarp();
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
@@ -600,21 +646,17 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
         }
         *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
       } else if constexpr (S::OFFS) {
-        const uint64_t lo8 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];  // images 0..7
-        const uint64_t lo = compact7((lo8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
-        if constexpr (WC == 8) {  // lossless64: fields 0..7 + image 8's field at bit 56
-          const uint64_t f8 = (m[p][2] & 0xFFu) >> 1;
-          *reinterpret_cast<uint64_t*>(slot + (lane * 16 + sl) * 8) = lo | (f8 << 56);
+        const uint2 lo = pack7x8(m[p][0], m[p][1]);  // fields of images 0..7, bits 0..55
+        if constexpr (WC == 8) {  // lossless64: image 8's field at bit 56
+          *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) =
+              make_uint2(lo.x, lo.y + (m[p][2] & 0xFEu) * (1u << 23));
         } else {  // lossless128: fields 0..15, images 16/17 at bits 112/119
-          const uint64_t hi8 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
-          const uint64_t hi = compact7((hi8 >> 1) & 0x7F7F7F7F7F7F7F7Full);
-          const uint64_t f16 = ((x16[p >> 2] >> (8 * (p & 3))) & 0xFFu) >> 1;
-          const uint64_t f17 = ((x17[p >> 2] >> (8 * (p & 3))) & 0xFFu) >> 1;
-          const uint64_t w0 = lo | (hi << 56);
-          const uint64_t w1 = (hi >> 8) | (f16 << 48) | (f17 << 55);
+          const uint2 hi = pack7x8(m[p][2], m[p][3]);  // images 8..15 -> bits 56..111
+          const uint32_t b16 = (x16[p >> 2] >> (8 * (p & 3))) & 0xFEu;
+          const uint32_t b17 = (x17[p >> 2] >> (8 * (p & 3))) & 0xFEu;
           *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) =
-              make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1),
-                         static_cast<uint32_t>(w1 >> 32));
+              make_uint4(lo.x, lo.y + hi.x * (1u << 24), (hi.x >> 8) + hi.y * (1u << 24),
+                         (hi.y >> 8) + b16 * (1u << 15) + b17 * (1u << 22));
         }
       } else if constexpr (WC == 16) {
         *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
@@ -863,22 +905,25 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
         const unsigned used = 7u * c.n;
         if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
         else bad |= (w1 >> (used - 64u)) != 0;
-        const uint64_t lo = expand7(w0 & 0x00FFFFFFFFFFFFFFull);  // images 0..7
-        m[p][0] = static_cast<uint32_t>(lo);
-        m[p][1] = static_cast<uint32_t>(lo >> 32);
+        // byte lanes hold field << 1: the pixel up to its parity bit
+        const uint2 lo = unpack7x8_shl1(m[p][0], m[p][1]);  // images 0..7 (bits 0..55)
+        const uint32_t w0hi = m[p][1], w1lo = m[p][2], w1hi = m[p][3];
+        m[p][0] = lo.x;
+        m[p][1] = lo.y;
         if constexpr (WC == 8) {
-          m[p][2] = static_cast<uint32_t>(w0 >> 56) & 0x7Fu;  // image 8
+          m[p][2] = (w0hi >> 23) & 0xFEu;  // image 8 (bits 56..62)
           m[p][3] = 0u;
         } else {
-          const uint64_t hi = expand7(((w0 >> 56) | (w1 << 8)) & 0x00FFFFFFFFFFFFFFull);  // images 8..15
-          m[p][2] = static_cast<uint32_t>(hi);
-          m[p][3] = static_cast<uint32_t>(hi >> 32);
-          x16[p >> 2] |= static_cast<uint32_t>((w1 >> 48) & 0x7Fu) << (8 * (p & 3));
-          x17[p >> 2] |= static_cast<uint32_t>((w1 >> 55) & 0x7Fu) << (8 * (p & 3));
+          // images 8..15: bits 56..111 = (w0 >> 56) | (w1 << 8)
+          const uint2 hi = unpack7x8_shl1(__funnelshift_r(w0hi, w1lo, 24), __funnelshift_r(w1lo, w1hi, 24));
+          m[p][2] = hi.x;
+          m[p][3] = hi.y;
+          x16[p >> 2] |= ((w1hi >> 15) & 0xFEu) << (8 * (p & 3));  // bits 112..118
+          x17[p >> 2] |= ((w1hi >> 22) & 0xFEu) << (8 * (p & 3));  // bits 119..125
         }
       }
     }
-    transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (fields for lossless)
+    transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (lossless: without their parity bits)
     if (valid) {
       if constexpr (!S::OFFS && !S::F64) {
         // range check (codec.cpp:189-194): bytes of images >= n must be zero
@@ -891,14 +936,14 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
       if (bad) latch_error(err, S::F64 ? kErrF64Range : kErrIntRange, g.chunk_base + k, c.n);
     }
     if constexpr (S::OFFS) {
-      // pixel = (field << 1) | parity (codec.cpp:196-201)
+      // pixel = (field << 1) | parity (codec.cpp:196-201); the shift is already in
 #pragma unroll
       for (int i = 0; i < S::NI; ++i) {
         uint32_t bits = 0;
         if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
         uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) row[q] = (row[q] << 1) | nibble_lsbs((bits >> (4 * q)) & 0xFu);
+        for (int q = 0; q < 4; ++q) row[q] |= nibble_lsbs((bits >> (4 * q)) & 0xFu);
       }
     }
     auto row_vec = [&](int i) -> uint4 {
