@@ -202,6 +202,17 @@ int optb_sbs_next_dev(optb_sbs* sbs, uint64_t n_batches, uint32_t shard, uint32_
 /* Same, all batches, host outputs (synchronous). */
 int optb_sbs_next_host(optb_sbs* sbs, uint64_t n_batches, int64_t* examples, int32_t* classes);
 uint64_t optb_sbs_batches_drawn(const optb_sbs* sbs);
+/* Testing aid (pure host, no device work): the host planner's view of one
+ * sampler call -- the reshuffle events of the next n batches after
+ * batches_before, in chain order (class and generation of each), given the
+ * per-class draw counts, class sizes and generations so far, and the chain
+ * state each event starts from when no draw is rejected (the seeds the host
+ * hands to the kernels; chain = the state before the call).  n_events gets
+ * the event count; more than max_events is OPTB_ERR_ARG. */
+int optb_sbs_plan_call(uint64_t n_classes, const uint64_t* counts, const uint64_t* class_sizes,
+                       const uint64_t* gen, uint64_t batches_before, uint64_t n, uint64_t chain,
+                       uint64_t max_events, uint64_t* ev_class, uint64_t* ev_gen, uint64_t* ev_seed,
+                       uint64_t* n_events, uint64_t* chain_after);
 /* Testing aid: force the exact serial rejection-sampling path for every
  * reshuffle (results are identical; only speed changes). */
 int optb_sbs_set_force_serial(optb_sbs* sbs, int32_t on);

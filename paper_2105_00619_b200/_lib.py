@@ -92,6 +92,8 @@ SIGNATURES = {
     "optb_sbs_next_host": (ct.c_int, [vp, ct.c_uint64, vp, vp]),
     "optb_sbs_batches_drawn": (ct.c_uint64, [vp]),
     "optb_sbs_set_force_serial": (ct.c_int, [vp, ct.c_int32]),
+    "optb_sbs_plan_call": (ct.c_int, [ct.c_uint64, u64p, u64p, u64p, ct.c_uint64, ct.c_uint64, ct.c_uint64,
+                                      ct.c_uint64, u64p, u64p, u64p, u64p, u64p]),
     "optb_sbs_set_profiling": (ct.c_int, [vp, ct.c_int32]),
     "optb_sbs_profile": (ct.c_int, [vp, fp, fp, fp]),
     "optb_gather_rows_dev": (ct.c_int, [vp, vp, ct.c_uint64, vp, ct.c_uint64, ct.c_int64, ct.c_uint64, vp,

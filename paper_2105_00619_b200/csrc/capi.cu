@@ -810,6 +810,35 @@ struct EvKey {
   uint64_t t;  // 1-based index of the event among its class's events in this call
 };
 
+// Lazy reshuffles of the next n batches (sampler.cpp:97): class c's draw D
+// (counted from the constructor) starts generation D / m_c when
+// D % m_c == 0 and D > 0.  Chain order is (batch, class, generation); the
+// classes are enumerated in order and each class's generations in order, so
+// a stable counting sort by batch gives the whole order in O(events +
+// batches) (N-GPU runs plan N x 97 batches per step; a comparison sort
+// dominated the host time).
+std::vector<EvKey> plan_events(uint64_t C, const uint64_t* counts, const uint64_t* m, const uint64_t* gen,
+                               uint64_t batches, uint64_t n, std::vector<uint64_t>* ev_count) {
+  std::vector<EvKey> gen_order;
+  ev_count->assign(C, 0);
+  std::vector<uint64_t> at(n + 2, 0);
+  for (uint64_t c = 0; c < C; ++c) {
+    const uint64_t cnt = counts[c], mm = m[c];
+    if (cnt == 0 || mm == 0) continue;
+    const uint64_t D1 = (batches + n) * cnt;
+    for (uint64_t g = gen[c] + 1; g * mm < D1; ++g) {
+      const uint64_t beta = (g * mm) / cnt;  // in [batches, batches + n)
+      gen_order.push_back({beta, c, g, g - gen[c]});
+      ++at[beta - batches + 1];
+      ++(*ev_count)[c];
+    }
+  }
+  for (uint64_t b = 0; b <= n; ++b) at[b + 1] += at[b];
+  std::vector<EvKey> keys(gen_order.size());
+  for (const EvKey& k : gen_order) keys[at[k.beta - batches]++] = k;
+  return keys;
+}
+
 // Lays out the generation pool for `keys` (already in chain order) starting at
 // element N: a reshuffling class c with E_c events gets E_c + 1 slots of m_c
 // (slot 0 = copy of its pre-call permutation).  Fills the event records and
@@ -1136,6 +1165,31 @@ int optb_sbs_profile(optb_sbs* s, float* upload_ms, float* reshuffle_ms, float* 
   return OPTB_OK;
 }
 
+int optb_sbs_plan_call(uint64_t n_classes, const uint64_t* counts, const uint64_t* class_sizes,
+                       const uint64_t* gen, uint64_t batches_before, uint64_t n, uint64_t chain, uint64_t max_events,
+                       uint64_t* ev_class, uint64_t* ev_gen, uint64_t* ev_seed, uint64_t* n_events,
+                       uint64_t* chain_after) {
+  if (!counts || !class_sizes || !gen || !n_events) return set_err(OPTB_ERR_ARG, "sbs plan: null argument");
+  for (uint64_t c = 0; c < n_classes; ++c)  // every generation started by the draws so far is counted
+    if (counts[c] && class_sizes[c] && (gen[c] + 1) * class_sizes[c] < batches_before * counts[c])
+      return set_err(OPTB_ERR_ARG, "sbs plan: generation of class %llu behind its draws",
+                     static_cast<unsigned long long>(c));
+  std::vector<uint64_t> ev_count;
+  const std::vector<EvKey> keys = plan_events(n_classes, counts, class_sizes, gen, batches_before, n, &ev_count);
+  *n_events = keys.size();
+  if (keys.size() > max_events) return set_err(OPTB_ERR_ARG, "sbs plan: %llu events > max_events",
+                                               static_cast<unsigned long long>(keys.size()));
+  for (size_t e = 0; e < keys.size(); ++e) {  // the host's walk of the chain (run_events)
+    if (ev_class) ev_class[e] = keys[e].cls;
+    if (ev_gen) ev_gen[e] = keys[e].g;
+    if (ev_seed) ev_seed[e] = chain;
+    const uint64_t mm = class_sizes[keys[e].cls];
+    chain = host_mix64(chain + (mm >= 2 ? mm : 1ull) * 0x9e3779b97f4a7c15ull);
+  }
+  if (chain_after) *chain_after = chain;
+  return OPTB_OK;
+}
+
 int optb_sbs_set_force_serial(optb_sbs* s, int32_t on) {
   if (!s) return set_err(OPTB_ERR_ARG, "sbs: null");
   s->force_serial = on ? 1 : 0;
@@ -1153,28 +1207,9 @@ int optb_sbs_next_dev(optb_sbs* s, uint64_t n, uint32_t shard, uint32_t n_shards
   const uint64_t C = s->C;
   // Lazy reshuffles (sampler.cpp:97): class c's draw D (counted from the
   // constructor) starts generation D / m_c when D % m_c == 0 and D > 0.
-  // Chain order is (batch, class, generation).  Classes are enumerated in
-  // order and each class's generations in order, so a stable counting sort
-  // by batch gives the whole order in O(events + batches) (N-GPU runs plan
-  // N x 97 batches per step here; a comparison sort dominated the host time).
-  std::vector<EvKey> gen_order;
-  std::vector<uint64_t> ev_count(C, 0);
-  const uint64_t beta0 = s->batches, n_beta = n + 1;
-  std::vector<uint32_t> at(n_beta + 1, 0);
-  for (uint64_t c = 0; c < C; ++c) {
-    const uint64_t cnt = s->counts[c], mm = s->m[c];
-    if (cnt == 0 || mm == 0) continue;
-    const uint64_t D1 = (s->batches + n) * cnt;
-    for (uint64_t g = s->gen[c] + 1; g * mm < D1; ++g) {
-      const uint64_t beta = (g * mm) / cnt;
-      gen_order.push_back({beta, c, g, g - s->gen[c]});
-      ++at[beta - beta0 + 1];
-      ++ev_count[c];
-    }
-  }
-  for (uint64_t b = 0; b < n_beta; ++b) at[b + 1] += at[b];
-  std::vector<EvKey> keys(gen_order.size());
-  for (const EvKey& k : gen_order) keys[at[k.beta - beta0]++] = k;
+  std::vector<uint64_t> ev_count;
+  const std::vector<EvKey> keys = plan_events(C, s->counts.data(), s->m.data(), s->gen.data(), s->batches, n,
+                                              &ev_count);
   // gather tables: drawn_before, generation at pool slot 0, its offset, stride
   std::vector<uint64_t> ga(4 * C);
   for (uint64_t c = 0; c < C; ++c) {

@@ -124,3 +124,58 @@ def test_model_skew(golden):
     cur = ModelCursor([8, 4, 4], by_class, 16, g["seed"])
     got = cur.next(13) + cur.next(37)
     assert got == a["skew_examples"].tolist()
+
+
+def _model_plan(counts, m, gen, batches, n, chain):
+    """ModelCursor.next's event enumeration + sort, and the no-rejection
+    chain walk that gives each event's start state."""
+    keys = []
+    for c, (cnt, mm) in enumerate(zip(counts, m)):
+        if cnt == 0 or mm == 0:
+            continue
+        d1 = (batches + n) * cnt
+        g = gen[c] + 1
+        while g * mm < d1:
+            keys.append(((g * mm) // cnt, c, g))
+            g += 1
+    keys.sort()
+    seeds = []
+    for _, c, _ in keys:
+        seeds.append(chain)
+        chain = mix(chain + (m[c] if m[c] >= 2 else 1) * GAMMA)
+    return keys, seeds, chain
+
+
+def test_host_planner_matches_model():
+    """optb_sbs_plan_call -- the C++ host planner the device path uses
+    (counting sort of the events by batch, the host's chain walk) -- equals
+    the Python model's sort and walk, on random class counts and sizes
+    (empty, single-example and large classes) and mid-stream states.  Pure
+    host code: runs without a GPU."""
+    import ctypes as ct
+    import paper_2105_00619_b200._lib as L
+    rng = np.random.default_rng(5)
+    u64 = lambda a: np.ascontiguousarray(a, np.uint64)  # noqa: E731
+    p = lambda a: a.ctypes.data_as(ct.POINTER(ct.c_uint64))  # noqa: E731
+    for trial in range(60):
+        C = int(rng.integers(1, 40))
+        counts = rng.integers(0, 9, C)
+        m = rng.choice([0, 1, 2, 3, 7, 50, 500, 4099], C)
+        batches = int(rng.integers(0, 300))
+        # a consistent generation state: generations started by draws so far
+        gen = np.array([(batches * c) // mm if mm and c else 0 for c, mm in zip(counts, m)])
+        gen = np.array([g - 1 if (mm and c and (batches * c) % mm == 0 and g > 0) else g
+                        for g, c, mm in zip(gen, counts, m)])
+        n = int(rng.integers(1, 200))
+        chain = int(rng.integers(0, 2 ** 63)) * 2 + 1
+        keys, seeds, after = _model_plan(counts.tolist(), m.tolist(), gen.tolist(), batches, n, chain)
+        cap = max(len(keys), 1)
+        ev_c, ev_g, ev_s = (np.zeros(cap, np.uint64) for _ in range(3))
+        ne, ca = ct.c_uint64(), ct.c_uint64()
+        L.check(L.lib.optb_sbs_plan_call(C, p(u64(counts)), p(u64(m)), p(u64(gen)), batches, n, chain, cap,
+                                         p(ev_c), p(ev_g), p(ev_s), ct.byref(ne), ct.byref(ca)))
+        assert ne.value == len(keys), trial
+        assert [int(x) for x in ev_c[:len(keys)]] == [k[1] for k in keys], trial
+        assert [int(x) for x in ev_g[:len(keys)]] == [k[2] for k in keys], trial
+        assert [int(x) for x in ev_s[:len(keys)]] == seeds, trial
+        assert ca.value == after, trial
