@@ -49,7 +49,7 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def config(world):
+def config(world, steps_per_draw=4):
     return {"workload": "C2: CIFAR-100-shaped 50000x32x32x3 u8 dataset in HBM, SBS (uniform 100 classes, "
                         "B=512, seed 1234) + exact128 gather-encode + decode to u8; 1 epoch = 97 batches "
                         "per GPU per step",
@@ -61,7 +61,8 @@ def config(world):
             "pipeline": "native optb_pipeline: SBS draws for the next steps on a side stream overlap the "
                         "current step's gather-encode + decode, one optb_roundtrip_dev launch per step (every warp "
                         "encodes its tiles into the HBM container stream, then decodes them back in write order); "
-                        "steps_per_draw epochs per sampler call"}
+                        "steps_per_draw epochs per sampler call",
+            "steps_per_draw": steps_per_draw}
 
 
 # ---------------------------------------------------------------- clocks
@@ -205,7 +206,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": config(world), "impl": "reference",
+            "config": config(world, args.steps_per_draw), "impl": "reference",
             "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": kind, "sample": sample},
             "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -311,7 +312,7 @@ def main():
                     help="steps of the same pipeline with separate encode / decode launches (per-kernel view)")
     ap.add_argument("--split-kernels", action="store_true",
                     help="headline with separate encode / decode launches instead of the fused round trip")
-    ap.add_argument("--steps-per-draw", type=int, default=2,
+    ap.add_argument("--steps-per-draw", type=int, default=4,
                     help="epochs of SBS draws computed per sampler call (amortises its fixed cost)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -610,7 +611,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": config(world),
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": config(world, args.steps_per_draw),
                 "roofline": roofline, "split_kernels": split, "exact64": exact64, "cpu_baseline": cpu, "e2e": e2e,
                 "e2e_zero_copy": e2e_zc,
                 "sharded_dataset": sharded, "sharded_dataset_a2a": sharded_a2a, "clocks": clk.summary(),
