@@ -240,7 +240,9 @@ int optb_inverse_perm_dev(optb_ctx* ctx, const int64_t* perm, uint64_t n, int64_
 int optb_owner_labels_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, uint64_t rows_per_shard,
                           uint32_t n_shards, int32_t* owner, void* stream);
 
-/* Peer-memory variant (no all-to-all, no staging, no host synchronisation):
+/* Peer-memory variant (no all-to-all, no staging, no host synchronisation) of
+ * the sharded gather -- the reference's Dataset::image_of (dataset.cpp:16-22)
+ * when the dataset's rows live on several GPUs:
  * every rank maps its peers' dataset shards into its address space with CUDA
  * IPC (NVLink / NVSwitch peer access) and the gather-encode kernel loads each
  * drawn row from the GPU that holds it, tile by tile.
@@ -337,7 +339,9 @@ int optb_pipeline_draws(const optb_pipeline* p, uint64_t step, const int64_t** e
                         const int32_t** classes);
 /* The pipeline's container planes (valid for the last enqueued step). */
 const void* optb_pipeline_containers(const optb_pipeline* p);
-/* The same step on host buffers (the E-D path for a dataset in host memory):
+/* The same step on host buffers (the E-D path for a dataset in host memory,
+ * as the reference's pipeline::run consumes an in-memory Dataset and hands
+ * decoded batches to the trainer, pipeline.cpp:181-244 / runner.cpp:264-311):
  * uploads dataset_host ([n_rows][row_stride] u8, pinned for overlap) into one
  * of two internal device buffers on a copy stream, runs optb_pipeline_step
  * on `stream` into an internal device buffer, and copies the decoded rows to
