@@ -430,6 +430,7 @@ def main():
                 break
     roofline = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
+                "frac_of_spec_8tbs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": kbytes,
                 "host_enqueue_us_per_step": round(t_enqueue / args.steps * 1e6, 1),
                 "kernels_ms": ({"sbs_side_stream": round(statistics.mean(t_sbs), 4),
