@@ -146,7 +146,7 @@ int optb_decode_dev(optb_ctx* ctx, const optb_layout* L, const void* containers,
 
 /* optb_encode_dev followed by optb_decode_dev of the same stream (same
  * results, containers and offsets materialised as by the two calls): one
- * persistent launch for the exact and f64 modes on the vector path (each
+ * persistent launch on the vector path (lossless modes: pixels % 512 == 0; each
  * warp encodes its tiles, then decodes them back from HBM), otherwise the two
  * launches.  The E-D pipeline step (pipeline.cpp:197-216 encode +
  * runner.cpp:292-309 decode) uses it. */

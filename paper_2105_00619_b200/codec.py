@@ -272,7 +272,7 @@ def decode_dev(L: Layout, containers, out, offsets=None, scale: float = 1.0, cla
 def roundtrip_dev(L: Layout, images, containers, out, offsets=None, row_index=None, scale: float = 1.0,
                   class_scale=None, class_bias=None, row_class=None, stream=None):
     """encode_dev then decode_dev of the same stream (optb_roundtrip_dev): one
-    fused launch for the exact / f64 modes, the two launches otherwise; the
+    fused launch on the vector path (lossless: P % 512 == 0), the two launches otherwise; the
     containers (and offsets) are materialised exactly as by the two calls."""
     import torch
     dt = {torch.uint8: U8, torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}[out.dtype]

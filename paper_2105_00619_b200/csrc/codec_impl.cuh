@@ -20,7 +20,7 @@
 //                         staging, fully coalesced 128/64-bit container stores.
 //   k_decode_vec<MODE,O,TMA>  K2/K4/K6: container words by one 2D TMA tensor
 //                         load per tile (128-byte hardware swizzle, mbarrier
-//                         completion; exact / f64 modes) or by cp.async into
+//                         completion; parity bits beside it) or by cp.async into
 //                         XOR-swizzled slots (+ lossless parity bits), per-mode
 //                         range check and unpack, transpose, u8 rows stored
 //                         directly or through a u8 tile with the fused

@@ -72,7 +72,7 @@ def main():
             out = torch.empty((rows, P), dtype=out_dtype, device=dev)
             t_enc = timeit(lambda: C.encode_dev(L, src, cont, offs, row_index=idx, stream=s), s)
             t_dec = timeit(lambda: C.decode_dev(L, cont, out, offsets=offs, scale=scale, stream=s), s)
-            # optb_roundtrip_dev: one fused launch for the exact / f64 modes
+            # optb_roundtrip_dev: one fused launch on the vector path
             t_rt = timeit(lambda: C.roundtrip_dev(L, src, cont, out, offsets=offs, row_index=idx, scale=scale,
                                                   stream=s), s)
             C.sync(0, s)
