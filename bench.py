@@ -65,6 +65,27 @@ def config(world, steps_per_draw=4):
             "steps_per_draw": steps_per_draw}
 
 
+# ---------------------------------------------------------------- collectives
+# The run's control-plane collectives (barriers, the max-over-ranks of device
+# times): NCCL with one process per GPU, gloo when ranks share a GPU (then the
+# per-rank times are summed so the whole-job rate is never overstated).
+COLL = {"group": None, "device": None, "op": None}
+
+
+def coll_barrier(dist):
+    g = COLL["group"]
+    if g is not None:
+        dist.barrier(group=g, device_ids=[COLL["device"].index])
+    else:
+        dist.barrier()
+
+
+def coll_reduce_ms(torch, dist, ms):
+    t = torch.tensor([float(ms)], device=COLL["device"])
+    dist.all_reduce(t, op=COLL["op"], group=COLL["group"])
+    return float(t.item())
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     """Samples SM clocks and throttle reasons with NVML during the timed region."""
@@ -265,7 +286,7 @@ def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, wo
             wait_all()
             torch.cuda.synchronize(dev)
             if world > 1:
-                dist.barrier()
+                coll_barrier(dist)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(args.e2e_steps):
@@ -281,9 +302,7 @@ def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, wo
             ok = bool(torch.equal(out_hosts[(k_state[0] - 1) % 2], ds_host[ex3.cpu()]))
             pipe2.close()
         if world > 1:
-            t = torch.tensor([ms], device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = coll_reduce_ms(torch, dist, ms)
         h2d_bytes = rows * P if zero_copy else ds_host.numel()
         results.append({"value": round(images_per_step / (ms / 1e3), 1), "unit": UNIT,
                         "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": rows * P,
@@ -329,22 +348,23 @@ def main():
     C, S = pkg.codec, pkg.sampler
     rank, world, local = env_rank()
     n_dev = torch.cuda.device_count()
-    # one process per GPU over NCCL; ranks > GPUs (a smoke run of the sharded
-    # path on one device) fall back to gloo for the barrier / max-over-ranks.
-    # A launcher that gives every rank its own single visible GPU
-    # (CUDA_VISIBLE_DEVICES per rank) is one process per GPU too.
-    isolated = world > 1 and n_dev == 1 and os.environ.get("CUDA_VISIBLE_DEVICES", "").count(",") == 0 \
-        and os.environ.get("CUDA_VISIBLE_DEVICES", "") != "" and os.environ.get("OPTB_SHARED_GPU") is None
-    oversub = world > n_dev and not isolated
-    local = 0 if isolated else local % n_dev
+    local = local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    red_dev = torch.device("cpu") if oversub else dev
+    oversub = False
     if world > 1:
-        if oversub:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        # Rendezvous over gloo, then compare the ranks' GPU UUIDs: one process
+        # per GPU (however the launcher maps devices) runs every collective of
+        # the run over NCCL; ranks sharing a GPU (a smoke run of the sharded
+        # path on one device) keep gloo -- NCCL refuses two ranks per GPU.
+        dist.init_process_group("gloo")
+        uuids = [None] * world
+        dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(local).uuid))
+        oversub = len(set(uuids)) < world
+        COLL["group"] = None if oversub else dist.new_group(backend="nccl")
+        COLL["device"] = torch.device("cpu") if oversub else dev
+        COLL["op"] = dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX
+    red_dev = torch.device("cpu") if oversub else dev
 
     stream = torch.cuda.Stream(dev)
     rows = BATCH * BATCHES_PER_STEP
@@ -373,7 +393,7 @@ def main():
         torch.cuda.synchronize(dev)
         launches0 = pkg._lib.launches(local)
         if world > 1:
-            dist.barrier()
+            coll_barrier(dist)
         torch.cuda.synchronize(dev)
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as clk:
@@ -386,7 +406,7 @@ def main():
             end.synchronize()
             t_wall = time.perf_counter() - t_wall0
         if world > 1:
-            dist.barrier()
+            coll_barrier(dist)
         C.sync(local, stream)
         launches = pkg._lib.launches(local) - launches0
     # per-kernel durations of the last (up to 60) timed steps -- the
@@ -399,9 +419,7 @@ def main():
         # one GPU per rank: max over ranks.  Oversubscribed smoke runs (ranks
         # share a GPU, whose timed regions may or may not overlap): the sum,
         # so the whole-job rate is never overstated.
-        t = torch.tensor([ms], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = coll_reduce_ms(torch, dist, ms)
     images_per_step = rows * world
     value = images_per_step / (ms / 1e3)
 
@@ -462,9 +480,7 @@ def main():
             e1.synchronize()
             sms_ = e0.elapsed_time(e1) / args.split_steps
             if world > 1:
-                t = torch.tensor([sms_], device=red_dev)
-                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-                sms_ = float(t.item())
+                sms_ = coll_reduce_ms(torch, dist, sms_)
             tim5 = [pipe5.timings(k) for k in range(max(args.warmup, args.warmup + args.split_steps - 60),
                                                      args.warmup + args.split_steps)]
             pipe5.close()
@@ -515,9 +531,7 @@ def main():
             e1.synchronize()
             ms7 = e0.elapsed_time(e1) / args.split_steps
             if world > 1:
-                t = torch.tensor([ms7], device=red_dev)
-                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-                ms7 = float(t.item())
+                ms7 = coll_reduce_ms(torch, dist, ms7)
             k7 = statistics.mean(pipe7.timings(k)[1] for k in range(max(args.warmup, args.warmup + args.split_steps
                                                                           - 60), args.warmup + args.split_steps))
             pipe7.close()
@@ -549,7 +563,7 @@ def main():
                 for _ in range(args.warmup):
                     pg.step(out, stream)
                 torch.cuda.synchronize(dev)
-                dist.barrier()
+                coll_barrier(dist)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 for _ in range(args.sharded_steps):
@@ -565,9 +579,7 @@ def main():
                 pok = bool(torch.equal(out, ds[ex6]))
                 remote = int(((ex6 // per) != rank).sum())
                 pg.close()
-                t = torch.tensor([pms], device=red_dev)
-                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-                pms = float(t.item())
+                pms = coll_reduce_ms(torch, dist, pms)
             sharded = {"value": round(images_per_step / (pms / 1e3), 1), "unit": UNIT, "ms_per_step": round(pms, 3),
                        "exchange": "peer memory: CUDA IPC-mapped shards read by the fused gather-encode-decode kernel "
                                    "(optb_roundtrip_rows_dev)" + (" -- ranks share one GPU (smoke run)" if oversub else
@@ -581,10 +593,10 @@ def main():
                 cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
                                                        device=local)
                 sg = ShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP, device=local,
-                                   exchange="gloo" if oversub else "nccl")
+                                   exchange="gloo" if oversub else "nccl", group=COLL["group"])
                 sg.step(out)
                 torch.cuda.synchronize(dev)
-                dist.barrier()
+                coll_barrier(dist)
                 t0 = time.perf_counter()
                 moved = 0
                 for _ in range(args.sharded_steps):
@@ -592,9 +604,7 @@ def main():
                     moved += (sum(recv) - recv[rank]) * P
                 torch.cuda.synchronize(dev)
                 sms = (time.perf_counter() - t0) / args.sharded_steps * 1e3
-                t = torch.tensor([sms], device=red_dev)
-                dist.all_reduce(t, op=dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX)
-                sms = float(t.item())
+                sms = coll_reduce_ms(torch, dist, sms)
             sharded_a2a = {"value": round(images_per_step / (sms / 1e3), 1), "unit": UNIT, "ms_per_step": round(sms, 3),
                            "exchange": "gloo (oversubscribed smoke run)" if oversub else "nccl all_to_all_single",
                            "bytes_exchanged_per_step_rank0": int(moved / args.sharded_steps),
