@@ -39,6 +39,7 @@ DATA_SEED = 7  # RunConfig::data_seed (runner.hpp:34)
 P = 32 * 32 * 3
 BATCHES_PER_STEP = N_EXAMPLES // BATCH  # 97: one epoch (runner.cpp:52-57)
 MODE = 1  # ExactInt128, the reference default (runner.hpp:52)
+TIMING_STRIDE = 8  # per-kernel timing events on every 8th step of the timed loops
 PER_CHUNK = 16
 METRIC = "images/sec encode+decode (and achieved HBM GB/s vs peak) at 1/2/4/8 B200"
 UNIT = "images/s"
@@ -381,9 +382,13 @@ def main():
     torch.cuda.synchronize(dev)
     # The native E-D pipeline (optb_pipeline_*): per step, SBS draws of step
     # k+1 on a side stream overlap gather-encode + decode of step k.
+    tstride = TIMING_STRIDE if args.steps >= 4 * TIMING_STRIDE else 1  # short runs: every step
+    # per-kernel timing events on every TIMING_STRIDE-th step only: an event
+    # between two round-trip launches stops the second from overlapping its
+    # launch ramp with the first one's drain (programmatic dependent launch)
     pipe = Pipeline(cur, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
                     device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
-                    split_kernels=args.split_kernels)
+                    split_kernels=args.split_kernels, timing_stride=tstride)
     L = pipe.layout
 
     with torch.cuda.stream(stream):
@@ -411,7 +416,7 @@ def main():
         launches = pkg._lib.launches(local) - launches0
     # per-kernel durations of the last (up to 60) timed steps -- the
     # pipeline keeps a 64-step ring of timing events
-    timed = range(max(args.warmup, args.warmup + args.steps - 60), args.warmup + args.steps)
+    timed = [k for k in range(args.warmup, args.warmup + args.steps) if k % tstride == 0][-60:]
     tim = [pipe.timings(k) for k in timed]
     t_sbs, t_enc, t_dec = [t[0] for t in tim], [t[1] for t in tim], [t[2] for t in tim]
     ms = start.elapsed_time(end) / args.steps
@@ -519,8 +524,10 @@ def main():
         with torch.cuda.stream(stream):
             cur7 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
                                                    device=local)
+            t7 = TIMING_STRIDE if args.split_steps >= 4 * TIMING_STRIDE else 1
             pipe7 = Pipeline(cur7, ds, 0, BATCH, BATCHES_PER_STEP, per_chunk=8, shard=rank, n_shards=world,
-                             device=local, record_timings=True, steps_per_draw=args.steps_per_draw)
+                             device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
+                             timing_stride=t7)
             for _ in range(args.warmup):
                 pipe7.step(out, stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -532,8 +539,8 @@ def main():
             ms7 = e0.elapsed_time(e1) / args.split_steps
             if world > 1:
                 ms7 = coll_reduce_ms(torch, dist, ms7)
-            k7 = statistics.mean(pipe7.timings(k)[1] for k in range(max(args.warmup, args.warmup + args.split_steps
-                                                                          - 60), args.warmup + args.split_steps))
+            k7 = statistics.mean(pipe7.timings(k)[1] for k in range(args.warmup, args.warmup + args.split_steps)
+                                 if k % t7 == 0)
             pipe7.close()
         b7 = 2 * (rows * P + C.container_bytes(C.layout(0, 8, P, BATCH, BATCHES_PER_STEP))) + rows * 8
         exact64 = {"mode": "exact64", "per_chunk": 8, "ms_per_step": round(ms7, 4),

@@ -324,6 +324,9 @@ typedef struct optb_pipeline_desc {
                               per-call reshuffle work when steps are short */
   uint32_t split_kernels;  /* 1: separate encode and decode launches per step;
                               0: optb_roundtrip_dev (one launch where it applies) */
+  uint32_t timing_stride;  /* with record_timings: time every timing_stride-th step
+                              only (0 = 1); events between launches stop consecutive
+                              round trips from overlapping their launch ramps */
 } optb_pipeline_desc;
 
 int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* desc, optb_pipeline** out);
@@ -354,9 +357,11 @@ int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint6
 /* Wait for every download enqueued by optb_pipeline_step_host: on the host
  * (stream NULL), or by making `stream` wait for the last one. */
 int optb_pipeline_host_wait(optb_pipeline* p, void* stream);
-/* Device-timed durations (ms) of a completed step (last 64 steps): its SBS
- * draws (side stream), its gather-encode and its decode (for a fused
- * round-trip step: the whole launch in enc_ms and 0 in dec_ms). */
+/* Device-timed durations (ms) of a completed, timed step (a multiple of
+ * timing_stride, among the last 64 * timing_stride steps): its SBS draws
+ * (side stream; the call that produced them, per step), its gather-encode
+ * and its decode (for a fused round-trip step: the whole launch in enc_ms
+ * and 0 in dec_ms). */
 int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, float* enc_ms,
                           float* dec_ms);
 void optb_pipeline_destroy(optb_pipeline* p);

@@ -49,7 +49,8 @@ class PipelineDesc(ct.Structure):
     """optb_pipeline_desc"""
     _fields_ = [("layout", Layout), ("dataset", vp), ("row_stride", ct.c_uint64), ("sbs", vp),
                 ("shard", ct.c_uint32), ("n_shards", ct.c_uint32), ("epilogue", Epilogue),
-                ("record_timings", ct.c_int32), ("steps_per_draw", ct.c_uint32), ("split_kernels", ct.c_uint32)]
+                ("record_timings", ct.c_int32), ("steps_per_draw", ct.c_uint32), ("split_kernels", ct.c_uint32),
+                ("timing_stride", ct.c_uint32)]
 
 
 LP = ct.POINTER(Layout)

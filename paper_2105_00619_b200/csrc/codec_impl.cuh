@@ -1084,6 +1084,12 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bars[kWarps * kStages];
   uint8_t* base = align1024(smem_raw);
+  // Programmatic dependent launch (the launcher sets the attribute): the next
+  // step's grid may be scheduled while this one drains, and this grid may be
+  // scheduled while the previous kernel in the stream drains -- but it
+  // touches no global memory before that kernel has completed and flushed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   encode_body<MODE, PTRS>(g, src, cont, offsets, base, RtRegion<MODE>::BYTES);
   // this warp's container stores (generic proxy) before its TMA reads of
   // them, and its staging writes before the TMA fills of the same slots
@@ -1391,7 +1397,25 @@ cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, voi
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(kernel, kThreads, smem, sms, items);
-  kernel<<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
+  // OPTB_PDL=0: plain launches (A/B runs).  PDL only overlaps kernel after
+  // kernel in one stream; event waits and copies in between serialise as usual.
+  static const bool pdl = [] { const char* v = getenv("OPTB_PDL"); return !(v && v[0] == '0'); }();
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kernel, cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
+    if (le != cudaSuccess) return le;
+  } else {
+    kernel<<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
+  }
   ++*launches;
   return cudaGetLastError();
 }

@@ -61,6 +61,7 @@ struct optb_pipeline {
   uint64_t step = 0;   // next step to deliver
   uint64_t calls = 0;  // SBS calls enqueued
   bool timing = false;
+  uint32_t tstride = 1;  // time every tstride-th step (and sampler call)
   // host leg (optb_pipeline_step_host): double-buffered device copies of the
   // host dataset and of the decoded rows, with their own copy streams
   struct Host {
@@ -81,11 +82,12 @@ int enqueue_draws(optb_pipeline* p) {
   if (c >= static_cast<uint64_t>(p->nbuf) && cudaStreamWaitEvent(p->side, p->enc_done[b], 0) != cudaSuccess)
     return cuda_fail("stream wait");
   const int r = static_cast<int>(c % kTimingRing);
-  if (p->timing) cudaEventRecord(p->t_s0[r], p->side);
+  const bool timed = p->timing;  // side stream: its events never sit between two round trips
+  if (timed) cudaEventRecord(p->t_s0[r], p->side);
   const uint64_t n = p->d.layout.n_batches * p->d.n_shards * p->spd;
   int st = optb_sbs_next_dev(p->d.sbs, n, p->d.shard, p->d.n_shards, p->ex[b], p->cls[b], p->side);
   if (st) return st;
-  if (p->timing) cudaEventRecord(p->t_s1[r], p->side);
+  if (timed) cudaEventRecord(p->t_s1[r], p->side);
   if (cudaEventRecord(p->sbs_done[b], p->side) != cudaSuccess) return cuda_fail("event record");
   ++p->calls;
   return OPTB_OK;
@@ -106,6 +108,7 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
   p->d = *d;
   p->spd = d->steps_per_draw ? d->steps_per_draw : 1;
   p->timing = d->record_timings != 0;
+  p->tstride = d->timing_stride ? d->timing_stride : 1;
   p->rows = optb_layout_rows(&d->layout);
   p->nbuf = d->n_shards >= 4 ? 3 : 2;
   bool ok = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) == cudaSuccess;
@@ -144,7 +147,8 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   const uint64_t k = p->step;
   const uint64_t call = k / p->spd, sub = k % p->spd;
   const int b = static_cast<int>(call % p->nbuf);
-  const int r = static_cast<int>(k % kTimingRing);
+  const int r = static_cast<int>((k / p->tstride) % kTimingRing);
+  const bool timed = p->timing && k % p->tstride == 0;
   int st;
   if (sub == 0) {
     st = enqueue_draws(p);  // the next call's draws overlap this call's steps
@@ -153,12 +157,12 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   }
   optb_epilogue e = p->d.epilogue;
   if (e.class_scale && !e.row_class) e.row_class = p->cls[b] + sub * p->rows;
-  if (p->timing) cudaEventRecord(p->t_e0[r], s);
+  if (timed) cudaEventRecord(p->t_e0[r], s);
   if (p->d.split_kernels) {
     st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
                          p->cont, p->offs, s);
     if (st) return st;
-    if (p->timing) cudaEventRecord(p->t_e1[r], s);
+    if (timed) cudaEventRecord(p->t_e1[r], s);
     if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
     st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
     if (st) return st;
@@ -166,10 +170,10 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
     st = optb_roundtrip_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
                             p->cont, p->offs, &e, out, s);
     if (st) return st;
-    if (p->timing) cudaEventRecord(p->t_e1[r], s);
+    if (timed) cudaEventRecord(p->t_e1[r], s);
     if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
   }
-  if (p->timing && p->d.split_kernels) cudaEventRecord(p->t_d1[r], s);  // fused: the launch ends at t_e1
+  if (timed && p->d.split_kernels) cudaEventRecord(p->t_d1[r], s);  // fused: the launch ends at t_e1
   ++p->step;
   return OPTB_OK;
 }
@@ -196,9 +200,10 @@ const void* optb_pipeline_containers(const optb_pipeline* p) { return p ? p->con
 
 int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, float* enc_ms,
                           float* dec_ms) {
-  if (!p || !p->timing || step >= p->step || step + kTimingRing <= p->step)
-    return arg_fail("timings: not recorded for that step (record_timings, last 64 steps)");
-  const int r = static_cast<int>(step % kTimingRing);
+  if (!p || !p->timing || step >= p->step || step % p->tstride ||
+      (p->step - 1 - step) / p->tstride >= static_cast<uint64_t>(kTimingRing))
+    return arg_fail("timings: not recorded for that step (record_timings, timing_stride, last 64 timed steps)");
+  const int r = static_cast<int>((step / p->tstride) % kTimingRing);
   const int rc = static_cast<int>((step / p->spd) % kTimingRing);
   cudaEvent_t last = p->d.split_kernels ? p->t_d1[r] : p->t_e1[r];
   if (cudaEventSynchronize(last) != cudaSuccess) return cuda_fail("synchronize");

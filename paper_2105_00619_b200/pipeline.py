@@ -25,7 +25,7 @@ class Pipeline:
     def __init__(self, cursor, dataset, mode, batch: int, batches_per_step: int, per_chunk=None,
                  shard: int = 0, n_shards: int = 1, out_dtype=None, scale: float = 1.0,
                  class_scale=None, class_bias=None, device: int = 0, record_timings: bool = False,
-                 steps_per_draw: int = 1, split_kernels: bool = False):
+                 steps_per_draw: int = 1, split_kernels: bool = False, timing_stride: int = 1):
         import torch
         from . import codec
         out_dtype = out_dtype or torch.uint8
@@ -40,7 +40,8 @@ class Pipeline:
         E = Epilogue(dt, float(scale), None if class_scale is None else ct.c_void_p(class_scale.data_ptr()),
                      None if class_bias is None else ct.c_void_p(class_bias.data_ptr()), None, 0)
         desc = PipelineDesc(self.layout, ct.c_void_p(dataset.data_ptr()), dataset.stride(0), cursor._h, shard,
-                            n_shards, E, 1 if record_timings else 0, steps_per_draw, 1 if split_kernels else 0)
+                            n_shards, E, 1 if record_timings else 0, steps_per_draw, 1 if split_kernels else 0,
+                            timing_stride)
         self._h = ct.c_void_p()
         check(lib.optb_pipeline_create(_lib.context(device), ct.byref(desc), ct.byref(self._h)))
         # one fused launch per step (optb_roundtrip_dev) on the vector path

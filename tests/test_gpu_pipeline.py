@@ -132,3 +132,32 @@ def test_pipeline_step_host_vs_oracle(pkg, oracle_mod, torch_cuda, dtype):
         got = outs[step] if dtype == "uint8" else outs[step].view(torch.int16)
         assert np.array_equal(got.numpy().view(want.dtype), want), step
     pipe.close()
+
+
+def test_pipeline_timing_stride(pkg, oracle_mod, torch_cuda):
+    """record_timings with timing_stride: only every stride-th step carries
+    timing events (the others launch back to back, overlapping via
+    programmatic dependent launch); their outputs are unaffected."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P = 64, 5, 768
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    pipe = Pipeline(cur, torch.from_numpy(ds).cuda(), 1, B, nb, per_chunk=16, record_timings=True,
+                    steps_per_draw=2, timing_stride=3)
+    outs = []
+    for _ in range(7):
+        o = torch.empty((B * nb, P), dtype=torch.uint8, device="cuda")
+        pipe.step(o)
+        outs.append(o)
+    pkg.codec.sync()
+    for step in (0, 3, 6):
+        s_ms, e_ms, d_ms = pipe.timings(step)
+        assert e_ms > 0 and d_ms == 0.0
+    for step in (1, 2, 4, 5):
+        with pytest.raises(pkg.errors.Error):
+            pipe.timings(step)
+    for step in range(7):
+        ex, _ = ref.next(nb)
+        assert torch.equal(outs[step].cpu(), torch.from_numpy(ds[ex])), step
+    pipe.close()
