@@ -42,6 +42,7 @@
 #include <set>
 #include <tuple>
 #include <type_traits>
+#include <utility>
 
 #include "internal.h"
 
@@ -364,6 +365,15 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // Requires P % 16 == 0 and 16-byte aligned rows / containers / outputs.
 constexpr int kStages = OPTB_VEC_STAGES;
 
+
+// Programmatic dependent launch (the launchers set the attribute, see
+// launch_k): the next kernel in the stream may be scheduled while this grid
+// drains, and this grid while the previous one drains -- but no global memory
+// is touched before the previous kernel has completed and flushed.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 // ------------------------------------------------------------------ K1 / K3
 // Gather-encode for the exact and lossless modes.  Stage slot layout on
@@ -688,6 +698,7 @@ template <int MODE, bool PTRS>
 __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
     k_encode_vec(Geom g, RowSrc src, uint8_t* __restrict__ cont, uint8_t* __restrict__ offsets) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
+  pdl_entry();
   encode_body<MODE, PTRS>(g, src, cont, offsets, smem_raw);
 }
 
@@ -1041,6 +1052,7 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
                  const uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bars[TMA ? kWarps * kStages : 1];
+  pdl_entry();
   decode_body<MODE, O, TMA>(&cmap, g, cont, offsets, e, out, err, TMA ? align1024(smem_raw) : smem_raw, bars);
 }
 
@@ -1084,12 +1096,7 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bars[kWarps * kStages];
   uint8_t* base = align1024(smem_raw);
-  // Programmatic dependent launch (the launcher sets the attribute): the next
-  // step's grid may be scheduled while this one drains, and this grid may be
-  // scheduled while the previous kernel in the stream drains -- but it
-  // touches no global memory before that kernel has completed and flushed.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_entry();
   encode_body<MODE, PTRS>(g, src, cont, offsets, base, RtRegion<MODE>::BYTES);
   // this warp's container stores (generic proxy) before its TMA reads of
   // them, and its staging writes before the TMA fills of the same slots
@@ -1281,6 +1288,33 @@ int grid_for(K kernel, int threads, size_t smem, int num_sms, uint64_t work_unit
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Launch with the programmatic-stream-serialization attribute (the kernel
+// calls pdl_entry() first).  The overlap happens only kernel after kernel in
+// one stream; event waits and copies in between serialise as usual.
+// OPTB_PDL=0: plain launches (A/B runs).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int threads, size_t smem, cudaStream_t s, Args&&... args) {
+  static const bool pdl = [] {
+    const char* v = getenv("OPTB_PDL");
+    return !(v && v[0] == '0');
+  }();
+  if (!pdl) {
+    kernel<<<grid, threads, smem, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int MODE>
 cudaError_t enc_generic(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
                         uint64_t* launches) {
@@ -1312,9 +1346,10 @@ cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(k_encode_vec<MODE, PTRS>, kThreads, smem, sms, items);
-  k_encode_vec<MODE, PTRS><<<grid, kThreads, smem, s>>>(g, rs, static_cast<uint8_t*>(cont), offs);
+  const cudaError_t le = launch_k(k_encode_vec<MODE, PTRS>, grid, kThreads, smem, s, g, rs,
+                                  static_cast<uint8_t*>(cont), offs);
   ++*launches;
-  return cudaGetLastError();
+  return le;
 }
 
 template <int MODE>
@@ -1372,10 +1407,10 @@ cudaError_t dec_vec_launch(const CUtensorMap& cm, const Geom& g, const void* con
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(k_decode_vec<MODE, O, TMA>, kThreads, smem, sms, items);
-  k_decode_vec<MODE, O, TMA><<<grid, kThreads, smem, s>>>(cm, g, static_cast<const uint8_t*>(cont), offs, e, out,
-                                                          err);
+  const cudaError_t le = launch_k(k_decode_vec<MODE, O, TMA>, grid, kThreads, smem, s, cm, g,
+                                  static_cast<const uint8_t*>(cont), offs, e, out, err);
   ++*launches;
-  return cudaGetLastError();
+  return le;
 }
 
 template <int MODE, int O>
@@ -1397,25 +1432,9 @@ cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, voi
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
   const int grid = grid_for(kernel, kThreads, smem, sms, items);
-  // OPTB_PDL=0: plain launches (A/B runs).  PDL only overlaps kernel after
-  // kernel in one stream; event waits and copies in between serialise as usual.
-  static const bool pdl = [] { const char* v = getenv("OPTB_PDL"); return !(v && v[0] == '0'); }();
-  if (pdl) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t le = cudaLaunchKernelEx(&cfg, kernel, cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
-    if (le != cudaSuccess) return le;
-  } else {
-    kernel<<<grid, kThreads, smem, s>>>(cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
-  }
+  const cudaError_t le = launch_k(kernel, grid, kThreads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs, e,
+                                  out, err);
+  if (le != cudaSuccess) return le;
   ++*launches;
   return cudaGetLastError();
 }
