@@ -481,10 +481,18 @@ __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> byte
 // warp_region: bytes of shared memory per warp (its ring), >= kStages * slot;
 // the fused kernel gives both bodies the same per-warp region so that a warp
 // in one phase never touches another warp's ring in the other phase.
-template <int MODE, bool PTRS>
+struct NoHook {
+  __device__ void operator()(int, bool) const {}
+};
+
+// on_last(free_stage, earlier_tiles): called at the top of the warp's last
+// tile (warp-uniform) with the ring stage that no copy will fill any more,
+// and whether the warp stored tiles in earlier iterations.
+template <int MODE, bool PTRS, typename Hook = NoHook>
 __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
                                             uint8_t* __restrict__ offsets, uint8_t* smem_base,
-                                            uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT) {
+                                            uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT,
+                                            Hook on_last = Hook{}) {
   const uint8_t* __restrict__ images = src.images;
   const uint64_t row_stride = src.stride;
   const int64_t* __restrict__ row_index = src.index;
@@ -558,6 +566,7 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   int stage = 0;
   Walk wc = walk_at(g, G, first + lane);  // the tile being transposed
   for (uint64_t base = first; base < items; base += stride) {
+    if (base + stride >= items) on_last((stage + 1) % kStages, base != first);
     issue((stage + kStages - 1) % kStages);
     fetch_rows();  // consumed by the next iteration's issue
     cp_async_wait<kStages - 1>();
@@ -734,11 +743,14 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + (((a + 1023u) & ~1023u) - a);
 }
 
+// start_stage / prefetched: the fused kernel may have issued the warp's first
+// tile already (into start_stage, mbarriers initialised by the caller).
 template <int MODE, int O, bool TMA>
 __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom& g, const uint8_t* __restrict__ cont,
                                             const uint8_t* __restrict__ offsets, const Epi& e,
                                             void* __restrict__ out, DevError* err, uint8_t* smem_base,
-                                            uint64_t* bars, uint32_t warp_region = 0) {
+                                            uint64_t* bars, uint32_t warp_region = 0, int start_stage = 0,
+                                            bool prefetched = false) {
   using S = VecMode<MODE>;
   constexpr int WC = S::WC;
   constexpr int SLOT = TMA ? DecSlot<MODE>::TMA : DecSlot<MODE>::RAW;
@@ -751,10 +763,12 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
   const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
   const uint64_t ostride = e.row_stride;
   if constexpr (TMA) {
-    if (lane == 0)
-      for (int st = 0; st < kStages; ++st) mbar_init(bar + st, 1);
-    fence_mbar_init();
-    __syncwarp();
+    if (!prefetched) {
+      if (lane == 0)
+        for (int st = 0; st < kStages; ++st) mbar_init(bar + st, 1);
+      fence_mbar_init();
+      __syncwarp();
+    }
   }
 
   const WalkStep step = walk_step(g, G, stride);
@@ -826,13 +840,15 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
     if constexpr (S::OFFS) walk_advance(wi, step, g, G);
   };
 
+  if (!prefetched) {
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue(first + s * stride, s);
-  int stage = 0;
-  uint32_t phase = 0;
+    for (int s = 0; s < kStages - 1; ++s) issue(first + s * stride, s);
+  }
+  int stage = start_stage;
+  uint32_t phase_bits = 0;  // parity of each stage's mbarrier
   for (uint64_t base = first; base < items; base += stride) {
     issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
-    if constexpr (TMA) mbar_wait(bar + stage, phase);
+    if constexpr (TMA) mbar_wait(bar + stage, (phase_bits >> stage) & 1u);
     if constexpr (!TMA || S::OFFS) {
       cp_async_wait<kStages - 1>();
       __syncwarp();
@@ -1038,10 +1054,8 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
       if constexpr (TMA) fence_proxy_async_smem();
     }
     __syncwarp();
-    if (++stage == kStages) {
-      stage = 0;
-      phase ^= 1u;
-    }
+    phase_bits ^= 1u << stage;
+    if (++stage == kStages) stage = 0;
   }
   if constexpr (!TMA || S::OFFS) cp_async_wait<0>();
 }
@@ -1097,13 +1111,46 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   __shared__ uint64_t bars[kWarps * kStages];
   uint8_t* base = align1024(smem_raw);
   pdl_entry();
-  encode_body<MODE, PTRS>(g, src, cont, offsets, base, RtRegion<MODE>::BYTES);
+  // The phase switch without a bubble: during its last encode tile a warp
+  // already loads its first decode tile (stored in its first iteration) into
+  // the ring stage no copy will fill any more -- when the two rings share the
+  // slot size (exact, f64) and the warp has encoded more than one tile.
+  constexpr bool kPrefetch = !VecMode<MODE>::OFFS && VecMode<MODE>::ENC_SLOT == DecSlot<MODE>::TMA && kStages == 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t* bar = bars + warp * kStages;
+  if constexpr (kPrefetch) {
+    if (lane == 0)
+      for (int st = 0; st < kStages; ++st) mbar_init(bar + st, 1);
+    fence_mbar_init();
+    __syncwarp();
+  }
+  int start_stage = 0;
+  bool prefetched = false;
+  auto prefetch_first = [&](int free_stage, bool earlier_tiles) {
+    if constexpr (kPrefetch) {
+      if (!earlier_tiles) return;
+      fence_proxy_async_global();  // the warp's container stores so far, before the TMA read
+      fence_proxy_async_smem();    // its writes to the free slot, before the TMA write
+      __syncwarp();
+      if (lane == 0) {
+        const uint64_t t0 = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
+        constexpr int WC = VecMode<MODE>::WC;
+        mbar_expect_tx(bar + free_stage, 512 * WC);
+        tma_load_2d(base + warp * RtRegion<MODE>::BYTES + free_stage * DecSlot<MODE>::TMA, &cmap, 0,
+                    static_cast<int>((t0 * 16 * WC) >> 7), bar + free_stage);
+      }
+      start_stage = free_stage;
+      prefetched = true;
+    }
+  };
+  encode_body<MODE, PTRS>(g, src, cont, offsets, base, RtRegion<MODE>::BYTES, prefetch_first);
   // this warp's container stores (generic proxy) before its TMA reads of
   // them, and its staging writes before the TMA fills of the same slots
   fence_proxy_async_global();
   fence_proxy_async_smem();
   __syncwarp();
-  decode_body<MODE, O, true>(&cmap, g, cont, offsets, e, out, err, base, bars, RtRegion<MODE>::BYTES);
+  decode_body<MODE, O, true>(&cmap, g, cont, offsets, e, out, err, base, bars, RtRegion<MODE>::BYTES, start_stage,
+                             prefetched);
 }
 
 // ------------------------------------------------------------------ generic
