@@ -484,15 +484,20 @@ __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> byte
 struct NoHook {
   __device__ void operator()(int, bool) const {}
 };
+struct NoTileHook {
+  __device__ void operator()(uint64_t) const {}
+};
 
 // on_last(free_stage, earlier_tiles): called at the top of the warp's last
 // tile (warp-uniform) with the ring stage that no copy will fill any more,
 // and whether the warp stored tiles in earlier iterations.
-template <int MODE, bool PTRS, typename Hook = NoHook>
+// after_tile(base): called once the warp has issued the container stores of
+// the tile at item base (warp-uniform, after a __syncwarp).
+template <int MODE, bool PTRS, typename Hook = NoHook, typename TileHook = NoTileHook>
 __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
                                             uint8_t* __restrict__ offsets, uint8_t* smem_base,
                                             uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT,
-                                            Hook on_last = Hook{}) {
+                                            Hook on_last = Hook{}, TileHook after_tile = TileHook{}) {
   const uint8_t* __restrict__ images = src.images;
   const uint64_t row_stride = src.stride;
   const int64_t* __restrict__ row_index = src.index;
@@ -698,6 +703,7 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       }
     }
     __syncwarp();
+    after_tile(base);
     stage = (stage + 1) % kStages;
   }
   cp_async_wait<0>();
@@ -743,6 +749,218 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + (((a + 1023u) & ~1023u) - a);
 }
 
+// One tile of the decode: the container words of items wc.t .. wc.t + 31
+// (lane L: item wc.t + L) are in the warp's slot (TMA: the 128B-swizzled box;
+// else the XOR-swizzled cp.async layout, lossless parity bits after the
+// words).  Range checks, unpack, transpose, epilogue stores.
+template <int MODE, int O, bool TMA>
+__device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint64_t items, uint8_t* slot,
+                                            const Epi& e, void* __restrict__ out, DevError* err) {
+  using S = VecMode<MODE>;
+  constexpr int WC = S::WC;
+  const int lane = threadIdx.x & 31;
+  const uint64_t ostride = e.row_stride;
+  const bool valid = wc.t < items;
+  const uint64_t k = wc.k, gi = wc.gi;
+  ChunkPos c{0, 0};
+  if (valid) c = walk_chunk(g, wc);
+  // raw words: m[p] = word of pixel 16*gi + p (low 8 bytes in [0..1] for WC 8)
+  uint32_t m[16][4];
+  if constexpr (TMA && WC == 16) {
+    const bool hi = (lane >> 2) & 1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int ra = 2 * lane + (hi ? 1 : 0), rb = 2 * lane + (hi ? 0 : 1);
+      const uint4 a = *reinterpret_cast<const uint4*>(slot + ra * 128 + ((j ^ (ra & 7)) << 4));
+      const uint4 b = *reinterpret_cast<const uint4*>(slot + rb * 128 + ((j ^ (rb & 7)) << 4));
+      m[j][0] = hi ? b.x : a.x;
+      m[j][1] = hi ? b.y : a.y;
+      m[j][2] = hi ? b.z : a.z;
+      m[j][3] = hi ? b.w : a.w;
+      m[j + 8][0] = hi ? a.x : b.x;
+      m[j + 8][1] = hi ? a.y : b.y;
+      m[j + 8][2] = hi ? a.z : b.z;
+      m[j + 8][3] = hi ? a.w : b.w;
+    }
+  } else if constexpr (TMA) {
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const uint4 v = *reinterpret_cast<const uint4*>(slot + lane * 128 + ((cc ^ (lane & 7)) << 4));
+      m[2 * cc][0] = v.x;
+      m[2 * cc][1] = v.y;
+      m[2 * cc + 1][0] = v.z;
+      m[2 * cc + 1][1] = v.w;
+      m[2 * cc][2] = m[2 * cc][3] = m[2 * cc + 1][2] = m[2 * cc + 1][3] = 0u;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const int sl = p ^ (lane & S::SW);
+      if constexpr (WC == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
+        m[p][0] = v.x;
+        m[p][1] = v.y;
+        m[p][2] = v.z;
+        m[p][3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
+        m[p][0] = v.x;
+        m[p][1] = v.y;
+        m[p][2] = m[p][3] = 0u;
+      }
+    }
+  }
+  uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
+  bool bad = false;
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
+    const uint64_t w1 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
+    if constexpr (S::F64) {
+      // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
+      const double acc = __longlong_as_double(static_cast<long long>(w0));
+      bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
+      if (acc < 0x1.0p64) {  // common case: the peel is the integer's bytes
+        const uint64_t iacc = static_cast<uint64_t>(acc);
+        m[p][0] = static_cast<uint32_t>(iacc);
+        m[p][1] = static_cast<uint32_t>(iacc >> 32);
+        m[p][2] = m[p][3] = 0u;
+      } else {
+        const uint4 v = f64_peel_big(acc);
+        m[p][0] = v.x;
+        m[p][1] = v.y;
+        m[p][2] = v.z;
+        m[p][3] = v.w;
+      }
+    } else if constexpr (S::OFFS) {
+      // range check (codec.cpp:189-194): bits >= 7n must be zero
+      const unsigned used = 7u * c.n;
+      if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
+      else bad |= (w1 >> (used - 64u)) != 0;
+      // byte lanes hold field << 1: the pixel up to its parity bit
+      const uint2 lo = unpack7x8_shl1(m[p][0], m[p][1]);  // images 0..7 (bits 0..55)
+      const uint32_t w0hi = m[p][1], w1lo = m[p][2], w1hi = m[p][3];
+      m[p][0] = lo.x;
+      m[p][1] = lo.y;
+      if constexpr (WC == 8) {
+        m[p][2] = (w0hi >> 23) & 0xFEu;  // image 8 (bits 56..62)
+        m[p][3] = 0u;
+      } else {
+        // images 8..15: bits 56..111 = (w0 >> 56) | (w1 << 8)
+        const uint2 hi = unpack7x8_shl1(__funnelshift_r(w0hi, w1lo, 24), __funnelshift_r(w1lo, w1hi, 24));
+        m[p][2] = hi.x;
+        m[p][3] = hi.y;
+        x16[p >> 2] |= ((w1hi >> 15) & 0xFEu) << (8 * (p & 3));  // bits 112..118
+        x17[p >> 2] |= ((w1hi >> 22) & 0xFEu) << (8 * (p & 3));  // bits 119..125
+      }
+    }
+  }
+  transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (lossless: without their parity bits)
+  if (valid) {
+    if constexpr (!S::OFFS && !S::F64) {
+      // range check (codec.cpp:189-194): bytes of images >= n must be zero
+      uint32_t hi = 0;
+#pragma unroll
+      for (int i = 0; i < S::NI; ++i)
+        if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
+      bad = hi != 0;
+    }
+    if (bad) latch_error(err, S::F64 ? kErrF64Range : kErrIntRange, g.chunk_base + k, c.n);
+  }
+  if constexpr (S::OFFS) {
+    // pixel = (field << 1) | parity (codec.cpp:196-201); the shift is already in
+#pragma unroll
+    for (int i = 0; i < S::NI; ++i) {
+      uint32_t bits = 0;
+      if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
+      uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) row[q] |= nibble_lsbs((bits >> (4 * q)) & 0xFu);
+    }
+  }
+  auto row_vec = [&](int i) -> uint4 {
+    if (i < 16) return make_uint4(m[i < 16 ? i : 0][0], m[i < 16 ? i : 0][1], m[i < 16 ? i : 0][2], m[i < 16 ? i : 0][3]);
+    if (i == 16) return make_uint4(x16[0], x16[1], x16[2], x16[3]);
+    return make_uint4(x17[0], x17[1], x17[2], x17[3]);
+  };
+  if constexpr (O == OPTB_OUT_U8) {
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < S::NI; ++i)
+        if (i < static_cast<int>(c.n))
+          stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16, row_vec(i));
+    }
+  } else {
+    __syncwarp();  // all lanes done reading the slot
+    // u8 tile in the same slot: image i, lane L's 16 pixels at i*512 + L*16
+#pragma unroll
+    for (int i = 0; i < S::NI; ++i) *reinterpret_cast<uint4*>(slot + i * 512 + lane * 16) = row_vec(i);
+    __syncwarp();
+    // epilogue: every lane stores 16 bytes per row -- PX = 4 fp32 or 8 half
+    // pixels, starting at pixel PX*(lane % LPS) of source lane L's group
+    constexpr int ES = (O == OPTB_OUT_F32) ? 4 : 2;
+    constexpr int PX = 16 / ES, LPS = 16 / PX, ROUNDS = 32 / (32 / LPS);
+#pragma unroll
+    for (int cc = 0; cc < ROUNDS; ++cc) {
+      const int L = lane / LPS + (32 / LPS) * cc;
+      const uint32_t r0lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0), L);
+      const uint32_t r0hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0 >> 32), L);
+      const uint32_t nL = __shfl_sync(0xffffffffu, valid ? c.n : 0u, L);
+      const uint32_t glo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi), L);
+      const uint32_t ghi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi >> 32), L);
+      const uint64_t r0L = (static_cast<uint64_t>(r0hi) << 32) | r0lo;
+      const uint64_t gL = (static_cast<uint64_t>(ghi) << 32) | glo;
+      const int sub = PX * (lane % LPS);
+      uint8_t* dst = static_cast<uint8_t*>(out) + (r0L * ostride + gL * 16 + sub) * ES;
+      const uint64_t dstep = ostride * ES;
+      const uint8_t* src = slot + L * 16 + sub;
+      auto put_row = [&](uint8_t* d, int i, const PxScale& sc, auto fast) {
+        constexpr bool F = decltype(fast)::value;
+        if constexpr (PX == 4) {
+          Out4::put<O, F>(d, *reinterpret_cast<const uint32_t*>(src + i * 512), sc);
+        } else {
+          Out8::put<O, F>(d, *reinterpret_cast<const uint2*>(src + i * 512), sc);
+        }
+      };
+      if (!e.class_scale) {  // one scale for every row (the runner's kPixelScale)
+        const PxScale sc = px_scale(e.scale, 0.0f, false);
+        if (sc.fast) {
+#pragma unroll
+          for (int i = 0; i < S::NI; ++i) {
+            if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::true_type{});
+            dst += dstep;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < S::NI; ++i) {
+            if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::false_type{});
+            dst += dstep;
+          }
+        }
+      } else {  // per-class (scale, bias) tables indexed by the row's class
+#pragma unroll
+        for (int i = 0; i < S::NI; ++i) {
+          if (i < static_cast<int>(nL)) {
+            float s, b;
+            bool aff;
+            row_affine(e, r0L + i, s, b, aff);
+            const PxScale sc = px_scale(s, b, aff);
+            if (sc.fast) {
+              put_row(dst, i, sc, std::true_type{});
+            } else {
+              put_row(dst, i, sc, std::false_type{});
+            }
+          }
+          dst += dstep;
+        }
+      }
+    }
+    // the slot's next fill is an async-proxy (TMA) write
+    if constexpr (TMA) fence_proxy_async_smem();
+  }
+  __syncwarp();
+}
+
 // start_stage / prefetched: the fused kernel may have issued the warp's first
 // tile already (into start_stage, mbarriers initialised by the caller).
 template <int MODE, int O, bool TMA>
@@ -761,7 +979,6 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
   const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
-  const uint64_t ostride = e.row_stride;
   if constexpr (TMA) {
     if (!prefetched) {
       if (lane == 0)
@@ -853,207 +1070,8 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
       cp_async_wait<kStages - 1>();
       __syncwarp();
     }
-    uint8_t* slot = ring + stage * SLOT;
-    const bool valid = wc.t < items;
-    const uint64_t k = wc.k, gi = wc.gi;
-    ChunkPos c{0, 0};
-    if (valid) c = walk_chunk(g, wc);
+    decode_tile<MODE, O, TMA>(g, wc, items, ring + stage * SLOT, e, out, err);
     walk_advance(wc, step, g, G);
-    // raw words: m[p] = word of pixel 16*gi + p (low 8 bytes in [0..1] for WC 8)
-    uint32_t m[16][4];
-    if constexpr (TMA && WC == 16) {
-      const bool hi = (lane >> 2) & 1;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int ra = 2 * lane + (hi ? 1 : 0), rb = 2 * lane + (hi ? 0 : 1);
-        const uint4 a = *reinterpret_cast<const uint4*>(slot + ra * 128 + ((j ^ (ra & 7)) << 4));
-        const uint4 b = *reinterpret_cast<const uint4*>(slot + rb * 128 + ((j ^ (rb & 7)) << 4));
-        m[j][0] = hi ? b.x : a.x;
-        m[j][1] = hi ? b.y : a.y;
-        m[j][2] = hi ? b.z : a.z;
-        m[j][3] = hi ? b.w : a.w;
-        m[j + 8][0] = hi ? a.x : b.x;
-        m[j + 8][1] = hi ? a.y : b.y;
-        m[j + 8][2] = hi ? a.z : b.z;
-        m[j + 8][3] = hi ? a.w : b.w;
-      }
-    } else if constexpr (TMA) {
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const uint4 v = *reinterpret_cast<const uint4*>(slot + lane * 128 + ((cc ^ (lane & 7)) << 4));
-        m[2 * cc][0] = v.x;
-        m[2 * cc][1] = v.y;
-        m[2 * cc + 1][0] = v.z;
-        m[2 * cc + 1][1] = v.w;
-        m[2 * cc][2] = m[2 * cc][3] = m[2 * cc + 1][2] = m[2 * cc + 1][3] = 0u;
-      }
-    } else {
-#pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        const int sl = p ^ (lane & S::SW);
-        if constexpr (WC == 16) {
-          const uint4 v = *reinterpret_cast<const uint4*>(slot + (lane * 16 + sl) * 16);
-          m[p][0] = v.x;
-          m[p][1] = v.y;
-          m[p][2] = v.z;
-          m[p][3] = v.w;
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2*>(slot + (lane * 16 + sl) * 8);
-          m[p][0] = v.x;
-          m[p][1] = v.y;
-          m[p][2] = m[p][3] = 0u;
-        }
-      }
-    }
-    uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
-    bool bad = false;
-#pragma unroll
-    for (int p = 0; p < 16; ++p) {
-      const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
-      const uint64_t w1 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
-      if constexpr (S::F64) {
-        // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
-        const double acc = __longlong_as_double(static_cast<long long>(w0));
-        bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
-        if (acc < 0x1.0p64) {  // common case: the peel is the integer's bytes
-          const uint64_t iacc = static_cast<uint64_t>(acc);
-          m[p][0] = static_cast<uint32_t>(iacc);
-          m[p][1] = static_cast<uint32_t>(iacc >> 32);
-          m[p][2] = m[p][3] = 0u;
-        } else {
-          const uint4 v = f64_peel_big(acc);
-          m[p][0] = v.x;
-          m[p][1] = v.y;
-          m[p][2] = v.z;
-          m[p][3] = v.w;
-        }
-      } else if constexpr (S::OFFS) {
-        // range check (codec.cpp:189-194): bits >= 7n must be zero
-        const unsigned used = 7u * c.n;
-        if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
-        else bad |= (w1 >> (used - 64u)) != 0;
-        // byte lanes hold field << 1: the pixel up to its parity bit
-        const uint2 lo = unpack7x8_shl1(m[p][0], m[p][1]);  // images 0..7 (bits 0..55)
-        const uint32_t w0hi = m[p][1], w1lo = m[p][2], w1hi = m[p][3];
-        m[p][0] = lo.x;
-        m[p][1] = lo.y;
-        if constexpr (WC == 8) {
-          m[p][2] = (w0hi >> 23) & 0xFEu;  // image 8 (bits 56..62)
-          m[p][3] = 0u;
-        } else {
-          // images 8..15: bits 56..111 = (w0 >> 56) | (w1 << 8)
-          const uint2 hi = unpack7x8_shl1(__funnelshift_r(w0hi, w1lo, 24), __funnelshift_r(w1lo, w1hi, 24));
-          m[p][2] = hi.x;
-          m[p][3] = hi.y;
-          x16[p >> 2] |= ((w1hi >> 15) & 0xFEu) << (8 * (p & 3));  // bits 112..118
-          x17[p >> 2] |= ((w1hi >> 22) & 0xFEu) << (8 * (p & 3));  // bits 119..125
-        }
-      }
-    }
-    transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (lossless: without their parity bits)
-    if (valid) {
-      if constexpr (!S::OFFS && !S::F64) {
-        // range check (codec.cpp:189-194): bytes of images >= n must be zero
-        uint32_t hi = 0;
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i)
-          if (i >= static_cast<int>(c.n)) hi |= m[i][0] | m[i][1] | m[i][2] | m[i][3];
-        bad = hi != 0;
-      }
-      if (bad) latch_error(err, S::F64 ? kErrF64Range : kErrIntRange, g.chunk_base + k, c.n);
-    }
-    if constexpr (S::OFFS) {
-      // pixel = (field << 1) | parity (codec.cpp:196-201); the shift is already in
-#pragma unroll
-      for (int i = 0; i < S::NI; ++i) {
-        uint32_t bits = 0;
-        if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
-        uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) row[q] |= nibble_lsbs((bits >> (4 * q)) & 0xFu);
-      }
-    }
-    auto row_vec = [&](int i) -> uint4 {
-      if (i < 16) return make_uint4(m[i < 16 ? i : 0][0], m[i < 16 ? i : 0][1], m[i < 16 ? i : 0][2], m[i < 16 ? i : 0][3]);
-      if (i == 16) return make_uint4(x16[0], x16[1], x16[2], x16[3]);
-      return make_uint4(x17[0], x17[1], x17[2], x17[3]);
-    };
-    if constexpr (O == OPTB_OUT_U8) {
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < S::NI; ++i)
-          if (i < static_cast<int>(c.n))
-            stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16, row_vec(i));
-      }
-    } else {
-      __syncwarp();  // all lanes done reading the slot
-      // u8 tile in the same slot: image i, lane L's 16 pixels at i*512 + L*16
-#pragma unroll
-      for (int i = 0; i < S::NI; ++i) *reinterpret_cast<uint4*>(slot + i * 512 + lane * 16) = row_vec(i);
-      __syncwarp();
-      // epilogue: every lane stores 16 bytes per row -- PX = 4 fp32 or 8 half
-      // pixels, starting at pixel PX*(lane % LPS) of source lane L's group
-      constexpr int ES = (O == OPTB_OUT_F32) ? 4 : 2;
-      constexpr int PX = 16 / ES, LPS = 16 / PX, ROUNDS = 32 / (32 / LPS);
-#pragma unroll
-      for (int cc = 0; cc < ROUNDS; ++cc) {
-        const int L = lane / LPS + (32 / LPS) * cc;
-        const uint32_t r0lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0), L);
-        const uint32_t r0hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(c.r0 >> 32), L);
-        const uint32_t nL = __shfl_sync(0xffffffffu, valid ? c.n : 0u, L);
-        const uint32_t glo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi), L);
-        const uint32_t ghi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(gi >> 32), L);
-        const uint64_t r0L = (static_cast<uint64_t>(r0hi) << 32) | r0lo;
-        const uint64_t gL = (static_cast<uint64_t>(ghi) << 32) | glo;
-        const int sub = PX * (lane % LPS);
-        uint8_t* dst = static_cast<uint8_t*>(out) + (r0L * ostride + gL * 16 + sub) * ES;
-        const uint64_t dstep = ostride * ES;
-        const uint8_t* src = slot + L * 16 + sub;
-        auto put_row = [&](uint8_t* d, int i, const PxScale& sc, auto fast) {
-          constexpr bool F = decltype(fast)::value;
-          if constexpr (PX == 4) {
-            Out4::put<O, F>(d, *reinterpret_cast<const uint32_t*>(src + i * 512), sc);
-          } else {
-            Out8::put<O, F>(d, *reinterpret_cast<const uint2*>(src + i * 512), sc);
-          }
-        };
-        if (!e.class_scale) {  // one scale for every row (the runner's kPixelScale)
-          const PxScale sc = px_scale(e.scale, 0.0f, false);
-          if (sc.fast) {
-#pragma unroll
-            for (int i = 0; i < S::NI; ++i) {
-              if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::true_type{});
-              dst += dstep;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < S::NI; ++i) {
-              if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::false_type{});
-              dst += dstep;
-            }
-          }
-        } else {  // per-class (scale, bias) tables indexed by the row's class
-#pragma unroll
-          for (int i = 0; i < S::NI; ++i) {
-            if (i < static_cast<int>(nL)) {
-              float s, b;
-              bool aff;
-              row_affine(e, r0L + i, s, b, aff);
-              const PxScale sc = px_scale(s, b, aff);
-              if (sc.fast) {
-                put_row(dst, i, sc, std::true_type{});
-              } else {
-                put_row(dst, i, sc, std::false_type{});
-              }
-            }
-            dst += dstep;
-          }
-        }
-      }
-      // the slot's next fill is an async-proxy (TMA) write
-      if constexpr (TMA) fence_proxy_async_smem();
-    }
-    __syncwarp();
     phase_bits ^= 1u << stage;
     if (++stage == kStages) stage = 0;
   }
@@ -1151,6 +1169,68 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   __syncwarp();
   decode_body<MODE, O, true>(&cmap, g, cont, offsets, e, out, err, base, bars, RtRegion<MODE>::BYTES, start_stage,
                              prefetched);
+}
+
+// The interleaved round trip (exact and f64 modes): a warp decodes each tile
+// one encode iteration after storing it -- encode tile j, decode tile j-1,
+// then one TMA load of tile j's container words into the warp's decode slot,
+// which lands while tile j+1 is being gathered and encoded.  The container
+// stream is still written to HBM in full (the stores are the same), but each
+// tile is read back while its lines are still in L2: per step the DRAM moves
+// the gathered rows in, the containers and the decoded rows out, and the
+// decode's container read is an L2 hit (ncu: dram bytes = the compulsory
+// 3 x ~153 MB instead of 4x).  Same per-warp tile sequence as the phase-
+// ordered kernel above, so the results are identical.
+template <int MODE>
+struct IlRegion {
+  static constexpr uint32_t ENC = kStages * VecMode<MODE>::ENC_SLOT;  // 1024-multiple
+  static constexpr uint32_t BYTES = ENC + DecSlot<MODE>::TMA;
+};
+template <int MODE, int O, bool PTRS, bool ONE_CTA = false>
+__global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
+    k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
+                   uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
+  static_assert(!VecMode<MODE>::OFFS, "lossless containers carry parity planes: phase-ordered kernel");
+  static_assert(IlRegion<MODE>::ENC % 1024 == 0, "decode slot must stay 1024-aligned");
+  constexpr int WC = VecMode<MODE>::WC;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ uint64_t bars[kWarps];
+  uint8_t* base = align1024(smem_raw);
+  pdl_entry();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t* bar = bars + warp;
+  uint8_t* dslot = base + warp * IlRegion<MODE>::BYTES + IlRegion<MODE>::ENC;
+  if (lane == 0) mbar_init(bar, 1);
+  fence_mbar_init();
+  __syncwarp();
+  const uint64_t G = g.P / 16;
+  const uint64_t items = g.chunks * G;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
+  const WalkStep step = walk_step(g, G, stride);
+  Walk wd = walk_at(g, G, (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32 + lane);
+  uint32_t phase = 0;
+  bool pending = false;
+  auto decode_pending = [&]() {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    decode_tile<MODE, O, true>(g, wd, items, dslot, e, out, err);  // ends with __syncwarp
+    walk_advance(wd, step, g, G);
+  };
+  auto after_tile = [&](uint64_t tile) {
+    if (pending) decode_pending();
+    // this tile's container stores (generic proxy) before the TMA read of
+    // them; the decode slot's generic writes (float epilogue) were fenced in
+    // decode_tile
+    fence_proxy_async_global();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_expect_tx(bar, 512 * WC);
+      tma_load_2d(dslot, &cmap, 0, static_cast<int>((tile * 16 * WC) >> 7), bar);
+    }
+    pending = true;
+  };
+  encode_body<MODE, PTRS>(g, src, cont, offsets, base, IlRegion<MODE>::BYTES, NoHook{}, after_tile);
+  if (pending) decode_pending();
 }
 
 // ------------------------------------------------------------------ generic
@@ -1470,9 +1550,34 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
   return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
 
+// OPTB_RT_INTERLEAVE=0 selects the phase-ordered fused kernel for every mode
+// (A/B runs; the interleaved one is the default where it applies).
+bool rt_interleave_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("OPTB_RT_INTERLEAVE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 template <int MODE, int O, bool PTRS, bool ONE_CTA>
 cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, const Epi& e,
                      void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  if constexpr (!VecMode<MODE>::OFFS) {
+    if (rt_interleave_enabled()) {
+      constexpr size_t smem = static_cast<size_t>(kWarps) * IlRegion<MODE>::BYTES + 1024;
+      auto kernel = k_roundtrip_il<MODE, O, PTRS, ONE_CTA>;
+      cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
+      if (ae != cudaSuccess) return ae;
+      const uint64_t items = g.chunks * (g.P / 16);
+      const int grid = grid_for(kernel, kThreads, smem, sms, items);
+      const cudaError_t le = launch_k(kernel, grid, kThreads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs,
+                                      e, out, err);
+      if (le != cudaSuccess) return le;
+      ++*launches;
+      return cudaGetLastError();
+    }
+  }
   constexpr size_t smem = static_cast<size_t>(kWarps) * RtRegion<MODE>::BYTES + 1024;
   auto kernel = k_roundtrip_vec<MODE, O, PTRS, ONE_CTA>;
   cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));

@@ -1,0 +1,127 @@
+// mixlab.cu -- HBM bandwidth of plain streaming kernels by read:write mix, the
+// ceiling for a kernel whose compulsory DRAM traffic has that mix.
+//
+// The interleaved fused round trip (k_roundtrip_il) moves, per step, the
+// gathered rows in and the containers + decoded rows out: one byte read for
+// every two written.  This probe times, on buffers far larger than L2 (so
+// every byte is a DRAM byte), grid-stride 16-byte kernels that
+//   read     read R bytes (sum, one word written per CTA)
+//   write    write W bytes
+//   copy     read N, write N           (1:1, the MEASURED_PEAKS copy shape)
+//   r1w2     read N, write 2N          (the round trip's compulsory mix)
+//   r1w3     read N, write 3N
+// each back to back over 3 rotating buffer sets (the next launch never finds
+// its inputs in L2), CUDA events, median of 20.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/mixlab.cu -o build/mixlab
+//   build/mixlab            # one JSON line per kernel and grid
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                              \
+      fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      exit(1);                                                                            \
+    }                                                                                     \
+  } while (0)
+
+__device__ __forceinline__ uint4 ld(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st(uint4* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+constexpr int U = 4;  // 16-byte accesses in flight per thread per stream
+
+// NW output streams per input stream (NR = 0: write-only; NW = 0: read-only)
+template <int NR, int NW>
+__global__ void __launch_bounds__(256) k_mix(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n16,
+                                             uint32_t* sink) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nt = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  for (uint64_t b = tid; b < n16; b += nt * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = b + u * nt;
+      v[u] = make_uint4(static_cast<uint32_t>(i), 1u, 2u, 3u);
+      if (NR && i < n16) v[u] = ld(in + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = b + u * nt;
+      if (i < n16) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) st(out + w * n16 + i, v[u]);
+        acc ^= v[u].x ^ v[u].w;
+      }
+    }
+  }
+  if (NW == 0 && acc == 0x9e3779b9u) sink[0] = acc;  // keeps the loads
+}
+
+template <int NR, int NW>
+void run(const char* name, int sms, int per_sm, uint64_t n16, std::vector<uint4*>& ins, std::vector<uint4*>& outs,
+         uint32_t* sink) {
+  const int grid = sms * per_sm;
+  cudaEvent_t ev[21];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  const int sets = static_cast<int>(ins.size());
+  for (int i = 0; i < 3; ++i) k_mix<NR, NW><<<grid, 256>>>(ins[i % sets], outs[i % sets], n16, sink);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(ev[0]));
+  for (int i = 0; i < 20; ++i) {
+    k_mix<NR, NW><<<grid, 256>>>(ins[i % sets], outs[i % sets], n16, sink);
+    CK(cudaEventRecord(ev[i + 1]));
+  }
+  CK(cudaEventSynchronize(ev[20]));
+  std::vector<float> t;
+  for (int i = 0; i < 20; ++i) {
+    float ms;
+    CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+    t.push_back(ms);
+  }
+  std::sort(t.begin(), t.end());
+  const double us = t[10] * 1e3;
+  const double rb = static_cast<double>(NR) * n16 * 16, wb = static_cast<double>(NW) * n16 * 16;
+  printf("{\"kernel\": \"%s\", \"grid\": \"%dx%d\", \"read_mb\": %.1f, \"write_mb\": %.1f, \"us\": %.2f, \"gbs\": %.1f}\n",
+         name, sms, per_sm, rb / 1e6, wb / 1e6, us, (rb + wb) / us / 1e3);
+  for (auto& e : ev) CK(cudaEventDestroy(e));
+}
+
+int main() {
+  int dev = 0, sms = 0;
+  CK(cudaSetDevice(dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const uint64_t n16 = 152567808ull / 16;  // one C2 step's rows (49664 x 3072 B)
+  std::vector<uint4*> ins(3), outs(3);
+  for (int s = 0; s < 3; ++s) {
+    CK(cudaMalloc(&ins[s], n16 * 16));
+    CK(cudaMalloc(&outs[s], 3 * n16 * 16));
+    CK(cudaMemset(ins[s], s + 1, n16 * 16));
+    CK(cudaMemset(outs[s], 0, 3 * n16 * 16));
+  }
+  uint32_t* sink;
+  CK(cudaMalloc(&sink, 4));
+  for (int per_sm : {4, 8, 16}) {
+    run<1, 0>("read", sms, per_sm, n16, ins, outs, sink);
+    run<0, 1>("write", sms, per_sm, n16, ins, outs, sink);
+    run<1, 1>("copy", sms, per_sm, n16, ins, outs, sink);
+    run<1, 2>("r1w2", sms, per_sm, n16, ins, outs, sink);
+    run<1, 3>("r1w3", sms, per_sm, n16, ins, outs, sink);
+  }
+  return 0;
+}

@@ -32,7 +32,7 @@ def short(name):
         tf = {"1": "true", "0": "false"}
         if base == "k_encode_vec":  # <MODE, PTRS>
             args = [MODES.get(args[0], args[0])] + [tf.get(a, a) for a in args[1:]]
-        elif base in ("k_decode_vec", "k_encode_generic", "k_decode_generic", "k_roundtrip_vec"):
+        elif base in ("k_decode_vec", "k_encode_generic", "k_decode_generic", "k_roundtrip_vec", "k_roundtrip_il"):
             args = [MODES.get(args[0], args[0])] + [OUTS.get(a, a) for a in args[1:2]] + \
                    [tf.get(a, a) for a in args[2:]]
         n = f"{base}<{','.join(args)}>"
@@ -95,13 +95,16 @@ def main():
                     "write-heavy kernels",
             "algorithmic_bytes_per_launch": {"k_encode_vec<exact128,false>": rows * P * 2 + rows * 8,
                                              "k_decode_vec<exact128,u8,true>": rows * P * 2,
-                                             "k_roundtrip_vec<exact128,u8,false,false>": rows * P * 4 + rows * 8},
+                                             "k_roundtrip_vec<exact128,u8,false,false>": rows * P * 4 + rows * 8,
+                                             # interleaved: the container re-read is an L2 hit
+                                             "k_roundtrip_il<exact128,u8,false,false>": rows * P * 3 + rows * 8},
             "kernels": kern}
     json.dump(summ, open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w"), indent=1)
     step = {}
     # the last fused-pipeline step of the launch list: its roundtrip launch and
     # the SBS launches of the draw call that fed it
-    last_rt = max(i for i, (_, k, _) in enumerate(out) if k.startswith("k_roundtrip_vec<exact128"))
+    last_rt = max(i for i, (_, k, _) in enumerate(out) if k.startswith(("k_roundtrip_vec<exact128",
+                                                                         "k_roundtrip_il<exact128")))
     for _, k, t in out[last_rt - 4:last_rt + 1]:
         step[k] = step.get(k, 0) + t
     tot = sum(step.values())
