@@ -350,6 +350,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int
       : "memory");
 }
 // order this thread's generic-proxy accesses before later async-proxy (TMA) ones
+// Bulk tensor store of a 1024-aligned smem box (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the issuing thread's bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// ... and their global writes are performed
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -493,11 +504,18 @@ struct NoTileHook {
 // and whether the warp stored tiles in earlier iterations.
 // after_tile(base): called once the warp has issued the container stores of
 // the tile at item base (warp-uniform, after a __syncwarp).
-template <int MODE, bool PTRS, typename Hook = NoHook, typename TileHook = NoTileHook>
+// BULK (exact / f64, 1024-aligned slots): the tile's container words are
+// written into its slot in the 128B-swizzled layout of the container tensor
+// map smap and leave in ONE bulk tensor store issued by lane 0 (instead of 16
+// shared loads + 16 global stores per lane); a slot is refilled only after
+// that store has read it.
+template <int MODE, bool PTRS, typename Hook = NoHook, typename TileHook = NoTileHook, bool BULK = false>
 __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
                                             uint8_t* __restrict__ offsets, uint8_t* smem_base,
                                             uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT,
-                                            Hook on_last = Hook{}, TileHook after_tile = TileHook{}) {
+                                            Hook on_last = Hook{}, TileHook after_tile = TileHook{},
+                                            const CUtensorMap* smap = nullptr) {
+  static_assert(!BULK || !VecMode<MODE>::OFFS, "bulk container stores: exact and f64 modes");
   const uint8_t* __restrict__ images = src.images;
   const uint64_t row_stride = src.stride;
   const int64_t* __restrict__ row_index = src.index;
@@ -551,6 +569,10 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   };
   auto issue = [&](int stage) {
     uint8_t* slot = ring + stage * S::ENC_SLOT;
+    if constexpr (BULK) {  // the slot's last bulk store has read it
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+    }
 #pragma unroll
     for (int i = 0; i < S::NI; ++i) {
       if (i < static_cast<int>(pend_n)) {
@@ -649,6 +671,59 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       }
     }
     __syncwarp();
+    if constexpr (BULK) {
+      // SWIZZLE_128B box: tile byte b at row b / 128, 16-byte chunk
+      // (b % 128) / 16 stored at chunk ^ (row & 7).  Same conflict-free
+      // orders as the decode's TMA reads (decode_tile).
+      auto f64_word = [&](int p) -> uint2 {
+        double acc = 0.0;
+        if (n <= 6u) {
+          const uint64_t word = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
+          acc = static_cast<double>(word & ((1ull << (8 * n)) - 1ull));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < static_cast<int>(n))
+              acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
+                                             pow256(i)));
+        }
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(acc));
+        return make_uint2(static_cast<uint32_t>(bits), static_cast<uint32_t>(bits >> 32));
+      };
+      if constexpr (WC == 16) {  // word p of lane L: row 2L + p/8, chunk p % 8
+        const bool hi = (lane >> 2) & 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int ra = 2 * lane + (hi ? 1 : 0), rb = 2 * lane + (hi ? 0 : 1);
+          const uint4 lo4 = make_uint4(m[j][0], m[j][1], m[j][2], m[j][3]);
+          const uint4 hi4 = make_uint4(m[j + 8][0], m[j + 8][1], m[j + 8][2], m[j + 8][3]);
+          *reinterpret_cast<uint4*>(slot + ra * 128 + ((j ^ (ra & 7)) << 4)) = hi ? hi4 : lo4;
+          *reinterpret_cast<uint4*>(slot + rb * 128 + ((j ^ (rb & 7)) << 4)) = hi ? lo4 : hi4;
+        }
+      } else {  // WC 8: words 2c, 2c+1 of lane L: row L, chunk c
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          uint2 a, b;
+          if constexpr (S::F64) {
+            a = f64_word(2 * cc);
+            b = f64_word(2 * cc + 1);
+          } else {
+            a = make_uint2(m[2 * cc][0], m[2 * cc][1]);
+            b = make_uint2(m[2 * cc + 1][0], m[2 * cc + 1][1]);
+          }
+          *reinterpret_cast<uint4*>(slot + lane * 128 + ((cc ^ (lane & 7)) << 4)) = make_uint4(a.x, a.y, b.x, b.y);
+        }
+      }
+      fence_proxy_async_smem();  // the slot's generic writes, before the bulk store reads them
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(smap, 0, static_cast<int>((base * 16 * WC) >> 7), slot);
+        bulk_commit();
+      }
+      after_tile(base);
+      stage = (stage + 1) % kStages;
+      continue;
+    }
 #pragma unroll
     for (int p = 0; p < 16; ++p) {
       const int sl = p ^ (lane & S::SW);
@@ -1181,6 +1256,11 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
 // decode's container read is an L2 hit (ncu: dram bytes = the compulsory
 // 3 x ~153 MB instead of 4x).  Same per-warp tile sequence as the phase-
 // ordered kernel above, so the results are identical.
+#ifndef OPTB_IL_BULK
+#define OPTB_IL_BULK 1
+#endif
+constexpr bool kIlBulk = OPTB_IL_BULK != 0;  // bulk tensor stores of the container tiles
+
 template <int MODE>
 struct IlRegion {
   static constexpr uint32_t ENC = kStages * VecMode<MODE>::ENC_SLOT;  // 1024-multiple
@@ -1218,10 +1298,13 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   };
   auto after_tile = [&](uint64_t tile) {
     if (pending) decode_pending();
-    // this tile's container stores (generic proxy) before the TMA read of
-    // them; the decode slot's generic writes (float epilogue) were fenced in
-    // decode_tile
-    fence_proxy_async_global();
+    // the decode slot's generic writes (float epilogue) were fenced in
+    // decode_tile; the tile's bulk store must be complete before the load
+    if (kIlBulk) {
+      if (lane == 0) bulk_wait0();
+    } else {
+      fence_proxy_async_global();  // this tile's container stores (generic proxy), before the TMA read
+    }
     __syncwarp();
     if (lane == 0) {
       mbar_expect_tx(bar, 512 * WC);
@@ -1229,7 +1312,8 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     }
     pending = true;
   };
-  encode_body<MODE, PTRS>(g, src, cont, offsets, base, IlRegion<MODE>::BYTES, NoHook{}, after_tile);
+  encode_body<MODE, PTRS, NoHook, decltype(after_tile), kIlBulk>(g, src, cont, offsets, base, IlRegion<MODE>::BYTES,
+                                                                  NoHook{}, after_tile, &cmap);
   if (pending) decode_pending();
 }
 
