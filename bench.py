@@ -528,6 +528,8 @@ def main():
         pc = pcie_probe.measure(torch, BATCH * BATCHES_PER_STEP * P)
         bound_ms = max(e2e["h2d_bytes_per_step"] / pc["h2d_gbs"], e2e["d2h_bytes_per_step"] / pc["d2h_gbs"],
                        (e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]) / pc["bidir_gbs"]) / 1e6
+        # (the probe's copies run once, after the e2e leg: a frac slightly
+        # above 1 means the link was a little faster during the leg)
         e2e["pcie"] = dict(pc, bound_ms_per_step=round(bound_ms, 3),
                            frac_of_pcie_bound=round(bound_ms / e2e["ms_per_step"], 3))
     # The same workload in exact64 (8 images per 64-bit word; SURVEY §8:
@@ -556,8 +558,12 @@ def main():
             k7 = statistics.mean(pipe7.timings(k)[1] for k in range(args.warmup, args.warmup + args.split_steps)
                                  if k % t7 == 0)
             pipe7.close()
-        b7 = 2 * (rows * P + C.container_bytes(C.layout(0, 8, P, BATCH, BATCHES_PER_STEP))) + rows * 8
+        cb7 = C.container_bytes(C.layout(0, 8, P, BATCH, BATCHES_PER_STEP))
+        # HBM bytes: rows in, containers out, rows out (+ the container
+        # re-read for the phase-ordered kernel; interleaved: an L2 hit)
+        b7 = 2 * rows * P + cb7 + rows * 8 + (0 if interleaved else cb7)
         exact64 = {"mode": "exact64", "per_chunk": 8, "ms_per_step": round(ms7, 4),
+                   "kernel": "k_roundtrip_il<exact64,u8>" if interleaved else "k_roundtrip_vec<exact64,u8>",
                    "value": round(images_per_step / (ms7 / 1e3), 1), "kernel_ms": round(k7, 4),
                    "kernel_gbs": round(b7 / (k7 / 1e3) / 1e9, 1), "kernel_frac": round(b7 / (k7 / 1e3) / 1e9 / peak, 4)}
 

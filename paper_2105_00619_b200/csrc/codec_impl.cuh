@@ -509,10 +509,11 @@ struct NoTileHook {
 // map smap and leave in ONE bulk tensor store issued by lane 0 (instead of 16
 // shared loads + 16 global stores per lane); a slot is refilled only after
 // that store has read it.
-template <int MODE, bool PTRS, typename Hook = NoHook, typename TileHook = NoTileHook, bool BULK = false>
+template <int MODE, bool PTRS, typename Hook = NoHook, typename TileHook = NoTileHook, bool BULK = false,
+          int NW = kWarps, int NS = kStages>
 __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
                                             uint8_t* __restrict__ offsets, uint8_t* smem_base,
-                                            uint32_t warp_region = kStages * VecMode<MODE>::ENC_SLOT,
+                                            uint32_t warp_region = NS * VecMode<MODE>::ENC_SLOT,
                                             Hook on_last = Hook{}, TileHook after_tile = TileHook{},
                                             const CUtensorMap* smap = nullptr) {
   static_assert(!BULK || !VecMode<MODE>::OFFS, "bulk container stores: exact and f64 modes");
@@ -525,8 +526,8 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   uint8_t* ring = smem_base + warp * warp_region;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
-  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * NW * 32;
+  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * NW + warp) * 32;
 
   const WalkStep step = walk_step(g, G, stride);
   // Dataset row ids of a tile are fetched one stage before its copies are
@@ -585,7 +586,7 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   };
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < NS - 1; ++s) {
     fetch_rows();
     issue(s);
   }
@@ -593,10 +594,10 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   int stage = 0;
   Walk wc = walk_at(g, G, first + lane);  // the tile being transposed
   for (uint64_t base = first; base < items; base += stride) {
-    if (base + stride >= items) on_last((stage + 1) % kStages, base != first);
-    issue((stage + kStages - 1) % kStages);
+    if (base + stride >= items) on_last((stage + 1) % NS, base != first);
+    issue((stage + NS - 1) % NS);
     fetch_rows();  // consumed by the next iteration's issue
-    cp_async_wait<kStages - 1>();
+    cp_async_wait<NS - 1>();
     __syncwarp();
     uint8_t* slot = ring + stage * S::ENC_SLOT;
     const uint64_t t = wc.t;
@@ -720,66 +721,65 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
         tma_store_2d(smap, 0, static_cast<int>((base * 16 * WC) >> 7), slot);
         bulk_commit();
       }
-      after_tile(base);
-      stage = (stage + 1) % kStages;
-      continue;
-    }
+      // after_tile + stage advance below
+    } else {
 #pragma unroll
-    for (int p = 0; p < 16; ++p) {
-      const int sl = p ^ (lane & S::SW);
-      if constexpr (S::F64) {
-        // acc += px_i * 256^i in binary64, i ascending (codec.cpp:116-120); the
-        // products are exact, the adds round in the reference's order
-        double acc = 0.0;
-        if (n <= 6u) {
-          // every partial sum is an integer < 2^48: exact, so the ordered sum
-          // is the packed integer itself (one conversion instead of 2n ops)
-          const uint64_t word = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
-          acc = static_cast<double>(word & ((1ull << (8 * n)) - 1ull));
+      for (int p = 0; p < 16; ++p) {
+        const int sl = p ^ (lane & S::SW);
+        if constexpr (S::F64) {
+          // acc += px_i * 256^i in binary64, i ascending (codec.cpp:116-120); the
+          // products are exact, the adds round in the reference's order
+          double acc = 0.0;
+          if (n <= 6u) {
+            // every partial sum is an integer < 2^48: exact, so the ordered sum
+            // is the packed integer itself (one conversion instead of 2n ops)
+            const uint64_t word = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
+            acc = static_cast<double>(word & ((1ull << (8 * n)) - 1ull));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < static_cast<int>(n))
+                acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
+                                               pow256(i)));
+          }
+          *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
+        } else if constexpr (S::OFFS) {
+          const uint2 lo = pack7x8(m[p][0], m[p][1]);  // fields of images 0..7, bits 0..55
+          if constexpr (WC == 8) {  // lossless64: image 8's field at bit 56
+            *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) =
+                make_uint2(lo.x, lo.y + (m[p][2] & 0xFEu) * (1u << 23));
+          } else {  // lossless128: fields 0..15, images 16/17 at bits 112/119
+            const uint2 hi = pack7x8(m[p][2], m[p][3]);  // images 8..15 -> bits 56..111
+            const uint32_t b16 = (x16[p >> 2] >> (8 * (p & 3))) & 0xFEu;
+            const uint32_t b17 = (x17[p >> 2] >> (8 * (p & 3))) & 0xFEu;
+            *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) =
+                make_uint4(lo.x, lo.y + hi.x * (1u << 24), (hi.x >> 8) + hi.y * (1u << 24),
+                           (hi.y >> 8) + b16 * (1u << 15) + b17 * (1u << 22));
+          }
+        } else if constexpr (WC == 16) {
+          *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
         } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i < static_cast<int>(n))
-              acc = __dadd_rn(acc, __dmul_rn(static_cast<double>((m[p][i >> 2] >> (8 * (i & 3))) & 0xffu),
-                                             pow256(i)));
-        }
-        *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
-      } else if constexpr (S::OFFS) {
-        const uint2 lo = pack7x8(m[p][0], m[p][1]);  // fields of images 0..7, bits 0..55
-        if constexpr (WC == 8) {  // lossless64: image 8's field at bit 56
-          *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) =
-              make_uint2(lo.x, lo.y + (m[p][2] & 0xFEu) * (1u << 23));
-        } else {  // lossless128: fields 0..15, images 16/17 at bits 112/119
-          const uint2 hi = pack7x8(m[p][2], m[p][3]);  // images 8..15 -> bits 56..111
-          const uint32_t b16 = (x16[p >> 2] >> (8 * (p & 3))) & 0xFEu;
-          const uint32_t b17 = (x17[p >> 2] >> (8 * (p & 3))) & 0xFEu;
-          *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) =
-              make_uint4(lo.x, lo.y + hi.x * (1u << 24), (hi.x >> 8) + hi.y * (1u << 24),
-                         (hi.y >> 8) + b16 * (1u << 15) + b17 * (1u << 22));
-        }
-      } else if constexpr (WC == 16) {
-        *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
-      } else {
-        *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) = make_uint2(m[p][0], m[p][1]);
-      }
-    }
-    __syncwarp();
-    uint8_t* dst = cont + base * 16 * WC;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int W = q * 32 + lane, L = W >> 4, p = W & 15;
-      if (base + L < items) {
-        const int sl = p ^ (L & S::SW);
-        if constexpr (WC == 16) {
-          stg16(dst + W * 16, *reinterpret_cast<const uint4*>(slot + (L * 16 + sl) * 16));
-        } else {
-          stg8(dst + W * 8, *reinterpret_cast<const uint2*>(slot + (L * 16 + sl) * 8));
+          *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) = make_uint2(m[p][0], m[p][1]);
         }
       }
+      __syncwarp();
+      uint8_t* dst = cont + base * 16 * WC;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int W = q * 32 + lane, L = W >> 4, p = W & 15;
+        if (base + L < items) {
+          const int sl = p ^ (L & S::SW);
+          if constexpr (WC == 16) {
+            stg16(dst + W * 16, *reinterpret_cast<const uint4*>(slot + (L * 16 + sl) * 16));
+          } else {
+            stg8(dst + W * 8, *reinterpret_cast<const uint2*>(slot + (L * 16 + sl) * 8));
+          }
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
     after_tile(base);
-    stage = (stage + 1) % kStages;
+    stage = (stage + 1) % NS;
   }
   cp_async_wait<0>();
 }
@@ -1261,33 +1261,52 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
 #endif
 constexpr bool kIlBulk = OPTB_IL_BULK != 0;  // bulk tensor stores of the container tiles
 
-template <int MODE>
-struct IlRegion {
-  static constexpr uint32_t ENC = kStages * VecMode<MODE>::ENC_SLOT;  // 1024-multiple
-  static constexpr uint32_t BYTES = ENC + DecSlot<MODE>::TMA;
+// Warps per CTA and input-ring depth of the interleaved kernel (one CTA per
+// SM).  DEEP: 5 warps x 4 stages -- fewer warps with deeper rings keep more
+// gathered rows in flight per SM, the faster shape for exact128 -> u8 on long
+// launches (C2 step 89.8 -> 85.2 us); the default 8 x 2 wins for float
+// outputs and short launches (few tiles per warp), measured with
+// tools/configs_bench.py.  OPTB_IL_WARPS / OPTB_IL_STAGES override both
+// shapes (sweeps).
+template <int MODE, bool DEEP>
+struct IlShape {
+#if defined(OPTB_IL_WARPS) && defined(OPTB_IL_STAGES)
+  static constexpr int NW = OPTB_IL_WARPS, NS = OPTB_IL_STAGES;
+#else
+  static constexpr int NW = DEEP ? 5 : 8;
+  static constexpr int NS = DEEP ? 4 : 2;
+#endif
 };
-template <int MODE, int O, bool PTRS, bool ONE_CTA = false>
+template <int MODE, bool DEEP>
+struct IlRegion {
+  static constexpr uint32_t ENC = IlShape<MODE, DEEP>::NS * VecMode<MODE>::ENC_SLOT;  // 1024-multiple
+  static constexpr uint32_t BYTES = ENC + DecSlot<MODE>::TMA;
+  static constexpr size_t SMEM = static_cast<size_t>(IlShape<MODE, DEEP>::NW) * BYTES + 1024;
+};
+template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP>
 __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   static_assert(!VecMode<MODE>::OFFS, "lossless containers carry parity planes: phase-ordered kernel");
-  static_assert(IlRegion<MODE>::ENC % 1024 == 0, "decode slot must stay 1024-aligned");
+  static_assert(IlRegion<MODE, DEEP>::ENC % 1024 == 0, "decode slot must stay 1024-aligned");
+  static_assert(IlRegion<MODE, DEEP>::SMEM <= 232448, "interleaved kernel: shared memory over the 227 KB limit");
   constexpr int WC = VecMode<MODE>::WC;
+  constexpr int NW = IlShape<MODE, DEEP>::NW, NS = IlShape<MODE, DEEP>::NS;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  __shared__ uint64_t bars[kWarps];
+  __shared__ uint64_t bars[NW];
   uint8_t* base = align1024(smem_raw);
   pdl_entry();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* bar = bars + warp;
-  uint8_t* dslot = base + warp * IlRegion<MODE>::BYTES + IlRegion<MODE>::ENC;
+  uint8_t* dslot = base + warp * IlRegion<MODE, DEEP>::BYTES + IlRegion<MODE, DEEP>::ENC;
   if (lane == 0) mbar_init(bar, 1);
   fence_mbar_init();
   __syncwarp();
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * NW * 32;
   const WalkStep step = walk_step(g, G, stride);
-  Walk wd = walk_at(g, G, (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32 + lane);
+  Walk wd = walk_at(g, G, (static_cast<uint64_t>(blockIdx.x) * NW + warp) * 32 + lane);
   uint32_t phase = 0;
   bool pending = false;
   auto decode_pending = [&]() {
@@ -1312,8 +1331,9 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     }
     pending = true;
   };
-  encode_body<MODE, PTRS, NoHook, decltype(after_tile), kIlBulk>(g, src, cont, offsets, base, IlRegion<MODE>::BYTES,
-                                                                  NoHook{}, after_tile, &cmap);
+  encode_body<MODE, PTRS, NoHook, decltype(after_tile), kIlBulk, NW, NS>(g, src, cont, offsets, base,
+                                                                          IlRegion<MODE, DEEP>::BYTES, NoHook{}, after_tile,
+                                                                          &cmap);
   if (pending) decode_pending();
 }
 
@@ -1634,6 +1654,23 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
   return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
 
+template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP>
+cudaError_t rt_il_launch(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
+                         const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  constexpr size_t smem = IlRegion<MODE, DEEP>::SMEM;
+  constexpr int threads = IlShape<MODE, DEEP>::NW * 32;
+  auto kernel = k_roundtrip_il<MODE, O, PTRS, ONE_CTA, DEEP>;
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
+  if (ae != cudaSuccess) return ae;
+  const uint64_t items = g.chunks * (g.P / 16);
+  const int grid = grid_for(kernel, threads, smem, sms, items);
+  const cudaError_t le =
+      launch_k(kernel, grid, threads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
+  if (le != cudaSuccess) return le;
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // OPTB_RT_INTERLEAVE=0 selects the phase-ordered fused kernel for every mode
 // (A/B runs; the interleaved one is the default where it applies).
 bool rt_interleave_enabled() {
@@ -1649,17 +1686,15 @@ cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, voi
                      void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   if constexpr (!VecMode<MODE>::OFFS) {
     if (rt_interleave_enabled()) {
-      constexpr size_t smem = static_cast<size_t>(kWarps) * IlRegion<MODE>::BYTES + 1024;
-      auto kernel = k_roundtrip_il<MODE, O, PTRS, ONE_CTA>;
-      cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
-      if (ae != cudaSuccess) return ae;
-      const uint64_t items = g.chunks * (g.P / 16);
-      const int grid = grid_for(kernel, kThreads, smem, sms, items);
-      const cudaError_t le = launch_k(kernel, grid, kThreads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs,
-                                      e, out, err);
-      if (le != cudaSuccess) return le;
-      ++*launches;
-      return cudaGetLastError();
+      const uint64_t tiles = (g.chunks * (g.P / 16) + 31) / 32;
+      if constexpr (MODE == OPTB_EXACT128 && O == OPTB_OUT_U8) {
+        // >= 16 tiles per warp; OPTB_IL_SHAPE=deep|wide forces a shape (tests)
+        const char* f = getenv("OPTB_IL_SHAPE");
+        const bool deep = f && f[0] ? f[0] == 'd' : tiles >= static_cast<uint64_t>(16 * IlShape<MODE, true>::NW) * sms;
+        if (deep)
+          return rt_il_launch<MODE, O, PTRS, ONE_CTA, true>(cm, g, rs, cont, offs, e, out, err, s, sms, launches);
+      }
+      return rt_il_launch<MODE, O, PTRS, ONE_CTA, false>(cm, g, rs, cont, offs, e, out, err, s, sms, launches);
     }
   }
   constexpr size_t smem = static_cast<size_t>(kWarps) * RtRegion<MODE>::BYTES + 1024;

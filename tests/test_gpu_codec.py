@@ -244,6 +244,28 @@ def test_roundtrip_dev_vs_oracle(pkg, oracle_mod, torch_cuda, mode, per_chunk, P
     assert np.array_equal(got.view(want.dtype), want)
 
 
+@pytest.mark.parametrize("shape", ["deep", "wide"])
+@pytest.mark.parametrize("P,B,nb", [(3072, 512, 2), (3072, 100, 3), (768, 1000, 1), (3056, 33, 5)])
+def test_roundtrip_il_shapes_vs_oracle(pkg, oracle_mod, torch_cuda, monkeypatch, shape, P, B, nb):
+    """exact128 -> u8 runs the interleaved kernel in its deep (5 warps x 4
+    stages) or wide (8 x 2) shape by launch size; both shapes, forced, on
+    small and ragged geometries (warps with 0, 1 or a partial tile) == oracle."""
+    torch, C, O = torch_cuda, pkg.codec, oracle_mod
+    monkeypatch.setenv("OPTB_IL_SHAPE", shape)
+    rng = np.random.default_rng(P + B + nb)
+    n_ds = B * nb
+    ds = rng.integers(0, 256, size=(n_ds, P), dtype=np.uint8)
+    idx = rng.integers(0, n_ds, size=B * nb).astype(np.int64)
+    L = C.layout(1, 16, P, B, nb)
+    cont, offs = C.alloc_stream(L)
+    out = torch.empty((B * nb, P), dtype=torch.uint8, device="cuda")
+    C.roundtrip_dev(L, torch.from_numpy(ds).cuda(), cont, out, offsets=offs, row_index=torch.from_numpy(idx).cuda())
+    C.sync()
+    rc, _ = O.encode_stream(ds, idx, 1, 16, B, nb)
+    assert np.array_equal(cont.cpu().numpy()[: rc.size], rc)
+    assert np.array_equal(out.cpu().numpy(), ds[idx])
+
+
 def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
     """Vector geometries take the fused single launch (lossless with P % 512 == 0)."""
     torch, C = torch_cuda, pkg.codec
@@ -287,6 +309,40 @@ def test_roundtrip_dev_full_size_properties(pkg, torch_cuda, mode, pc):
     if offs is not None:
         ob = C.offsets_bytes(L)
         assert torch.equal(offs[:ob], offs2[:ob])
+
+
+@pytest.mark.parametrize("mode,pc,P,B,nb,dtype", [
+    (1, 16, 3056, 4001, 16, "uint8"),    # deep interleaved shape: partial chunks, partial last tile
+    (1, 16, 3072, 4096, 16, "bfloat16"),  # wide shape, float epilogue, full size
+    (0, 8, 3056, 4001, 16, "uint8"),
+    (2, 16, 3056, 4001, 16, "uint8"),
+])
+def test_roundtrip_dev_full_size_ragged(pkg, torch_cuda, mode, pc, P, B, nb, dtype):
+    """Interleaved round trip at full size with ragged geometry (P / 16 odd,
+    a one-image last chunk per batch, a partial last warp tile): the fused
+    launch's containers equal optb_encode_dev's and its decoded rows equal
+    optb_decode_dev's on those containers (the split launches are checked
+    against the oracle above)."""
+    torch, C = torch_cuda, pkg.codec
+    rows = B * nb
+    ds = torch.randint(0, 256, (rows, P), dtype=torch.uint8, device="cuda")
+    idx = torch.randint(0, rows, (rows,), device="cuda")
+    L = C.layout(mode, pc, P, B, nb)
+    dt = getattr(torch, dtype)
+    sc = float(SCALE) if dtype != "uint8" else 1.0
+    cont, offs = C.alloc_stream(L)
+    out = torch.empty((rows, P), dtype=dt, device="cuda")
+    C.roundtrip_dev(L, ds, cont, out, offsets=offs, row_index=idx, scale=sc)
+    cont2, offs2 = C.alloc_stream(L)
+    C.encode_dev(L, ds, cont2, offs2, row_index=idx)
+    out2 = torch.empty_like(out)
+    C.decode_dev(L, cont2, out2, offsets=offs2, scale=sc)
+    C.sync()
+    nbytes = C.container_bytes(L)
+    assert torch.equal(cont[:nbytes], cont2[:nbytes])
+    assert torch.equal(out.view(torch.uint8), out2.view(torch.uint8))
+    if dtype == "uint8" and pc <= C.capacity(mode):
+        assert torch.equal(out, ds[idx])
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])

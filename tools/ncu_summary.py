@@ -101,11 +101,16 @@ def main():
             "kernels": kern}
     json.dump(summ, open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w"), indent=1)
     step = {}
-    # the last fused-pipeline step of the launch list: its roundtrip launch and
-    # the SBS launches of the draw call that fed it
-    last_rt = max(i for i, (_, k, _) in enumerate(out) if k.startswith(("k_roundtrip_vec<exact128",
-                                                                         "k_roundtrip_il<exact128")))
-    for _, k, t in out[last_rt - 4:last_rt + 1]:
+    # the last draw call of the fused pipeline in the launch list: its SBS
+    # launches and the roundtrip launches (steps_per_draw of them) they fed
+    is_rt = [k.startswith(("k_roundtrip_vec<exact128", "k_roundtrip_il<exact128")) for _, k, _ in out]
+    last_rt = max(i for i, r in enumerate(is_rt) if r)
+    lo = last_rt
+    while lo > 0 and is_rt[lo - 1]:
+        lo -= 1
+    while lo > 0 and not is_rt[lo - 1]:
+        lo -= 1
+    for _, k, t in out[lo:last_rt + 1]:
         step[k] = step.get(k, 0) + t
     tot = sum(step.values())
     for k, t in sorted(step.items(), key=lambda x: -x[1]):

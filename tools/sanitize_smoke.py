@@ -65,17 +65,24 @@ def main():
         L = C.layout(mode, pc, P, B, nb)
         rc, ro = O.encode_stream(ds, idx, mode, pc, B, nb)
         ptrs = C.shard_row_ptrs_dev(idx_d, torch.tensor([ds_d.data_ptr()], dtype=torch.int64, device=dev), 64, P)
-        for dt in (torch.uint8, torch.float32, torch.bfloat16):
-            for rows_api in (False, True):
-                cont, offs = C.alloc_stream(L)
-                out = torch.empty((B * nb, P), dtype=dt, device=dev)
-                if rows_api:
-                    C.roundtrip_rows_dev(L, ptrs, cont, out, offsets=offs, scale=1 / 255)
-                else:
-                    C.roundtrip_dev(L, ds_d, cont, out, offsets=offs, row_index=idx_d, scale=1 / 255)
-                C.sync()
-                assert np.array_equal(cont.cpu().numpy()[: rc.size], rc)
-                n_checks += 1
+        # interleaved kernel in both shapes (exact128 -> u8 picks deep / wide
+        # by launch size; forced here)
+        for shape in ("wide", "deep") if mode == 1 else ("",):
+            os.environ["OPTB_IL_SHAPE"] = shape
+            for dt in (torch.uint8, torch.float32, torch.bfloat16):
+                for rows_api in (False, True):
+                    cont, offs = C.alloc_stream(L)
+                    out = torch.empty((B * nb, P), dtype=dt, device=dev)
+                    if rows_api:
+                        C.roundtrip_rows_dev(L, ptrs, cont, out, offsets=offs, scale=1 / 255)
+                    else:
+                        C.roundtrip_dev(L, ds_d, cont, out, offsets=offs, row_index=idx_d, scale=1 / 255)
+                    C.sync()
+                    assert np.array_equal(cont.cpu().numpy()[: rc.size], rc)
+                    if dt == torch.uint8 and pc <= C.capacity(mode):
+                        assert np.array_equal(out.cpu().numpy(), ds[idx])
+                    n_checks += 1
+        os.environ.pop("OPTB_IL_SHAPE", None)
     labels = (np.arange(3000) % 7).astype(np.int32)
     offs_d, mem_d = S.class_index_dev(labels, 7)
     p = S.plan([1 / 7] * 7, 21, 5)
