@@ -492,6 +492,11 @@ __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> byte
 // warp_region: bytes of shared memory per warp (its ring), >= kStages * slot;
 // the fused kernel gives both bodies the same per-warp region so that a warp
 // in one phase never touches another warp's ring in the other phase.
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  const uint32_t a = smem_u32(p);
+  return p + (((a + 1023u) & ~1023u) - a);
+}
+
 struct NoHook {
   __device__ void operator()(int, bool) const {}
 };
@@ -782,6 +787,10 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
     stage = (stage + 1) % NS;
   }
   cp_async_wait<0>();
+  if constexpr (BULK) {  // the slots stay allocated until the stores have read them
+    if (lane == 0) bulk_wait0();
+    __syncwarp();
+  }
 }
 
 template <int MODE, bool PTRS>
@@ -790,6 +799,18 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   pdl_entry();
   encode_body<MODE, PTRS>(g, src, cont, offsets, smem_raw);
+}
+
+// Exact and f64 encode with the container tiles leaving as bulk tensor
+// stores (one per tile, issued by lane 0) instead of per-lane stores.
+template <int MODE, bool PTRS>
+__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+    k_encode_bulk(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
+                  uint8_t* __restrict__ offsets) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  pdl_entry();
+  encode_body<MODE, PTRS, NoHook, NoTileHook, true>(g, src, cont, offsets, align1024(smem_raw),
+                                                    kStages * VecMode<MODE>::ENC_SLOT, NoHook{}, NoTileHook{}, &cmap);
 }
 
 // ------------------------------------------------------------------ K2 / K4
@@ -819,10 +840,6 @@ struct DecSlot {
   static constexpr int TMA = (RAW + 1023) / 1024 * 1024;
 };
 
-__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  const uint32_t a = smem_u32(p);
-  return p + (((a + 1023u) & ~1023u) - a);
-}
 
 // One tile of the decode: the container words of items wc.t .. wc.t + 31
 // (lane L: item wc.t + L) are in the warp's slot (TMA: the 128B-swizzled box;
@@ -1569,9 +1586,33 @@ cudaError_t dec_generic(const Geom& g, const void* cont, const uint8_t* offs, co
   return cudaGetLastError();
 }
 
+bool container_map(CUtensorMap* m, const void* cont, uint64_t bytes, int wc);
+// OPTB_ENCODE_BULK=0 selects the per-lane container stores (A/B runs)
+bool encode_bulk_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("OPTB_ENCODE_BULK");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 template <int MODE, bool PTRS>
 cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
                       uint64_t* launches) {
+  if constexpr (!VecMode<MODE>::OFFS) {
+    CUtensorMap cm;
+    if (encode_bulk_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC)) {
+      const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT + 1024;
+      auto kernel = k_encode_bulk<MODE, PTRS>;
+      cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
+      if (ae != cudaSuccess) return ae;
+      const uint64_t items = g.chunks * (g.P / 16);
+      const int grid = grid_for(kernel, kThreads, smem, sms, items);
+      const cudaError_t le = launch_k(kernel, grid, kThreads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs);
+      ++*launches;
+      return le;
+    }
+  }
   const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
   cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_encode_vec<MODE, PTRS>), static_cast<int>(smem));
   if (ae != cudaSuccess) return ae;
