@@ -437,13 +437,14 @@ def main():
     fused = pipe.fused
     if fused and statistics.mean(t_dec) > 0.005:
         raise RuntimeError("pipeline reported separate decode launches on the fused path")
-    # The fused launch for exact128 is the interleaved kernel (k_roundtrip_il,
-    # unless OPTB_RT_INTERLEAVE=0 -- mirrors rt_interleave_enabled() in
-    # codec_impl.cuh): each container tile is read back while still in L2, so
-    # its HBM bytes are the compulsory ones -- gathered rows + row ids in,
-    # containers + decoded rows out.  The SURVEY 8(d) figure (which also
-    # counts the container re-read) is reported beside it.
-    interleaved = fused and os.environ.get("OPTB_RT_INTERLEAVE", "1") != "0"
+    # The fused launch for exact128 is the interleaved kernel (k_roundtrip_il;
+    # the library reports which kernel the last step ran): each container
+    # tile is read back while still in L2, so its HBM bytes are the
+    # compulsory ones -- gathered rows + row ids in, containers + decoded rows
+    # out.  The SURVEY 8(d) figure (which also counts the container re-read)
+    # is reported beside it.
+    rt_kind = C.last_roundtrip_kind()
+    interleaved = fused and rt_kind.startswith("interleaved")
     l2_bytes = 0
     if interleaved:
         kname, kms, kbytes = "k_roundtrip_il<exact128,u8>", enc_ms, enc_bytes + rows * P
@@ -462,7 +463,7 @@ def main():
             if kn == kname or kn.startswith(kname[:-1] + ","):
                 traffic = kv.get("dram_bytes_per_launch")
                 break
-    roofline = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+    roofline = {"bound": "hbm", "kernel": kname, "kernel_kind": rt_kind, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
                 "frac_of_spec_8tbs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": kbytes,
@@ -557,13 +558,14 @@ def main():
                 ms7 = coll_reduce_ms(torch, dist, ms7)
             k7 = statistics.mean(pipe7.timings(k)[1] for k in range(args.warmup, args.warmup + args.split_steps)
                                  if k % t7 == 0)
+            il7 = C.last_roundtrip_kind().startswith("interleaved")
             pipe7.close()
         cb7 = C.container_bytes(C.layout(0, 8, P, BATCH, BATCHES_PER_STEP))
         # HBM bytes: rows in, containers out, rows out (+ the container
         # re-read for the phase-ordered kernel; interleaved: an L2 hit)
-        b7 = 2 * rows * P + cb7 + rows * 8 + (0 if interleaved else cb7)
+        b7 = 2 * rows * P + cb7 + rows * 8 + (0 if il7 else cb7)
         exact64 = {"mode": "exact64", "per_chunk": 8, "ms_per_step": round(ms7, 4),
-                   "kernel": "k_roundtrip_il<exact64,u8>" if interleaved else "k_roundtrip_vec<exact64,u8>",
+                   "kernel": "k_roundtrip_il<exact64,u8>" if il7 else "k_roundtrip_vec<exact64,u8>",
                    "value": round(images_per_step / (ms7 / 1e3), 1), "kernel_ms": round(k7, 4),
                    "kernel_gbs": round(b7 / (k7 / 1e3) / 1e9, 1), "kernel_frac": round(b7 / (k7 / 1e3) / 1e9 / peak, 4)}
 

@@ -146,10 +146,12 @@ int optb_decode_dev(optb_ctx* ctx, const optb_layout* L, const void* containers,
 
 /* optb_encode_dev followed by optb_decode_dev of the same stream (same
  * results, containers and offsets materialised as by the two calls): one
- * persistent launch on the vector path (lossless modes: pixels % 512 == 0; each
- * warp encodes its tiles, then decodes them back from HBM), otherwise the two
- * launches.  The E-D pipeline step (pipeline.cpp:197-216 encode +
- * runner.cpp:292-309 decode) uses it. */
+ * persistent launch on the vector path (lossless modes: pixels % 512 == 0),
+ * otherwise the two launches.  Exact / f64 modes: each warp decodes a tile one
+ * iteration after storing it, so the container re-read is served from L2
+ * (interleaved kernel); lossless: each warp encodes all its tiles, then decodes
+ * them back (phase-ordered kernel).  The E-D pipeline step
+ * (pipeline.cpp:197-216 encode + runner.cpp:292-309 decode) uses it. */
 int optb_roundtrip_dev(optb_ctx* ctx, const optb_layout* L, const uint8_t* images,
                        uint64_t row_stride, const int64_t* row_index, void* containers,
                        uint8_t* offsets, const optb_epilogue* E, void* out, void* stream);
@@ -253,6 +255,18 @@ int optb_owner_labels_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, ui
 int optb_shard_row_ptrs_dev(optb_ctx* ctx, const int64_t* examples, uint64_t n, const uint64_t* bases,
                             uint32_t n_shards, uint64_t rows_per_shard, uint64_t row_stride,
                             uint64_t* row_ptrs, void* stream);
+/* Which kernel the calling thread's most recent optb_roundtrip_dev /
+ * optb_roundtrip_rows_dev / pipeline step ran (no reference counterpart: for
+ * the caller's byte accounting -- the interleaved kernels read the containers
+ * back from L2, not HBM). */
+#define OPTB_RT_NONE 0
+#define OPTB_RT_SPLIT 1            /* optb_encode_dev + optb_decode_dev launches */
+#define OPTB_RT_PHASE_ORDERED 2    /* k_roundtrip_vec */
+#define OPTB_RT_INTERLEAVED 3      /* k_roundtrip_il, 8 warps x 2 stages */
+#define OPTB_RT_INTERLEAVED_DEEP 4 /* k_roundtrip_il, 5 warps x 4 stages */
+#define OPTB_RT_INTERLEAVED_LANE_ST 5 /* k_roundtrip_il, 8 x 2, per-lane container stores */
+int optb_last_roundtrip_kind(void);
+
 /* optb_encode_dev / optb_roundtrip_dev reading stream row r from the absolute
  * device-accessible address row_ptrs[r] (device array): this GPU's HBM, a
  * peer GPU's HBM opened with optb_ipc_open, or mapped pinned host memory.

@@ -81,6 +81,7 @@ SIGNATURES = {
     "optb_encode_dev": (ct.c_int, [vp, LP, vp, ct.c_uint64, vp, vp, vp, vp]),
     "optb_decode_dev": (ct.c_int, [vp, LP, vp, vp, EP, vp, vp]),
     "optb_roundtrip_dev": (ct.c_int, [vp, LP, vp, ct.c_uint64, vp, vp, vp, EP, vp, vp]),
+    "optb_last_roundtrip_kind": (ct.c_int, []),
     "optb_encode_host": (ct.c_int, [vp, LP, vp, vp, vp]),
     "optb_decode_host": (ct.c_int, [vp, LP, vp, vp, EP, vp]),
     "optb_sbs_plan": (ct.c_int, [f64p, ct.c_uint64, ct.c_uint64, u64p]),

@@ -283,6 +283,31 @@ def roundtrip_dev(L: Layout, images, containers, out, offsets=None, row_index=No
                                  _stream(stream, dev)))
 
 
+RT_KINDS = {0: "none", 1: "split", 2: "phase_ordered", 3: "interleaved", 4: "interleaved_deep",
+            5: "interleaved_lane_st"}
+
+
+def last_roundtrip_kind() -> str:
+    """Kernel of this thread's most recent roundtrip_dev / pipeline step
+    (optb_last_roundtrip_kind): "split" (two launches), "phase_ordered",
+    "interleaved", "interleaved_deep" or "interleaved_lane_st".  The interleaved kernels read the
+    containers back from L2, so their HBM bytes exclude the container re-read."""
+    return RT_KINDS[lib.optb_last_roundtrip_kind()]
+
+
+def roundtrip_hbm_bytes(L: Layout, out_elem_size: int, gathered: bool) -> int:
+    """HBM bytes of one round trip of layout L by the kernel that last ran:
+    rows in (+ 8 B row ids when gathered), containers (+ parity planes) out,
+    decoded rows out, and the container (+ plane) re-read unless the
+    interleaved kernel served it from L2 (SURVEY 8(d) per-image figures)."""
+    rows = L.batch * L.n_batches
+    cb, ob = container_bytes(L), offsets_bytes(L)
+    b = rows * L.pixels + cb + ob + (rows * 8 if gathered else 0) + rows * L.pixels * out_elem_size
+    if not last_roundtrip_kind().startswith("interleaved"):
+        b += cb + ob
+    return b
+
+
 def encode_rows_dev(L: Layout, row_ptrs, containers, offsets=None, aligned16: bool = True, stream=None):
     """Gather-encode from absolute row addresses (optb_encode_rows_dev):
     stream row r packs the P bytes at row_ptrs[r] (int64 device tensor of

@@ -431,6 +431,8 @@ int optb_roundtrip_rows_dev(optb_ctx* c, const optb_layout* L, const uint64_t* r
                    stream);
 }
 
+int optb_last_roundtrip_kind(void) { return optb_b200::g_rt_kind; }
+
 int optb_synth_pixels_dev(optb_ctx* c, uint64_t seed, uint64_t first_row, uint64_t n_rows,
                           uint64_t pixels, uint8_t* out, uint64_t row_stride, void* stream) {
   if (!c || !out) return set_err(OPTB_ERR_ARG, "synth: null");

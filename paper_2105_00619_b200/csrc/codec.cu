@@ -69,8 +69,11 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
   }
 }
 
+thread_local int g_rt_kind = OPTB_RT_NONE;
+
 cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rs, void* containers, uint8_t* offsets, const Epi& e,
                              void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  g_rt_kind = OPTB_RT_SPLIT;  // unless a fused launcher below takes it
   const int es = e.dtype == OPTB_OUT_U8 ? 1 : e.dtype == OPTB_OUT_F32 ? 4 : 2;
   const bool vec = vec_ok(g) && rows_vec_ok(rs) && aligned16(containers) && aligned16(out) &&
                    (e.row_stride * es) % 16 == 0;

@@ -1281,10 +1281,6 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
 // decode's container read is an L2 hit (ncu: dram bytes = the compulsory
 // 3 x ~153 MB instead of 4x).  Same per-warp tile sequence as the phase-
 // ordered kernel above, so the results are identical.
-#ifndef OPTB_IL_BULK
-#define OPTB_IL_BULK 1
-#endif
-constexpr bool kIlBulk = OPTB_IL_BULK != 0;  // bulk tensor stores of the container tiles
 
 // Warps per CTA and input-ring depth of the interleaved kernel (one CTA per
 // SM).  DEEP: 5 warps x 4 stages -- fewer warps with deeper rings keep more
@@ -1308,7 +1304,7 @@ struct IlRegion {
   static constexpr uint32_t BYTES = ENC + DecSlot<MODE>::TMA;
   static constexpr size_t SMEM = static_cast<size_t>(IlShape<MODE, DEEP>::NW) * BYTES + 1024;
 };
-template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP>
+template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP, bool BULK_ST>
 __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
@@ -1318,7 +1314,7 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   // a bulk store); the parity bits come with the words, as NI 64-byte bulk
   // copies on the same mbarrier (P % 512 == 0: a tile lies in one chunk and
   // image i's 512 bits are 64 contiguous, 64-aligned plane bytes)
-  constexpr bool BULK = kIlBulk && !S::OFFS;
+  constexpr bool BULK = BULK_ST && !S::OFFS;
   static_assert(IlRegion<MODE, DEEP>::SMEM <= 232448, "interleaved kernel: shared memory over the 227 KB limit");
   constexpr int WC = VecMode<MODE>::WC;
   constexpr int NW = IlShape<MODE, DEEP>::NW, NS = IlShape<MODE, DEEP>::NS;
@@ -1719,12 +1715,12 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
   return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
 
-template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP>
+template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP, bool BULK_ST = true>
 cudaError_t rt_il_launch(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
                          const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   constexpr size_t smem = IlRegion<MODE, DEEP>::SMEM;
   constexpr int threads = IlShape<MODE, DEEP>::NW * 32;
-  auto kernel = k_roundtrip_il<MODE, O, PTRS, ONE_CTA, DEEP>;
+  auto kernel = k_roundtrip_il<MODE, O, PTRS, ONE_CTA, DEEP, BULK_ST>;
   cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
@@ -1733,17 +1729,15 @@ cudaError_t rt_il_launch(const CUtensorMap& cm, const Geom& g, const RowSrc& rs,
       launch_k(kernel, grid, threads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs, e, out, err);
   if (le != cudaSuccess) return le;
   ++*launches;
+  g_rt_kind = DEEP ? OPTB_RT_INTERLEAVED_DEEP : BULK_ST ? OPTB_RT_INTERLEAVED : OPTB_RT_INTERLEAVED_LANE_ST;
   return cudaGetLastError();
 }
 
 // OPTB_RT_INTERLEAVE=0 selects the phase-ordered fused kernel for every mode
 // (A/B runs; the interleaved one is the default where it applies).
-bool rt_interleave_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("OPTB_RT_INTERLEAVE");
-    return !(v && v[0] == '0');
-  }();
-  return on;
+bool rt_interleave_enabled() {  // read per call (probes switch it at run time)
+  const char* v = getenv("OPTB_RT_INTERLEAVE");
+  return !(v && v[0] == '0');
 }
 
 template <int MODE, int O, bool PTRS, bool ONE_CTA>
@@ -1753,12 +1747,24 @@ cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, voi
   // bulk copies beside the words' TMA load) measured slower for these
   // integer-pipe-bound modes (C3 n=9: 138 -> 174 us, n=18: 148 -> 164 us)
   if constexpr (!VecMode<MODE>::OFFS) {
+    const uint64_t tiles = (g.chunks * (g.P / 16) + 31) / 32;
+    const char* f = getenv("OPTB_IL_SHAPE");  // deep | wide: force a shape (tests, probes)
+    const bool forced = f && f[0];
+    // float outputs from 3 tiles per warp: per-lane container stores instead
+    // of bulk stores (the epilogue's longer decode leaves the per-lane stores
+    // time to drain, while a bulk store must complete before the warp
+    // reloads its tile: C4 bf16 one batch per launch 32.8 -> 31.9 us, 8 per
+    // launch 232 -> 229 us; tools/il_probe.py).  OPTB_IL_BULK=0|1 forces it.
+    const double per_warp = static_cast<double>(tiles) / (IlShape<MODE, false>::NW * static_cast<double>(sms));
+    const char* fb = getenv("OPTB_IL_BULK");
+    const bool lane_st = fb && fb[0] ? fb[0] == '0' : (O != OPTB_OUT_U8 && per_warp >= 3.0);
     if (rt_interleave_enabled()) {
-      const uint64_t tiles = (g.chunks * (g.P / 16) + 31) / 32;
+      if (lane_st && !(forced && f[0] == 'd'))
+        return rt_il_launch<MODE, O, PTRS, ONE_CTA, false, false>(cm, g, rs, cont, offs, e, out, err, s, sms,
+                                                                  launches);
       if constexpr (MODE == OPTB_EXACT128 && O == OPTB_OUT_U8) {
-        // >= 16 tiles per warp; OPTB_IL_SHAPE=deep|wide forces a shape (tests)
-        const char* f = getenv("OPTB_IL_SHAPE");
-        const bool deep = f && f[0] ? f[0] == 'd' : tiles >= static_cast<uint64_t>(16 * IlShape<MODE, true>::NW) * sms;
+        // deep shape from 12 tiles per warp (il_probe: the shapes tie at ~12)
+        const bool deep = forced ? f[0] == 'd' : tiles >= static_cast<uint64_t>(12 * IlShape<MODE, true>::NW) * sms;
         if (deep)
           return rt_il_launch<MODE, O, PTRS, ONE_CTA, true>(cm, g, rs, cont, offs, e, out, err, s, sms, launches);
       }
@@ -1775,6 +1781,7 @@ cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, voi
                                   out, err);
   if (le != cudaSuccess) return le;
   ++*launches;
+  g_rt_kind = OPTB_RT_PHASE_ORDERED;
   return cudaGetLastError();
 }
 

@@ -16,6 +16,10 @@ namespace optb_b200 {
 // different devices may share one process.
 cudaError_t ensure_smem_attr(const void* kernel, int bytes);
 
+// Which kernel the most recent fused round trip of this thread ran
+// (OPTB_RT_* in optb_cuda.h); set by launch_roundtrip's launchers.
+extern thread_local int g_rt_kind;
+
 // Sets the calling thread's optb_last_error() text; returns `code`.
 int set_error_text(int code, const std::string& message);
 

@@ -280,8 +280,16 @@ def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
         C.roundtrip_dev(L, ds, cont, out, offsets=offs)
         C.sync()
         assert pkg._lib.launches(0) - n0 == launches, mode
+        assert C.last_roundtrip_kind() == ("phase_ordered" if mode >= 3 else "interleaved"), mode
         if pc <= C.capacity(mode):
             assert torch.equal(out, ds)
+    # off the vector path: two launches
+    L = C.layout(1, 16, 108, 40, 2)
+    cont, offs = C.alloc_stream(L)
+    C.roundtrip_dev(L, torch.randint(0, 256, (80, 108), dtype=torch.uint8, device="cuda"), cont,
+                    torch.empty((80, 108), dtype=torch.uint8, device="cuda"))
+    C.sync()
+    assert C.last_roundtrip_kind() == "split"
 
 
 @pytest.mark.parametrize("mode,pc", [(3, 9), (4, 18), (2, 6), (0, 8), (1, 16)])

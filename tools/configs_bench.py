@@ -76,6 +76,8 @@ def main():
             t_rt = timeit(lambda: C.roundtrip_dev(L, src, cont, out, offsets=offs, row_index=idx, scale=scale,
                                                   stream=s), s)
             C.sync(0, s)
+            rt_kind = C.last_roundtrip_kind()
+            rt_b = C.roundtrip_hbm_bytes(L, out.element_size(), gather)
         cb, ob = C.container_bytes(L), C.offsets_bytes(L)
         es = out.element_size()
         enc_b = rows * P + cb + ob + (rows * 8 if gather else 0)
@@ -90,9 +92,7 @@ def main():
              "roundtrip_fused": P % 16 == 0 and (mode in (0, 1, 2) or P % 512 == 0)}
         # interleaved fused kernel (exact / f64): the container re-read is an
         # L2 hit, the HBM bytes are rows in + containers and rows out
-        il = r["roundtrip_fused"] and mode in (0, 1, 2) and os.environ.get("OPTB_RT_INTERLEAVE", "1") != "0"
-        rt_b = enc_b + rows * P * es if il else enc_b + dec_b
-        r.update({"roundtrip_interleaved": il, "roundtrip_hbm_bytes": rt_b,
+        r.update({"roundtrip_kernel": rt_kind, "roundtrip_hbm_bytes": rt_b,
                   "roundtrip_frac": round(rt_b / t_rt / 1e9 / pk, 3)})
         res[name] = r
         del src, cont, out
@@ -131,13 +131,14 @@ def main():
         t_split = timeit(lambda: one(False), s, reps=16, warm=8)
         t_fused = timeit(lambda: one(True), s, reps=16, warm=8)
         C.sync(0, s)
-    # rows read + containers written (+ read back: split launches only) + bf16 out
-    b4_split = 256 * IMG * 5
-    b4 = 256 * IMG * (4 if os.environ.get("OPTB_RT_INTERLEAVE", "1") != "0" else 5)
+        k4 = C.last_roundtrip_kind()
+        b4 = C.roundtrip_hbm_bytes(L4, 2, False)
+    b4_split = 256 * IMG * 5  # rows read + containers written and read back + bf16 out
     res["C4_per_batch_bf16"] = {"images_per_launch": 256, "split_us": round(t_split * 1e6, 1),
                                 "fused_us": round(t_fused * 1e6, 1),
                                 "images_per_s_split": round(256 / t_split, 1),
                                 "images_per_s_fused": round(256 / t_fused, 1),
+                                "fused_kernel": k4,
                                 "split_frac": round(b4_split / t_split / 1e9 / pk, 3),
                                 "fused_frac": round(b4 / t_fused / 1e9 / pk, 3)}
     del bat
