@@ -811,14 +811,44 @@ __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
 
 // Exact and f64 encode with the container tiles leaving as bulk tensor
 // stores (one per tile, issued by lane 0) instead of per-lane stores.
-template <int MODE, bool PTRS>
-__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+// Warps per CTA and ring depth of the separate encode / decode launches
+// (configs_bench sweep over 8x2, 6x3, 5x4, 4x5): the bulk-store encode runs
+// 6 warps x 3 stages (C3 n=16 72.6 -> 68.6 us, f64 90.1 -> 79.9, C4 108.5 ->
+// 99.3); the decode 8 x 2, except exact128 into float outputs at 4 warps x 5
+// stages (C4 bf16 174 -> 154 us).  OPTB_SPLIT_WARPS / OPTB_SPLIT_STAGES
+// override both (tuning builds).
+template <int NW_, int NS_, int MODE>
+struct ShapeT {
+#if defined(OPTB_SPLIT_WARPS) && defined(OPTB_SPLIT_STAGES)
+  static constexpr int NW = OPTB_SPLIT_WARPS, NS = OPTB_SPLIT_STAGES;
+#else
+  static constexpr int NW = NW_, NS = NS_;
+#endif
+  static constexpr int MIN_BLOCKS = NW == kWarps && NS == kStages ? VecMode<MODE>::MIN_BLOCKS : 1;
+};
+// DEEP: the shape for long launches (>= 12 tiles per warp at 8 warps per
+// SM); short launches keep 8 x 2 (one 256-image ImageNet batch: 42.0 ->
+// 35.8 us for the pair).
+template <int MODE, bool DEEP>
+struct EncShape : ShapeT<DEEP ? 6 : kWarps, DEEP ? 3 : kStages, MODE> {};
+template <int MODE, int O, bool DEEP>
+struct DecShape : ShapeT<(DEEP && MODE == OPTB_EXACT128 && O != OPTB_OUT_U8) ? 4 : kWarps,
+                         (DEEP && MODE == OPTB_EXACT128 && O != OPTB_OUT_U8) ? 5 : kStages, MODE> {};
+inline bool split_deep(const Geom& g, int sms) {
+  const uint64_t tiles = (g.chunks * (g.P / 16) + 31) / 32;
+  return tiles >= static_cast<uint64_t>(12 * kWarps) * sms;
+}
+
+template <int MODE, bool PTRS, bool DEEP>
+__global__ void __launch_bounds__(EncShape<MODE, DEEP>::NW * 32, EncShape<MODE, DEEP>::MIN_BLOCKS)
     k_encode_bulk(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                   uint8_t* __restrict__ offsets) {
+  constexpr int NW = EncShape<MODE, DEEP>::NW, NS = EncShape<MODE, DEEP>::NS;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   pdl_entry();
-  encode_body<MODE, PTRS, NoHook, NoTileHook, true>(g, src, cont, offsets, align1024(smem_raw),
-                                                    kStages * VecMode<MODE>::ENC_SLOT, NoHook{}, NoTileHook{}, &cmap);
+  encode_body<MODE, PTRS, NoHook, NoTileHook, true, NW, NS>(g, src, cont, offsets, align1024(smem_raw),
+                                                            NS * VecMode<MODE>::ENC_SLOT, NoHook{}, NoTileHook{},
+                                                            &cmap);
 }
 
 // ------------------------------------------------------------------ K2 / K4
@@ -1063,7 +1093,7 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
 
 // start_stage / prefetched: the fused kernel may have issued the warp's first
 // tile already (into start_stage, mbarriers initialised by the caller).
-template <int MODE, int O, bool TMA>
+template <int MODE, int O, bool TMA, int NW = kWarps, int NS = kStages>
 __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom& g, const uint8_t* __restrict__ cont,
                                             const uint8_t* __restrict__ offsets, const Epi& e,
                                             void* __restrict__ out, DevError* err, uint8_t* smem_base,
@@ -1073,16 +1103,16 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
   constexpr int WC = S::WC;
   constexpr int SLOT = TMA ? DecSlot<MODE>::TMA : DecSlot<MODE>::RAW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* ring = smem_base + warp * (warp_region ? warp_region : kStages * SLOT);
-  uint64_t* bar = bars + warp * kStages;
+  uint8_t* ring = smem_base + warp * (warp_region ? warp_region : NS * SLOT);
+  uint64_t* bar = bars + warp * NS;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps * 32;
-  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * kWarps + warp) * 32;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * NW * 32;
+  const uint64_t first = (static_cast<uint64_t>(blockIdx.x) * NW + warp) * 32;
   if constexpr (TMA) {
     if (!prefetched) {
       if (lane == 0)
-        for (int st = 0; st < kStages; ++st) mbar_init(bar + st, 1);
+        for (int st = 0; st < NS; ++st) mbar_init(bar + st, 1);
       fence_mbar_init();
       __syncwarp();
     }
@@ -1159,33 +1189,35 @@ __device__ __forceinline__ void decode_body(const CUtensorMap* cmap, const Geom&
 
   if (!prefetched) {
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) issue(first + s * stride, s);
+    for (int s = 0; s < NS - 1; ++s) issue(first + s * stride, s);
   }
   int stage = start_stage;
   uint32_t phase_bits = 0;  // parity of each stage's mbarrier
   for (uint64_t base = first; base < items; base += stride) {
-    issue(base + (kStages - 1) * stride, (stage + kStages - 1) % kStages);
+    issue(base + (NS - 1) * stride, (stage + NS - 1) % NS);
     if constexpr (TMA) mbar_wait(bar + stage, (phase_bits >> stage) & 1u);
     if constexpr (!TMA || S::OFFS) {
-      cp_async_wait<kStages - 1>();
+      cp_async_wait<NS - 1>();
       __syncwarp();
     }
     decode_tile<MODE, O, TMA>(g, wc, items, ring + stage * SLOT, e, out, err);
     walk_advance(wc, step, g, G);
     phase_bits ^= 1u << stage;
-    if (++stage == kStages) stage = 0;
+    if (++stage == NS) stage = 0;
   }
   if constexpr (!TMA || S::OFFS) cp_async_wait<0>();
 }
 
-template <int MODE, int O, bool TMA>
-__global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
+template <int MODE, int O, bool TMA, bool DEEP>
+__global__ void __launch_bounds__(DecShape<MODE, O, DEEP>::NW * 32, DecShape<MODE, O, DEEP>::MIN_BLOCKS)
     k_decode_vec(const __grid_constant__ CUtensorMap cmap, Geom g, const uint8_t* __restrict__ cont,
                  const uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
+  constexpr int NW = DecShape<MODE, O, DEEP>::NW, NS = DecShape<MODE, O, DEEP>::NS;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  __shared__ uint64_t bars[TMA ? kWarps * kStages : 1];
+  __shared__ uint64_t bars[TMA ? NW * NS : 1];
   pdl_entry();
-  decode_body<MODE, O, TMA>(&cmap, g, cont, offsets, e, out, err, TMA ? align1024(smem_raw) : smem_raw, bars);
+  decode_body<MODE, O, TMA, NW, NS>(&cmap, g, cont, offsets, e, out, err, TMA ? align1024(smem_raw) : smem_raw,
+                                    bars);
 }
 
 // ------------------------------------------------------------------ K1+K2 fused
@@ -1616,21 +1648,30 @@ bool encode_bulk_enabled() {
   return on;
 }
 
+template <int MODE, bool PTRS, bool DEEP>
+cudaError_t enc_bulk_launch(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs,
+                            cudaStream_t s, int sms, uint64_t* launches) {
+  constexpr int threads = EncShape<MODE, DEEP>::NW * 32;
+  const size_t smem = static_cast<size_t>(EncShape<MODE, DEEP>::NW) * EncShape<MODE, DEEP>::NS *
+                          VecMode<MODE>::ENC_SLOT + 1024;
+  auto kernel = k_encode_bulk<MODE, PTRS, DEEP>;
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
+  if (ae != cudaSuccess) return ae;
+  const uint64_t items = g.chunks * (g.P / 16);
+  const int grid = grid_for(kernel, threads, smem, sms, items);
+  const cudaError_t le = launch_k(kernel, grid, threads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs);
+  ++*launches;
+  return le;
+}
+
 template <int MODE, bool PTRS>
 cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
                       uint64_t* launches) {
   if constexpr (!VecMode<MODE>::OFFS) {
     CUtensorMap cm;
     if (encode_bulk_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC)) {
-      const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT + 1024;
-      auto kernel = k_encode_bulk<MODE, PTRS>;
-      cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(smem));
-      if (ae != cudaSuccess) return ae;
-      const uint64_t items = g.chunks * (g.P / 16);
-      const int grid = grid_for(kernel, kThreads, smem, sms, items);
-      const cudaError_t le = launch_k(kernel, grid, kThreads, smem, s, cm, g, rs, static_cast<uint8_t*>(cont), offs);
-      ++*launches;
-      return le;
+      if (split_deep(g, sms)) return enc_bulk_launch<MODE, PTRS, true>(cm, g, rs, cont, offs, s, sms, launches);
+      return enc_bulk_launch<MODE, PTRS, false>(cm, g, rs, cont, offs, s, sms, launches);
     }
   }
   const size_t smem = static_cast<size_t>(kWarps) * kStages * VecMode<MODE>::ENC_SLOT;
@@ -1690,16 +1731,17 @@ bool tma_decode_enabled() {
   return on;
 }
 
-template <int MODE, int O, bool TMA>
+template <int MODE, int O, bool TMA, bool DEEP>
 cudaError_t dec_vec_launch(const CUtensorMap& cm, const Geom& g, const void* cont, const uint8_t* offs,
                            const Epi& e, void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  const size_t smem = TMA ? static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::TMA + 1024
-                          : static_cast<size_t>(kWarps) * kStages * DecSlot<MODE>::RAW;
-  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_decode_vec<MODE, O, TMA>), static_cast<int>(smem));
+  constexpr int NW = DecShape<MODE, O, DEEP>::NW, NS = DecShape<MODE, O, DEEP>::NS;
+  const size_t smem = TMA ? static_cast<size_t>(NW) * NS * DecSlot<MODE>::TMA + 1024
+                          : static_cast<size_t>(NW) * NS * DecSlot<MODE>::RAW;
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_decode_vec<MODE, O, TMA, DEEP>), static_cast<int>(smem));
   if (ae != cudaSuccess) return ae;
   const uint64_t items = g.chunks * (g.P / 16);
-  const int grid = grid_for(k_decode_vec<MODE, O, TMA>, kThreads, smem, sms, items);
-  const cudaError_t le = launch_k(k_decode_vec<MODE, O, TMA>, grid, kThreads, smem, s, cm, g,
+  const int grid = grid_for(k_decode_vec<MODE, O, TMA, DEEP>, NW * 32, smem, sms, items);
+  const cudaError_t le = launch_k(k_decode_vec<MODE, O, TMA, DEEP>, grid, NW * 32, smem, s, cm, g,
                                   static_cast<const uint8_t*>(cont), offs, e, out, err);
   ++*launches;
   return le;
@@ -1710,9 +1752,10 @@ cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const 
                     DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   CUtensorMap cm;
   if (tma_decode_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
-    return dec_vec_launch<MODE, O, true>(cm, g, cont, offs, e, out, err, s, sms, launches);
+    return split_deep(g, sms) ? dec_vec_launch<MODE, O, true, true>(cm, g, cont, offs, e, out, err, s, sms, launches)
+                              : dec_vec_launch<MODE, O, true, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
   memset(&cm, 0, sizeof cm);
-  return dec_vec_launch<MODE, O, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
+  return dec_vec_launch<MODE, O, false, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
 }
 
 template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP, bool BULK_ST = true>
