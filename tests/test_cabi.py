@@ -56,6 +56,20 @@ def test_metadata(pkg):
     assert pkg._lib.lib.optb_layout_rows(ct.byref(L)) == 300
 
 
+def test_roundtrip_kind_constants(pkg):
+    """codec.RT_KINDS mirrors the OPTB_RT_* kernel kinds of the header, and the
+    byte accounting counts the container re-read only for the kernels that
+    read it from HBM; no round trip has run in this (CPU) process."""
+    src = open(HEADER).read()
+    consts = {int(v): n for n, v in re.findall(r"#define OPTB_RT_(\w+) (\d+)", src)}
+    C = pkg.codec
+    assert {k: v.lower() for k, v in consts.items()} == C.RT_KINDS
+    assert C.last_roundtrip_kind() == "none"
+    L = C.layout(1, 16, 3072, 512, 97)
+    rows, cb = 512 * 97, C.container_bytes(L)
+    assert C.roundtrip_hbm_bytes(L, 1, True) == rows * 3072 * 2 + rows * 8 + 2 * cb  # "none": as two launches
+
+
 def test_layout_check_messages(pkg):
     lib = pkg._lib.lib
     cases = [((0, 9, 10, 10, 1), 3, "encode: 9 images exceed exact64 capacity of 8"),
