@@ -61,8 +61,8 @@ def config(world, steps_per_draw=4):
                   "containers + 152.6 MB of decoded rows through it",
             "pipeline": "native optb_pipeline: SBS draws for the next steps on a side stream overlap the "
                         "current step's gather-encode + decode, one optb_roundtrip_dev launch per step (every warp "
-                        "encodes its tiles into the HBM container stream, then decodes them back in write order); "
-                        "steps_per_draw epochs per sampler call",
+                        "stores each encoded tile into the HBM container stream and decodes it one tile later, "
+                        "reading it back while it is still in L2); steps_per_draw epochs per sampler call",
             "steps_per_draw": steps_per_draw}
 
 

@@ -30,7 +30,7 @@ def short(name):
         base, args = n.split("<", 1)
         args = [a.strip().replace("(int)", "").replace("(bool)", "") for a in args.rstrip(">").split(",")]
         tf = {"1": "true", "0": "false"}
-        if base == "k_encode_vec":  # <MODE, PTRS>
+        if base in ("k_encode_vec", "k_encode_bulk"):  # <MODE, PTRS[, DEEP]>
             args = [MODES.get(args[0], args[0])] + [tf.get(a, a) for a in args[1:]]
         elif base in ("k_decode_vec", "k_encode_generic", "k_decode_generic", "k_roundtrip_vec", "k_roundtrip_il"):
             args = [MODES.get(args[0], args[0])] + [OUTS.get(a, a) for a in args[1:2]] + \
@@ -94,6 +94,9 @@ def main():
                     "not counted in dram__bytes_write, so traffic is below the algorithmic bytes for the "
                     "write-heavy kernels",
             "algorithmic_bytes_per_launch": {"k_encode_vec<exact128,false>": rows * P * 2 + rows * 8,
+                                             "k_encode_bulk<exact128,false,true>": rows * P * 2 + rows * 8,
+                                             "k_decode_vec<exact128,u8,true,true>": rows * P * 2,
+                                             "k_roundtrip_il<exact128,u8,false,false,true,true>": rows * P * 3 + rows * 8,
                                              "k_decode_vec<exact128,u8,true>": rows * P * 2,
                                              "k_roundtrip_vec<exact128,u8,false,false>": rows * P * 4 + rows * 8,
                                              # interleaved: the container re-read is an L2 hit
