@@ -25,9 +25,15 @@
 //                         range check and unpack, transpose, u8 rows stored
 //                         directly or through a u8 tile with the fused
 //                         fp32/fp16/bf16 epilogue.
-//   k_roundtrip_vec<MODE,O>  K1+K2 in one persistent launch (optb_roundtrip_dev,
-//                         the E-D pipeline step): each warp encodes its tiles
-//                         into HBM, then decodes the same tiles back.
+//   k_encode_bulk<MODE>   K1/K5 for exact and f64: as k_encode_vec, but each
+//                         tile's words are laid out in the container tensor
+//                         map's 128B swizzle and leave as one bulk tensor store.
+//   k_roundtrip_il<MODE,O>  K1+K2 in one persistent launch (optb_roundtrip_dev,
+//                         the E-D pipeline step), exact and f64: each warp
+//                         stores an encoded tile, then decodes it one tile
+//                         later by TMA while its lines are still in L2.
+//   k_roundtrip_vec<MODE,O>  the same, phase-ordered (lossless modes): each
+//                         warp encodes all its tiles, then decodes them back.
 //   k_{en,de}code_generic any P / stride / alignment: one pixel per lane,
 //                         warp ballots for the parity plane.
 #include <cuda.h>
@@ -354,14 +360,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, int
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, int c0, int c1, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m), "r"(c0),
                "r"(c1), "r"(smem_u32(src))
-               : "memory");
-}
-// 1D bulk copy global -> shared completing on an mbarrier (16-byte aligned,
-// size a multiple of 16)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -1341,12 +1339,9 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   static_assert(IlRegion<MODE, DEEP>::ENC % 1024 == 0, "decode slot must stay 1024-aligned");
-  using S = VecMode<MODE>;
-  // lossless: per-lane container stores (the 7-bit words are not laid out for
-  // a bulk store); the parity bits come with the words, as NI 64-byte bulk
-  // copies on the same mbarrier (P % 512 == 0: a tile lies in one chunk and
-  // image i's 512 bits are 64 contiguous, 64-aligned plane bytes)
-  constexpr bool BULK = BULK_ST && !S::OFFS;
+  // exact / f64 only: lossless stays phase-ordered (see rt_vec_t)
+  static_assert(!VecMode<MODE>::OFFS, "interleaved round trip: exact and f64 modes");
+  constexpr bool BULK = BULK_ST;
   static_assert(IlRegion<MODE, DEEP>::SMEM <= 232448, "interleaved kernel: shared memory over the 227 KB limit");
   constexpr int WC = VecMode<MODE>::WC;
   constexpr int NW = IlShape<MODE, DEEP>::NW, NS = IlShape<MODE, DEEP>::NS;
@@ -1365,7 +1360,6 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * NW * 32;
   const WalkStep step = walk_step(g, G, stride);
   Walk wd = walk_at(g, G, (static_cast<uint64_t>(blockIdx.x) * NW + warp) * 32 + lane);
-  Walk wi = wd;  // the tile being loaded (lossless: its chunk and group for the parity bits)
   uint32_t phase = 0;
   bool pending = false;
   auto decode_pending = [&]() {
@@ -1381,23 +1375,13 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
     if constexpr (BULK) {
       if (lane == 0) bulk_wait0();
     } else {
-      // this tile's container (and parity) stores, generic proxy, before
-      // the async-proxy reads of them
-      fence_proxy_async_global();
+      fence_proxy_async_global();  // this tile's container stores (generic proxy), before the TMA read
     }
     __syncwarp();
     if (lane == 0) {
-      uint32_t n = 0;
-      if constexpr (S::OFFS) n = walk_chunk(g, wi).n;
-      mbar_expect_tx(bar, 512 * WC + n * 64);
+      mbar_expect_tx(bar, 512 * WC);
       tma_load_2d(dslot, &cmap, 0, static_cast<int>((tile * 16 * WC) >> 7), bar);
-      if constexpr (S::OFFS) {
-        const uint8_t* plane = offsets + wi.k * g.ostride + 2 * wi.gi;  // lane 0: the tile's first group
-        for (uint32_t i = 0; i < n; ++i)
-          bulk_g2s(dslot + S::WORDS_B + i * 64, plane + (static_cast<uint64_t>(i) * g.P) / 8, 64, bar);
-      }
     }
-    if constexpr (S::OFFS) walk_advance(wi, step, g, G);
     pending = true;
   };
   encode_body<MODE, PTRS, NoHook, decltype(after_tile), BULK, NW, NS>(g, src, cont, offsets, base,
@@ -1786,9 +1770,10 @@ bool rt_interleave_enabled() {  // read per call (probes switch it at run time)
 template <int MODE, int O, bool PTRS, bool ONE_CTA>
 cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, const Epi& e,
                      void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
-  // lossless stays phase-ordered: the interleaved form (parity bits as 64-byte
-  // bulk copies beside the words' TMA load) measured slower for these
-  // integer-pipe-bound modes (C3 n=9: 138 -> 174 us, n=18: 148 -> 164 us)
+  // lossless stays phase-ordered: an interleaved form (the tile's parity
+  // bits as 64-byte bulk copies beside the words' TMA load) measured slower
+  // for these integer-pipe-bound modes (C3 n=9: 138 -> 174 us, n=18: 148 ->
+  // 164 us) and was dropped
   if constexpr (!VecMode<MODE>::OFFS) {
     const uint64_t tiles = (g.chunks * (g.P / 16) + 31) / 32;
     const char* f = getenv("OPTB_IL_SHAPE");  // deep | wide: force a shape (tests, probes)
