@@ -1334,8 +1334,11 @@ struct IlRegion {
   static constexpr uint32_t BYTES = ENC + DecSlot<MODE>::TMA;
   static constexpr size_t SMEM = static_cast<size_t>(IlShape<MODE, DEEP>::NW) * BYTES + 1024;
 };
+#ifndef OPTB_IL_DEEP_MAXREG
+#define OPTB_IL_DEEP_MAXREG 232  // 5 warps per SM: registers are free (C2 583 -> 591 M img/s)
+#endif
 template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP, bool BULK_ST>
-__global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
+__global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   static_assert(IlRegion<MODE, DEEP>::ENC % 1024 == 0, "decode slot must stay 1024-aligned");
