@@ -410,14 +410,7 @@ int roundtrip_checks(optb_ctx* c, const optb_layout* L, const optb_epilogue* E) 
 int optb_roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
                        const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E,
                        void* out, void* stream) {
-  int st = roundtrip_checks(c, L, E);
-  if (st) return st;
-  if (optb_layout_rows(L) == 0) return OPTB_OK;
-  if (!images || !containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
-    return set_err(OPTB_ERR_ARG, "roundtrip: null buffer");
-  if (row_stride == 0) row_stride = L->pixels;
-  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
-  return roundtrip(c, L, RowSrc{images, row_stride, row_index, nullptr, 0}, containers, offsets, E, out, stream);
+  return optb_b200::roundtrip_dev(c, L, images, row_stride, row_index, containers, offsets, E, out, stream, false);
 }
 
 int optb_roundtrip_rows_dev(optb_ctx* c, const optb_layout* L, const uint64_t* row_ptrs, int32_t rows_aligned16,
@@ -444,6 +437,21 @@ int optb_synth_pixels_dev(optb_ctx* c, uint64_t seed, uint64_t first_row, uint64
 }
 
 }  // extern "C"
+
+int optb_b200::roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
+                             const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E,
+                             void* out, void* stream, bool early) {
+  int st = roundtrip_checks(c, L, E);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!images || !containers || !out || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "roundtrip: null buffer");
+  if (row_stride == 0) row_stride = L->pixels;
+  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
+  return roundtrip(c, L, RowSrc{images, row_stride, row_index, nullptr, 0, early ? 1 : 0}, containers, offsets, E,
+                   out, stream);
+}
+
 
 // ------------------------------------------------------------------ host pipeline
 namespace {
@@ -732,6 +740,8 @@ struct optb_sbs {
   int32_t* d_cl = nullptr;
   uint64_t ex_cap = 0;
 };
+
+uint64_t optb_b200::sbs_examples(const optb_sbs* s) { return s ? s->N : 0; }
 
 namespace {
 

@@ -1,6 +1,9 @@
 // codec.cu -- dispatch of the optb codec kernels (the kernels themselves are in
 // codec_impl.cuh, instantiated per mode variant by codec_v<N>.cu), the
 // synthetic-data kernel, and the shared launch helpers.
+#include <mutex>
+#include <unordered_map>
+
 #include "codec_impl.cuh"
 
 namespace optb_b200 {
@@ -70,6 +73,22 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
 }
 
 thread_local int g_rt_kind = OPTB_RT_NONE;
+
+namespace {
+std::mutex g_tag_mu;
+std::unordered_map<cudaStream_t, uint64_t> g_tags;
+uint64_t g_tag_next = 1;
+}  // namespace
+
+uint64_t stream_tag(cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g_tag_mu);
+  auto it = g_tags.find(s);
+  return it == g_tags.end() ? 0 : it->second;
+}
+void bump_stream_tag(cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g_tag_mu);
+  g_tags[s] = g_tag_next++;
+}
 
 cudaError_t launch_roundtrip(const Geom& g, const RowSrc& rs, void* containers, uint8_t* offsets, const Epi& e,
                              void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {

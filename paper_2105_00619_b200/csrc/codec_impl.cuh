@@ -391,6 +391,8 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ------------------------------------------------------------------ K1 / K3
 // Gather-encode for the exact and lossless modes.  Stage slot layout on
@@ -520,6 +522,9 @@ struct NoTileHook {
 // map smap and leave in ONE bulk tensor store issued by lane 0 (instead of 16
 // shared loads + 16 global stores per lane); a slot is refilled only after
 // that store has read it.
+// src.early: the kernel started without griddepcontrol.wait (only the rows
+// and row ids are read before it, RowSrc::early): every lane waits for the
+// previous grid before the warp's first global write.
 template <int MODE, bool PTRS, typename Hook = NoHook, typename TileHook = NoTileHook, bool BULK = false,
           int NW = kWarps, int NS = kStages>
 __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, uint8_t* __restrict__ cont,
@@ -654,6 +659,7 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       }
     }
     transpose16<S::NT, 16>(m);  // m[p] = bytes of images 0..15 at pixel p
+    if (src.early && base == first) pdl_wait();
     if constexpr (S::OFFS) {
       // parity planes of images 0..min(NI,16)-1 from the transposed bytes:
       // lo[q] / hi[q] collect the low bits of pixels 0..7 / 8..15 of images
@@ -1351,7 +1357,12 @@ __global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : RtRegs<MODE, ONE_CTA>:
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bars[NW];
   uint8_t* base = align1024(smem_raw);
-  pdl_entry();
+  // programmatic dependent launch: the next grid may start now.  With
+  // src.early (the pipeline's steps) this one gathers its first tiles while
+  // the previous step's grid drains and waits for it (griddepcontrol.wait)
+  // before its first global write; otherwise it waits here.
+  pdl_trigger();
+  if (!src.early) pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* bar = bars + warp;
   uint8_t* dslot = base + warp * IlRegion<MODE, DEEP>::BYTES + IlRegion<MODE, DEEP>::ENC;
@@ -1585,6 +1596,7 @@ cudaError_t launch_k(void (*kernel)(KArgs...), int grid, int threads, size_t sme
     const char* v = getenv("OPTB_PDL");
     return !(v && v[0] == '0');
   }();
+  bump_stream_tag(s);  // this kernel triggers its dependents early (pdl_entry / pdl_trigger)
   if (!pdl) {
     kernel<<<grid, threads, smem, s>>>(std::forward<Args>(args)...);
     return cudaGetLastError();

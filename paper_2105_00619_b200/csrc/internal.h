@@ -64,7 +64,25 @@ struct RowSrc {
   const int64_t* index;
   const uint64_t* ptrs;
   int32_t ptrs_aligned16;  // every ptrs[r] is 16-byte aligned (vector path)
+  // the rows and row ids may be read before the previous kernel in the stream
+  // has completed (it cannot have written them): the interleaved round trip
+  // then gathers its first tiles while that kernel drains (programmatic
+  // dependent launch) and waits for it before its first global write
+  int32_t early;
 };
+
+// A tag per stream that changes with every kernel the library launches with
+// programmatic dependent launch (launch_k).  The pipeline compares it with
+// the tag after its previous step: equal means no library kernel that can
+// trigger its dependents early was launched on that stream in between.
+uint64_t stream_tag(cudaStream_t s);
+void bump_stream_tag(cudaStream_t s);
+// Examples in a cursor's class index (row ids drawn are < this).
+uint64_t sbs_examples(const optb_sbs* s);
+// optb_roundtrip_dev with RowSrc::early set as given (the pipeline step).
+int roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
+                  const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E, void* out,
+                  void* stream, bool early);
 
 // Kernel launchers (codec.cu).  Return cudaError_t of the launch; `launches`
 // is incremented by the number of kernels enqueued.

@@ -60,6 +60,11 @@ struct optb_pipeline {
               t_e1[kTimingRing] = {}, t_d1[kTimingRing] = {};
   uint64_t step = 0;   // next step to deliver
   uint64_t calls = 0;  // SBS calls enqueued
+  // the previous fused step's stream and that stream's launch tag after it
+  // (stream_tag): the next step may gather early if nothing that can trigger
+  // its dependents early was launched there since (RowSrc::early)
+  cudaStream_t last_stream = nullptr;
+  uint64_t last_tag = 0;
   bool timing = false;
   uint32_t tstride = 1;  // time every tstride-th step (and sampler call)
   // host leg (optb_pipeline_step_host): double-buffered device copies of the
@@ -167,9 +172,21 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
     st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
     if (st) return st;
   } else {
-    st = optb_roundtrip_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
-                            p->cont, p->offs, &e, out, s);
+    // early gather: the kernel right before this step in the stream is this
+    // pipeline's previous step (or a kernel that does not trigger early),
+    // which writes only the containers and its `out` -- unless `out`
+    // overlaps the dataset rows
+    const uint64_t ds_bytes = optb_b200::sbs_examples(p->d.sbs) * p->d.row_stride;
+    const uint64_t out_row = e.out_row_stride ? e.out_row_stride : p->d.layout.pixels;
+    const uint64_t out_bytes = p->rows * out_row * (e.out_dtype == OPTB_OUT_U8 ? 1 : e.out_dtype == OPTB_OUT_F32 ? 4 : 2);
+    const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), d0 = reinterpret_cast<uintptr_t>(p->d.dataset);
+    const bool disjoint = ds_bytes && (o0 + out_bytes <= d0 || d0 + ds_bytes <= o0);
+    const bool early = disjoint && p->last_tag && p->last_stream == s && optb_b200::stream_tag(s) == p->last_tag;
+    st = optb_b200::roundtrip_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
+                                  p->cont, p->offs, &e, out, s, early);
     if (st) return st;
+    p->last_stream = s;
+    p->last_tag = optb_b200::stream_tag(s);
     if (timed) cudaEventRecord(p->t_e1[r], s);
     if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
   }

@@ -161,3 +161,47 @@ def test_pipeline_timing_stride(pkg, oracle_mod, torch_cuda):
         ex, _ = ref.next(nb)
         assert torch.equal(outs[step].cpu(), torch.from_numpy(ds[ex])), step
     pipe.close()
+
+
+@pytest.mark.parametrize("spd", [1, 4])
+def test_pipeline_back_to_back_steps_early_gather(pkg, oracle_mod, torch_cuda, spd):
+    """Steps enqueued back to back without a host sync (each step's round trip
+    may start gathering while the previous one drains: RowSrc::early), each
+    into its own output, all equal to the oracle; then a library decode that
+    rewrites the dataset in the same stream between two steps (a kernel that
+    triggers its dependents early): the next step must gather the new rows."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    C = pkg.codec
+    N = 4096
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch, N=N)
+    B, nb, P = 64, 40, 768  # 2560 rows per step
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    ds_d = torch.from_numpy(ds).cuda()
+    s = torch.cuda.Stream()
+    pipe = Pipeline(cur, ds_d, 1, B, nb, steps_per_draw=spd)
+    outs = [torch.empty((B * nb, P), dtype=torch.uint8, device="cuda") for _ in range(8)]
+    with torch.cuda.stream(s):
+        for o in outs:
+            pipe.step(o, s)
+    s.synchronize()
+    for k, o in enumerate(outs):
+        ex, _ = ref.next(nb)
+        assert np.array_equal(o.cpu().numpy(), ds[ex]), k
+    # a second dataset written into ds_d by optb_decode_dev on the same stream
+    new = O.synth_pixels(11, 0, N, P)
+    L2 = C.layout(1, 16, P, N, 1)
+    cont2, _ = C.alloc_stream(L2)
+    new_d = torch.from_numpy(new).cuda()
+    outs2 = [torch.empty((B * nb, P), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    with torch.cuda.stream(s):
+        C.encode_dev(L2, new_d, cont2, stream=s)
+        pipe.step(outs2[0], s)  # still the old rows? no: encode_dev does not write ds_d
+        C.decode_dev(L2, cont2, ds_d, stream=s)  # ds_d := new, in stream order
+        pipe.step(outs2[1], s)
+    s.synchronize()
+    ex0, _ = ref.next(nb)
+    ex1, _ = ref.next(nb)
+    assert np.array_equal(outs2[0].cpu().numpy(), ds[ex0])
+    assert np.array_equal(outs2[1].cpu().numpy(), new[ex1])
+    pipe.close()
