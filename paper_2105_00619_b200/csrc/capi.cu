@@ -327,19 +327,7 @@ int optb_ctx_sync(optb_ctx* c, void* stream) {
 // ------------------------------------------------------------------ codec, device
 int optb_encode_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
                     const int64_t* row_index, void* containers, uint8_t* offsets, void* stream) {
-  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
-  int st = optb_layout_check(L);
-  if (st) return st;
-  if (optb_layout_rows(L) == 0) return OPTB_OK;
-  if (!images || !containers || (optb_mode_has_offsets(L->mode) && !offsets))
-    return set_err(OPTB_ERR_ARG, "encode: null buffer");
-  if (row_stride == 0) row_stride = L->pixels;
-  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
-  const Geom g = make_geom(L);
-  const RowSrc rs{images, row_stride, row_index, nullptr, 0};
-  cudaError_t e = launch_encode(g, rs, containers, offsets, static_cast<cudaStream_t>(stream), c->sms, &c->launches);
-  if (e != cudaSuccess) return cuda_err(e, "encode launch");
-  return OPTB_OK;
+  return optb_b200::encode_dev(c, L, images, row_stride, row_index, containers, offsets, stream, false);
 }
 
 int optb_encode_rows_dev(optb_ctx* c, const optb_layout* L, const uint64_t* row_ptrs, int32_t rows_aligned16,
@@ -437,6 +425,24 @@ int optb_synth_pixels_dev(optb_ctx* c, uint64_t seed, uint64_t first_row, uint64
 }
 
 }  // extern "C"
+
+int optb_b200::encode_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
+                           const int64_t* row_index, void* containers, uint8_t* offsets, void* stream, bool early) {
+  if (!c) return set_err(OPTB_ERR_ARG, "ctx: null");
+  int st = optb_layout_check(L);
+  if (st) return st;
+  if (optb_layout_rows(L) == 0) return OPTB_OK;
+  if (!images || !containers || (optb_mode_has_offsets(L->mode) && !offsets))
+    return set_err(OPTB_ERR_ARG, "encode: null buffer");
+  if (row_stride == 0) row_stride = L->pixels;
+  if (row_stride < L->pixels) return set_err(OPTB_ERR_ARG, "encode: row_stride < pixels");
+  const Geom g = make_geom(L);
+  const RowSrc rs{images, row_stride, row_index, nullptr, 0, early ? 1 : 0};
+  cudaError_t e = launch_encode(g, rs, containers, offsets, static_cast<cudaStream_t>(stream), c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "encode launch");
+  return OPTB_OK;
+}
+
 
 int optb_b200::roundtrip_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
                              const int64_t* row_index, void* containers, uint8_t* offsets, const optb_epilogue* E,

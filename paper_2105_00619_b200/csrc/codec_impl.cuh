@@ -615,6 +615,9 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
     fetch_rows();  // consumed by the next iteration's issue
     cp_async_wait<NS - 1>();
     __syncwarp();
+    // src.early: this iteration's stores (parity bits below, the words
+    // after the transpose) are the warp's first global writes
+    if (src.early && base == first) pdl_wait();
     uint8_t* slot = ring + stage * S::ENC_SLOT;
     const uint64_t t = wc.t;
     uint32_t n = 0;
@@ -659,7 +662,6 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       }
     }
     transpose16<S::NT, 16>(m);  // m[p] = bytes of images 0..15 at pixel p
-    if (src.early && base == first) pdl_wait();
     if constexpr (S::OFFS) {
       // parity planes of images 0..min(NI,16)-1 from the transposed bytes:
       // lo[q] / hi[q] collect the low bits of pixels 0..7 / 8..15 of images
@@ -809,7 +811,8 @@ template <int MODE, bool PTRS>
 __global__ void __launch_bounds__(kThreads, VecMode<MODE>::MIN_BLOCKS)
     k_encode_vec(Geom g, RowSrc src, uint8_t* __restrict__ cont, uint8_t* __restrict__ offsets) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  pdl_entry();
+  pdl_trigger();
+  if (!src.early) pdl_wait();  // early: encode_body waits before the first store
   encode_body<MODE, PTRS>(g, src, cont, offsets, smem_raw);
 }
 
@@ -849,7 +852,8 @@ __global__ void __launch_bounds__(EncShape<MODE, DEEP>::NW * 32, EncShape<MODE, 
                   uint8_t* __restrict__ offsets) {
   constexpr int NW = EncShape<MODE, DEEP>::NW, NS = EncShape<MODE, DEEP>::NS;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  pdl_entry();
+  pdl_trigger();
+  if (!src.early) pdl_wait();  // early: encode_body waits before the first store
   encode_body<MODE, PTRS, NoHook, NoTileHook, true, NW, NS>(g, src, cont, offsets, align1024(smem_raw),
                                                             NS * VecMode<MODE>::ENC_SLOT, NoHook{}, NoTileHook{},
                                                             &cmap);

@@ -163,34 +163,34 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   optb_epilogue e = p->d.epilogue;
   if (e.class_scale && !e.row_class) e.row_class = p->cls[b] + sub * p->rows;
   if (timed) cudaEventRecord(p->t_e0[r], s);
+  // early gather (RowSrc::early): the kernel right before this step in the
+  // stream is this pipeline's previous step (or a kernel that does not
+  // trigger early), which writes only the containers and its `out` -- unless
+  // `out` overlaps the dataset rows
+  const uint64_t ds_bytes = optb_b200::sbs_examples(p->d.sbs) * p->d.row_stride;
+  const uint64_t out_row = e.out_row_stride ? e.out_row_stride : p->d.layout.pixels;
+  const uint64_t out_bytes = p->rows * out_row * (e.out_dtype == OPTB_OUT_U8 ? 1 : e.out_dtype == OPTB_OUT_F32 ? 4 : 2);
+  const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), d0 = reinterpret_cast<uintptr_t>(p->d.dataset);
+  const bool disjoint = ds_bytes && (o0 + out_bytes <= d0 || d0 + ds_bytes <= o0);
+  const bool early = disjoint && p->last_tag && p->last_stream == s && optb_b200::stream_tag(s) == p->last_tag;
   if (p->d.split_kernels) {
-    st = optb_encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
-                         p->cont, p->offs, s);
+    st = optb_b200::encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
+                               p->cont, p->offs, s, early);
     if (st) return st;
     if (timed) cudaEventRecord(p->t_e1[r], s);
     if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
     st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
     if (st) return st;
   } else {
-    // early gather: the kernel right before this step in the stream is this
-    // pipeline's previous step (or a kernel that does not trigger early),
-    // which writes only the containers and its `out` -- unless `out`
-    // overlaps the dataset rows
-    const uint64_t ds_bytes = optb_b200::sbs_examples(p->d.sbs) * p->d.row_stride;
-    const uint64_t out_row = e.out_row_stride ? e.out_row_stride : p->d.layout.pixels;
-    const uint64_t out_bytes = p->rows * out_row * (e.out_dtype == OPTB_OUT_U8 ? 1 : e.out_dtype == OPTB_OUT_F32 ? 4 : 2);
-    const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), d0 = reinterpret_cast<uintptr_t>(p->d.dataset);
-    const bool disjoint = ds_bytes && (o0 + out_bytes <= d0 || d0 + ds_bytes <= o0);
-    const bool early = disjoint && p->last_tag && p->last_stream == s && optb_b200::stream_tag(s) == p->last_tag;
     st = optb_b200::roundtrip_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
                                   p->cont, p->offs, &e, out, s, early);
     if (st) return st;
-    p->last_stream = s;
-    p->last_tag = optb_b200::stream_tag(s);
     if (timed) cudaEventRecord(p->t_e1[r], s);
     if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
   }
   if (timed && p->d.split_kernels) cudaEventRecord(p->t_d1[r], s);  // fused: the launch ends at t_e1
+  p->last_stream = s;
+  p->last_tag = optb_b200::stream_tag(s);
   ++p->step;
   return OPTB_OK;
 }

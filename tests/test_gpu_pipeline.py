@@ -163,8 +163,9 @@ def test_pipeline_timing_stride(pkg, oracle_mod, torch_cuda):
     pipe.close()
 
 
-@pytest.mark.parametrize("spd", [1, 4])
-def test_pipeline_back_to_back_steps_early_gather(pkg, oracle_mod, torch_cuda, spd):
+@pytest.mark.parametrize("mode,split,spd", [(1, False, 1), (1, False, 4), (1, True, 1), (4, True, 2), (0, True, 1),
+                                             (0, False, 2)])
+def test_pipeline_back_to_back_steps_early_gather(pkg, oracle_mod, torch_cuda, mode, split, spd):
     """Steps enqueued back to back without a host sync (each step's round trip
     may start gathering while the previous one drains: RowSrc::early), each
     into its own output, all equal to the oracle; then a library decode that
@@ -179,7 +180,7 @@ def test_pipeline_back_to_back_steps_early_gather(pkg, oracle_mod, torch_cuda, s
     cur = S.BatchCursor.from_device_index(p, offs, mem)
     ds_d = torch.from_numpy(ds).cuda()
     s = torch.cuda.Stream()
-    pipe = Pipeline(cur, ds_d, 1, B, nb, steps_per_draw=spd)
+    pipe = Pipeline(cur, ds_d, mode, B, nb, per_chunk=C.capacity(mode), steps_per_draw=spd, split_kernels=split)
     outs = [torch.empty((B * nb, P), dtype=torch.uint8, device="cuda") for _ in range(8)]
     with torch.cuda.stream(s):
         for o in outs:
