@@ -463,7 +463,11 @@ def main():
             if kn == kname or kn.startswith(kname[:-1] + ","):
                 traffic = kv.get("dram_bytes_per_launch")
                 break
-    roofline = {"bound": "hbm", "kernel": kname, "kernel_kind": rt_kind, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+    roofline = {"bound": "hbm", "kernel": kname, "kernel_kind": rt_kind,
+                "launch_timing": ("CUDA events on the launching stream around every %d-th timed step's launch; "
+                                  "those launches cannot overlap their neighbours (an event sits between), so this "
+                                  "is the isolated launch duration -- back-to-back steps overlap ramp and tail "
+                                  "(step_gbs)" % tstride), "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
                 "frac_of_spec_8tbs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": kbytes,
