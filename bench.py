@@ -467,7 +467,8 @@ def main():
                 "launch_timing": ("CUDA events on the launching stream around every %d-th timed step's launch; "
                                   "those launches cannot overlap their neighbours (an event sits between), so this "
                                   "is the isolated launch duration -- back-to-back steps overlap ramp and tail "
-                                  "(step_gbs)" % tstride), "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                                  "(step_gbs)" % tstride),
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
                 "frac_of_spec_8tbs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": kbytes,
