@@ -1,27 +1,33 @@
 """Benchmark: images/s encode+decode (and achieved HBM GB/s vs peak) per BASELINE.json.
 
-Workload (BASELINE.json configs[1], "C2"): CIFAR-100-shaped synthetic dataset
-(50 000 x 32x32x3 u8, labels e % 100) resident in HBM; selective batch
-sampling with uniform weights over 100 classes, batch 512, seed 1234; every
-step is one epoch of the reference's draw stream (floor(50000/512) = 97
-batches per GPU): SBS draws (optb_sbs_next_dev) -> gather-encode of the
-drawn rows into exact128 containers (optb_encode_dev) -> decode of every
-container back to u8 rows (optb_decode_dev).  Containers are materialised in
-HBM between the kernels.  N GPUs: one process per GPU, each draws the global
-stream's batches t % N == rank (weak scaling, no collective on the data path).
+Headline workload (BASELINE.json configs[4], "C5"): a 2^20-image synthetic
+CIFAR-shaped stream (1 048 576 x 32x32x3 u8 = 3.2 GB, labels e % 100)
+resident in HBM on every GPU; selective batch sampling with uniform weights
+over 100 classes, batch 512, seed 1234; every step is one epoch of the
+reference's draw stream per GPU (floor(2^20 / 512) = 2048 batches): SBS draws
+(side stream) -> gather-encode of the drawn rows into exact128 containers ->
+decode back to u8 rows, one fused launch per step (optb_pipeline_step).
+Containers are materialised in HBM.  N GPUs: one process per GPU, each keeps
+the global stream's batches t % N == rank (weak scaling, no collective on the
+data path).  C1-C4 and the round-1 C2 headline are reported as sub-keys
+under "configs".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Rank 0 prints one JSON line.  `--impl reference` times the reference's own
-CPU implementation (oracle/_ref, compiled from /root/reference's sources)
-on the host cores over a bounded sample of the same workload.
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks.  Rank 0 prints one JSON line.
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, compiled from /root/reference's sources) on the host cores over
+a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -31,15 +37,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_EXAMPLES = 50000
+N_EXAMPLES = 1 << 20           # C5: 2^20-image stream
 N_CLASSES = 100
 BATCH = 512
 SEED = 1234
-DATA_SEED = 7  # RunConfig::data_seed (runner.hpp:34)
+DATA_SEED = 7                  # RunConfig::data_seed (runner.hpp:34)
 P = 32 * 32 * 3
-BATCHES_PER_STEP = N_EXAMPLES // BATCH  # 97: one epoch (runner.cpp:52-57)
-MODE = 1  # ExactInt128, the reference default (runner.hpp:52)
-TIMING_STRIDE = 8  # per-kernel timing events on every 8th step of the timed loops
+BATCHES_PER_STEP = N_EXAMPLES // BATCH  # 2048: one epoch per GPU (runner.cpp:52-57)
+MODE = 1                       # ExactInt128, the reference default (runner.hpp:52)
 PER_CHUNK = 16
 METRIC = "images/sec encode+decode (and achieved HBM GB/s vs peak) at 1/2/4/8 B200"
 UNIT = "images/s"
@@ -50,26 +55,25 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def config(world, steps_per_draw=4):
-    return {"workload": "C2: CIFAR-100-shaped 50000x32x32x3 u8 dataset in HBM, SBS (uniform 100 classes, "
-                        "B=512, seed 1234) + exact128 gather-encode + decode to u8; 1 epoch = 97 batches "
-                        "per GPU per step",
+def config(world):
+    return {"workload": "C5: 2^20-image CIFAR-shaped stream (1048576 x 32x32x3 u8, 3.2 GB) in HBM per GPU, SBS "
+                        "(uniform 100 classes, B=512, seed 1234) + exact128 gather-encode + decode to u8; one step = "
+                        "one epoch = 2048 batches per GPU",
             "global_batch": BATCH, "batches_per_step_per_gpu": BATCHES_PER_STEP, "mode": "exact128",
-            "per_chunk": PER_CHUNK, "image": [32, 32, 3], "decode_out": "u8",
-            "parallelism": f"independent batch shards x{world} (t % N == rank)",
-            "l2": "inputs larger than L2: 153.6 MB dataset (> 126 MB L2), and every step streams 152.6 MB of "
-                  "containers + 152.6 MB of decoded rows through it",
-            "pipeline": "native optb_pipeline: SBS draws for the next steps on a side stream overlap the "
-                        "current step's gather-encode + decode, one optb_roundtrip_dev launch per step (every warp "
-                        "stores each encoded tile into the HBM container stream and decodes it one tile later, "
-                        "reading it back while it is still in L2); steps_per_draw epochs per sampler call",
-            "steps_per_draw": steps_per_draw}
+            "per_chunk": PER_CHUNK, "image": [32, 32, 3], "decode_out": "u8", "dataset_images": N_EXAMPLES,
+            "parallelism": f"independent batch shards x{world} (t % N == rank), no data-path collective",
+            "l2": "inputs larger than L2: 3.2 GB dataset (25x the 126 MB L2); every step streams 3.2 GB of "
+                  "gathered rows in and 3.2 GB of containers + 3.2 GB of decoded rows out",
+            "pipeline": "native optb_pipeline: the next epoch's SBS draws on a side stream overlap the current "
+                        "step's gather-encode + decode, one optb_roundtrip_dev launch per step (each warp "
+                        "stores an encoded tile into the HBM container stream and decodes it one tile later, "
+                        "reading it back while it is still in L2)"}
 
 
 # ---------------------------------------------------------------- collectives
-# The run's control-plane collectives (barriers, the max-over-ranks of device
-# times): NCCL with one process per GPU, gloo when ranks share a GPU (then the
-# per-rank times are summed so the whole-job rate is never overstated).
+# Control-plane collectives of the run (barriers, the max over ranks of the
+# device times): NCCL with one process per GPU, gloo when ranks share a GPU
+# (then the per-rank times are summed so the whole-job rate is never overstated).
 COLL = {"group": None, "device": None, "op": None}
 
 
@@ -146,68 +150,131 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram read+write bytes per launch of the roofline kernel from the
-    committed ncu --set full summary (profiles/ncu_summary.json), if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def ncu_traffic(kname):
+    """dram read+write bytes per launch of `kname` from the committed ncu
+    --set full summary (profiles/ncu_summary.json), with the capture's tag."""
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d
     except Exception:  # noqa: BLE001
-        return None
+        return None, None
+    for kn, kv in d.get("kernels", {}).items():  # ncu names carry every template argument
+        if kn == kname or kn.startswith(kname[:-1] + ","):
+            return kv.get("dram_bytes_per_launch"), d.get("tag")
+    return None, None
 
 
-# ---------------------------------------------------------------- reference arm
-def reference_rate(n_batches_sample: int, threads: int, repeats: int = 1):
-    """Time the reference CPU path (oracle/_ref = the reference compiled from
-    its own sources; else the C oracle port) on a bounded sample: SBS draws
-    with the reference BatchCursor, then per batch image_of gather +
-    codec::encode per chunk + codec::decode per chunk, batches split over
-    `threads` host threads.  Returns (images/s, kind, sample description)."""
-    import ctypes as ct
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
+
+# ---------------------------------------------------------------- reference side (checker + CPU baseline)
+# Everything below that touches oracle/ is the CHECKER and the CPU BASELINE:
+# the reference library compiled from its own sources (oracle/_ref), or the C
+# restatement when it was not built.  It never runs inside a timed GPU region.
+class RefStream:
+    """The reference BatchCursor over the headline stream (checker): yields
+    this rank's draws of step k, in order."""
+
+    def __init__(self, labels, world, rank):
+        import ctypes as ct
+
+        import oracle as O
+        self.O, self.ct, self.world, self.rank = O, ct, world, rank
+        self.off = np.zeros(N_CLASSES + 1, np.uint64)
+        self.mem = np.zeros(len(labels), np.int64)
+        if O.ref_available():
+            R = O.REF
+            buf = ct.create_string_buffer(512)
+            R.ref_class_index(O.ptr(labels, O.i32p), len(labels), N_CLASSES, O.ptr(self.off, O.u64p),
+                              O.ptr(self.mem, O.i64p), buf, 512)
+            w = np.full(N_CLASSES, 1.0 / N_CLASSES)
+            st = ct.c_int(0)
+            self.h = R.ref_cursor_create(O.ptr(w, O.f64p), N_CLASSES, BATCH, SEED, O.ptr(self.off, O.u64p),
+                                         O.ptr(self.mem, O.i64p), ct.byref(st), buf, 512)
+            self.kind = "reference"
+        else:
+            self.off, self.mem = O.class_index(labels, N_CLASSES)
+            self.cur = O.Cursor(O.sbs_plan([1.0 / N_CLASSES] * N_CLASSES, BATCH), self.off, self.mem, BATCH, SEED)
+            self.h, self.kind = None, "port"
+        self.steps = 0
+
+    def next_batches(self, n):
+        if self.h is not None:
+            ex = np.zeros(n * BATCH, np.int64)
+            self.O.REF.ref_cursor_next(self.h, n, self.O.ptr(ex, self.O.i64p), None)
+            return ex
+        return self.cur.next(n)[0]
+
+    def step(self, batches_per_rank):
+        ex = self.next_batches(batches_per_rank * self.world).reshape(-1, BATCH)
+        self.steps += 1
+        return np.ascontiguousarray(ex[self.rank::self.world].reshape(-1))
+
+    def close(self):
+        if self.h is not None:
+            self.O.REF.ref_cursor_destroy(self.h)
+            self.h = None
+
+
+class RefBaseline:
+    """The reference CPU path (oracle/_ref = the reference compiled from its
+    own sources; else the C oracle port) on the headline stream: per sample,
+    BatchCursor::next draws, then per batch image_of gather + codec::encode
+    per 16-image chunk + codec::decode, batches split over `threads` host
+    threads (the functions are reentrant)."""
+
+    def __init__(self, ds, labels):
+        import oracle as O
+        self.O, self.ds, self.labels = O, ds, labels
+        if O.ref_available():
+            self.rs = RefStream(labels, 1, 0)
+            self.dsh = O.REF.ref_dataset_create(O.ptr(ds, O.u8p), ds.shape[0], 32, 32, 3)
+            self.kind = "reference"
+        else:
+            off, mem = O.class_index(labels, N_CLASSES)
+            self.cur = O.Cursor(O.sbs_plan([1.0 / N_CLASSES] * N_CLASSES, BATCH), off, mem, BATCH, SEED)
+            self.dsh, self.kind = None, "port"
+
+    def rate(self, n_batches: int, threads: int):
+        import ctypes as ct
+        O = self.O
+        t0 = time.perf_counter()
+        if self.dsh is not None:
+            ex = np.zeros(n_batches * BATCH, np.int64)
+            O.REF.ref_cursor_next(self.rs.h, n_batches, O.ptr(ex, O.i64p), None)
+            t_sbs = time.perf_counter() - t0
+            chk = ct.c_uint64(0)
+            secs = O.REF.ref_bench_roundtrip(self.dsh, MODE, O.ptr(ex, O.i64p), n_batches, BATCH, threads, 0,
+                                             ct.byref(chk)) + t_sbs
+        else:
+            threads = 1
+            ex, _ = self.cur.next(n_batches)
+            cont, _ = O.encode_stream(self.ds, ex, MODE, PER_CHUNK, BATCH, n_batches)
+            O.decode_stream(cont, None, MODE, PER_CHUNK, P, BATCH, n_batches)
+            secs = time.perf_counter() - t0
+        sample = (f"{n_batches} batches x {BATCH} images of the C5 stream (BatchCursor::next draws + image_of "
+                  f"gather + codec::encode/decode per 16-image chunk), {threads} host threads")
+        return n_batches * BATCH / secs, sample, threads
+
+    def close(self):
+        if self.dsh is not None:
+            self.O.REF.ref_dataset_destroy(self.dsh)
+            self.rs.close()
+            self.dsh = None
+
+
+def host_dataset():
     import oracle as O
     labels = (np.arange(N_EXAMPLES) % N_CLASSES).astype(np.int32)
-    ds = O.synth_pixels(DATA_SEED, 0, N_EXAMPLES, P)
-    rates = []
-    if O.ref_available():
-        R = O.REF
-        off = np.zeros(N_CLASSES + 1, np.uint64)
-        mem = np.zeros(N_EXAMPLES, np.int64)
-        buf = ct.create_string_buffer(512)
-        R.ref_class_index(O.ptr(labels, O.i32p), N_EXAMPLES, N_CLASSES, O.ptr(off, O.u64p), O.ptr(mem, O.i64p),
-                          buf, 512)
-        w = np.full(N_CLASSES, 1.0 / N_CLASSES)
-        st = ct.c_int(0)
-        h = R.ref_cursor_create(O.ptr(w, O.f64p), N_CLASSES, BATCH, SEED, O.ptr(off, O.u64p), O.ptr(mem, O.i64p),
-                                ct.byref(st), buf, 512)
-        dsh = R.ref_dataset_create(O.ptr(ds, O.u8p), N_EXAMPLES, 32, 32, 3)
-        ex = np.zeros(n_batches_sample * BATCH, np.int64)
-        chk = ct.c_uint64(0)
-        for _ in range(repeats):
-            t0 = time.perf_counter()
-            R.ref_cursor_next(h, n_batches_sample, O.ptr(ex, O.i64p), None)
-            t_sbs = time.perf_counter() - t0
-            secs = R.ref_bench_roundtrip(dsh, MODE, O.ptr(ex, O.i64p), n_batches_sample, BATCH, threads, 0,
-                                         ct.byref(chk))
-            rates.append(n_batches_sample * BATCH / (secs + t_sbs))
-        R.ref_dataset_destroy(dsh)
-        R.ref_cursor_destroy(h)
-        kind = "reference"
-    else:
-        off, mem = O.class_index(labels, N_CLASSES)
-        cur = O.Cursor(O.sbs_plan([1.0 / N_CLASSES] * N_CLASSES, BATCH), off, mem, BATCH, SEED)
-        for _ in range(repeats):
-            t0 = time.perf_counter()
-            ex, _ = cur.next(n_batches_sample)
-            cont, _ = O.encode_stream(ds, ex, MODE, PER_CHUNK, BATCH, n_batches_sample)
-            O.decode_stream(cont, None, MODE, PER_CHUNK, P, BATCH, n_batches_sample)
-            rates.append(n_batches_sample * BATCH / (time.perf_counter() - t0))
-        kind, threads = "port", 1
-    sample = (f"{n_batches_sample} batches x {BATCH} images of the C2 stream (SBS draws + image_of gather + "
-              f"codec::encode/decode per 16-image chunk), {threads} host threads, median of {repeats}")
-    return statistics.median(rates), kind, sample, threads
+    return O.synth_pixels(DATA_SEED, 0, N_EXAMPLES, P), labels
 
 
 def run_reference(args):
@@ -215,129 +282,274 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
+    ds, labels = host_dataset()
+    rb = RefBaseline(ds, labels)
     sample_batches = max(threads * 2, 8)
     for _ in range(args.warmup):
-        reference_rate(sample_batches, threads, 1)
+        rb.rate(sample_batches, threads)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, kind, sample, used = reference_rate(sample_batches, threads, 1)
+        v, sample, used = rb.rate(sample_batches, threads)
         vals.append(v)
     wall = time.perf_counter() - t0
+    rb.close()
     v = statistics.median(vals)
     line = {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": config(world, args.steps_per_draw), "impl": "reference",
-            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": kind, "sample": sample},
+            "config": config(world), "impl": "reference",
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": rb.kind,
+                             "sample": sample + f", median of {args.steps} steps", "cpu_model": cpu_model()},
             "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
-def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, world, rows, images_per_step, red_dev):
-    """End-to-end steps with host buffers in and out (see main).  Two legs:
-    optb_pipeline_step_host -- ONE C-ABI call per step: the epoch's pinned host
+
+# ---------------------------------------------------------------- launcher
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch this script with N ranks, one
+    per GPU, and pass rank 0's line through."""
+    import torch
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {n_dev} GPU(s) visible", file=sys.stderr, flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: launching " + " ".join(cmd[2:6]), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def b2b_time(torch, fn, stream, reps, warm=3):
+    """Per-launch time of `reps` back-to-back calls: CUDA events only around
+    the whole run (an event between two launches would stop them from
+    overlapping ramp and drain)."""
+    for _ in range(warm):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps / 1e3
+
+
+# ---------------------------------------------------------------- the other BASELINE configs
+def config_suite(torch, pkg, dev, stream, peak, quick=False):
+    """C1-C4 (and C2 with SBS) on this GPU: the fused round trip
+    (optb_roundtrip_dev) and the separate encode / decode launches, each
+    timed back to back over a working set larger than L2.  Fractions: HBM
+    bytes of the kernel that ran (interleaved: the container re-read is an L2
+    hit) and the SURVEY 8(d) bytes (all encode + decode bytes) over the
+    measured copy peak."""
+    from paper_2105_00619_b200.pipeline import Pipeline
+    C, S = pkg.codec, pkg.sampler
+    res = {}
+    reps = 5 if quick else 10
+
+    def case(name, mode, per_chunk, Pp, B, nb, out_dtype=None, scale=1.0, rotate=1):
+        out_dtype = out_dtype or torch.uint8
+        L = C.layout(mode, per_chunk, Pp, B, nb)
+        rows = B * nb
+        with torch.cuda.stream(stream):
+            bufs = []
+            for _ in range(rotate):
+                src = torch.randint(0, 256, (rows, Pp), dtype=torch.uint8, device=dev)
+                cont, offs = C.alloc_stream(L, dev.index)
+                out = torch.empty((rows, Pp), dtype=out_dtype, device=dev)
+                bufs.append((src, cont, offs, out))
+            k = [0]
+
+            def pick():
+                b = bufs[k[0] % rotate]
+                k[0] += 1
+                return b
+
+            def rt():
+                src, cont, offs, out = pick()
+                C.roundtrip_dev(L, src, cont, out, offsets=offs, scale=scale, stream=stream)
+
+            def enc():
+                src, cont, offs, _ = pick()
+                C.encode_dev(L, src, cont, offs, stream=stream)
+
+            def dec():
+                _, cont, offs, out = pick()
+                C.decode_dev(L, cont, out, offsets=offs, scale=scale, stream=stream)
+            t_rt = b2b_time(torch, rt, stream, reps * rotate)
+            C.sync(dev.index, stream)
+            kind = C.last_roundtrip_kind()
+            rt_b = C.roundtrip_hbm_bytes(L, out.element_size(), False)
+            t_enc = b2b_time(torch, enc, stream, reps * rotate)
+            t_dec = b2b_time(torch, dec, stream, reps * rotate)
+            C.sync(dev.index, stream)
+            # check: the fused round trip reproduces the input (every mode is
+            # exact below its exact capacity; checker only, outside the timing)
+            src, cont, offs, out = bufs[0]
+            C.roundtrip_dev(L, src, cont, out, offsets=offs, scale=1.0, stream=stream)
+            C.sync(dev.index, stream)
+            ok = bool(torch.equal(out.to(torch.float32) if out.dtype != torch.uint8 else out,
+                                  src.to(torch.float32) if out.dtype != torch.uint8 else src))
+        cb, ob = C.container_bytes(L), C.offsets_bytes(L)
+        es = out.element_size()
+        enc_b = rows * Pp + cb + ob
+        dec_b = cb + ob + rows * Pp * es
+        s8d = enc_b + dec_b
+        res[name] = {"mode": C.mode_name(mode), "per_chunk": per_chunk, "images_per_launch": rows, "P": Pp,
+                     "out": str(out_dtype).replace("torch.", ""), "value": round(rows / t_rt, 1), "unit": UNIT,
+                     "kernel": kind, "roundtrip_us": round(t_rt * 1e6, 2),
+                     "hbm_bytes_per_launch": rt_b, "hbm_frac": round(rt_b / t_rt / 1e9 / peak, 4),
+                     "survey_8d_bytes_per_launch": s8d, "survey_8d_frac": round(s8d / t_rt / 1e9 / peak, 4),
+                     "encode_us": round(t_enc * 1e6, 2), "decode_us": round(t_dec * 1e6, 2),
+                     "encode_frac": round(enc_b / t_enc / 1e9 / peak, 4),
+                     "decode_frac": round(dec_b / t_dec / 1e9 / peak, 4),
+                     "split_value": round(rows / (t_enc + t_dec), 1), "check": ok}
+        del bufs
+        torch.cuda.empty_cache()
+
+    scale = float(np.float32(1.0) / np.float32(255.0))
+    # C1: CIFAR-10 batches of 128, exact64 (8 -> 1), streamed 512 batches per launch
+    case("C1_exact64_u8", 0, 8, 3072, 128, 512)
+    case("C1_exact64_f32", 0, 8, 3072, 128, 512, torch.float32, scale)
+    # C3: packing-ratio sweep on batches of 4096, 16 batches per launch
+    for n in (2, 4, 8):
+        case(f"C3_n{n}_exact64", 0, n, 3072, 4096, 16)
+    case("C3_n16_exact128", 1, 16, 3072, 4096, 16)
+    if not quick:
+        case("C3_n9_lossless64", 3, 9, 3072, 4096, 16)
+        case("C3_n18_lossless128", 4, 18, 3072, 4096, 16)
+        case("C3_n6_f64", 2, 6, 3072, 4096, 16)
+    # C4: ImageNet 256 x 224x224x3, 16x packing, fused decode -> bf16: one
+    # 256-image batch per launch rotating over 8 batches (each launch's
+    # 154 MB working set was evicted by the seven before it), and 8 batches
+    # per launch
+    IMG = 224 * 224 * 3
+    case("C4_exact128_bf16", 1, 16, IMG, 256, 1, torch.bfloat16, scale, rotate=8)
+    case("C4_exact128_bf16_8batches", 1, 16, IMG, 256, 8, torch.bfloat16, scale)
+    if not quick:
+        case("C4_exact128_u8_8batches", 1, 16, IMG, 256, 8)
+
+    # C2: the CIFAR-100 workload with SBS (the round-1 headline): 50 000
+    # images, one epoch = 97 batches per step, draws 4 epochs per sampler call
+    N2, nb2 = 50000, 50000 // BATCH
+    with torch.cuda.stream(stream):
+        ctx = pkg._lib.context(dev.index)
+        import ctypes as ct
+        ds2 = torch.empty((N2, P), dtype=torch.uint8, device=dev)
+        pkg._lib.check(pkg._lib.lib.optb_synth_pixels_dev(ctx, DATA_SEED, 0, N2, P, ct.c_void_p(ds2.data_ptr()), P,
+                                                          ct.c_void_p(stream.cuda_stream)))
+        lab2 = torch.arange(N2, device=dev, dtype=torch.int32) % N_CLASSES
+        offs2, mem2 = S.class_index_dev(lab2, N_CLASSES, device=dev.index)
+        out2 = torch.empty((nb2 * BATCH, P), dtype=torch.uint8, device=dev)
+        for mode, pc, key in ((1, 16, "C2_sbs_exact128_u8"), (0, 8, "C2_sbs_exact64_u8")):
+            cur2 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs2, mem2,
+                                                   device=dev.index)
+            pipe2 = Pipeline(cur2, ds2, mode, BATCH, nb2, per_chunk=pc, device=dev.index, steps_per_draw=4)
+            t2 = b2b_time(torch, lambda: pipe2.step(out2, stream), stream, 40 if quick else 100, warm=8)
+            C.sync(dev.index, stream)
+            kind = C.last_roundtrip_kind()
+            L2 = pipe2.layout
+            rows2 = nb2 * BATCH
+            cb2 = C.container_bytes(L2)
+            hbm2 = 2 * rows2 * P + rows2 * 8 + cb2 + (0 if kind.startswith("interleaved") else cb2)
+            s8d2 = 2 * rows2 * P + rows2 * 8 + 2 * cb2
+            res[key] = {"mode": C.mode_name(mode), "per_chunk": pc, "images_per_step": rows2,
+                        "value": round(rows2 / t2, 1), "unit": UNIT, "ms_per_step": round(t2 * 1e3, 4),
+                        "kernel": kind, "hbm_bytes_per_step": hbm2, "hbm_frac": round(hbm2 / t2 / 1e9 / peak, 4),
+                        "survey_8d_frac": round(s8d2 / t2 / 1e9 / peak, 4),
+                        "note": "50000-image dataset (1.2x L2), 97 batches per step, SBS 4 epochs per sampler call"}
+            pipe2.close()
+        del ds2, out2
+        torch.cuda.empty_cache()
+    return res
+
+
+# ---------------------------------------------------------------- e2e
+def run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, world, rows, images_per_step,
+            ref_rows):
+    """End to end through the C ABI with HOST buffers, every step:
+    optb_pipeline_step_host -- ONE call per step: the epoch's pinned host
     dataset is uploaded into one of two device buffers (copy engine), the step
     runs, the decoded rows are downloaded into pinned host memory (second copy
-    engine); consecutive calls overlap both PCIe directions and the kernels --
-    and a zero-copy leg in which the gather kernel reads the drawn rows
-    straight from pinned host memory."""
-    out_shape = (rows, P)
-    oversub = red_dev.type == "cpu"  # ranks share GPUs: per-rank times summed
+    engine); consecutive calls overlap both PCIe directions and the kernels.
+    `ref_rows(k)` gives the reference cursor's rows of step k (checker)."""
     ds_host = ds.cpu().pin_memory()
-    d2h = torch.cuda.Stream(dev)
     plan2 = S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED)
-    results = []
-    for zero_copy in (False, True):
-        cur2 = S.BatchCursor.from_device_index(plan2, offs, mem, device=dev.index)
-        pipe2 = Pipeline(cur2, ds_host if zero_copy else ds, MODE, BATCH, BATCHES_PER_STEP,
-                         per_chunk=PER_CHUNK, shard=rank, n_shards=world, device=dev.index,
-                         steps_per_draw=args.steps_per_draw)
-        outs = [torch.empty(out_shape, dtype=torch.uint8, device=dev) for _ in range(2)]
-        out_hosts = [torch.empty(out_shape, dtype=torch.uint8).pin_memory() for _ in range(2)]
-        ev = lambda: torch.cuda.Event()  # noqa: E731
-        dec_done, down_done = [ev(), ev()], [ev(), ev()]
-        k_state = [0]
+    cur2 = S.BatchCursor.from_device_index(plan2, offs, mem, device=dev.index)
+    pipe2 = Pipeline(cur2, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
+                     device=dev.index)
+    out_hosts = [torch.empty((rows, P), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    k = [0]
 
-        def step():
-            k = k_state[0]
-            b = k % 2
-            if not zero_copy:
-                pipe2.step_host(ds_host, out_hosts[b], stream)
-            else:
-                if k >= 2:
-                    stream.wait_event(down_done[b])
-                pipe2.step(outs[b], stream)
-                dec_done[b].record(stream)
-                d2h.wait_event(dec_done[b])
-                with torch.cuda.stream(d2h):
-                    out_hosts[b].copy_(outs[b], non_blocking=True)
-                down_done[b].record(d2h)
-            k_state[0] += 1
+    def step():
+        pipe2.step_host(ds_host, out_hosts[k[0] % 2], stream)
+        k[0] += 1
 
-        def wait_all():
-            if not zero_copy:
-                pipe2.host_wait(stream)
-            else:
-                stream.wait_event(down_done[(k_state[0] - 1) % 2])
-
-        with torch.cuda.stream(stream):
-            for _ in range(max(4, args.warmup)):  # includes the sampler's generation-pool growth
-                step()
-            wait_all()
-            torch.cuda.synchronize(dev)
-            if world > 1:
-                coll_barrier(dist)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.e2e_steps):
-                step()
-            wait_all()
-            e1.record(stream)
-            e1.synchronize()
-            torch.cuda.synchronize(dev)
-            ms = e0.elapsed_time(e1) / args.e2e_steps
-            cur3 = S.BatchCursor.from_device_index(plan2, offs, mem, device=dev.index)
-            for _ in range(k_state[0]):
-                ex3, _ = cur3.next_dev(BATCHES_PER_STEP * world, shard=rank, n_shards=world)
-            ok = bool(torch.equal(out_hosts[(k_state[0] - 1) % 2], ds_host[ex3.cpu()]))
-            pipe2.close()
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            step()
+        pipe2.host_wait(stream)
+        torch.cuda.synchronize(dev)
         if world > 1:
-            ms = coll_reduce_ms(torch, dist, ms)
-        h2d_bytes = rows * P if zero_copy else ds_host.numel()
-        results.append({"value": round(images_per_step / (ms / 1e3), 1), "unit": UNIT,
-                        "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": rows * P,
-                        "ms_per_step": round(ms, 3), "check": ok,
-                        "path": ("pinned host dataset read zero-copy by the gather-encode kernel -> decode -> "
-                                 "D2H of the decoded rows (copy stream, double-buffered)") if zero_copy else
-                                ("optb_pipeline_step_host, one C-ABI call per step: bulk H2D of the epoch's pinned "
-                                 "host dataset into one of two device buffers (copy engine) -> SBS draws + fused "
-                                 "gather-encode-decode -> D2H of the decoded rows to pinned host (second copy "
-                                 "engine); consecutive steps overlap both PCIe directions")})
-    return results[0], results[1]
+            coll_barrier(dist)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            step()
+        pipe2.host_wait(stream)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / args.e2e_steps
+    last = k[0] - 1
+    want = ref_rows(last)
+    ok = None if want is None else bool(torch.equal(out_hosts[last % 2], ds_host[torch.from_numpy(want)]))
+    pipe2.close()
+    if world > 1:
+        ms = coll_reduce_ms(torch, dist, ms)
+    h2d, d2h = ds_host.numel(), rows * P
+    del out_hosts, ds_host
+    return {"value": round(images_per_step / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3),
+            "pcie_gbs_achieved": round((h2d + d2h) / (ms / 1e3) / 1e9, 1), "check": ok,
+            "check_against": "rank 0: the decoded rows of the last step == dataset rows the reference cursor draws",
+            "path": ("optb_pipeline_step_host, one C-ABI call per step: bulk H2D of the epoch's pinned host dataset "
+                     "(3.2 GB) into one of two device buffers (copy engine) -> SBS draws + fused "
+                     "gather-encode-decode -> D2H of the decoded rows (3.2 GB) to pinned host (second copy engine); "
+                     "consecutive steps overlap both PCIe directions and the kernels")}
 
 
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--sharded-steps", type=int, default=3,
-                    help="N > 1 only: steps of the dataset-sharded (all-to-all) variant")
+                    help="N > 1 only: steps of the dataset-sharded variants")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--split-steps", type=int, default=50,
-                    help="steps of the same pipeline with separate encode / decode launches (per-kernel view)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 / C2 sub-keys")
+    ap.add_argument("--no-check", action="store_true", help="skip the reference check of the last step")
+    ap.add_argument("--probe-steps", type=int, default=6,
+                    help="steps of the per-kernel timing pass (events around every launch)")
     ap.add_argument("--split-kernels", action="store_true",
                     help="headline with separate encode / decode launches instead of the fused round trip")
-    ap.add_argument("--steps-per-draw", type=int, default=4,
-                    help="epochs of SBS draws computed per sampler call (amortises its fixed cost)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
 
     import ctypes as ct
 
@@ -348,6 +560,8 @@ def main():
     from paper_2105_00619_b200.pipeline import Pipeline
     C, S = pkg.codec, pkg.sampler
     rank, world, local = env_rank()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr, flush=True)
     n_dev = torch.cuda.device_count()
     local = local % n_dev
     torch.cuda.set_device(local)
@@ -355,9 +569,8 @@ def main():
     oversub = False
     if world > 1:
         # Rendezvous over gloo, then compare the ranks' GPU UUIDs: one process
-        # per GPU (however the launcher maps devices) runs every collective of
-        # the run over NCCL; ranks sharing a GPU (a smoke run of the sharded
-        # path on one device) keep gloo -- NCCL refuses two ranks per GPU.
+        # per GPU runs every collective of the run over NCCL; ranks sharing a
+        # GPU (a smoke run on one device) keep gloo -- NCCL refuses that.
         dist.init_process_group("gloo")
         uuids = [None] * world
         dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(local).uuid))
@@ -365,9 +578,13 @@ def main():
         COLL["group"] = None if oversub else dist.new_group(backend="nccl")
         COLL["device"] = torch.device("cpu") if oversub else dev
         COLL["op"] = dist.ReduceOp.SUM if oversub else dist.ReduceOp.MAX
-    red_dev = torch.device("cpu") if oversub else dev
+        if not oversub:
+            coll_barrier(dist)  # first NCCL collective: the communicator is up
+        print(f"bench.py: rank {rank}/{world} on cuda:{local} ({uuids[rank]}), control plane "
+              f"{'gloo (GPUs shared)' if oversub else 'NCCL'}", file=sys.stderr, flush=True)
+    peak, peak_kind = measured_peak()
 
-    stream = torch.cuda.Stream(dev, priority=int(os.environ.get("OPTB_BENCH_PRIO", "0")))
+    stream = torch.cuda.Stream(dev)
     rows = BATCH * BATCHES_PER_STEP
     with torch.cuda.stream(stream):
         ctx = pkg._lib.context(local)
@@ -380,17 +597,12 @@ def main():
         cur = S.BatchCursor.from_device_index(plan, offs, mem, device=local)
         out = torch.empty((rows, P), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize(dev)
-    # The native E-D pipeline (optb_pipeline_*): per step, SBS draws of step
-    # k+1 on a side stream overlap gather-encode + decode of step k.
-    tstride = TIMING_STRIDE if args.steps >= 4 * TIMING_STRIDE else 1  # short runs: every step
-    # per-kernel timing events on every TIMING_STRIDE-th step only: an event
-    # between two round-trip launches stops the second from overlapping its
-    # launch ramp with the first one's drain (programmatic dependent launch)
-    pipe = Pipeline(cur, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
-                    device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
-                    split_kernels=args.split_kernels, timing_stride=tstride)
-    L = pipe.layout
 
+    # ---- headline: K back-to-back pipeline steps, CUDA events only around
+    # the whole timed region (an event between two round trips would stop
+    # the next one from overlapping its launch ramp with this one's drain)
+    pipe = Pipeline(cur, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world,
+                    device=local, split_kernels=args.split_kernels)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             pipe.step(out, stream)
@@ -410,264 +622,229 @@ def main():
             t_enqueue = time.perf_counter() - t_wall0
             end.synchronize()
             t_wall = time.perf_counter() - t_wall0
+        torch.cuda.synchronize(dev)
         if world > 1:
             coll_barrier(dist)
         C.sync(local, stream)
         launches = pkg._lib.launches(local) - launches0
-    # per-kernel durations of the last (up to 60) timed steps -- the
-    # pipeline keeps a 64-step ring of timing events
-    timed = [k for k in range(args.warmup, args.warmup + args.steps) if k % tstride == 0][-60:]
-    tim = [pipe.timings(k) for k in timed]
-    t_sbs, t_enc, t_dec = [t[0] for t in tim], [t[1] for t in tim], [t[2] for t in tim]
+    rt_kind = C.last_roundtrip_kind()
+    fused = pipe.fused
+    cont_bytes = C.container_bytes(pipe.layout)
     ms = start.elapsed_time(end) / args.steps
+    ms_local = ms
     if world > 1:
-        # one GPU per rank: max over ranks.  Oversubscribed smoke runs (ranks
-        # share a GPU, whose timed regions may or may not overlap): the sum,
-        # so the whole-job rate is never overstated.
         ms = coll_reduce_ms(torch, dist, ms)
     images_per_step = rows * world
     value = images_per_step / (ms / 1e3)
 
-    # roofline for the dominant kernel (per-launch algorithmic bytes / launch time)
-    enc_ms, dec_ms = statistics.mean(t_enc), statistics.mean(t_dec)
-    cont_bytes = C.container_bytes(L)
-    enc_bytes = rows * P + cont_bytes + rows * 8  # gathered rows + containers + row index
-    dec_bytes = cont_bytes + rows * P
-    peak, peak_kind = measured_peak()
-    fused = pipe.fused
-    if fused and statistics.mean(t_dec) > 0.005:
-        raise RuntimeError("pipeline reported separate decode launches on the fused path")
-    # The fused launch for exact128 is the interleaved kernel (k_roundtrip_il;
-    # the library reports which kernel the last step ran): each container
-    # tile is read back while still in L2, so its HBM bytes are the
-    # compulsory ones -- gathered rows + row ids in, containers + decoded rows
-    # out.  The SURVEY 8(d) figure (which also counts the container re-read)
-    # is reported beside it.
-    rt_kind = C.last_roundtrip_kind()
+    # ---- check (reference cursor = checker, outside every timed region):
+    # the last timed step's decoded rows are the dataset rows the reference
+    # cursor draws, and its containers are their exact128 packing (at
+    # capacity: the [16][P] -> [P][16] byte transpose of each chunk)
+    ref = None
+    check = None
+    if rank == 0 and not args.no_check:
+        try:
+            ref = RefStream(labels.cpu().numpy(), world, rank)
+            for _ in range(args.warmup + args.steps - 1):
+                ref.step(BATCHES_PER_STEP)
+            want = torch.from_numpy(ref.step(BATCHES_PER_STEP)).to(dev)
+            rows_ok = bool(torch.equal(out, ds[want]))
+            cont = _dev_bytes(torch, pipe.containers_ptr(), cont_bytes, dev)
+            packed = ds[want].view(-1, PER_CHUNK, P).transpose(1, 2).contiguous().view(-1)
+            cont_ok = bool(torch.equal(cont, packed))
+            check = {"ok": rows_ok and cont_ok, "decoded_rows": rows_ok, "containers": cont_ok,
+                     "against": f"{ref.kind} BatchCursor (oracle/_ref = the reference compiled from its sources) "
+                                "draws of the last timed step, rank 0's batches"}
+            del cont, packed, want
+        except Exception as ex:  # noqa: BLE001
+            check = {"ok": False, "error": f"{type(ex).__name__}: {ex}"[:300]}
+
+    # ---- per-kernel durations: a separate pass with events around every
+    # launch (isolated launches, no overlap with their neighbours)
+    probe = Pipeline(S.BatchCursor.from_device_index(plan, offs, mem, device=local), ds, MODE, BATCH,
+                     BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank, n_shards=world, device=local,
+                     record_timings=True, split_kernels=args.split_kernels)
+    with torch.cuda.stream(stream):
+        for _ in range(2 + args.probe_steps):
+            probe.step(out, stream)
+        C.sync(local, stream)
+    tim = [probe.timings(k) for k in range(2, 2 + args.probe_steps)]
+    probe.close()
+    t_sbs = statistics.mean(t[0] for t in tim)
+    t_k1 = statistics.mean(t[1] for t in tim)
+    t_k2 = statistics.mean(t[2] for t in tim)
+
+    # ---- roofline of the dominant kernel.  The timed region runs nothing
+    # but the step's launches on this stream (the draws are on the side
+    # stream), so the kernel's average launch duration over the timed region
+    # is the region time / K.
     interleaved = fused and rt_kind.startswith("interleaved")
-    l2_bytes = 0
-    if interleaved:
-        kname, kms, kbytes = "k_roundtrip_il<exact128,u8>", enc_ms, enc_bytes + rows * P
-        l2_bytes = cont_bytes
-    elif fused:  # phase-ordered: every byte of encode + decode is an HBM byte
-        kname, kms, kbytes = "k_roundtrip_vec<exact128,u8>", enc_ms, enc_bytes + dec_bytes
-    elif enc_ms >= dec_ms:
-        kname, kms, kbytes = "k_encode_vec<exact128>", enc_ms, enc_bytes
+    gathered = rows * P + rows * 8      # gathered rows + row ids in
+    if fused:
+        kname = "k_roundtrip_il<exact128,u8>" if interleaved else "k_roundtrip_vec<exact128,u8>"
+        kbytes = gathered + cont_bytes + rows * P + (0 if interleaved else cont_bytes)
+        k_ms_region = ms_local
     else:
-        kname, kms, kbytes = "k_decode_vec<exact128,u8>", dec_ms, dec_bytes
-    achieved = kbytes / (kms / 1e3) / 1e9
-    nsum = ncu_traffic()
-    traffic = None
-    if nsum:  # ncu names carry every template argument: match on the prefix
-        for kn, kv in nsum.get("kernels", {}).items():
-            if kn == kname or kn.startswith(kname[:-1] + ","):
-                traffic = kv.get("dram_bytes_per_launch")
-                break
+        kname, kbytes = "k_encode_bulk<exact128>", gathered + cont_bytes
+        k_ms_region = ms_local * t_k1 / (t_k1 + t_k2)
+    s8d_bytes = gathered + 2 * cont_bytes + rows * P
+    achieved = kbytes / (k_ms_region / 1e3) / 1e9
+    traffic, traffic_tag = ncu_traffic(kname)
     roofline = {"bound": "hbm", "kernel": kname, "kernel_kind": rt_kind,
-                "launch_timing": ("CUDA events on the launching stream around every %d-th timed step's launch; "
-                                  "those launches cannot overlap their neighbours (an event sits between), so this "
-                                  "is the isolated launch duration -- back-to-back steps overlap ramp and tail "
-                                  "(step_gbs)" % tstride),
-                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "peak_source": peak_kind, "traffic": traffic,
+                "launch_timing": "CUDA events around the timed region on the launching stream, which runs only "
+                                 "this kernel (one launch per step, back to back): region time / K",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "peak_source": peak_kind, "traffic": traffic, "traffic_source": f"profiles/ncu_summary.json ({traffic_tag})",
                 "frac_of_spec_8tbs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": kbytes,
-                "l2_served_bytes_per_launch": l2_bytes,
-                "survey_8d_bytes_per_launch": kbytes + l2_bytes,
-                "survey_8d_gbs": round((kbytes + l2_bytes) / (kms / 1e3) / 1e9, 1),
-                "host_enqueue_us_per_step": round(t_enqueue / args.steps * 1e6, 1),
-                "kernels_ms": ({"sbs_side_stream": round(statistics.mean(t_sbs), 4),
-                                "roundtrip": round(enc_ms, 4)} if fused else
-                               {"sbs_side_stream": round(statistics.mean(t_sbs), 4), "encode": round(enc_ms, 4),
-                                "decode": round(dec_ms, 4)}),
-                "step_gbs": round((kbytes if fused else enc_bytes + dec_bytes) / (ms / 1e3) / 1e9, 1),
-                "step_frac": round((kbytes if fused else enc_bytes + dec_bytes) / (ms / 1e3) / 1e9 / peak, 4)}
+                "algorithmic_bytes_note": ("compulsory HBM bytes: 3072 B gathered row + 8 B row id in, 3072 B "
+                                           "container + 3072 B decoded row out per image; the container re-read "
+                                           "is served from L2" if interleaved else "every encode + decode byte"),
+                "survey_8d_bytes_per_launch": s8d_bytes,
+                "survey_8d_gbs": round(s8d_bytes / (k_ms_region / 1e3) / 1e9, 1),
+                "isolated_launch_ms": round(t_k1, 4),
+                "isolated_launch_frac": round(kbytes / (t_k1 / 1e3) / 1e9 / peak, 4),
+                "sbs_side_stream_ms_per_step": round(t_sbs, 4),
+                "host_enqueue_us_per_step": round(t_enqueue / args.steps * 1e6, 1)}
     if not fused:
-        roofline["encode_gbs"] = round(enc_bytes / (enc_ms / 1e3) / 1e9, 1)
-        roofline["decode_gbs"] = round(dec_bytes / (dec_ms / 1e3) / 1e9, 1)
-    # the same pipeline with separate encode / decode launches per step
-    # (optb_encode_dev + optb_decode_dev), for the per-kernel view
-    split = None
-    if fused and args.split_steps > 0:
-        with torch.cuda.stream(stream):
-            cur5 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                   device=local)
-            pipe5 = Pipeline(cur5, ds, MODE, BATCH, BATCHES_PER_STEP, per_chunk=PER_CHUNK, shard=rank,
-                             n_shards=world, device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
-                             split_kernels=True)
-            for _ in range(args.warmup):
-                pipe5.step(out, stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.split_steps):
-                pipe5.step(out, stream)
-            e1.record(stream)
-            e1.synchronize()
-            sms_ = e0.elapsed_time(e1) / args.split_steps
-            if world > 1:
-                sms_ = coll_reduce_ms(torch, dist, sms_)
-            tim5 = [pipe5.timings(k) for k in range(max(args.warmup, args.warmup + args.split_steps - 60),
-                                                     args.warmup + args.split_steps)]
-            pipe5.close()
-        e5, d5 = statistics.mean(t[1] for t in tim5), statistics.mean(t[2] for t in tim5)
-        split = {"ms_per_step": round(sms_, 4), "value": round(images_per_step / (sms_ / 1e3), 1),
-                 "encode_ms": round(e5, 4), "decode_ms": round(d5, 4),
-                 "encode_gbs": round(enc_bytes / (e5 / 1e3) / 1e9, 1),
-                 "decode_gbs": round(dec_bytes / (d5 / 1e3) / 1e9, 1)}
+        roofline["decode_isolated_ms"] = round(t_k2, 4)
 
-    # e2e: host buffers in and out, every step.  The epoch's input rows live
-    # in pinned host memory; each step uploads the dataset epoch with one bulk
-    # H2D copy (copy engine) into one of two device buffers while the previous
-    # step computes, gathers / encodes / decodes from it, and copies the
-    # decoded rows back to pinned host memory on a D2H stream (double-buffered,
-    # so both PCIe directions and the kernels overlap).  The zero-copy variant
-    # (the gather kernel reads the drawn rows straight from pinned memory) is
-    # reported alongside.
-    e2e = e2e_zc = None
+    configs = None
+    if not args.no_configs and rank == 0:
+        configs = config_suite(torch, pkg, dev, stream, peak, quick=world > 1)
+
+    e2e = None
     if args.e2e_steps > 0:
-        e2e, e2e_zc = run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, world, rows,
-                              images_per_step, red_dev)
-        # this box's pinned-memory PCIe bandwidth (same-size copies, same
-        # run): the e2e leg is transfer-bound, so its bound is what these allow
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import pcie_probe
-        pc = pcie_probe.measure(torch, BATCH * BATCHES_PER_STEP * P)
-        bound_ms = max(e2e["h2d_bytes_per_step"] / pc["h2d_gbs"], e2e["d2h_bytes_per_step"] / pc["d2h_gbs"],
-                       (e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]) / pc["bidir_gbs"]) / 1e6
-        # (the probe's copies run once, after the e2e leg: a frac slightly
-        # above 1 means the link was a little faster during the leg)
-        e2e["pcie"] = dict(pc, bound_ms_per_step=round(bound_ms, 3),
-                           frac_of_pcie_bound=round(bound_ms / e2e["ms_per_step"], 3))
-    # The same workload in exact64 (8 images per 64-bit word; SURVEY §8:
-    # BASELINE.json does not name C2's mode -- the headline uses the
-    # reference default exact128, this is the other exact mode)
-    exact64 = None
-    if args.split_steps > 0:
-        with torch.cuda.stream(stream):
-            cur7 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                   device=local)
-            t7 = TIMING_STRIDE if args.split_steps >= 4 * TIMING_STRIDE else 1
-            pipe7 = Pipeline(cur7, ds, 0, BATCH, BATCHES_PER_STEP, per_chunk=8, shard=rank, n_shards=world,
-                             device=local, record_timings=True, steps_per_draw=args.steps_per_draw,
-                             timing_stride=t7)
-            for _ in range(args.warmup):
-                pipe7.step(out, stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.split_steps):
-                pipe7.step(out, stream)
-            e1.record(stream)
-            e1.synchronize()
-            ms7 = e0.elapsed_time(e1) / args.split_steps
-            if world > 1:
-                ms7 = coll_reduce_ms(torch, dist, ms7)
-            k7 = statistics.mean(pipe7.timings(k)[1] for k in range(args.warmup, args.warmup + args.split_steps)
-                                 if k % t7 == 0)
-            il7 = C.last_roundtrip_kind().startswith("interleaved")
-            pipe7.close()
-        cb7 = C.container_bytes(C.layout(0, 8, P, BATCH, BATCHES_PER_STEP))
-        # HBM bytes: rows in, containers out, rows out (+ the container
-        # re-read for the phase-ordered kernel; interleaved: an L2 hit)
-        b7 = 2 * rows * P + cb7 + rows * 8 + (0 if il7 else cb7)
-        exact64 = {"mode": "exact64", "per_chunk": 8, "ms_per_step": round(ms7, 4),
-                   "kernel": "k_roundtrip_il<exact64,u8>" if il7 else "k_roundtrip_vec<exact64,u8>",
-                   "value": round(images_per_step / (ms7 / 1e3), 1), "kernel_ms": round(k7, 4),
-                   "kernel_gbs": round(b7 / (k7 / 1e3) / 1e9, 1), "kernel_frac": round(b7 / (k7 / 1e3) / 1e9 / peak, 4)}
+        def ref_rows(k):
+            if ref is None:
+                return None
+            r2 = RefStream(labels.cpu().numpy(), world, rank)
+            for _ in range(k):
+                r2.step(BATCHES_PER_STEP)
+            w = r2.step(BATCHES_PER_STEP)
+            r2.close()
+            return w
+        pipe.close()
+        pipe = None
+        torch.cuda.empty_cache()
+        e2e = run_e2e(args, torch, dist, S, Pipeline, ds, offs, mem, stream, dev, rank, world, rows,
+                      images_per_step, ref_rows)
 
-    # N > 1: the optional dataset-sharded variants (each rank holds 1/N of the
-    # dataset), reported separately from the headline.  "peer": the shards are
-    # mapped over CUDA IPC and the fused roundtrip kernel gathers each drawn
-    # row from the GPU that owns it (NVLink peer loads), device-timed with
-    # CUDA events, max over ranks.  "a2a": drawn rows cross ranks in one
-    # all-to-all per step (host-driven, wall clock around synchronised steps).
-    sharded = sharded_a2a = None
+    # ---- N > 1: the optional dataset-sharded variants (each rank holds 1/N
+    # of the dataset), reported separately from the headline
+    sharded = None
     if world > 1 and args.sharded_steps > 0:
-        from paper_2105_00619_b200.sharded import PeerShardedGather, ShardedGather
-        per = (N_EXAMPLES + world - 1) // world
-        # optional legs: a failure (e.g. peers not mappable when each process
-        # sees one GPU) is reported in the line instead of ending the run
-        with torch.cuda.stream(stream):
-            local_rows = ds[rank * per:(rank + 1) * per].clone()
-        try:
-            with torch.cuda.stream(stream):
-                cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                       device=local)
-                pg = PeerShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP,
-                                       device=local)
-                for _ in range(args.warmup):
-                    pg.step(out, stream)
-                torch.cuda.synchronize(dev)
-                coll_barrier(dist)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(args.sharded_steps):
-                    pg.step(out, stream)
-                e1.record(stream)
-                e1.synchronize()
-                pms = e0.elapsed_time(e1) / args.sharded_steps
-                # check the last step against the replicated dataset
-                cur6 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                       device=local)
-                for _ in range(args.warmup + args.sharded_steps):
-                    ex6, _ = cur6.next_dev(BATCHES_PER_STEP * world, shard=rank, n_shards=world)
-                pok = bool(torch.equal(out, ds[ex6]))
-                remote = int(((ex6 // per) != rank).sum())
-                pg.close()
-                pms = coll_reduce_ms(torch, dist, pms)
-            sharded = {"value": round(images_per_step / (pms / 1e3), 1), "unit": UNIT, "ms_per_step": round(pms, 3),
-                       "exchange": "peer memory: CUDA IPC-mapped shards read by the fused gather-encode-decode kernel "
-                                   "(optb_roundtrip_rows_dev)" + (" -- ranks share one GPU (smoke run)" if oversub else
-                                                                 " over NVLink / NVSwitch"),
-                       "rows_from_peers_per_step_rank0": remote, "bytes_from_peers_per_step_rank0": remote * P,
-                       "check": pok, "timing": "CUDA events on the launching stream, max over ranks (sum when ranks share a GPU)"}
-        except Exception as ex:  # noqa: BLE001
-            sharded = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
-        try:
-            with torch.cuda.stream(stream):
-                cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
-                                                       device=local)
-                sg = ShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP, device=local,
-                                   exchange="gloo" if oversub else "nccl", group=COLL["group"])
-                sg.step(out)
-                torch.cuda.synchronize(dev)
-                coll_barrier(dist)
-                t0 = time.perf_counter()
-                moved = 0
-                for _ in range(args.sharded_steps):
-                    _, recv = sg.step(out)
-                    moved += (sum(recv) - recv[rank]) * P
-                torch.cuda.synchronize(dev)
-                sms = (time.perf_counter() - t0) / args.sharded_steps * 1e3
-                sms = coll_reduce_ms(torch, dist, sms)
-            sharded_a2a = {"value": round(images_per_step / (sms / 1e3), 1), "unit": UNIT, "ms_per_step": round(sms, 3),
-                           "exchange": "gloo (oversubscribed smoke run)" if oversub else "nccl all_to_all_single",
-                           "bytes_exchanged_per_step_rank0": int(moved / args.sharded_steps),
-                           "timing": "host wall clock around synchronised steps (the exchange is host-driven)"}
-
-        except Exception as ex:  # noqa: BLE001
-            sharded_a2a = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
+        sharded = run_sharded(args, torch, dist, S, ds, offs, mem, out, stream, dev, rank, world, oversub,
+                              images_per_step)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU baseline runs at N = 1 only
         threads = os.cpu_count() or 1
-        v, kind, sample, used = reference_rate(max(threads * 2, 8), threads, 3)
-        cpu = {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": kind, "sample": sample}
+        ds_h, lab_h = host_dataset()
+        rb = RefBaseline(ds_h, lab_h)
+        runs = [rb.rate(max(threads * 2, 8), threads) for _ in range(3)]
+        runs1 = [rb.rate(4, 1) for _ in range(3)]
+        rb.close()
+        v, sample, used = sorted(runs)[1]
+        v1, sample1, _ = sorted(runs1)[1]
+        cpu = {"value": round(v, 1), "unit": UNIT, "cores": used, "kind": rb.kind, "sample": sample + ", median of 3",
+               "single_thread": {"value": round(v1, 1), "cores": 1, "sample": sample1 + ", median of 3"},
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+        del ds_h
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": config(world, args.steps_per_draw),
-                "roofline": roofline, "split_kernels": split, "exact64": exact64, "cpu_baseline": cpu, "e2e": e2e,
-                "e2e_zero_copy": e2e_zc,
-                "sharded_dataset": sharded, "sharded_dataset_a2a": sharded_a2a, "clocks": clk.summary(),
-                "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 4)}
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based SplitMix64 pixels, seed 7)",
+                "config": config(world), "roofline": roofline, "check": check, "cpu_baseline": cpu, "e2e": e2e,
+                "configs": configs, "sharded_dataset": sharded, "clocks": clk.summary(),
+                "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 4),
+                "timing": "CUDA events on the launching stream around the K timed steps only; max over ranks"}
         if oversub:
             line["oversubscribed"] = f"{world} ranks on {n_dev} GPU(s): per-rank device times summed"
         print(json.dumps(line), flush=True)
-    pipe.close()
+    if pipe is not None:
+        pipe.close()
+    if ref is not None:
+        ref.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _dev_bytes(torch, ptr, n, dev):
+    """A uint8 view of n device bytes at ptr (library-owned memory)."""
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_Arr(), device=dev)
+
+
+def run_sharded(args, torch, dist, S, ds, offs, mem, out, stream, dev, rank, world, oversub, images_per_step):
+    """Dataset-sharded global gather (optional).  "peer": the
+    shards are mapped over CUDA IPC and the fused round-trip kernel gathers
+    each drawn row from the GPU that owns it (NVLink peer loads), device-timed
+    with CUDA events, max over ranks.  "a2a": the drawn rows cross ranks in
+    one NCCL all-to-all per step (host-driven, wall clock)."""
+    from paper_2105_00619_b200.sharded import PeerShardedGather, ShardedGather
+    per = (N_EXAMPLES + world - 1) // world
+    res = {}
+    with torch.cuda.stream(stream):
+        local_rows = ds[rank * per:(rank + 1) * per].clone()
+    try:
+        with torch.cuda.stream(stream):
+            cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                   device=dev.index)
+            pg = PeerShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP,
+                                   device=dev.index)
+            for _ in range(args.warmup):
+                pg.step(out, stream)
+            torch.cuda.synchronize(dev)
+            coll_barrier(dist)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.sharded_steps):
+                pg.step(out, stream)
+            e1.record(stream)
+            e1.synchronize()
+            pms = e0.elapsed_time(e1) / args.sharded_steps
+            cur6 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                   device=dev.index)
+            for _ in range(args.warmup + args.sharded_steps):
+                ex6, _ = cur6.next_dev(BATCHES_PER_STEP * world, shard=rank, n_shards=world)
+            pok = bool(torch.equal(out, ds[ex6]))
+            remote = int(((ex6 // per) != rank).sum())
+            pg.close()
+            pms = coll_reduce_ms(torch, dist, pms)
+        res["peer"] = {"value": round(images_per_step / (pms / 1e3), 1), "unit": UNIT, "ms_per_step": round(pms, 3),
+                       "exchange": "CUDA IPC-mapped shards read by the fused gather-encode-decode kernel "
+                                   "(optb_roundtrip_rows_dev)" + (" -- ranks share one GPU" if oversub else
+                                                                  " over NVLink / NVSwitch"),
+                       "rows_from_peers_per_step_rank0": remote, "check": pok,
+                       "timing": "CUDA events on the launching stream, max over ranks"}
+    except Exception as ex:  # noqa: BLE001
+        res["peer"] = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
+    try:
+        with torch.cuda.stream(stream):
+            cur4 = S.BatchCursor.from_device_index(S.plan([1.0 / N_CLASSES] * N_CLASSES, BATCH, SEED), offs, mem,
+                                                   device=dev.index)
+            sg = ShardedGather(cur4, local_rows, N_EXAMPLES, rank, world, BATCH, BATCHES_PER_STEP,
+                               device=dev.index, exchange="gloo" if oversub else "nccl", group=COLL["group"])
+            sg.step(out)
+            torch.cuda.synchronize(dev)
+            coll_barrier(dist)
+            t0 = time.perf_counter()
+            for _ in range(args.sharded_steps):
+                sg.step(out)
+            torch.cuda.synchronize(dev)
+            sms = (time.perf_counter() - t0) / args.sharded_steps * 1e3
+            sms = coll_reduce_ms(torch, dist, sms)
+        res["a2a"] = {"value": round(images_per_step / (sms / 1e3), 1), "unit": UNIT, "ms_per_step": round(sms, 3),
+                      "exchange": "gloo (ranks share a GPU)" if oversub else "nccl all_to_all_single",
+                      "timing": "host wall clock around synchronised steps (the exchange is host-driven)"}
+    except Exception as ex:  # noqa: BLE001
+        res["a2a"] = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
+    return res
 
 
 if __name__ == "__main__":

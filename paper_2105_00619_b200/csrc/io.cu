@@ -223,6 +223,40 @@ __global__ void k_records_to_hwc(const uint8_t* __restrict__ src, uint64_t n_rec
   }
 }
 
+// Records too large to stage whole (P + 1 beyond the shared-memory budget,
+// e.g. 299x299x3): one CTA per (record, pixel tile).  The tile's bytes of
+// every channel plane are staged with coalesced loads, then written
+// channel-interleaved.
+__global__ void k_records_to_hwc_tiled(const uint8_t* __restrict__ src, uint64_t n_rec, uint32_t hw, uint32_t ch,
+                                       uint32_t tile, uint32_t n_classes, uint8_t* __restrict__ dst,
+                                       int32_t* __restrict__ labels, unsigned long long* bad) {
+  extern __shared__ uint8_t rec[];
+  const uint64_t P = static_cast<uint64_t>(hw) * ch;
+  const uint64_t tiles = (hw + tile - 1) / tile;
+  for (uint64_t w = blockIdx.x; w < n_rec * tiles; w += gridDim.x) {
+    const uint64_t r = w / tiles, px0 = (w - r * tiles) * tile;
+    const uint32_t npx = static_cast<uint32_t>(hw - px0 < tile ? hw - px0 : tile);
+    const uint8_t* s = src + r * (P + 1);
+    if (px0 == 0 && threadIdx.x == 0) {
+      labels[r] = s[0];
+      if (s[0] >= n_classes) atomicMin(bad, static_cast<unsigned long long>(r));
+    }
+    for (uint32_t i = threadIdx.x; i < npx * ch; i += blockDim.x) {
+      const uint32_t cc = i / npx, px = i - cc * npx;
+      rec[i] = s[1 + static_cast<uint64_t>(cc) * hw + px0 + px];
+    }
+    __syncthreads();
+    uint8_t* d = dst + r * P + px0 * ch;
+    for (uint32_t o = threadIdx.x; o < npx * ch; o += blockDim.x) {
+      const uint32_t px = o / ch, cc = o - px * ch;
+      d[o] = rec[cc * npx + px];
+    }
+    __syncthreads();
+  }
+}
+
+constexpr uint64_t kRecordStageBytes = 96 * 1024;  // whole-record staging up to this size
+
 }  // namespace
 
 extern "C" int optb_load_records_dev(optb_ctx* ctx, const char* path, uint32_t h, uint32_t w, uint32_t c,
@@ -270,14 +304,39 @@ extern "C" int optb_load_records_dev(optb_ctx* ctx, const char* path, uint32_t h
     return io_fail(OPTB_ERR_FORMAT, std::string("records: cannot read ") + path);
   }
   const unsigned long long none = ~0ull;
-  cudaMemcpy(bad, &none, sizeof none, cudaMemcpyHostToDevice);
-  cudaMemcpy(dev, host, size, cudaMemcpyHostToDevice);
-  const unsigned grid = static_cast<unsigned>(n < 148 * 8 ? n : 148 * 8);
-  if (P + 1 > 48 * 1024)
-    cudaFuncSetAttribute(k_records_to_hwc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P + 1));
-  k_records_to_hwc<<<grid, 256, P + 1>>>(dev, n, h * w, c, n_classes, pixels, labels, bad);
+  cudaError_t e = cudaMemcpy(bad, &none, sizeof none, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dev, host, size, cudaMemcpyHostToDevice);
+  if (P + 1 <= kRecordStageBytes) {
+    const unsigned grid = static_cast<unsigned>(n < 148 * 8 ? n : 148 * 8);
+    if (e == cudaSuccess && P + 1 > 48 * 1024)
+      e = cudaFuncSetAttribute(k_records_to_hwc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P + 1));
+    if (e == cudaSuccess) k_records_to_hwc<<<grid, 256, P + 1>>>(dev, n, h * w, c, n_classes, pixels, labels, bad);
+  } else {
+    // tile of pixels whose bytes over all channels fit the staging budget
+    const uint64_t hw = static_cast<uint64_t>(h) * w;
+    const uint64_t t = (32 * 1024) / c ? (32 * 1024) / c : 1;
+    const uint32_t tile = static_cast<uint32_t>(t < hw ? t : hw);
+    const uint64_t smem = static_cast<uint64_t>(tile) * c;
+    if (smem > kRecordStageBytes) {
+      release();
+      return io_fail(OPTB_ERR_SHAPE, "records: " + std::to_string(c) + " channels exceed the staging budget");
+    }
+    if (e == cudaSuccess && smem > 48 * 1024)
+      e = cudaFuncSetAttribute(k_records_to_hwc_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem));
+    const uint64_t work = n * ((hw + tile - 1) / tile);
+    const unsigned grid = static_cast<unsigned>(work < 148 * 8 ? work : 148 * 8);
+    if (e == cudaSuccess)
+      k_records_to_hwc_tiled<<<grid, 256, smem>>>(dev, n, static_cast<uint32_t>(hw), c, tile, n_classes, pixels,
+                                                  labels, bad);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    release();
+    return io_fail(OPTB_ERR_CUDA, std::string("records: kernel launch: ") + cudaGetErrorString(e));
+  }
   unsigned long long first_bad = none;
-  const cudaError_t e = cudaMemcpy(&first_bad, bad, sizeof first_bad, cudaMemcpyDeviceToHost);
+  e = cudaMemcpy(&first_bad, bad, sizeof first_bad, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) {
     release();
     return io_fail(OPTB_ERR_CUDA, std::string("records: ") + cudaGetErrorString(e));

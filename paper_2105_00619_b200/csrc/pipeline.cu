@@ -65,6 +65,8 @@ struct optb_pipeline {
   // its dependents early was launched there since (RowSrc::early)
   cudaStream_t last_stream = nullptr;
   uint64_t last_tag = 0;
+  uintptr_t last_out = 0;  // the previous step's output range (what it wrote)
+  uint64_t last_out_bytes = 0;
   bool timing = false;
   uint32_t tstride = 1;  // time every tstride-th step (and sampler call)
   // host leg (optb_pipeline_step_host): double-buffered device copies of the
@@ -163,24 +165,36 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   optb_epilogue e = p->d.epilogue;
   if (e.class_scale && !e.row_class) e.row_class = p->cls[b] + sub * p->rows;
   if (timed) cudaEventRecord(p->t_e0[r], s);
-  // early gather (RowSrc::early): the kernel right before this step in the
-  // stream is this pipeline's previous step (or a kernel that does not
-  // trigger early), which writes only the containers and its `out` -- unless
-  // `out` overlaps the dataset rows
+  // early gather (RowSrc::early): before its griddepcontrol.wait the step
+  // reads only the dataset rows and its draws.  Allowed when the kernel right
+  // before it in the stream is this pipeline's previous step (stream tag
+  // unchanged since), which wrote only the containers and the previous `out`
+  // -- so the dataset must be disjoint from that `out` and from this one.  A
+  // kernel launched from outside the library in between does not trigger its
+  // dependents early (or, if a caller's kernel does, it must not write the
+  // dataset after its trigger).
   const uint64_t ds_bytes = optb_b200::sbs_examples(p->d.sbs) * p->d.row_stride;
   const uint64_t out_row = e.out_row_stride ? e.out_row_stride : p->d.layout.pixels;
   const uint64_t out_bytes = p->rows * out_row * (e.out_dtype == OPTB_OUT_U8 ? 1 : e.out_dtype == OPTB_OUT_F32 ? 4 : 2);
   const uintptr_t o0 = reinterpret_cast<uintptr_t>(out), d0 = reinterpret_cast<uintptr_t>(p->d.dataset);
-  const bool disjoint = ds_bytes && (o0 + out_bytes <= d0 || d0 + ds_bytes <= o0);
+  auto apart = [&](uintptr_t a, uint64_t na) { return a + na <= d0 || d0 + ds_bytes <= a; };
+  const bool disjoint = ds_bytes && apart(o0, out_bytes) && apart(p->last_out, p->last_out_bytes);
   const bool early = disjoint && p->last_tag && p->last_stream == s && optb_b200::stream_tag(s) == p->last_tag;
   if (p->d.split_kernels) {
     st = optb_b200::encode_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
                                p->cont, p->offs, s, early);
     if (st) return st;
     if (timed) cudaEventRecord(p->t_e1[r], s);
-    if (sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess) return cuda_fail("event record");
+    // the draw buffer is free for the side stream once nothing reads it: the
+    // encode reads the examples, the decode reads the classes when the
+    // per-class epilogue takes them from this step's draws
+    const bool dec_reads_cls = e.class_scale && !p->d.epilogue.row_class;
+    if (!dec_reads_cls && sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess)
+      return cuda_fail("event record");
     st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &e, out, s);
     if (st) return st;
+    if (dec_reads_cls && sub + 1 == p->spd && cudaEventRecord(p->enc_done[b], s) != cudaSuccess)
+      return cuda_fail("event record");
   } else {
     st = optb_b200::roundtrip_dev(p->ctx, &p->d.layout, p->d.dataset, p->d.row_stride, p->ex[b] + sub * p->rows,
                                   p->cont, p->offs, &e, out, s, early);
@@ -191,6 +205,8 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   if (timed && p->d.split_kernels) cudaEventRecord(p->t_d1[r], s);  // fused: the launch ends at t_e1
   p->last_stream = s;
   p->last_tag = optb_b200::stream_tag(s);
+  p->last_out = o0;
+  p->last_out_bytes = out_bytes;
   ++p->step;
   return OPTB_OK;
 }
@@ -244,6 +260,10 @@ int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint6
   if (!p || !dataset_host || !out_host || !n_rows) return arg_fail("step_host: null buffer or empty dataset");
   if (row_stride == 0) row_stride = p->d.layout.pixels;
   if (row_stride < p->d.layout.pixels) return arg_fail("step_host: row_stride < pixels");
+  // the draws index every example of the sampler's class index
+  if (n_rows < optb_b200::sbs_examples(p->d.sbs))
+    return arg_fail(("step_host: " + std::to_string(n_rows) + " dataset rows, the sampler draws from " +
+                     std::to_string(optb_b200::sbs_examples(p->d.sbs)) + " examples").c_str());
   auto& h = p->host;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t es = p->d.epilogue.out_dtype == OPTB_OUT_U8 ? 1 : p->d.epilogue.out_dtype == OPTB_OUT_F32 ? 4 : 2;

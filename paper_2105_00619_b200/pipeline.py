@@ -36,7 +36,13 @@ class Pipeline:
         self.rows = batch * batches_per_step
         self.P = P
         self.device = device
-        self._keep = (cursor, dataset, class_scale, class_bias)
+        # objects the native pipeline points into: the cursor and class tables
+        # for its lifetime, the dataset until set_dataset replaces it, and the
+        # host buffers of the last two step_host calls (one per double-buffer
+        # slot) until host_wait
+        self._keep = (cursor, class_scale, class_bias)
+        self._dataset = dataset
+        self._host_bufs = []
         E = Epilogue(dt, float(scale), None if class_scale is None else ct.c_void_p(class_scale.data_ptr()),
                      None if class_bias is None else ct.c_void_p(class_bias.data_ptr()), None, 0)
         desc = PipelineDesc(self.layout, ct.c_void_p(dataset.data_ptr()), dataset.stride(0), cursor._h, shard,
@@ -65,7 +71,7 @@ class Pipeline:
         import torch
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
-        self._keep = self._keep[:4] + (dataset_host, out_host)
+        self._host_bufs = (self._host_bufs + [(dataset_host, out_host)])[-2:]
         check(lib.optb_pipeline_step_host(self._h, ct.c_void_p(dataset_host.data_ptr()), dataset_host.shape[0],
                                           dataset_host.stride(0), ct.c_void_p(out_host.data_ptr()),
                                           ct.c_void_p(stream.cuda_stream)))
@@ -75,11 +81,13 @@ class Pipeline:
         """Every step_host download has landed (stream None: block the host),
         or `stream` waits for them (device-side)."""
         check(lib.optb_pipeline_host_wait(self._h, None if stream is None else ct.c_void_p(stream.cuda_stream)))
+        if stream is None:  # every transfer has landed
+            self._host_bufs = []
 
     def set_dataset(self, dataset):
         """Rows for subsequent steps come from `dataset` (same shape)."""
-        self._keep = self._keep + (dataset,)
         check(lib.optb_pipeline_set_dataset(self._h, ct.c_void_p(dataset.data_ptr()), dataset.stride(0)))
+        self._dataset = dataset
 
     def timings(self, step: int):
         s, e, d = ct.c_float(), ct.c_float(), ct.c_float()

@@ -47,12 +47,17 @@ def test_pipeline_steps_vs_oracle(pkg, oracle_mod, torch_cuda, mode, dtype, spd,
     pipe.close()
 
 
-@pytest.mark.parametrize("G", [2, 4])  # 4 shards: three draw buffers, two calls ahead
-def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda, G):
+@pytest.mark.parametrize("G,split", [(1, True), (2, False), (2, True), (4, False)])  # 4: three draw buffers
+def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda, G, split):
+    """Per-class epilogue fed by the step's own draw classes.  With split
+    launches the decode reads the draw buffer's classes after the encode: the
+    side stream must not refill that buffer before the decode ran (steps
+    enqueued back to back, no host sync, so a premature reuse shows)."""
     torch, O = torch_cuda, oracle_mod
     from paper_2105_00619_b200.pipeline import Pipeline
     S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
     B, nb, P = 64, 3, 768
+    n_steps = 6
     ds_d = torch.from_numpy(ds).cuda()
     cs = torch.linspace(0.001, 0.01, 10, device="cuda")
     cb = torch.linspace(-1, 1, 10, device="cuda")
@@ -60,15 +65,15 @@ def test_pipeline_sharded_and_class_epilogue(pkg, oracle_mod, torch_cuda, G):
     for r in range(G):
         cur = S.BatchCursor.from_device_index(p, offs, mem)
         pipe = Pipeline(cur, ds_d, 1, B, nb, shard=r, n_shards=G, out_dtype=torch.float32, class_scale=cs,
-                        class_bias=cb)
+                        class_bias=cb, split_kernels=split)
         outs[r] = []
-        for _ in range(3):
+        for _ in range(n_steps):
             o = torch.empty((B * nb, P), dtype=torch.float32, device="cuda")
             pipe.step(o)
             outs[r].append(o)
         pkg.codec.sync()
         pipe.close()
-    for step in range(3):
+    for step in range(n_steps):
         ex, cl = ref.next(nb * G)
         ex, cl = ex.reshape(nb * G, B), cl.reshape(nb * G, B)
         for r in range(G):
@@ -205,4 +210,56 @@ def test_pipeline_back_to_back_steps_early_gather(pkg, oracle_mod, torch_cuda, m
     ex1, _ = ref.next(nb)
     assert np.array_equal(outs2[0].cpu().numpy(), ds[ex0])
     assert np.array_equal(outs2[1].cpu().numpy(), new[ex1])
+    pipe.close()
+
+
+def test_pipeline_dataset_is_previous_output(pkg, oracle_mod, torch_cuda):
+    """A step whose dataset is the PREVIOUS step's output (set_dataset to the
+    buffer the step before wrote, enqueued back to back): it must not gather
+    before that step finished writing -- the early-gather check compares the
+    dataset with the previous step's output range as well as its own."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    N = 4096
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch, N=N)
+    B, nb, P = 64, N // 64, 768  # one step's output is a full dataset
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    a = torch.from_numpy(ds).cuda()
+    b = torch.empty_like(a)
+    c = torch.empty_like(a)
+    s = torch.cuda.Stream()
+    pipe = Pipeline(cur, a, 1, B, nb, per_chunk=16)
+    with torch.cuda.stream(s):
+        pipe.step(c, s)   # warm: a -> c
+        pipe.step(b, s)   # a -> b
+        pipe.set_dataset(b)
+        pipe.step(c, s)   # b -> c, right behind the step that writes b
+    s.synchronize()
+    ex0, _ = ref.next(nb)
+    ex1, _ = ref.next(nb)
+    ex2, _ = ref.next(nb)
+    step1 = ds[ex1]
+    assert np.array_equal(b.cpu().numpy(), step1)
+    assert np.array_equal(c.cpu().numpy(), step1[ex2])
+    pipe.close()
+
+
+def test_pipeline_step_host_rejects_short_dataset(pkg, oracle_mod, torch_cuda):
+    """step_host with fewer dataset rows than the sampler's examples is an
+    argument error (the draws would read past the end of the upload)."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P = 64, 2, 768
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    pipe = Pipeline(cur, torch.from_numpy(ds).cuda(), 1, B, nb, per_chunk=16)
+    short = torch.from_numpy(ds[:100]).pin_memory()
+    out = torch.empty((B * nb, P), dtype=torch.uint8).pin_memory()
+    with pytest.raises(pkg.errors.Error, match="100 dataset rows, the sampler draws from 4000 examples"):
+        pipe.step_host(short, out)
+    # the pipeline is still usable
+    pipe.step_host(torch.from_numpy(ds).pin_memory(), out)
+    pipe.host_wait()
+    ex, _ = ref.next(nb)
+    assert np.array_equal(out.numpy(), ds[ex])
     pipe.close()

@@ -17,7 +17,8 @@ def _write(tmp_path, n, h, w, c, n_classes, seed=0, name="rec.bin"):
     return p, rec.tobytes()
 
 
-@pytest.mark.parametrize("h,w,c,n", [(32, 32, 3, 500), (2, 2, 3, 7), (5, 3, 1, 11), (224, 224, 3, 3)])
+@pytest.mark.parametrize("h,w,c,n", [(32, 32, 3, 500), (2, 2, 3, 7), (5, 3, 1, 11), (224, 224, 3, 3),
+                                          (299, 299, 3, 5), (17, 13, 40000, 2)])
 def test_records_vs_oracle(pkg, oracle_mod, torch_cuda, tmp_path, h, w, c, n):
     C = pkg.codec
     path, raw = _write(tmp_path, n, h, w, c, 10)
@@ -43,3 +44,12 @@ def test_records_errors(pkg, torch_cuda, tmp_path):
         C.load_records_dev(str(tmp_path / "nope.bin"), shape, 10, max_records=4)
     with pytest.raises(E.ShapeError, match="extents must be positive"):
         C.load_records_dev(str(path), C.ImageShape(0, 2, 3), 10, max_records=4)
+
+
+def test_records_large_label_error(pkg, torch_cuda, tmp_path):
+    """Records past the whole-record staging budget take the tiled kernel;
+    its label check names the first offending record like the staged one."""
+    C, E = pkg.codec, pkg.errors
+    path, raw = _write(tmp_path, 6, 299, 299, 3, 10, seed=3)
+    with pytest.raises(E.FormatError, match=r"^records: label \d+ outside 2 classes in "):
+        C.load_records_dev(str(path), C.ImageShape(299, 299, 3), 2, max_records=6)
