@@ -192,6 +192,11 @@ int optb_sbs_create(optb_ctx* ctx, const uint64_t* counts, uint64_t n_classes, u
                     uint64_t seed, const uint64_t* class_offsets, const int64_t* members,
                     int32_t members_on_device, optb_sbs** out);
 void optb_sbs_destroy(optb_sbs* sbs);
+/* A copy of a BatchCursor (the reference class is copyable,
+ * sampler.hpp:45-68; a copy continues the identical stream independently):
+ * waits for the calls enqueued on `sbs`, then duplicates its permutations,
+ * chain state and position. */
+int optb_sbs_clone(const optb_sbs* sbs, optb_sbs** out);
 
 /* BatchCursor::next (sampler.cpp:91-104) n_batches times.  Writes the
  * class-major draws of the batches beta0 + t (t < n_batches) with

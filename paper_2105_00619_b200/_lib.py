@@ -90,6 +90,7 @@ SIGNATURES = {
     "optb_sbs_create":(ct.c_int, [vp, u64p, ct.c_uint64, ct.c_uint64, ct.c_uint64, u64p, vp,
                                    ct.c_int32, ct.POINTER(vp)]),
     "optb_sbs_destroy": (None, [vp]),
+    "optb_sbs_clone": (ct.c_int, [vp, ct.POINTER(vp)]),
     "optb_sbs_next_dev": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, vp, vp, vp]),
     "optb_sbs_next_host": (ct.c_int, [vp, ct.c_uint64, vp, vp]),
     "optb_sbs_batches_drawn": (ct.c_uint64, [vp]),

@@ -115,12 +115,25 @@ def build_cli(force: bool = False) -> str:
     return CLI_BIN
 
 
+API_BENCH_SRC = os.path.join(ROOT, "tools", "shim_api_bench.cpp")
+API_BENCH_BIN = os.path.join(PKG, "optb_shim_api_bench")
+
+
+def build_api_bench(force: bool = False) -> str:
+    """The reference runner's call pattern over the drop-in shim (bench.py shim_api)."""
+    if force or _stale(API_BENCH_BIN, [API_BENCH_SRC, SHIM_LIB_NAME]):
+        _run(["g++", "-std=c++20", "-O3", "-Wall", "-I" + os.path.join(CSRC, "shim", "include"), API_BENCH_SRC,
+              "-o", API_BENCH_BIN, "-L" + PKG, "-loptb_shim", "-loptb_cuda", "-Wl,-rpath,$ORIGIN"])
+    return API_BENCH_BIN
+
+
 def build(force: bool = False) -> None:
     build_cuda(force)
     if os.path.isdir(os.path.join(CSRC, "shim", "src")) and all(
             os.path.exists(os.path.join(CSRC, "shim", "src", f)) for f in SHIM_SOURCES):
         build_shim(force)
         build_cli(force)
+        build_api_bench(force)
         build_ref_suites(force)
 
 

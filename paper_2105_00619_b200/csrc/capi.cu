@@ -169,10 +169,28 @@ struct optb_ctx {
   uint64_t ci_words = 0;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
+  // pinned error-latch words for the small-call host path: [0] the reset
+  // value, [1] the read-back (both stream ordered, no extra synchronisation)
+  DevError* pin_err = nullptr;
 };
 
 namespace {
 
+
+// The reference message of a latched device error (optb_ctx_sync).
+int latch_status(const DevError& h) {
+  const unsigned n = static_cast<unsigned>(h.key & 0xff);
+  switch (h.kind) {
+    case kErrIntRange:  // codec.cpp:191-194
+      return set_err(OPTB_ERR_FORMAT, "decode: container value exceeds range of %u packed images", n);
+    case kErrF64Range:  // codec.cpp:165-170
+      return set_err(OPTB_ERR_FORMAT, "decode: container value out of range for %u images", n);
+    case kErrLabel:  // sampler.cpp:58-61
+      return set_err(OPTB_ERR, "sampler: label %lld outside %llu classes", static_cast<long long>(h.label),
+                     static_cast<unsigned long long>(h.aux));
+  }
+  return set_err(OPTB_ERR, "device error %u", h.kind);
+}
 
 int reset_err(optb_ctx* c, cudaStream_t s) {
   DevError z{0, 0, ~0ull, 0, 0};
@@ -262,6 +280,11 @@ int optb_ctx_create(int device, optb_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_kern[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming);
   }
+  if (cudaHostAlloc(&c->pin_err, 2 * sizeof(DevError), cudaHostAllocDefault) != cudaSuccess) {
+    optb_ctx_destroy(c);
+    return cuda_err(cudaGetLastError(), "ctx create");
+  }
+  c->pin_err[0] = DevError{0, 0, ~0ull, 0, 0};
   int st = reset_err(c, c->s_compute);
   if (st) {
     optb_ctx_destroy(c);
@@ -290,6 +313,7 @@ void optb_ctx_destroy(optb_ctx* c) {
   if (c->ci_scratch) cudaFree(c->ci_scratch);
   if (c->tmp) cudaFree(c->tmp);
   if (c->d_err) cudaFree(c->d_err);
+  if (c->pin_err) cudaFreeHost(c->pin_err);
   if (c->s_compute) cudaStreamDestroy(c->s_compute);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
@@ -311,17 +335,7 @@ int optb_ctx_sync(optb_ctx* c, void* stream) {
   }
   int st = reset_err(c, c->s_compute);
   if (st) return st;
-  const unsigned n = static_cast<unsigned>(h.key & 0xff);
-  switch (h.kind) {
-    case kErrIntRange:  // codec.cpp:191-194
-      return set_err(OPTB_ERR_FORMAT, "decode: container value exceeds range of %u packed images", n);
-    case kErrF64Range:  // codec.cpp:165-170
-      return set_err(OPTB_ERR_FORMAT, "decode: container value out of range for %u images", n);
-    case kErrLabel:  // sampler.cpp:58-61
-      return set_err(OPTB_ERR, "sampler: label %lld outside %llu classes",
-                     static_cast<long long>(h.label), static_cast<unsigned long long>(h.aux));
-  }
-  return set_err(OPTB_ERR, "device error %u", h.kind);
+  return latch_status(h);
 }
 
 // ------------------------------------------------------------------ codec, device
@@ -550,6 +564,63 @@ int ensure_slots(optb_ctx* c, size_t in_b, size_t out_b, size_t off_b) {
 
 constexpr uint64_t kSliceTarget = 32ull << 20;
 
+// Small host calls (the drop-in API encodes / decodes one chunk per call,
+// runner.cpp:77-90, nn.cpp:182): the call's latency is the cost, so one
+// stream, one H2D, one kernel, one D2H and ONE synchronisation -- no
+// cross-stream events, no pointer-attribute queries, the error latch reset
+// and read back in stream order through pinned words.
+constexpr uint64_t kSmallCall = 8ull << 20;
+
+int small_encode(optb_ctx* c, const optb_layout* L, const uint8_t* images, void* containers, uint8_t* offsets) {
+  const uint64_t P = L->pixels, rows = optb_layout_rows(L);
+  const uint64_t cb = optb_layout_container_bytes(L), ob = optb_layout_offsets_bytes(L);
+  int st = ensure_slots(c, rows * P, cb, ob);
+  if (st) return st;
+  cudaStream_t s = c->s_compute;
+  memcpy(c->pin_in[0], images, rows * P);
+  CK(cudaMemcpyAsync(c->dev_in[0], c->pin_in[0], rows * P, cudaMemcpyHostToDevice, s), "H2D");
+  cudaError_t e = launch_encode(make_geom(L), RowSrc{c->dev_in[0], P, nullptr, nullptr, 0}, c->dev_out[0],
+                                c->dev_off[0], s, c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "encode launch");
+  CK(cudaMemcpyAsync(c->pin_out[0], c->dev_out[0], cb, cudaMemcpyDeviceToHost, s), "D2H");
+  if (ob) CK(cudaMemcpyAsync(c->pin_off[0], c->dev_off[0], ob, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaStreamSynchronize(s), "sync");
+  memcpy(containers, c->pin_out[0], cb);
+  if (ob) memcpy(offsets, c->pin_off[0], ob);
+  g_err.clear();
+  return OPTB_OK;
+}
+
+int small_decode(optb_ctx* c, const optb_layout* L, const void* containers, const uint8_t* offsets,
+                 const optb_epilogue* E, void* out) {
+  const uint64_t P = L->pixels, rows = optb_layout_rows(L);
+  const uint64_t cb = optb_layout_container_bytes(L), ob = optb_layout_offsets_bytes(L);
+  const uint64_t outb = rows * P * out_elem_bytes(E->out_dtype);
+  int st = ensure_slots(c, cb, outb, ob);
+  if (st) return st;
+  cudaStream_t s = c->s_compute;
+  memcpy(c->pin_in[0], containers, cb);
+  if (ob) memcpy(c->pin_off[0], offsets, ob);
+  CK(cudaMemcpyAsync(c->d_err, &c->pin_err[0], sizeof(DevError), cudaMemcpyHostToDevice, s), "reset error latch");
+  CK(cudaMemcpyAsync(c->dev_in[0], c->pin_in[0], cb, cudaMemcpyHostToDevice, s), "H2D");
+  if (ob) CK(cudaMemcpyAsync(c->dev_off[0], c->pin_off[0], ob, cudaMemcpyHostToDevice, s), "H2D");
+  cudaError_t e = launch_decode(make_geom(L), c->dev_in[0], c->dev_off[0], make_epi(E, P), c->dev_out[0], c->d_err,
+                                s, c->sms, &c->launches);
+  if (e != cudaSuccess) return cuda_err(e, "decode launch");
+  CK(cudaMemcpyAsync(c->pin_out[0], c->dev_out[0], outb, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(&c->pin_err[1], c->d_err, sizeof(DevError), cudaMemcpyDeviceToHost, s), "read error latch");
+  CK(cudaStreamSynchronize(s), "sync");
+  const DevError h = c->pin_err[1];
+  if (h.kind != kErrNone) {
+    CK(cudaMemcpyAsync(c->d_err, &c->pin_err[0], sizeof(DevError), cudaMemcpyHostToDevice, s), "reset error latch");
+    CK(cudaStreamSynchronize(s), "sync");
+    return latch_status(h);
+  }
+  memcpy(out, c->pin_out[0], outb);
+  g_err.clear();
+  return OPTB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -564,6 +635,8 @@ int optb_encode_host(optb_ctx* c, const optb_layout* L, const uint8_t* images, v
   if (optb_layout_rows(L) == 0) return OPTB_OK;
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   const uint64_t P = L->pixels;
+  if (optb_layout_rows(L) * P + optb_layout_container_bytes(L) <= kSmallCall)
+    return small_encode(c, L, images, containers, offsets);
   const uint32_t wc = optb_container_value_bytes(L->mode);
   const uint64_t ost = optb_offsets_stride(L->mode, P, L->per_chunk);
   const auto slices = plan_slices(L, P, kSliceTarget);
@@ -642,6 +715,8 @@ int optb_decode_host(optb_ctx* c, const optb_layout* L, const void* containers,
   const size_t es = out_elem_bytes(E->out_dtype);
   const uint64_t ors = E->out_row_stride ? E->out_row_stride : P;
   if (ors != P) return set_err(OPTB_ERR_ARG, "decode_host: out_row_stride must be 0 or P");
+  if (optb_layout_container_bytes(L) + optb_layout_rows(L) * P * es <= kSmallCall)
+    return small_decode(c, L, containers, offsets, E, out);
   // slice on container bytes per row (one chunk of per_chunk rows is P*wc)
   const auto slices = plan_slices(L, (P * wc + L->per_chunk - 1) / L->per_chunk, kSliceTarget);
   uint64_t max_rows = 0, max_chunks = 0;
@@ -1140,6 +1215,66 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
   rc = run_events(s, keys, pk, nullptr, nullptr, nullptr, st);
   if (rc) return fail(rc);
   if (cudaStreamSynchronize(st) != cudaSuccess) return fail(cuda_err(cudaGetLastError(), "sbs ctor"));
+  *out = s;
+  g_err.clear();
+  return OPTB_OK;
+}
+
+int optb_sbs_clone(const optb_sbs* src, optb_sbs** out) {
+  if (!src || !out) return set_err(OPTB_ERR_ARG, "sbs: null argument");
+  *out = nullptr;
+  optb_ctx* c = src->ctx;
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  // every call enqueued on the source (any stream) has finished: its device
+  // chain and permutations are the state after its last call
+  CK(cudaDeviceSynchronize(), "sbs clone");
+  auto* s = new optb_sbs();
+  s->ctx = c;
+  s->C = src->C;
+  s->B = src->B;
+  s->N = src->N;
+  s->counts = src->counts;
+  s->m = src->m;
+  s->off = src->off;
+  s->prefix = src->prefix;
+  s->gen = src->gen;
+  s->batches = src->batches;
+  s->force_serial = src->force_serial;
+  s->small_ids = src->small_ids;
+  s->max_m = src->max_m;
+  auto fail = [&](int code) {
+    optb_sbs_destroy(s);
+    return code;
+  };
+  for (int r = 0; r < optb_sbs::kRing; ++r)
+    if (cudaEventCreateWithFlags(&s->uploaded[r], cudaEventDisableTiming) != cudaSuccess)
+      return fail(cuda_err(cudaGetLastError(), "sbs event"));
+  if (cudaMalloc(&s->d_chain, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemcpy(s->d_chain, src->d_chain, 8, cudaMemcpyDeviceToDevice) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs chain"));
+  unsigned long long chain = 0;
+  if (cudaMemcpy(&chain, src->d_chain, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs chain"));
+  s->host_chain = chain;  // the device chain is authoritative (a serial redo may have moved it)
+  if (cudaHostAlloc(&s->diverged_h, 16, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->diverged_d), s->diverged_h, 0) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs mapped counter"));
+  *s->diverged_h = 0;
+  int rc = ensure_pool(s, std::max<uint64_t>(s->N, 1), c->s_compute);
+  if (rc) return fail(rc);
+  if (s->N && cudaMemcpy(s->d_pool, src->d_pool, s->N * 8, cudaMemcpyDeviceToDevice) != cudaSuccess)
+    return fail(cuda_err(cudaGetLastError(), "sbs permutations"));
+  {  // static arrays: same bytes as the source's (layout of optb_sbs_create)
+    size_t bytes = 0;
+    auto add = [&](size_t b) { bytes = (bytes + 15) / 16 * 16 + b; };
+    add(s->C * 8);
+    add((s->C + 1) * 8);
+    add(s->C * 8);
+    add(s->B * 4);
+    if (cudaMalloc(&s->d_static, bytes + 16) != cudaSuccess ||
+        cudaMemcpy(s->d_static, src->d_static, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess)
+      return fail(cuda_err(cudaGetLastError(), "sbs static"));
+  }
   *out = s;
   g_err.clear();
   return OPTB_OK;

@@ -5,6 +5,7 @@
 // order, after the draws come back (sampler.cpp:99).
 #include "optb/sampler.hpp"
 
+#include <algorithm>
 #include <string>
 
 #include "optb_cuda.h"
@@ -58,9 +59,26 @@ BatchCursor::~BatchCursor() {
   if (handle_) optb_sbs_destroy(handle_);
 }
 
+BatchCursor::BatchCursor(const BatchCursor& other)
+    : plan_(other.plan_), hook_(other.hook_), ring_ex_(other.ring_ex_), ring_cls_(other.ring_cls_),
+      ring_pos_(other.ring_pos_), ring_len_(other.ring_len_), refill_(other.refill_) {
+  if (other.handle_) shim::check(optb_sbs_clone(other.handle_, &handle_));
+}
+
+BatchCursor& BatchCursor::operator=(const BatchCursor& other) {
+  if (this != &other) {
+    BatchCursor copy(other);
+    *this = std::move(copy);
+  }
+  return *this;
+}
+
 BatchCursor::BatchCursor(BatchCursor&& other) noexcept
-    : plan_(std::move(other.plan_)), handle_(other.handle_), hook_(std::move(other.hook_)) {
+    : plan_(std::move(other.plan_)), handle_(other.handle_), hook_(std::move(other.hook_)),
+      ring_ex_(std::move(other.ring_ex_)), ring_cls_(std::move(other.ring_cls_)), ring_pos_(other.ring_pos_),
+      ring_len_(other.ring_len_), refill_(other.refill_) {
   other.handle_ = nullptr;
+  other.ring_pos_ = other.ring_len_ = 0;
 }
 
 BatchCursor& BatchCursor::operator=(BatchCursor&& other) noexcept {
@@ -69,17 +87,33 @@ BatchCursor& BatchCursor::operator=(BatchCursor&& other) noexcept {
     plan_ = std::move(other.plan_);
     handle_ = other.handle_;
     hook_ = std::move(other.hook_);
+    ring_ex_ = std::move(other.ring_ex_);
+    ring_cls_ = std::move(other.ring_cls_);
+    ring_pos_ = other.ring_pos_;
+    ring_len_ = other.ring_len_;
+    refill_ = other.refill_;
     other.handle_ = nullptr;
+    other.ring_pos_ = other.ring_len_ = 0;
   }
   return *this;
 }
 
 std::vector<Draw> BatchCursor::next() {
   const std::size_t B = plan_.batch_size;
-  std::vector<int64_t> ex(B);
-  std::vector<int32_t> cls(B);
-  shim::check(optb_sbs_next_host(handle_, 1, ex.data(), cls.data()));
+  if (ring_pos_ == ring_len_) {  // refill: one device call draws refill_ batches
+    ring_ex_.resize(refill_ * B);
+    ring_cls_.resize(refill_ * B);
+    shim::check(optb_sbs_next_host(handle_, refill_, ring_ex_.data(), ring_cls_.data()));
+    ring_pos_ = 0;
+    ring_len_ = refill_;
+    // grow geometrically: a caller drawing a handful of batches pays for
+    // few extra, a long stream amortises the device round trip
+    refill_ = std::min<std::size_t>(refill_ * 2, std::max<std::size_t>(1, (std::size_t{1} << 20) / (B ? B : 1)));
+  }
   std::vector<Draw> batch(B);
+  const int64_t* ex = ring_ex_.data() + ring_pos_ * B;
+  const int32_t* cls = ring_cls_.data() + ring_pos_ * B;
+  ++ring_pos_;
   for (std::size_t r = 0; r < B; ++r) {
     batch[r] = Draw{static_cast<std::size_t>(ex[r]), static_cast<std::size_t>(cls[r])};
     if (hook_) hook_(batch[r].cls, batch[r].example);

@@ -127,6 +127,17 @@ class BatchCursor:
                                   ct.c_void_p(members.data_ptr()), 1, ct.byref(self._h)))
         return self
 
+    def __copy__(self) -> "BatchCursor":
+        """A copy continues the identical stream independently (the reference
+        class is copyable, sampler.hpp:45-68): optb_sbs_clone."""
+        other = BatchCursor.__new__(BatchCursor)
+        other._plan, other._device, other._hook = self._plan, self._device, self._hook
+        other._h = ct.c_void_p()
+        check(lib.optb_sbs_clone(self._h, ct.byref(other._h)))
+        return other
+
+    copy = __copy__
+
     def set_preprocess_hook(self, hook: Optional[PreprocessHook]) -> None:
         self._hook = hook
 

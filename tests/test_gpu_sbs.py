@@ -227,3 +227,29 @@ def test_rejection_with_calls_in_flight(golden, pkg, torch_cuda, case):
         ex, _ = cur.next_dev(rest)
         torch.cuda.synchronize()
         assert np.array_equal(ex.cpu().numpy(), want[got.size: got.size + ex.numel()])
+
+
+def test_cursor_copy_forks_identical_stream(pkg, oracle_mod, torch_cuda):
+    """A copy of a cursor (optb_sbs_clone; the reference class is copyable,
+    sampler.hpp:45-68) continues the identical stream independently -- taken
+    mid-stream, with device calls still in flight, across lazy reshuffles."""
+    import copy
+    torch, S, O = torch_cuda, pkg.sampler, oracle_mod
+    n = 3000
+    labels = (np.arange(n) % 7).astype(np.int32)
+    p = S.plan([1 / 7] * 7, 64, 77)
+    offs, mem = S.class_index_dev(torch.from_numpy(labels).cuda(), 7)
+    cur = S.BatchCursor.from_device_index(p, offs, mem)
+    ro, rm = O.class_index(labels, 7)
+    oc = O.Cursor(O.sbs_plan([1 / 7] * 7, 64), ro, rm, 64, 77)
+    ex, _ = cur.next_dev(30)           # in flight when the copy is taken
+    twin = copy.copy(cur)
+    rex, _ = oc.next(30)
+    assert np.array_equal(ex.cpu().numpy(), rex)
+    want, _ = oc.next(90)              # 90 more batches: several reshuffles of every class
+    a, _ = cur.next_dev(90)
+    b, _ = twin.next_dev(45)
+    b2, _ = twin.next_dev(45)
+    assert np.array_equal(a.cpu().numpy(), want)
+    assert np.array_equal(torch.cat([b, b2]).cpu().numpy(), want)
+    assert twin.batches_drawn() == cur.batches_drawn() == 120
