@@ -31,7 +31,7 @@ CUDA_SOURCES = ["codec.cu"] + [f"codec_v{v}.cu" for v in range(6)] + ["sbs.cu", 
                                                                       "peer.cu"]
 CUDA_LIB_NAME = os.path.join(PKG, "liboptb_cuda.so")
 SHIM_LIB_NAME = os.path.join(PKG, "liboptb_shim.so")
-SHIM_SOURCES = ["codec.cpp", "sampler.cpp", "nn.cpp"]
+SHIM_SOURCES = ["codec.cpp", "sampler.cpp", "nn.cpp", "pipeline.cpp", "metering.cpp"]
 
 
 def _run(cmd):
@@ -72,14 +72,14 @@ def build_shim(force: bool = False) -> str:
     srcs = [os.path.join(CSRC, "shim", "src", f) for f in SHIM_SOURCES]
     hdrs = [os.path.join(inc, "optb", h) for h in os.listdir(os.path.join(inc, "optb"))]
     if force or _stale(SHIM_LIB_NAME, srcs + hdrs + [CUDA_LIB_NAME]):
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + inc,
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-pthread", "-I" + inc,
               "-I" + INCLUDE] + srcs + ["-o", SHIM_LIB_NAME, "-L" + PKG, "-loptb_cuda",
                                         "-Wl,-rpath,$ORIGIN"])
     return SHIM_LIB_NAME
 
 
 REF_TESTS = "/root/reference/proj/tests"
-REF_SUITES = ["test_codec.cpp", "test_sampler.cpp"]
+REF_SUITES = ["test_codec.cpp", "test_sampler.cpp", "test_pipeline.cpp"]
 REF_SUITES_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "ref_suites_on_b200")
 
 
@@ -96,7 +96,7 @@ def build_ref_suites(force: bool = False):
     if not force and not _stale(REF_SUITES_BIN, srcs + [SHIM_LIB_NAME, CUDA_LIB_NAME]):
         return REF_SUITES_BIN
     os.makedirs(os.path.dirname(REF_SUITES_BIN), exist_ok=True)
-    _run(["g++", "-std=c++20", "-O2", "-w", "-I" + os.path.join(ROOT, "tests", "cpp"),
+    _run(["g++", "-std=c++20", "-O2", "-w", "-pthread", "-I" + os.path.join(ROOT, "tests", "cpp"),
           "-I" + os.path.join(CSRC, "shim", "include"), "-I" + INCLUDE, "-I" + REF_TESTS] + srcs +
          ["-o", REF_SUITES_BIN, "-L" + PKG, "-loptb_shim", "-loptb_cuda", "-Wl,-rpath," + PKG,
           "-Wl,-rpath,$ORIGIN/../../../paper_2105_00619_b200"])
@@ -127,6 +127,21 @@ def build_api_bench(force: bool = False) -> str:
     return API_BENCH_BIN
 
 
+SHIM_TESTS_SRC = os.path.join(ROOT, "tests", "cpp", "shim_extra.cpp")
+SHIM_TESTS_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "shim_extra")
+
+
+def build_shim_tests(force: bool = False) -> str:
+    """tests/cpp/shim_extra.cpp (cursor copies, acceptance criteria 1/6/8,
+    the GPU pipeline) against the shim; needs no reference sources."""
+    if force or _stale(SHIM_TESTS_BIN, [SHIM_TESTS_SRC, SHIM_LIB_NAME, CUDA_LIB_NAME]):
+        os.makedirs(os.path.dirname(SHIM_TESTS_BIN), exist_ok=True)
+        _run(["g++", "-std=c++20", "-O2", "-w", "-pthread", "-I" + os.path.join(ROOT, "tests", "cpp"),
+              "-I" + os.path.join(CSRC, "shim", "include"), SHIM_TESTS_SRC, "-o", SHIM_TESTS_BIN, "-L" + PKG,
+              "-loptb_shim", "-loptb_cuda", "-Wl,-rpath,$ORIGIN/../../../paper_2105_00619_b200"])
+    return SHIM_TESTS_BIN
+
+
 def build(force: bool = False) -> None:
     build_cuda(force)
     if os.path.isdir(os.path.join(CSRC, "shim", "src")) and all(
@@ -134,6 +149,7 @@ def build(force: bool = False) -> None:
         build_shim(force)
         build_cli(force)
         build_api_bench(force)
+        build_shim_tests(force)
         build_ref_suites(force)
 
 

@@ -823,6 +823,21 @@ struct optb_sbs {
 };
 
 uint64_t optb_b200::sbs_examples(const optb_sbs* s) { return s ? s->N : 0; }
+namespace {
+int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st);
+}
+// Pool size for any call of up to n batches: class c starts at most
+// floor(n * count_c / m_c) + 1 generations in it and gets one more slot for
+// its pre-call permutation (run_events layout).  Growing the pool inside a
+// call synchronises the call's stream, which in a pipeline waits for the
+// step that last used the draw buffer -- so the pipeline reserves up front.
+int optb_b200::sbs_reserve(optb_sbs* s, uint64_t n) {
+  if (!s) return OPTB_OK;
+  uint64_t need = s->N;
+  for (uint64_t c = 0; c < s->C; ++c)
+    if (s->m[c] >= 2 && s->counts[c]) need += (n * s->counts[c] / s->m[c] + 2) * s->m[c];
+  return ensure_pool(s, std::max<uint64_t>(need, 1), s->ctx->s_compute);
+}
 
 namespace {
 
@@ -884,7 +899,7 @@ int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
 
 int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st) {
   if (s->pool_cap >= elems) return OPTB_OK;
-  const uint64_t cap = std::max<uint64_t>(elems, s->pool_cap * 3 / 2);
+  const uint64_t cap = std::max<uint64_t>(elems, s->pool_cap * 2);
   int64_t* p = nullptr;
   CK(cudaStreamSynchronize(st), "sbs pool");
   CK(cudaMalloc(&p, cap * sizeof(int64_t)), "sbs pool");

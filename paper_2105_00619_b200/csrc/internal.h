@@ -79,6 +79,8 @@ uint64_t stream_tag(cudaStream_t s);
 void bump_stream_tag(cudaStream_t s);
 // Examples in a cursor's class index (row ids drawn are < this).
 uint64_t sbs_examples(const optb_sbs* s);
+// Grow the cursor's generation pool for calls of up to n batches now.
+int sbs_reserve(optb_sbs* s, uint64_t n_batches);
 // optb_encode_dev with RowSrc::early set as given (the split pipeline step).
 int encode_dev(optb_ctx* c, const optb_layout* L, const uint8_t* images, uint64_t row_stride,
                const int64_t* row_index, void* containers, uint8_t* offsets, void* stream, bool early);

@@ -137,6 +137,13 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
     optb_pipeline_destroy(p);
     return cuda_fail("CUDA call failed");
   }
+  // the sampler's generation pool for one call (growing it mid-stream would
+  // synchronise the side stream with the step in flight)
+  st = optb_b200::sbs_reserve(d->sbs, d->layout.n_batches * d->n_shards * p->spd);
+  if (st) {
+    optb_pipeline_destroy(p);
+    return st;
+  }
   for (int c = 0; c + 1 < p->nbuf; ++c) {  // the first calls' draws start right away
     st = enqueue_draws(p);
     if (st) {

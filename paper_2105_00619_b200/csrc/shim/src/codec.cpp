@@ -50,6 +50,33 @@ void check(int status) {
 }  // namespace shim
 }  // namespace optb
 
+namespace optb::shim {
+
+codec::EncodedBatch make_encoded(codec::CodecMode mode, const codec::ImageShape& shape, std::size_t n,
+                                 const uint8_t* plane, const uint8_t* offsets) {
+  using namespace codec;
+  const std::size_t P = shape.pixel_count(), wc = container_value_bytes(mode);
+  EncodedBatch enc;
+  enc.mode = mode;
+  enc.shape = shape;
+  enc.n_images = static_cast<uint8_t>(n);
+  if (mode == CodecMode::Float64Faithful) {
+    enc.packed_f64.resize(P);
+    std::memcpy(enc.packed_f64.data(), plane, P * 8);
+    return enc;
+  }
+  enc.packed.resize(P);
+  for (std::size_t p = 0; p < P; ++p) {
+    u128 v = 0;
+    std::memcpy(&v, plane + p * wc, wc);  // little-endian low bytes
+    enc.packed[p] = v;
+  }
+  if (mode_has_offsets(mode)) enc.offsets.assign(offsets, offsets + (n * P + 7) / 8);
+  return enc;
+}
+
+}  // namespace optb::shim
+
 namespace optb::codec {
 
 std::size_t capacity(CodecMode mode) {
@@ -106,23 +133,7 @@ EncodedBatch encode(std::span<const Image> images, CodecMode mode) {
   std::vector<uint8_t> plane(P * wc);
   std::vector<uint8_t> offs(std::max<uint64_t>(optb_layout_offsets_bytes(&L), 16));
   shim::check(optb_encode_host(shim::context(), &L, rows.data(), plane.data(), offs.data()));
-  EncodedBatch enc;
-  enc.mode = mode;
-  enc.shape = images[0].shape;
-  enc.n_images = static_cast<uint8_t>(n);
-  if (mode == CodecMode::Float64Faithful) {
-    enc.packed_f64.resize(P);
-    std::memcpy(enc.packed_f64.data(), plane.data(), P * 8);
-    return enc;
-  }
-  enc.packed.resize(P);
-  for (std::size_t p = 0; p < P; ++p) {
-    u128 v = 0;
-    std::memcpy(&v, plane.data() + p * wc, wc);  // little-endian low bytes
-    enc.packed[p] = v;
-  }
-  if (mode_has_offsets(mode)) enc.offsets.assign(offs.begin(), offs.begin() + (n * P + 7) / 8);
-  return enc;
+  return shim::make_encoded(mode, images[0].shape, n, plane.data(), offs.data());
 }
 
 std::vector<Image> decode(const EncodedBatch& enc) {

@@ -1,5 +1,5 @@
 """Drop-in proof: the reference's OWN unit suites (proj/tests/test_codec.cpp,
-test_sampler.cpp, doctest_main.cpp), compiled unmodified against the C++
+test_sampler.cpp, test_pipeline.cpp, doctest_main.cpp), compiled unmodified against the C++
 shim headers (paper_2105_00619_b200/csrc/shim/include/optb/*.hpp) and linked
 with liboptb_shim.so + liboptb_cuda.so, pass on the GPU.  The binary is built
 by __graft_entry__.build() where /root/reference exists and travels with the
@@ -16,8 +16,20 @@ BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "ref_suites_on_b200")
 
 
 @pytest.mark.skipif(not os.path.exists(BIN), reason="reference suites binary not built (no /root/reference here)")
-@pytest.mark.parametrize("suite", ["codec", "sampler"])
+@pytest.mark.parametrize("suite", ["codec", "sampler", "pipeline"])
 def test_reference_suites_pass_on_drop_in(suite, torch_cuda):
     r = subprocess.run([BIN, f"-ts={suite}"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "failed: 0" in r.stdout, r.stdout
+
+
+EXTRA = os.path.join(ROOT, "tests", "cpp", "_bin", "shim_extra")
+
+
+def test_shim_extra_suite(torch_cuda):
+    """tests/cpp/shim_extra.cpp: BatchCursor copies fork the identical stream,
+    the hook order across ring refills, acceptance criteria 1 / 6 / 8 restated
+    on the drop-in, and the one-call-per-epoch GPU encode of pipeline::run."""
+    r = subprocess.run([EXTRA], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "failed: 0" in r.stdout, r.stdout
