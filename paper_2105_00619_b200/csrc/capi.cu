@@ -825,6 +825,7 @@ struct optb_sbs {
 uint64_t optb_b200::sbs_examples(const optb_sbs* s) { return s ? s->N : 0; }
 namespace {
 int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st);
+int ensure_call_slot(optb_sbs* s, int r, size_t bytes, cudaStream_t st);
 }
 // Pool size for any call of up to n batches: class c starts at most
 // floor(n * count_c / m_c) + 1 generations in it and gets one more slot for
@@ -833,10 +834,23 @@ int ensure_pool(optb_sbs* s, uint64_t elems, cudaStream_t st);
 // step that last used the draw buffer -- so the pipeline reserves up front.
 int optb_b200::sbs_reserve(optb_sbs* s, uint64_t n) {
   if (!s) return OPTB_OK;
-  uint64_t need = s->N;
-  for (uint64_t c = 0; c < s->C; ++c)
-    if (s->m[c] >= 2 && s->counts[c]) need += (n * s->counts[c] / s->m[c] + 2) * s->m[c];
-  return ensure_pool(s, std::max<uint64_t>(need, 1), s->ctx->s_compute);
+  uint64_t need = s->N, events = 0;
+  for (uint64_t c = 0; c < s->C; ++c) {
+    if (!s->counts[c]) continue;
+    const uint64_t e = n * s->counts[c] / std::max<uint64_t>(s->m[c], 1) + 1;
+    events += e;
+    if (s->m[c] >= 2) need += (e + 1) * s->m[c];
+  }
+  int rc = ensure_pool(s, std::max<uint64_t>(need, 1), s->ctx->s_compute);
+  if (rc) return rc;
+  // the call block: event records, seeds, per-class lists and the gather
+  // tables (run_events / optb_sbs_next_dev), 16-byte padded pieces
+  const size_t block = events * (sizeof(SbsEvent) + 8 + 4) + s->C * (4 + 8 + 8 + 32) + 1024;
+  for (int r = 0; r < optb_sbs::kRing; ++r) {
+    rc = ensure_call_slot(s, r, block, s->ctx->s_compute);
+    if (rc) return rc;
+  }
+  return OPTB_OK;
 }
 
 namespace {
@@ -865,11 +879,9 @@ struct Packer {
   }
 };
 
-int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
-  const size_t bytes = std::max<size_t>(pk.buf.size(), 16);
-  const int r = s->ring;
-  s->ring = (s->ring + 1) % optb_sbs::kRing;
-  CK(cudaEventSynchronize(s->uploaded[r]), "sbs upload");  // this pinned slot is free again
+// Pinned slot r and the device block hold at least `bytes` (growing the
+// device block waits for the calls in flight on `st`).
+int ensure_call_slot(optb_sbs* s, int r, size_t bytes, cudaStream_t st) {
   if (s->h_call_cap[r] < bytes) {
     if (s->h_call[r]) cudaFreeHost(s->h_call[r]);
     s->h_call[r] = nullptr;
@@ -885,6 +897,16 @@ int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
     CK(cudaMalloc(&s->d_call, bytes * 2), "sbs call block");
     s->call_cap = bytes * 2;
   }
+  return OPTB_OK;
+}
+
+int upload_call(optb_sbs* s, const Packer& pk, cudaStream_t st) {
+  const size_t bytes = std::max<size_t>(pk.buf.size(), 16);
+  const int r = s->ring;
+  s->ring = (s->ring + 1) % optb_sbs::kRing;
+  CK(cudaEventSynchronize(s->uploaded[r]), "sbs upload");  // this pinned slot is free again
+  int rc = ensure_call_slot(s, r, bytes, st);
+  if (rc) return rc;
   memcpy(s->h_call[r], pk.buf.data(), pk.buf.size());
   // A kernel pulls the block over PCIe from the mapped pinned slot instead of
   // a cudaMemcpyAsync: an H2D copy would queue on the copy engine behind any
@@ -1023,7 +1045,10 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
   rc = upload_call(s, pk, st);
   if (s->prof) cudaEventRecord(s->pe[1], st);
   if (rc) return rc;
-  if (E == 0) return OPTB_OK;
+  if (E == 0) {
+    if (s->prof) cudaEventRecord(s->pe[2], st);
+    return OPTB_OK;
+  }
   uint8_t* d = s->d_call;
   ChainArgs a;
   a.ev = reinterpret_cast<const SbsEvent*>(d + o_ev);

@@ -108,7 +108,7 @@ std::vector<Draw> BatchCursor::next() {
     ring_len_ = refill_;
     // grow geometrically: a caller drawing a handful of batches pays for
     // few extra, a long stream amortises the device round trip
-    refill_ = std::min<std::size_t>(refill_ * 2, std::max<std::size_t>(1, (std::size_t{1} << 20) / (B ? B : 1)));
+    refill_ = std::min<std::size_t>(refill_ * 2, std::max<std::size_t>(1, (std::size_t{1} << 16) / (B ? B : 1)));
   }
   std::vector<Draw> batch(B);
   const int64_t* ex = ring_ex_.data() + ring_pos_ * B;
