@@ -318,7 +318,7 @@ def spawn(args):
     per GPU, and pass rank 0's line through."""
     import torch
     n_dev = torch.cuda.device_count()
-    if n_dev < args.gpus:
+    if n_dev < args.gpus and not args.oversubscribe:
         print(f"bench.py: --gpus {args.gpus} but only {n_dev} GPU(s) visible", file=sys.stderr, flush=True)
         return 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
@@ -542,6 +542,9 @@ def main():
     ap.add_argument("--no-check", action="store_true", help="skip the reference check of the last step")
     ap.add_argument("--probe-steps", type=int, default=6,
                     help="steps of the per-kernel timing pass (events around every launch)")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="allow --gpus N above the visible GPU count (ranks share GPUs: a smoke run of the N-rank "
+                         "path; device times are summed)")
     ap.add_argument("--split-kernels", action="store_true",
                     help="headline with separate encode / decode launches instead of the fused round trip")
     args = ap.parse_args()
@@ -738,7 +741,7 @@ def main():
         sharded = run_sharded(args, torch, dist, S, ds, offs, mem, out, stream, dev, rank, world, oversub,
                               images_per_step)
 
-    cpu = None
+    cpu = shim_api = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU baseline runs at N = 1 only
         threads = os.cpu_count() or 1
         ds_h, lab_h = host_dataset()
@@ -752,13 +755,14 @@ def main():
                "single_thread": {"value": round(v1, 1), "cores": 1, "sample": sample1 + ", median of 3"},
                "cpu_model": cpu_model(), "nproc": os.cpu_count()}
         del ds_h
+        shim_api = run_shim_api()
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic (counter-based SplitMix64 pixels, seed 7)",
                 "config": config(world), "roofline": roofline, "check": check, "cpu_baseline": cpu, "e2e": e2e,
-                "configs": configs, "sharded_dataset": sharded, "clocks": clk.summary(),
+                "configs": configs, "shim_api": shim_api, "sharded_dataset": sharded, "clocks": clk.summary(),
                 "gpu_launches": int(launches), "wall_s_timed": round(t_wall, 4),
                 "timing": "CUDA events on the launching stream around the K timed steps only; max over ranks"}
         if oversub:
@@ -771,6 +775,31 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_shim_api(n_batches=200):
+    """The reference runner's call pattern through the unchanged C++ API
+    (tools/shim_api_bench.cpp: one BatchCursor::next per batch, image_of +
+    codec::encode per 16-image chunk, codec::decode per chunk; C2 stream, one
+    host thread) built twice: against the drop-in shim (GPU underneath) and
+    against the reference itself (oracle/_ref/ref_api_bench, compiled from
+    its sources).  Same stream, same checksum."""
+    res = {}
+    for key, path in (("drop_in", os.path.join(ROOT, "paper_2105_00619_b200", "optb_shim_api_bench")),
+                      ("reference", os.path.join(ROOT, "oracle", "_ref", "ref_api_bench"))):
+        if not os.path.exists(path):
+            res[key] = {"unavailable": f"{os.path.relpath(path, ROOT)} not built"}
+            continue
+        try:
+            r = subprocess.run([path, "50000", str(n_batches)], capture_output=True, text=True, timeout=300)
+            res[key] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as ex:  # noqa: BLE001
+            res[key] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
+    d, r = res.get("drop_in", {}), res.get("reference", {})
+    if "images_per_s" in d and "images_per_s" in r:
+        res["speedup"] = round(d["images_per_s"] / r["images_per_s"], 3)
+        res["same_stream"] = d.get("checksum") == r.get("checksum")
+    return res
 
 
 def _dev_bytes(torch, ptr, n, dev):

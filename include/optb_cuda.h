@@ -349,6 +349,14 @@ typedef struct optb_pipeline_desc {
 } optb_pipeline_desc;
 
 int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* desc, optb_pipeline** out);
+/* Warm start (pipeline.cpp:154-177, PipelineConfig::warm_start): the epoch
+ * dumped as <dir>/batch_<epoch>_<k>.optb is loaded and validated once
+ * (optb_load_dev) into the pipeline's device planes; every step then only
+ * decodes it with `epilogue` into the caller's buffer -- no sampler, no
+ * encode.  Class tables need epilogue->row_class (there are no draws). */
+int optb_pipeline_create_warm(optb_ctx* ctx, const optb_layout* layout, uint32_t h, uint32_t w, uint32_t c,
+                              const char* dir, uint64_t epoch, const optb_epilogue* epilogue,
+                              int32_t record_timings, optb_pipeline** out);
 /* Enqueue the next step; `out` receives optb_layout_rows(layout) decoded rows. */
 int optb_pipeline_step(optb_pipeline* p, void* out, void* stream);
 /* Rows for subsequent steps come from `dataset` (e.g. a double-buffered

@@ -115,6 +115,8 @@ SIGNATURES = {
     "optb_load_records_dev": (ct.c_int, [vp, ct.c_char_p, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp,
                                          vp, ct.c_uint64, u64p]),
     "optb_pipeline_create":(ct.c_int, [vp, ct.POINTER(PipelineDesc), ct.POINTER(vp)]),
+    "optb_pipeline_create_warm": (ct.c_int, [vp, LP, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p,
+                                             ct.c_uint64, EP, ct.c_int32, ct.POINTER(vp)]),
     "optb_pipeline_step": (ct.c_int, [vp, vp, vp]),
     "optb_pipeline_set_dataset": (ct.c_int, [vp, vp, ct.c_uint64]),
     "optb_pipeline_step_host": (ct.c_int, [vp, vp, ct.c_uint64, ct.c_uint64, vp, vp]),

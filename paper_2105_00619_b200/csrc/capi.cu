@@ -172,6 +172,7 @@ struct optb_ctx {
   // pinned error-latch words for the small-call host path: [0] the reset
   // value, [1] the read-back (both stream ordered, no extra synchronisation)
   DevError* pin_err = nullptr;
+  DevError* d_err_small = nullptr;  // the small host calls' own latch (synchronous calls)
 };
 
 namespace {
@@ -285,6 +286,11 @@ int optb_ctx_create(int device, optb_ctx** out) {
     return cuda_err(cudaGetLastError(), "ctx create");
   }
   c->pin_err[0] = DevError{0, 0, ~0ull, 0, 0};
+  if (cudaMalloc(&c->d_err_small, sizeof(DevError)) != cudaSuccess ||
+      cudaMemcpy(c->d_err_small, &c->pin_err[0], sizeof(DevError), cudaMemcpyHostToDevice) != cudaSuccess) {
+    optb_ctx_destroy(c);
+    return cuda_err(cudaGetLastError(), "ctx create");
+  }
   int st = reset_err(c, c->s_compute);
   if (st) {
     optb_ctx_destroy(c);
@@ -314,6 +320,7 @@ void optb_ctx_destroy(optb_ctx* c) {
   if (c->tmp) cudaFree(c->tmp);
   if (c->d_err) cudaFree(c->d_err);
   if (c->pin_err) cudaFreeHost(c->pin_err);
+  if (c->d_err_small) cudaFree(c->d_err_small);
   if (c->s_compute) cudaStreamDestroy(c->s_compute);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
@@ -551,9 +558,9 @@ int ensure_slots(optb_ctx* c, size_t in_b, size_t out_b, size_t off_b) {
     c->slot_out = std::max(c->slot_out, out_b);
     c->slot_off = std::max<size_t>(std::max(c->slot_off, off_b), 16);
     for (int i = 0; i < optb_ctx::kSlots; ++i) {
-      CK(cudaHostAlloc(&c->pin_in[i], c->slot_in, cudaHostAllocDefault), "pinned staging");
-      CK(cudaHostAlloc(&c->pin_out[i], c->slot_out, cudaHostAllocDefault), "pinned staging");
-      CK(cudaHostAlloc(&c->pin_off[i], c->slot_off, cudaHostAllocDefault), "pinned staging");
+      CK(cudaHostAlloc(&c->pin_in[i], c->slot_in, cudaHostAllocMapped | cudaHostAllocPortable), "pinned staging");
+      CK(cudaHostAlloc(&c->pin_out[i], c->slot_out, cudaHostAllocMapped | cudaHostAllocPortable), "pinned staging");
+      CK(cudaHostAlloc(&c->pin_off[i], c->slot_off, cudaHostAllocMapped | cudaHostAllocPortable), "pinned staging");
       CK(cudaMalloc(&c->dev_in[i], c->slot_in), "device staging");
       CK(cudaMalloc(&c->dev_out[i], c->slot_out), "device staging");
       CK(cudaMalloc(&c->dev_off[i], c->slot_off), "device staging");
@@ -565,11 +572,21 @@ int ensure_slots(optb_ctx* c, size_t in_b, size_t out_b, size_t off_b) {
 constexpr uint64_t kSliceTarget = 32ull << 20;
 
 // Small host calls (the drop-in API encodes / decodes one chunk per call,
-// runner.cpp:77-90, nn.cpp:182): the call's latency is the cost, so one
-// stream, one H2D, one kernel, one D2H and ONE synchronisation -- no
-// cross-stream events, no pointer-attribute queries, the error latch reset
-// and read back in stream order through pinned words.
-constexpr uint64_t kSmallCall = 8ull << 20;
+// runner.cpp:77-90, nn.cpp:182): latency is the cost, and every dependent
+// copy adds a DMA <-> SM hand-off of several microseconds.  So the kernel
+// runs ZERO-COPY on the context's pinned staging (mapped into the device
+// address space): it gathers the rows over PCIe and stores its results
+// straight into pinned memory -- one kernel, one synchronisation (decode adds
+// one 32-byte read of its own error latch).  The generic kernels take plain
+// loads / stores to system memory; offset planes of lossless encodes are
+// zeroed on the host first.
+constexpr uint64_t kSmallCall = 4ull << 20;
+
+template <typename T>
+T* mapped(T* host) {
+  void* d = nullptr;
+  return cudaHostGetDevicePointer(&d, host, 0) == cudaSuccess ? static_cast<T*>(d) : nullptr;
+}
 
 int small_encode(optb_ctx* c, const optb_layout* L, const uint8_t* images, void* containers, uint8_t* offsets) {
   const uint64_t P = L->pixels, rows = optb_layout_rows(L);
@@ -578,12 +595,13 @@ int small_encode(optb_ctx* c, const optb_layout* L, const uint8_t* images, void*
   if (st) return st;
   cudaStream_t s = c->s_compute;
   memcpy(c->pin_in[0], images, rows * P);
-  CK(cudaMemcpyAsync(c->dev_in[0], c->pin_in[0], rows * P, cudaMemcpyHostToDevice, s), "H2D");
-  cudaError_t e = launch_encode(make_geom(L), RowSrc{c->dev_in[0], P, nullptr, nullptr, 0}, c->dev_out[0],
-                                c->dev_off[0], s, c->sms, &c->launches);
+  if (ob) memset(c->pin_off[0], 0, ob);
+  uint8_t *src = mapped(c->pin_in[0]), *dst = mapped(c->pin_out[0]), *odst = mapped(c->pin_off[0]);
+  if (!src || !dst || !odst) return cuda_err(cudaGetLastError(), "mapped staging");
+  const Geom g = make_geom(L);
+  cudaError_t e = launch_encode_generic(g, RowSrc{src, P, nullptr, nullptr, 0}, dst, odst, s, c->sms,
+                                                 &c->launches);
   if (e != cudaSuccess) return cuda_err(e, "encode launch");
-  CK(cudaMemcpyAsync(c->pin_out[0], c->dev_out[0], cb, cudaMemcpyDeviceToHost, s), "D2H");
-  if (ob) CK(cudaMemcpyAsync(c->pin_off[0], c->dev_off[0], ob, cudaMemcpyDeviceToHost, s), "D2H");
   CK(cudaStreamSynchronize(s), "sync");
   memcpy(containers, c->pin_out[0], cb);
   if (ob) memcpy(offsets, c->pin_off[0], ob);
@@ -601,19 +619,16 @@ int small_decode(optb_ctx* c, const optb_layout* L, const void* containers, cons
   cudaStream_t s = c->s_compute;
   memcpy(c->pin_in[0], containers, cb);
   if (ob) memcpy(c->pin_off[0], offsets, ob);
-  CK(cudaMemcpyAsync(c->d_err, &c->pin_err[0], sizeof(DevError), cudaMemcpyHostToDevice, s), "reset error latch");
-  CK(cudaMemcpyAsync(c->dev_in[0], c->pin_in[0], cb, cudaMemcpyHostToDevice, s), "H2D");
-  if (ob) CK(cudaMemcpyAsync(c->dev_off[0], c->pin_off[0], ob, cudaMemcpyHostToDevice, s), "H2D");
-  cudaError_t e = launch_decode(make_geom(L), c->dev_in[0], c->dev_off[0], make_epi(E, P), c->dev_out[0], c->d_err,
-                                s, c->sms, &c->launches);
+  uint8_t *src = mapped(c->pin_in[0]), *dst = mapped(c->pin_out[0]), *osrc = mapped(c->pin_off[0]);
+  if (!src || !dst || !osrc) return cuda_err(cudaGetLastError(), "mapped staging");
+  cudaError_t e = launch_decode_generic(make_geom(L), src, osrc, make_epi(E, P), dst, c->d_err_small, s, c->sms,
+                                        &c->launches);
   if (e != cudaSuccess) return cuda_err(e, "decode launch");
-  CK(cudaMemcpyAsync(c->pin_out[0], c->dev_out[0], outb, cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(&c->pin_err[1], c->d_err, sizeof(DevError), cudaMemcpyDeviceToHost, s), "read error latch");
+  CK(cudaMemcpyAsync(&c->pin_err[1], c->d_err_small, sizeof(DevError), cudaMemcpyDeviceToHost, s), "error latch");
   CK(cudaStreamSynchronize(s), "sync");
   const DevError h = c->pin_err[1];
-  if (h.kind != kErrNone) {
-    CK(cudaMemcpyAsync(c->d_err, &c->pin_err[0], sizeof(DevError), cudaMemcpyHostToDevice, s), "reset error latch");
-    CK(cudaStreamSynchronize(s), "sync");
+  if (h.kind != kErrNone) {  // rare: report, and clear the latch for the next call
+    CK(cudaMemcpy(c->d_err_small, &c->pin_err[0], sizeof(DevError), cudaMemcpyHostToDevice), "error latch");
     return latch_status(h);
   }
   memcpy(out, c->pin_out[0], outb);

@@ -72,6 +72,30 @@ cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* 
   }
 }
 
+// The plain grid-stride kernels, whatever the alignment: the small host
+// calls run them straight on mapped pinned memory (zero-copy over PCIe).
+cudaError_t launch_encode_generic(const Geom& g, const RowSrc& rs, void* containers, uint8_t* offsets,
+                                  cudaStream_t s, int sms, uint64_t* launches) {
+  switch (g.mode) {
+    case OPTB_EXACT64: return encode_v0(g, rs, false, containers, offsets, s, sms, launches);
+    case OPTB_EXACT128: return encode_v1(g, rs, false, containers, offsets, s, sms, launches);
+    case OPTB_F64: return encode_v2(g, rs, false, containers, offsets, s, sms, launches);
+    case OPTB_LOSSLESS64: return encode_v3(g, rs, false, containers, offsets, s, sms, launches);
+    default: return encode_v4(g, rs, false, containers, offsets, s, sms, launches);
+  }
+}
+
+cudaError_t launch_decode_generic(const Geom& g, const void* containers, const uint8_t* offsets, const Epi& e,
+                                  void* out, DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
+  switch (g.mode) {
+    case OPTB_EXACT64: return decode_v0(g, containers, offsets, e, false, out, err, s, sms, launches);
+    case OPTB_EXACT128: return decode_v1(g, containers, offsets, e, false, out, err, s, sms, launches);
+    case OPTB_F64: return decode_v2(g, containers, offsets, e, false, out, err, s, sms, launches);
+    case OPTB_LOSSLESS64: return decode_v3(g, containers, offsets, e, false, out, err, s, sms, launches);
+    default: return decode_v4(g, containers, offsets, e, false, out, err, s, sms, launches);
+  }
+}
+
 thread_local int g_rt_kind = OPTB_RT_NONE;
 
 namespace {

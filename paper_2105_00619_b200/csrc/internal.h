@@ -96,6 +96,11 @@ cudaError_t launch_encode(const Geom& g, const RowSrc& rows, void* containers, u
 cudaError_t launch_decode(const Geom& g, const void* containers, const uint8_t* offsets,
                           const Epi& e, void* out, DevError* err, cudaStream_t s, int num_sms,
                           uint64_t* launches);
+// The generic (any alignment, plain loads / stores) kernels only.
+cudaError_t launch_encode_generic(const Geom& g, const RowSrc& rows, void* containers, uint8_t* offsets,
+                                  cudaStream_t s, int num_sms, uint64_t* launches);
+cudaError_t launch_decode_generic(const Geom& g, const void* containers, const uint8_t* offsets, const Epi& e,
+                                  void* out, DevError* err, cudaStream_t s, int num_sms, uint64_t* launches);
 // Encode + decode of the same stream in one launch (vector path; lossless
 // modes need P % 512 == 0);
 // cudaErrorNotSupported when the geometry needs the separate launches.

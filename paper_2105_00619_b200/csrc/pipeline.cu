@@ -68,6 +68,7 @@ struct optb_pipeline {
   uintptr_t last_out = 0;  // the previous step's output range (what it wrote)
   uint64_t last_out_bytes = 0;
   bool timing = false;
+  bool warm = false;     // warm start: decode the loaded epoch every step
   uint32_t tstride = 1;  // time every tstride-th step (and sampler call)
   // host leg (optb_pipeline_step_host): double-buffered device copies of the
   // host dataset and of the decoded rows, with their own copy streams
@@ -155,10 +156,59 @@ int optb_pipeline_create(optb_ctx* ctx, const optb_pipeline_desc* d, optb_pipeli
   return OPTB_OK;
 }
 
+int optb_pipeline_create_warm(optb_ctx* ctx, const optb_layout* layout, uint32_t h, uint32_t w, uint32_t c,
+                              const char* dir, uint64_t epoch, const optb_epilogue* epilogue, int32_t record_timings,
+                              optb_pipeline** out) {
+  if (!ctx || !layout || !dir || !epilogue || !out) return arg_fail("create_warm: null argument");
+  *out = nullptr;
+  int st = optb_layout_check(layout);
+  if (st) return st;
+  if ((epilogue->class_scale || epilogue->class_bias) && !epilogue->row_class)
+    return arg_fail("create_warm: class tables need row_class (a warm start has no draws)");
+  auto* p = new optb_pipeline();
+  p->ctx = ctx;
+  p->d.layout = *layout;
+  p->d.epilogue = *epilogue;
+  p->d.n_shards = 1;
+  p->warm = true;
+  p->timing = record_timings != 0;
+  p->rows = optb_layout_rows(layout);
+  bool ok = cudaMalloc(&p->cont, optb_layout_container_bytes(layout) + 16) == cudaSuccess;
+  const uint64_t ob = optb_layout_offsets_bytes(layout);
+  if (ok && ob) ok = cudaMalloc(&p->offs, ob) == cudaSuccess;
+  for (int r = 0; r < kTimingRing && ok && p->timing; ++r)
+    ok = cudaEventCreate(&p->t_e0[r]) == cudaSuccess && cudaEventCreate(&p->t_e1[r]) == cudaSuccess &&
+         cudaEventCreate(&p->t_d1[r]) == cudaSuccess;
+  if (!ok) {
+    optb_pipeline_destroy(p);
+    return cuda_fail("CUDA call failed");
+  }
+  // the dumped epoch is read and validated once (pipeline.cpp:154-177 run_warm)
+  st = optb_load_dev(ctx, layout, h, w, c, dir, epoch, p->cont, p->offs);
+  if (st) {
+    optb_pipeline_destroy(p);
+    return st;
+  }
+  *out = p;
+  return OPTB_OK;
+}
+
 int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
   if (!p || !out) return arg_fail("step: null pipeline or output");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t k = p->step;
+  if (p->warm) {  // no sampler, no encode: the loaded containers decode into `out`
+    const int r = static_cast<int>(k % kTimingRing);
+    if (p->timing) {
+      cudaEventRecord(p->t_e0[r], s);
+      cudaEventRecord(p->t_e1[r], s);
+    }
+    const int st = optb_decode_dev(p->ctx, &p->d.layout, p->cont, p->offs, &p->d.epilogue, out, s);
+    if (st) return st;
+    if (p->timing) cudaEventRecord(p->t_d1[r], s);
+    ++p->step;
+    return OPTB_OK;
+  }
   const uint64_t call = k / p->spd, sub = k % p->spd;
   const int b = static_cast<int>(call % p->nbuf);
   const int r = static_cast<int>((k / p->tstride) % kTimingRing);
@@ -220,6 +270,7 @@ int optb_pipeline_step(optb_pipeline* p, void* out, void* stream) {
 
 int optb_pipeline_set_dataset(optb_pipeline* p, const uint8_t* dataset, uint64_t row_stride) {
   if (!p || !dataset) return arg_fail("set_dataset: null pipeline or dataset");
+  if (p->warm) return arg_fail("set_dataset: a warm-start pipeline has no dataset");
   p->d.dataset = dataset;
   p->d.row_stride = row_stride;
   return OPTB_OK;
@@ -245,15 +296,18 @@ int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, 
     return arg_fail("timings: not recorded for that step (record_timings, timing_stride, last 64 timed steps)");
   const int r = static_cast<int>((step / p->tstride) % kTimingRing);
   const int rc = static_cast<int>((step / p->spd) % kTimingRing);
-  cudaEvent_t last = p->d.split_kernels ? p->t_d1[r] : p->t_e1[r];
+  const bool two = p->d.split_kernels || p->warm;  // a separate decode interval
+  cudaEvent_t last = two ? p->t_d1[r] : p->t_e1[r];
   if (cudaEventSynchronize(last) != cudaSuccess) return cuda_fail("synchronize");
-  if (sbs_ms) {  // the SBS call that produced this step's draws, per step
+  if (sbs_ms && p->warm) {
+    *sbs_ms = 0.0f;
+  } else if (sbs_ms) {  // the SBS call that produced this step's draws, per step
     if (cudaEventElapsedTime(sbs_ms, p->t_s0[rc], p->t_s1[rc]) != cudaSuccess) return cuda_fail("event timing");
     *sbs_ms /= static_cast<float>(p->spd);
   }
   if (enc_ms && cudaEventElapsedTime(enc_ms, p->t_e0[r], p->t_e1[r]) != cudaSuccess) return cuda_fail("event timing");
   if (dec_ms) {
-    if (!p->d.split_kernels) {
+    if (!two) {
       *dec_ms = 0.0f;  // one fused launch: all of it is in enc_ms
     } else if (cudaEventElapsedTime(dec_ms, p->t_e1[r], p->t_d1[r]) != cudaSuccess) {
       return cuda_fail("CUDA call failed");
@@ -265,6 +319,7 @@ int optb_pipeline_timings(const optb_pipeline* p, uint64_t step, float* sbs_ms, 
 int optb_pipeline_step_host(optb_pipeline* p, const uint8_t* dataset_host, uint64_t n_rows, uint64_t row_stride,
                             void* out_host, void* stream) {
   if (!p || !dataset_host || !out_host || !n_rows) return arg_fail("step_host: null buffer or empty dataset");
+  if (p->warm) return arg_fail("step_host: a warm-start pipeline has no dataset");
   if (row_stride == 0) row_stride = p->d.layout.pixels;
   if (row_stride < p->d.layout.pixels) return arg_fail("step_host: row_stride < pixels");
   // the draws index every example of the sampler's class index

@@ -56,6 +56,29 @@ class Pipeline:
                       and dataset.data_ptr() % 16 == 0 and (int(mode) in (0, 1, 2) or P % 512 == 0))
         self.steps = 0
 
+    @classmethod
+    def warm(cls, mode, batch: int, batches_per_step: int, shape, directory: str, epoch: int = 0, per_chunk=None,
+             out_dtype=None, scale: float = 1.0, device: int = 0, record_timings: bool = False):
+        """Warm start (optb_pipeline_create_warm; PipelineConfig::warm_start,
+        pipeline.cpp:154-177): the dumped epoch <directory>/batch_<epoch>_<k>.optb
+        is loaded once and every step decodes it into the caller's buffer."""
+        import torch
+        from . import codec
+        out_dtype = out_dtype or torch.uint8
+        dt = {torch.uint8: U8, torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}[out_dtype]
+        self = cls.__new__(cls)
+        P = shape.pixel_count()
+        self.layout = Layout(int(mode), per_chunk or codec.capacity(mode), P, batch, batches_per_step)
+        self.rows, self.P, self.device = batch * batches_per_step, P, device
+        self._keep, self._dataset, self._host_bufs = (), None, []
+        self.fused, self.steps = False, 0
+        E = Epilogue(dt, float(scale), None, None, None, 0)
+        self._h = ct.c_void_p()
+        check(lib.optb_pipeline_create_warm(_lib.context(device), ct.byref(self.layout), shape.height, shape.width,
+                                            shape.channels, str(directory).encode(), epoch, ct.byref(E),
+                                            1 if record_timings else 0, ct.byref(self._h)))
+        return self
+
     def step(self, out, stream=None):
         import torch
         if stream is None:

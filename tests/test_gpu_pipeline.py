@@ -263,3 +263,41 @@ def test_pipeline_step_host_rejects_short_dataset(pkg, oracle_mod, torch_cuda):
     ex, _ = ref.next(nb)
     assert np.array_equal(out.numpy(), ds[ex])
     pipe.close()
+
+
+def test_pipeline_warm_start_vs_oracle(pkg, oracle_mod, torch_cuda, tmp_path):
+    """Warm start (PipelineConfig::warm_start, pipeline.cpp:154-177): an
+    epoch dumped in OPTB files (optb_dump_dev) is loaded once and every step
+    decodes it again -- equal to the oracle's decode of the oracle's encode
+    of the reference-stream draws, every step; a missing dump is a
+    FormatError at creation."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    C = pkg.codec
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P = 64, 5, 768
+    shape = C.ImageShape(16, 16, 3)
+    ref_ex, _ = ref.next(nb)
+    for mode in (1, 4):
+        n = C.capacity(mode)
+        L = C.layout(mode, n, P, B, nb)
+        want_c, want_o = O.encode_stream(ds, ref_ex, mode, n, B, nb)
+        cont, offs_ = C.alloc_stream(L)
+        cont[: want_c.size].copy_(torch.from_numpy(want_c))
+        if want_o is not None:
+            offs_[: want_o.size].copy_(torch.from_numpy(want_o))
+        d = tmp_path / f"warm{mode}"
+        C.dump_dev(L, cont, offs_, shape, str(d), 0)
+        warm = Pipeline.warm(mode, B, nb, shape, str(d), 0, per_chunk=n, out_dtype=torch.float32, scale=SCALE,
+                             record_timings=True)
+        want = O.decode_stream(want_c, want_o, mode, n, P, B, nb, out_dtype=O.F32, scale=SCALE)
+        for k in range(3):
+            o = torch.empty((B * nb, P), dtype=torch.float32, device="cuda")
+            warm.step(o)
+            C.sync()
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), want.view(np.uint32)), (mode, k)
+            s_ms, e_ms, d_ms = warm.timings(k)
+            assert s_ms == 0.0 and d_ms > 0
+        warm.close()
+    with pytest.raises(pkg.errors.FormatError):
+        Pipeline.warm(1, B, nb, shape, str(tmp_path / "missing"), 0)
