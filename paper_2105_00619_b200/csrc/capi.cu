@@ -281,7 +281,7 @@ int optb_ctx_create(int device, optb_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_kern[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming);
   }
-  if (cudaHostAlloc(&c->pin_err, 2 * sizeof(DevError), cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaHostAlloc(&c->pin_err, 2 * sizeof(DevError), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
     optb_ctx_destroy(c);
     return cuda_err(cudaGetLastError(), "ctx create");
   }
@@ -573,20 +573,35 @@ constexpr uint64_t kSliceTarget = 32ull << 20;
 
 // Small host calls (the drop-in API encodes / decodes one chunk per call,
 // runner.cpp:77-90, nn.cpp:182): latency is the cost, and every dependent
-// copy adds a DMA <-> SM hand-off of several microseconds.  So the kernel
-// runs ZERO-COPY on the context's pinned staging (mapped into the device
-// address space): it gathers the rows over PCIe and stores its results
-// straight into pinned memory -- one kernel, one synchronisation (decode adds
-// one 32-byte read of its own error latch).  The generic kernels take plain
-// loads / stores to system memory; offset planes of lossless encodes are
-// zeroed on the host first.
+// copy adds a DMA <-> SM hand-off of several microseconds.  Where the vector
+// kernels apply, the kernel runs ZERO-COPY on the context's pinned staging
+// (mapped into the device address space): 16-byte cp.async gathers of the
+// rows over PCIe, per-lane stores of its results straight into pinned memory
+// (g_sysmem: no tensor-map transfers) -- one launch and one synchronisation;
+// the decode's error latch is copied out by a second tiny kernel (a kernel to
+// kernel hand-off, not a DMA).  Other geometries stage through device memory:
+// H2D, kernel, D2H, still on one stream with one synchronisation.
 constexpr uint64_t kSmallCall = 4ull << 20;
+
+__global__ void k_latch_out(const DevError* __restrict__ d, DevError* __restrict__ h) {
+  if (threadIdx.x == 0) *h = *d;
+}
 
 template <typename T>
 T* mapped(T* host) {
   void* d = nullptr;
   return cudaHostGetDevicePointer(&d, host, 0) == cudaSuccess ? static_cast<T*>(d) : nullptr;
 }
+
+bool small_vec(const optb_layout* L) {
+  const bool lossless = L->mode == OPTB_LOSSLESS64 || L->mode == OPTB_LOSSLESS128;
+  return L->pixels % (lossless ? 32 : 16) == 0;
+}
+
+struct SysmemScope {  // the launches inside read / write mapped host memory
+  SysmemScope() { g_sysmem = true; }
+  ~SysmemScope() { g_sysmem = false; }
+};
 
 int small_encode(optb_ctx* c, const optb_layout* L, const uint8_t* images, void* containers, uint8_t* offsets) {
   const uint64_t P = L->pixels, rows = optb_layout_rows(L);
@@ -595,12 +610,20 @@ int small_encode(optb_ctx* c, const optb_layout* L, const uint8_t* images, void*
   if (st) return st;
   cudaStream_t s = c->s_compute;
   memcpy(c->pin_in[0], images, rows * P);
-  if (ob) memset(c->pin_off[0], 0, ob);
-  uint8_t *src = mapped(c->pin_in[0]), *dst = mapped(c->pin_out[0]), *odst = mapped(c->pin_off[0]);
-  if (!src || !dst || !odst) return cuda_err(cudaGetLastError(), "mapped staging");
   const Geom g = make_geom(L);
-  cudaError_t e = launch_encode_generic(g, RowSrc{src, P, nullptr, nullptr, 0}, dst, odst, s, c->sms,
-                                                 &c->launches);
+  cudaError_t e;
+  if (small_vec(L)) {
+    uint8_t *src = mapped(c->pin_in[0]), *dst = mapped(c->pin_out[0]), *odst = mapped(c->pin_off[0]);
+    if (!src || !dst || !odst) return cuda_err(cudaGetLastError(), "mapped staging");
+    SysmemScope scope;
+    e = launch_encode(g, RowSrc{src, P, nullptr, nullptr, 0}, dst, odst, s, c->sms, &c->launches);
+  } else {
+    CK(cudaMemcpyAsync(c->dev_in[0], c->pin_in[0], rows * P, cudaMemcpyHostToDevice, s), "H2D");
+    e = launch_encode(g, RowSrc{c->dev_in[0], P, nullptr, nullptr, 0}, c->dev_out[0], c->dev_off[0], s, c->sms,
+                      &c->launches);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->pin_out[0], c->dev_out[0], cb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && ob) e = cudaMemcpyAsync(c->pin_off[0], c->dev_off[0], ob, cudaMemcpyDeviceToHost, s);
+  }
   if (e != cudaSuccess) return cuda_err(e, "encode launch");
   CK(cudaStreamSynchronize(s), "sync");
   memcpy(containers, c->pin_out[0], cb);
@@ -619,12 +642,26 @@ int small_decode(optb_ctx* c, const optb_layout* L, const void* containers, cons
   cudaStream_t s = c->s_compute;
   memcpy(c->pin_in[0], containers, cb);
   if (ob) memcpy(c->pin_off[0], offsets, ob);
-  uint8_t *src = mapped(c->pin_in[0]), *dst = mapped(c->pin_out[0]), *osrc = mapped(c->pin_off[0]);
-  if (!src || !dst || !osrc) return cuda_err(cudaGetLastError(), "mapped staging");
-  cudaError_t e = launch_decode_generic(make_geom(L), src, osrc, make_epi(E, P), dst, c->d_err_small, s, c->sms,
-                                        &c->launches);
+  const Geom g = make_geom(L);
+  const Epi ep = make_epi(E, P);
+  DevError* h_latch = mapped(&c->pin_err[1]);
+  if (!h_latch) return cuda_err(cudaGetLastError(), "mapped latch");
+  cudaError_t e;
+  if (small_vec(L)) {
+    uint8_t *src = mapped(c->pin_in[0]), *dst = mapped(c->pin_out[0]), *osrc = mapped(c->pin_off[0]);
+    if (!src || !dst || !osrc) return cuda_err(cudaGetLastError(), "mapped staging");
+    SysmemScope scope;
+    e = launch_decode(g, src, osrc, ep, dst, c->d_err_small, s, c->sms, &c->launches);
+  } else {
+    CK(cudaMemcpyAsync(c->dev_in[0], c->pin_in[0], cb, cudaMemcpyHostToDevice, s), "H2D");
+    if (ob) CK(cudaMemcpyAsync(c->dev_off[0], c->pin_off[0], ob, cudaMemcpyHostToDevice, s), "H2D");
+    e = launch_decode(g, c->dev_in[0], c->dev_off[0], ep, c->dev_out[0], c->d_err_small, s, c->sms, &c->launches);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->pin_out[0], c->dev_out[0], outb, cudaMemcpyDeviceToHost, s);
+  }
   if (e != cudaSuccess) return cuda_err(e, "decode launch");
-  CK(cudaMemcpyAsync(&c->pin_err[1], c->d_err_small, sizeof(DevError), cudaMemcpyDeviceToHost, s), "error latch");
+  k_latch_out<<<1, 32, 0, s>>>(c->d_err_small, h_latch);
+  ++c->launches;
+  CK(cudaGetLastError(), "latch copy");
   CK(cudaStreamSynchronize(s), "sync");
   const DevError h = c->pin_err[1];
   if (h.kind != kErrNone) {  // rare: report, and clear the latch for the next call

@@ -97,6 +97,7 @@ cudaError_t launch_decode_generic(const Geom& g, const void* containers, const u
 }
 
 thread_local int g_rt_kind = OPTB_RT_NONE;
+thread_local bool g_sysmem = false;
 
 namespace {
 std::mutex g_tag_mu;

@@ -1672,7 +1672,7 @@ cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs
                       uint64_t* launches) {
   if constexpr (!VecMode<MODE>::OFFS) {
     CUtensorMap cm;
-    if (encode_bulk_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC)) {
+    if (encode_bulk_enabled() && !g_sysmem && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC)) {
       if (split_deep(g, sms)) return enc_bulk_launch<MODE, PTRS, true>(cm, g, rs, cont, offs, s, sms, launches);
       return enc_bulk_launch<MODE, PTRS, false>(cm, g, rs, cont, offs, s, sms, launches);
     }
@@ -1754,7 +1754,7 @@ template <int MODE, int O>
 cudaError_t dec_vec(const Geom& g, const void* cont, const uint8_t* offs, const Epi& e, void* out,
                     DevError* err, cudaStream_t s, int sms, uint64_t* launches) {
   CUtensorMap cm;
-  if (tma_decode_enabled() && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
+  if (tma_decode_enabled() && !g_sysmem && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC))
     return split_deep(g, sms) ? dec_vec_launch<MODE, O, true, true>(cm, g, cont, offs, e, out, err, s, sms, launches)
                               : dec_vec_launch<MODE, O, true, false>(cm, g, cont, offs, e, out, err, s, sms, launches);
   memset(&cm, 0, sizeof cm);

@@ -16,6 +16,12 @@ namespace optb_b200 {
 // different devices may share one process.
 cudaError_t ensure_smem_attr(const void* kernel, int bytes);
 
+// Set by the caller around a launch whose buffers are mapped pinned host
+// memory (the small host calls run zero-copy): the vector kernels then move
+// data with cp.async / per-lane loads and stores only, no tensor-map (TMA)
+// transfers.
+extern thread_local bool g_sysmem;
+
 // Which kernel the most recent fused round trip of this thread ran
 // (OPTB_RT_* in optb_cuda.h); set by launch_roundtrip's launchers.
 extern thread_local int g_rt_kind;

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (run here, on the CPU box).
 
-    python tools/ncu_summary.py gpurun_out/launches3.csv gpurun_out/prof3.ncu-rep [more.ncu-rep ...] r01
+    python tools/ncu_summary.py [--launches gpurun_out/launches.csv] gpurun_out/k.ncu-rep [more.ncu-rep ...] r02
 
 Writes profiles/<tag>_launches.csv (kernel, duration per launch: the
 `--metrics gpu__time_duration.sum` launch list) and profiles/ncu_summary.json
@@ -53,8 +53,7 @@ def launches(path, tag):
     dst = os.path.join(ROOT, "profiles", f"{tag}_launches.csv")
     with open(dst, "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised replay:\n"
-                "# compare shares of the step, not absolutes); bench.py --steps 4 --warmup 3 --e2e-steps 0 "
-                "--split-steps 4 --no-cpu-baseline\n")
+                "# compare shares of the step, not absolutes)\n")
         f.write("id,kernel,duration_ns\n")
         for i, k, t in out:
             f.write(f"{i},{k},{t:.0f}\n")
@@ -78,48 +77,39 @@ def full(path):
                 m[k] = {"value": v, "unit": unit}
         rb = m.get("dram__bytes_read.sum", {}).get("value", 0.0)
         wb = m.get("dram__bytes_write.sum", {}).get("value", 0.0)
-        kern.setdefault(short(d["Kernel Name"]), {"metrics": m, "dram_bytes_per_launch": rb + wb})
+        kern[short(d["Kernel Name"])] = {"metrics": m, "dram_bytes_per_launch": rb + wb}
     return kern
 
 
 def main():
-    lcsv, tag, reps = sys.argv[1], sys.argv[-1], sys.argv[2:-1]
-    out = launches(lcsv, tag)
+    """ncu_summary.py [--launches LIST.csv] REP.ncu-rep [REP ...] TAG"""
+    args = sys.argv[1:]
+    lcsv = None
+    if args and args[0] == "--launches":
+        lcsv, args = args[1], args[2:]
+    tag, reps = args[-1], args[:-1]
+    if lcsv:
+        out = launches(lcsv, tag)
+        tot = sum(t for _, _, t in out) or 1.0
+        per = {}
+        for _, k, t in out:
+            per[k] = per.get(k, 0.0) + t
+        for k, t in sorted(per.items(), key=lambda x: -x[1])[:20]:
+            print(f"{k:60s} {t / 1e3:10.1f} us  {100 * t / tot:5.1f} %")
     kern = {}
     for rep in reps:
-        kern.update(full(rep))
-    rows, P = 97 * 512, 3072
-    summ = {"source": f"ncu --set full --clock-control none --import-source on on bench.py (tag {tag}, B200)",
+        for k, v in full(rep).items():
+            kern[k] = v  # the last capture of a kernel wins (the warmed launch)
+    summ = {"source": f"ncu --set full --clock-control none --import-source on (tag {tag}, B200)",
+            "tag": tag,
             "note": "ncu flushes caches before each replayed kernel; writes still dirty in L2 at kernel end are "
                     "not counted in dram__bytes_write, so traffic is below the algorithmic bytes for the "
                     "write-heavy kernels",
-            "algorithmic_bytes_per_launch": {"k_encode_vec<exact128,false>": rows * P * 2 + rows * 8,
-                                             "k_encode_bulk<exact128,false,true>": rows * P * 2 + rows * 8,
-                                             "k_decode_vec<exact128,u8,true,true>": rows * P * 2,
-                                             "k_roundtrip_il<exact128,u8,false,false,true,true>": rows * P * 3 + rows * 8,
-                                             "k_decode_vec<exact128,u8,true>": rows * P * 2,
-                                             "k_roundtrip_vec<exact128,u8,false,false>": rows * P * 4 + rows * 8,
-                                             # interleaved: the container re-read is an L2 hit
-                                             "k_roundtrip_il<exact128,u8,false,false>": rows * P * 3 + rows * 8},
             "kernels": kern}
     json.dump(summ, open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w"), indent=1)
-    step = {}
-    # the last draw call of the fused pipeline in the launch list: its SBS
-    # launches and the roundtrip launches (steps_per_draw of them) they fed
-    is_rt = [k.startswith(("k_roundtrip_vec<exact128", "k_roundtrip_il<exact128")) for _, k, _ in out]
-    last_rt = max(i for i, r in enumerate(is_rt) if r)
-    lo = last_rt
-    while lo > 0 and is_rt[lo - 1]:
-        lo -= 1
-    while lo > 0 and not is_rt[lo - 1]:
-        lo -= 1
-    for _, k, t in out[lo:last_rt + 1]:
-        step[k] = step.get(k, 0) + t
-    tot = sum(step.values())
-    for k, t in sorted(step.items(), key=lambda x: -x[1]):
-        print(f"{k:40s} {t / 1e3:8.1f} us  {100 * t / tot:5.1f} %")
     for k, v in kern.items():
-        print(k, v["dram_bytes_per_launch"], v["metrics"].get("gpu__time_duration.sum"))
+        t = v["metrics"].get("gpu__time_duration.sum", {})
+        print(f"{k:70s} dram {v['dram_bytes_per_launch'] / 1e6:9.2f} MB  {t.get('value')} {t.get('unit')}")
 
 
 if __name__ == "__main__":
