@@ -14,7 +14,9 @@
 // its inputs in L2), CUDA events, median of 20.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/mixlab.cu -o build/mixlab
-//   build/mixlab            # one JSON line per kernel and grid
+//   build/mixlab [MB]       # one JSON line per kernel and grid; MB = input
+//                           # bytes per launch (default one C2 step, 152.6;
+//                           # 3221 = one C5 epoch), plus cudaMemcpyAsync D2D
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -102,13 +104,16 @@ void run(const char* name, int sms, int per_sm, uint64_t n16, std::vector<uint4*
   for (auto& e : ev) CK(cudaEventDestroy(e));
 }
 
-int main() {
+int main(int argc, char** argv) {
   int dev = 0, sms = 0;
   CK(cudaSetDevice(dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const uint64_t n16 = 152567808ull / 16;  // one C2 step's rows (49664 x 3072 B)
-  std::vector<uint4*> ins(3), outs(3);
-  for (int s = 0; s < 3; ++s) {
+  uint64_t n16 = 152567808ull / 16;  // one C2 step's rows (49664 x 3072 B)
+  if (argc > 1) n16 = static_cast<uint64_t>(atof(argv[1]) * 1e6) / 16;
+  // rotate over enough buffer sets that a launch never finds its inputs in L2
+  const int sets = n16 * 16 > (1ull << 30) ? 2 : 3;
+  std::vector<uint4*> ins(sets), outs(sets);
+  for (int s = 0; s < sets; ++s) {
     CK(cudaMalloc(&ins[s], n16 * 16));
     CK(cudaMalloc(&outs[s], 3 * n16 * 16));
     CK(cudaMemset(ins[s], s + 1, n16 * 16));
@@ -116,6 +121,25 @@ int main() {
   }
   uint32_t* sink;
   CK(cudaMalloc(&sink, 4));
+  {  // the driver's copy: cudaMemcpyAsync device to device
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    for (int i = 0; i < 3; ++i) CK(cudaMemcpyAsync(outs[i % sets], ins[i % sets], n16 * 16, cudaMemcpyDeviceToDevice));
+    std::vector<float> t;
+    for (int i = 0; i < 10; ++i) {
+      CK(cudaEventRecord(a));
+      CK(cudaMemcpyAsync(outs[i % sets], ins[i % sets], n16 * 16, cudaMemcpyDeviceToDevice));
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      t.push_back(ms);
+    }
+    std::sort(t.begin(), t.end());
+    printf("{\"kernel\": \"memcpy_d2d\", \"read_mb\": %.1f, \"write_mb\": %.1f, \"us\": %.2f, \"gbs\": %.1f}\n",
+           n16 * 16 / 1e6, n16 * 16 / 1e6, t[0] * 1e3, 2.0 * n16 * 16 / (t[0] * 1e3) / 1e3);
+  }
   for (int per_sm : {4, 8, 16}) {
     run<1, 0>("read", sms, per_sm, n16, ins, outs, sink);
     run<0, 1>("write", sms, per_sm, n16, ins, outs, sink);

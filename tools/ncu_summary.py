@@ -19,6 +19,10 @@ KEEP = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__shared_mem_per_block_dynamic"]
+# plus every metric with one of these prefixes (stall sampling, pipe usage)
+KEEP_PREFIX = ("smsp__pcsamp_warps_issue_stalled_", "sm__inst_executed_pipe_", "smsp__issue_active.avg.pct",
+               "sm__pipe_alu_cycles_active.avg.pct", "sm__pipe_fma_cycles_active.avg.pct",
+               "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "dram__throughput.avg.pct")
 MODES = {"0": "exact64", "1": "exact128", "2": "f64", "3": "lossless64", "4": "lossless128"}
 OUTS = {"0": "u8", "1": "f32", "2": "f16", "3": "bf16"}
 
@@ -61,16 +65,29 @@ def launches(path, tag):
 
 
 def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
+    """Per-kernel metrics of one capture: an .ncu-rep (exported here) or its
+    `--page raw --csv` export (tools/ncu_cases.sh)."""
+    if path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = [r for r in csv.reader(raw.splitlines())]
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    rows = rows[start:]
     hdr, units = rows[0], rows[1]
     kern = {}
     for r in rows[2:]:
+        if len(r) != len(hdr):
+            continue
         d, u = dict(zip(hdr, r)), dict(zip(hdr, units))
         m = {}
-        for k in KEEP:
-            if k in d and d[k] != "":
-                v, unit = float(d[k].replace(",", "")), u[k]
+        names = KEEP + [k for k in hdr if k.startswith(KEEP_PREFIX) and k not in KEEP]
+        for k in names:
+            if k in d and d[k] not in ("", "0", "n/a"):
+                try:
+                    v, unit = float(d[k].replace(",", "")), u[k]
+                except ValueError:
+                    continue
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit)
                 if scale:
                     v, unit = v * scale, "byte"
@@ -88,6 +105,10 @@ def main():
     if args and args[0] == "--launches":
         lcsv, args = args[1], args[2:]
     tag, reps = args[-1], args[:-1]
+    raw_dir = None
+    if reps and reps[0] == "--raw":  # a tools/ncu_cases.sh directory: <case>.raw.csv per case
+        raw_dir = reps[1]
+        reps = [os.path.join(raw_dir, f) for f in sorted(os.listdir(raw_dir)) if f.endswith(".raw.csv")]
     if lcsv:
         out = launches(lcsv, tag)
         tot = sum(t for _, _, t in out) or 1.0
@@ -98,8 +119,9 @@ def main():
             print(f"{k:60s} {t / 1e3:10.1f} us  {100 * t / tot:5.1f} %")
     kern = {}
     for rep in reps:
+        case = os.path.basename(rep).split(".")[0] + ":" if raw_dir else ""
         for k, v in full(rep).items():
-            kern[k] = v  # the last capture of a kernel wins (the warmed launch)
+            kern[case + k] = v  # the last capture of a kernel wins (the warmed launch)
     summ = {"source": f"ncu --set full --clock-control none --import-source on (tag {tag}, B200)",
             "tag": tag,
             "note": "ncu flushes caches before each replayed kernel; writes still dirty in L2 at kernel end are "
