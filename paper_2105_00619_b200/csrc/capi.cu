@@ -871,6 +871,8 @@ struct optb_sbs {
   // scratch for next_host
   int64_t* d_ex = nullptr;
   int32_t* d_cl = nullptr;
+  int64_t* h_ex = nullptr;  // pinned bounce buffers of optb_sbs_next_host
+  int32_t* h_cl = nullptr;
   uint64_t ex_cap = 0;
 };
 
@@ -1386,6 +1388,8 @@ void optb_sbs_destroy(optb_sbs* s) {
   }
   if (s->d_ex) cudaFree(s->d_ex);
   if (s->d_cl) cudaFree(s->d_cl);
+  if (s->h_ex) cudaFreeHost(s->h_ex);
+  if (s->h_cl) cudaFreeHost(s->h_cl);
   for (auto& e : s->pe)
     if (e) cudaEventDestroy(e);
   delete s;
@@ -1519,21 +1523,34 @@ int optb_sbs_next_host(optb_sbs* s, uint64_t n, int64_t* examples, int32_t* clas
   if (n == 0) return OPTB_OK;
   const uint64_t rows = n * s->B;
   if (s->ex_cap < rows) {
+    // sized once for the drop-in cursor's largest refill (64 Ki draws): a
+    // growing caller does not pay a synchronising cudaMalloc per refill
+    const uint64_t cap = rows > (1ull << 16) ? rows : (1ull << 16);
     if (s->d_ex) cudaFree(s->d_ex);
     if (s->d_cl) cudaFree(s->d_cl);
+    if (s->h_ex) cudaFreeHost(s->h_ex);
+    if (s->h_cl) cudaFreeHost(s->h_cl);
     s->d_ex = nullptr;
     s->d_cl = nullptr;
+    s->h_ex = nullptr;
+    s->h_cl = nullptr;
     s->ex_cap = 0;
-    CK(cudaMalloc(&s->d_ex, rows * 8), "sbs scratch");
-    CK(cudaMalloc(&s->d_cl, rows * 4), "sbs scratch");
-    s->ex_cap = rows;
+    CK(cudaMalloc(&s->d_ex, cap * 8), "sbs scratch");
+    CK(cudaMalloc(&s->d_cl, cap * 4), "sbs scratch");
+    CK(cudaHostAlloc(&s->h_ex, cap * 8, cudaHostAllocDefault), "sbs pinned scratch");
+    CK(cudaHostAlloc(&s->h_cl, cap * 4, cudaHostAllocDefault), "sbs pinned scratch");
+    s->ex_cap = cap;
   }
   cudaStream_t st = s->ctx->s_compute;
   int rc = optb_sbs_next_dev(s, n, 0, 1, s->d_ex, s->d_cl, st);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(examples, s->d_ex, rows * 8, cudaMemcpyDeviceToHost, st), "sbs D2H");
-  if (classes) CK(cudaMemcpyAsync(classes, s->d_cl, rows * 4, cudaMemcpyDeviceToHost, st), "sbs D2H");
+  // pinned bounce buffers: an async DMA instead of the driver's staged
+  // pageable copy; the caller's arrays are filled by memcpy
+  CK(cudaMemcpyAsync(s->h_ex, s->d_ex, rows * 8, cudaMemcpyDeviceToHost, st), "sbs D2H");
+  if (classes) CK(cudaMemcpyAsync(s->h_cl, s->d_cl, rows * 4, cudaMemcpyDeviceToHost, st), "sbs D2H");
   CK(cudaStreamSynchronize(st), "sbs sync");
+  memcpy(examples, s->h_ex, rows * 8);
+  if (classes) memcpy(classes, s->h_cl, rows * 4);
   g_err.clear();
   return OPTB_OK;
 }
