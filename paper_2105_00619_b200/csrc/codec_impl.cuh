@@ -422,7 +422,10 @@ struct VecMode {
   static constexpr int ROWS_B = NI * 512;                              // staged input rows
   static constexpr int WORDS_B = 512 * WC;                             // container words of a tile
   static constexpr int PAR_B = OFFS ? NI * 64 : 0;                     // staged parity bits (decode)
-  static constexpr int ENC_SLOT = ROWS_B > WORDS_B ? ROWS_B : WORDS_B;
+  // lossless slots rounded up to 1024 bytes: the bulk tensor store reads a
+  // 128B-swizzled box, which must start 1024-aligned
+  static constexpr int ENC_RAW = ROWS_B > WORDS_B ? ROWS_B : WORDS_B;
+  static constexpr int ENC_SLOT = OFFS ? (ENC_RAW + 1023) / 1024 * 1024 : ENC_RAW;
   static constexpr int DEC_SLOT = (WORDS_B + PAR_B) > ROWS_B ? (WORDS_B + PAR_B) : ROWS_B;
   static constexpr int MIN_BLOCKS = (WC == 16 || NI == 16) ? 1 : 2;
 };
@@ -532,7 +535,6 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
                                             uint32_t warp_region = NS * VecMode<MODE>::ENC_SLOT,
                                             Hook on_last = Hook{}, TileHook after_tile = TileHook{},
                                             const CUtensorMap* smap = nullptr) {
-  static_assert(!BULK || !VecMode<MODE>::OFFS, "bulk container stores: exact and f64 modes");
   const uint8_t* __restrict__ images = src.images;
   const uint64_t row_stride = src.stride;
   const int64_t* __restrict__ row_index = src.index;
@@ -690,6 +692,19 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
         }
       }
     }
+    // lossless container words (codec.cpp:128-134): pixel p's 7-bit fields
+    auto ll_word8 = [&](int p) -> uint2 {  // lossless64: images 0..7, image 8's field at bit 56
+      const uint2 lo = pack7x8(m[p][0], m[p][1]);
+      return make_uint2(lo.x, lo.y + (m[p][2] & 0xFEu) * (1u << 23));
+    };
+    auto ll_word16 = [&](int p) -> uint4 {  // lossless128: fields 0..15, images 16/17 at bits 112/119
+      const uint2 lo = pack7x8(m[p][0], m[p][1]);  // images 0..7 -> bits 0..55
+      const uint2 hi = pack7x8(m[p][2], m[p][3]);  // images 8..15 -> bits 56..111
+      const uint32_t b16 = (x16[p >> 2] >> (8 * (p & 3))) & 0xFEu;
+      const uint32_t b17 = (x17[p >> 2] >> (8 * (p & 3))) & 0xFEu;
+      return make_uint4(lo.x, lo.y + hi.x * (1u << 24), (hi.x >> 8) + hi.y * (1u << 24),
+                        (hi.y >> 8) + b16 * (1u << 15) + b17 * (1u << 22));
+    };
     __syncwarp();
     if constexpr (BULK) {
       // SWIZZLE_128B box: tile byte b at row b / 128, 16-byte chunk
@@ -715,8 +730,14 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int ra = 2 * lane + (hi ? 1 : 0), rb = 2 * lane + (hi ? 0 : 1);
-          const uint4 lo4 = make_uint4(m[j][0], m[j][1], m[j][2], m[j][3]);
-          const uint4 hi4 = make_uint4(m[j + 8][0], m[j + 8][1], m[j + 8][2], m[j + 8][3]);
+          uint4 lo4, hi4;
+          if constexpr (S::OFFS) {
+            lo4 = ll_word16(j);
+            hi4 = ll_word16(j + 8);
+          } else {
+            lo4 = make_uint4(m[j][0], m[j][1], m[j][2], m[j][3]);
+            hi4 = make_uint4(m[j + 8][0], m[j + 8][1], m[j + 8][2], m[j + 8][3]);
+          }
           *reinterpret_cast<uint4*>(slot + ra * 128 + ((j ^ (ra & 7)) << 4)) = hi ? hi4 : lo4;
           *reinterpret_cast<uint4*>(slot + rb * 128 + ((j ^ (rb & 7)) << 4)) = hi ? lo4 : hi4;
         }
@@ -727,6 +748,9 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
           if constexpr (S::F64) {
             a = f64_word(2 * cc);
             b = f64_word(2 * cc + 1);
+          } else if constexpr (S::OFFS) {
+            a = ll_word8(2 * cc);
+            b = ll_word8(2 * cc + 1);
           } else {
             a = make_uint2(m[2 * cc][0], m[2 * cc][1]);
             b = make_uint2(m[2 * cc + 1][0], m[2 * cc + 1][1]);
@@ -763,17 +787,10 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
           }
           *reinterpret_cast<double*>(slot + (lane * 16 + sl) * 8) = acc;
         } else if constexpr (S::OFFS) {
-          const uint2 lo = pack7x8(m[p][0], m[p][1]);  // fields of images 0..7, bits 0..55
-          if constexpr (WC == 8) {  // lossless64: image 8's field at bit 56
-            *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) =
-                make_uint2(lo.x, lo.y + (m[p][2] & 0xFEu) * (1u << 23));
-          } else {  // lossless128: fields 0..15, images 16/17 at bits 112/119
-            const uint2 hi = pack7x8(m[p][2], m[p][3]);  // images 8..15 -> bits 56..111
-            const uint32_t b16 = (x16[p >> 2] >> (8 * (p & 3))) & 0xFEu;
-            const uint32_t b17 = (x17[p >> 2] >> (8 * (p & 3))) & 0xFEu;
-            *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) =
-                make_uint4(lo.x, lo.y + hi.x * (1u << 24), (hi.x >> 8) + hi.y * (1u << 24),
-                           (hi.y >> 8) + b16 * (1u << 15) + b17 * (1u << 22));
+          if constexpr (WC == 8) {
+            *reinterpret_cast<uint2*>(slot + (lane * 16 + sl) * 8) = ll_word8(p);
+          } else {
+            *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = ll_word16(p);
           }
         } else if constexpr (WC == 16) {
           *reinterpret_cast<uint4*>(slot + (lane * 16 + sl) * 16) = make_uint4(m[p][0], m[p][1], m[p][2], m[p][3]);
@@ -1670,10 +1687,16 @@ cudaError_t enc_bulk_launch(const CUtensorMap& cm, const Geom& g, const RowSrc& 
 template <int MODE, bool PTRS>
 cudaError_t enc_vec_t(const Geom& g, const RowSrc& rs, void* cont, uint8_t* offs, cudaStream_t s, int sms,
                       uint64_t* launches) {
-  if constexpr (!VecMode<MODE>::OFFS) {
+  // lossless128 keeps the per-lane container stores (C3 n=18: 73.4 us
+  // against 75.7 with bulk stores); lossless64 gains (79.9 -> 75.4 us)
+  if constexpr (MODE != OPTB_LOSSLESS128) {
     CUtensorMap cm;
     if (encode_bulk_enabled() && !g_sysmem && container_map(&cm, cont, g.chunks * g.P * VecMode<MODE>::WC, VecMode<MODE>::WC)) {
-      if (split_deep(g, sms)) return enc_bulk_launch<MODE, PTRS, true>(cm, g, rs, cont, offs, s, sms, launches);
+      // lossless (integer-pipe bound) keeps 8 x 2 at every size: the deep
+      // shape's register budget leaves one 6-warp CTA per SM (C3 n=9 74 ->
+      // 87 us), too few warps to hide the ALU dependency chains
+      if (!VecMode<MODE>::OFFS && split_deep(g, sms))
+        return enc_bulk_launch<MODE, PTRS, true>(cm, g, rs, cont, offs, s, sms, launches);
       return enc_bulk_launch<MODE, PTRS, false>(cm, g, rs, cont, offs, s, sms, launches);
     }
   }
