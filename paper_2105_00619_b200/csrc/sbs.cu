@@ -23,6 +23,7 @@
 //   K10  k_gather: the class-major draws of any subset of batches (sharding).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -262,10 +263,17 @@ __global__ void __launch_bounds__(64) k_shuffle(ChainArgs a, int use_smem) {
 // memory -- no serial swap loop (tests/test_chain_model.py and the GPU parity
 // tests pin it against the reference sequence).
 constexpr int kParThreads = 256;
+// Threads per CTA of K9a / K9b when a call carries many generations per
+// class (a rank drawing the stream of N ranks): each CTA's chain of
+// dependent shared-memory passes is latency bound, so 4x the threads cut
+// the per-CTA time, and these CTAs only run in the gaps the persistent codec
+// kernel leaves.
+constexpr int kParThreadsWide = 1024;
 constexpr uint32_t kParMaxM = 11776;  // 18 bytes of shared memory per element
 
 size_t par_smem_bytes(uint32_t m) { return 4ull * (4ull * m + 2) + 2ull * (m + 2); }
 
+template <int T>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -277,13 +285,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
   if (lane == 31) warp_tot[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = lane < kParThreads / 32 ? warp_tot[lane] : 0u;
+    uint32_t w = lane < T / 32 ? warp_tot[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    if (lane < kParThreads / 32) warp_tot[lane] = w;
+    if (lane < T / 32) warp_tot[lane] = w;
   }
   __syncthreads();
   const uint32_t before = warp ? warp_tot[warp - 1] : 0u;
@@ -301,9 +309,10 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
 // parallel Fisher-Yates plus one gather per generation, instead of one
 // Fisher-Yates per generation: it stays flat when a rank draws the batches
 // of all N ranks per step (N-GPU runs).
-__global__ void __launch_bounds__(kParThreads) k_fy_gen(ChainArgs a) {
+template <int T>
+__global__ void __launch_bounds__(T) k_fy_gen(ChainArgs a) {
   extern __shared__ uint32_t sh[];
-  __shared__ uint32_t warp_tot[kParThreads / 32];
+  __shared__ uint32_t warp_tot[T / 32];
   if (*a.chain != a.expect_start) return;  // stale host seeds: K9b flags, K8 redoes serially
   const uint32_t e = a.cls_list[blockIdx.x];
   const SbsEvent E = a.ev[e];
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(kParThreads) k_fy_gen(ChainArgs a) {
   uint32_t* bk = off + (m + 1);    // [m]      steps bucketed by target
   uint16_t* cnt = reinterpret_cast<uint16_t*>(bk + m);  // [m] bucket sizes
   const uint64_t s = a.seeds[e];
-  const uint32_t per = (m + kParThreads - 1) / kParThreads;
+  const uint32_t per = (m + T - 1) / T;
   const uint32_t lo = min(m, threadIdx.x * per), hi = min(m, lo + per);
   bool rej = false;
   for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) cnt[x] = 0;
@@ -331,7 +340,7 @@ __global__ void __launch_bounds__(kParThreads) k_fy_gen(ChainArgs a) {
   }
   uint32_t local = 0;
   for (uint32_t x = lo; x < hi; ++x) local += cnt[x];
-  uint32_t run = block_exclusive_scan(local, warp_tot);
+  uint32_t run = block_exclusive_scan<T>(local, warp_tot);
   for (uint32_t x = lo; x < hi; ++x) {
     off[x] = run;
     run += cnt[x];
@@ -435,7 +444,8 @@ __global__ void __launch_bounds__(kFyWarps * 32) k_fy_gen_warp(ChainArgs a, uint
 // prefetch != 0: the class's generations fit in shared memory after the two
 // permutation buffers, and are all loaded in one sweep (every load in flight
 // at once) before the composition, which then runs from shared memory only.
-__global__ void __launch_bounds__(kParThreads) k_compose(ChainArgs a, int prefetch) {
+template <int T>
+__global__ void __launch_bounds__(T) k_compose(ChainArgs a, int prefetch) {
   extern __shared__ uint32_t sh[];
   const uint32_t b = a.cls_begin[blockIdx.x], end = a.cls_begin[blockIdx.x + 1];
   const SbsEvent first = a.ev[a.cls_list[b]];
@@ -609,14 +619,21 @@ cudaError_t launch_class_index(const int32_t* labels, uint64_t n, uint64_t C,
 cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen, uint32_t max_m,
                               uint64_t max_gen_words, int force, cudaStream_t s, uint64_t* launches) {
   if (n_cls > 0 && max_m != 0xffffffffu && max_m <= kParMaxM) {
-    cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(k_fy_gen),
-                                      static_cast<int>(par_smem_bytes(kParMaxM)));
+    // wide CTAs from 4 generations per class (OPTB_SBS_WIDE=0|1 forces)
+    static const int wide_env = [] {
+      const char* v = getenv("OPTB_SBS_WIDE");
+      return v && v[0] ? (v[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool wide = wide_env >= 0 ? wide_env == 1 : true;
+    auto fy = wide ? k_fy_gen<kParThreadsWide> : k_fy_gen<kParThreads>;
+    auto comp = wide ? k_compose<kParThreadsWide> : k_compose<kParThreads>;
+    cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(fy), static_cast<int>(par_smem_bytes(kParMaxM)));
     if (ae != cudaSuccess) return ae;
     // prefetch the generations into shared memory when the largest class's
     // (gens x m) words fit in 64 KB beside the two permutation buffers
     const size_t pref = static_cast<size_t>(max_gen_words) * 4 <= 64 * 1024 ? static_cast<size_t>(max_gen_words) * 4 : 0;
     const size_t csmem = 8 * static_cast<size_t>(max_m) + pref;
-    ae = ensure_smem_attr(reinterpret_cast<const void*>(k_compose), static_cast<int>(8 * kParMaxM + 64 * 1024));
+    ae = ensure_smem_attr(reinterpret_cast<const void*>(comp), static_cast<int>(8 * kParMaxM + 64 * 1024));
     if (ae != cudaSuccess) return ae;
     if (max_m <= kFyWarpMaxM) {
       ae = ensure_smem_attr(reinterpret_cast<const void*>(k_fy_gen_warp),
@@ -625,9 +642,9 @@ cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen
       k_fy_gen_warp<<<(n_gen + kFyWarps - 1) / kFyWarps, kFyWarps * 32, fy_warp_smem_bytes(max_m), s>>>(a, n_gen,
                                                                                                       max_m);
     } else {
-      k_fy_gen<<<n_gen, kParThreads, par_smem_bytes(max_m), s>>>(a);
+      fy<<<n_gen, wide ? kParThreadsWide : kParThreads, par_smem_bytes(max_m), s>>>(a);
     }
-    k_compose<<<n_cls, kParThreads, csmem, s>>>(a, pref ? 1 : 0);
+    comp<<<n_cls, wide ? kParThreadsWide : kParThreads, csmem, s>>>(a, pref ? 1 : 0);
     *launches += 2;
   } else if (n_cls > 0) {
     size_t smem = (kJWin + static_cast<size_t>(max_m)) * sizeof(uint32_t);
