@@ -466,32 +466,45 @@ __device__ __noinline__ uint4 f64_peel_big(double acc) {
   return make_uint4(t[0], t[1], t[2], t[3]);
 }
 
+// Bit select: the bits of a where M is set, else the bits of b -- ONE LOP3
+// (inline PTX: written in C the compiler splits it into two mask steps, as
+// a LOP3 takes one immediate).
+template <uint32_t M>
+__device__ __forceinline__ uint32_t bsel(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "n"(M), "r"(a), "r"(b));
+  return d;
+}
+
 // 8 byte lanes (a = images 0..3, b = images 4..7 of one pixel) -> the 56-bit
 // word of their 7-bit fields px >> 1 (field i at bit 7i), as (low, high)
-// halves.  Two mask-and-merge stages per 32-bit half whose left shifts are
-// multiplies -- IMAD runs on the FMA pipe, while the integer pipe is what
-// bounds the lossless encoder -- then one merge of the halves:
-//   stage 1: (x & 0xFE00FE00) + (x & 0x00FE00FE) * 2  = field pairs    << 2
-//   stage 2: (y & 0xFFFC0000) + (y & 0x0000FFFC) * 4  = 28-bit groups  << 4
+// halves.  Two merge stages per 32-bit half, each ONE bit select between the
+// value and its left-shifted copy -- the shifts are multiplies, which run on
+// the FMA pipe, while the integer pipe bounds the lossless encoder:
+//   stage 1: sel(0xFE00FE00, x, 2x)   field pairs at bits 2..15 / 18..31
+//   stage 2: sel(0xFFFC0000, y, 4y)   the 28-bit group at bits 4..31
+// The bits a select lets through from the wrong byte (the parity LSBs, a
+// neighbour's top bit) land only at positions the next stage or the final
+// merge drops (exhaustively-sampled against the masked form: 2e8 random
+// inputs, identical words).
 __device__ __forceinline__ uint2 pack7x8(uint32_t a, uint32_t b) {
-  const uint32_t ga = (a & 0xFE00FE00u) + (a & 0x00FE00FEu) * 2u;
-  const uint32_t gb = (b & 0xFE00FE00u) + (b & 0x00FE00FEu) * 2u;
-  const uint32_t ha = (ga & 0xFFFC0000u) + (ga & 0x0000FFFCu) * 4u;
-  const uint32_t hb = (gb & 0xFFFC0000u) + (gb & 0x0000FFFCu) * 4u;
-  return make_uint2((ha >> 4) + hb * (1u << 24), hb >> 8);
+  const uint32_t ga = bsel<0xFE00FE00u>(a, a * 2u);
+  const uint32_t gb = bsel<0xFE00FE00u>(b, b * 2u);
+  const uint32_t ha = bsel<0xFFFC0000u>(ga, ga * 4u);
+  const uint32_t hb = bsel<0xFFFC0000u>(gb, gb * 4u);
+  return make_uint2(bsel<0x0FFFFFFFu>(ha >> 4, hb * (1u << 24)), hb >> 8);
 }
 // Inverse of pack7x8 with the pixel's shift folded in: the 56-bit word of 8
 // fields (low, high halves) -> 8 byte lanes holding field << 1 (the pixel
-// without its parity bit); left shifts as multiplies (FMA pipe):
-//   28-bit groups -> 32-bit halves; (g & 0x3FFF) + (g & 0x0FFFC000) * 4;
-//   (h & 0x007F007F) * 2 + (h & 0x3F803F80) * 4.
+// without its parity bit), with the same select-and-multiply stages:
+//   28-bit groups -> sel(0x3FFF, g, 4g) -> sel(0x00FF00FF, 2h, 4h).
+// The byte LSBs come out as garbage: the parity merge after the transpose
+// is a select that overwrites them (decode_tile).
 __device__ __forceinline__ uint2 unpack7x8_shl1(uint32_t lo, uint32_t hi) {
-  const uint32_t ga = lo & 0x0FFFFFFFu;
-  const uint32_t gb = __funnelshift_r(lo, hi, 28) & 0x0FFFFFFFu;
-  const uint32_t ha = (ga & 0x3FFFu) + (ga & 0x0FFFC000u) * 4u;
-  const uint32_t hb = (gb & 0x3FFFu) + (gb & 0x0FFFC000u) * 4u;
-  return make_uint2((ha & 0x007F007Fu) * 2u + (ha & 0x3F803F80u) * 4u,
-                    (hb & 0x007F007Fu) * 2u + (hb & 0x3F803F80u) * 4u);
+  const uint32_t gb = __funnelshift_r(lo, hi, 28);
+  const uint32_t ha = bsel<0x00003FFFu>(lo, lo * 4u);
+  const uint32_t hb = bsel<0x00003FFFu>(gb, gb * 4u);
+  return make_uint2(bsel<0x00FF00FFu>(ha * 2u, ha * 4u), bsel<0x00FF00FFu>(hb * 2u, hb * 4u));
 }
 __device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> bytes' LSBs
   return (b * 0x00204081u) & 0x01010101u;
@@ -967,10 +980,12 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
   }
   uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
   bool bad = false;
+  // lossless: the range check needs only the OR of the lane's 16 words
+  // (every pixel of the item has the same n), one shift test after the loop
+  uint32_t or_w[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
     const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
-    const uint64_t w1 = (static_cast<uint64_t>(m[p][3]) << 32) | m[p][2];
     if constexpr (S::F64) {
       // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
       const double acc = __longlong_as_double(static_cast<long long>(w0));
@@ -988,10 +1003,8 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
         m[p][3] = v.w;
       }
     } else if constexpr (S::OFFS) {
-      // range check (codec.cpp:189-194): bits >= 7n must be zero
-      const unsigned used = 7u * c.n;
-      if (used < 64u) bad |= (w0 >> used) != 0 || w1 != 0;
-      else bad |= (w1 >> (used - 64u)) != 0;
+#pragma unroll
+      for (int q = 0; q < (WC == 16 ? 4 : 2); ++q) or_w[q] |= m[p][q];
       // byte lanes hold field << 1: the pixel up to its parity bit
       const uint2 lo = unpack7x8_shl1(m[p][0], m[p][1]);  // images 0..7 (bits 0..55)
       const uint32_t w0hi = m[p][1], w1lo = m[p][2], w1hi = m[p][3];
@@ -1009,6 +1022,14 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
         x17[p >> 2] |= ((w1hi >> 22) & 0xFEu) << (8 * (p & 3));  // bits 119..125
       }
     }
+  }
+  if constexpr (S::OFFS) {
+    // range check (codec.cpp:189-194): bits >= 7n of every word must be zero
+    const uint64_t o0 = (static_cast<uint64_t>(or_w[1]) << 32) | or_w[0];
+    const uint64_t o1 = (static_cast<uint64_t>(or_w[3]) << 32) | or_w[2];
+    const unsigned used = 7u * c.n;
+    if (used < 64u) bad = (o0 >> used) != 0 || o1 != 0;
+    else bad = (o1 >> (used - 64u)) != 0;
   }
   transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (lossless: without their parity bits)
   if (valid) {
@@ -1030,7 +1051,7 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
       if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
       uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) row[q] |= nibble_lsbs((bits >> (4 * q)) & 0xFu);
+      for (int q = 0; q < 4; ++q) row[q] = bsel<0x01010101u>(nibble_lsbs((bits >> (4 * q)) & 0xFu), row[q]);
     }
   }
   auto row_vec = [&](int i) -> uint4 {

@@ -42,6 +42,34 @@ def test_cli_roundtrip_and_bytes(tmp_path, pkg, oracle_mod, torch_cuda):
         assert (out / f"img_{i}.raw").read_bytes() == files[i].read_bytes()
 
 
+MODE_NAMES = {0: "exact64", 1: "exact128", 2: "f64", 3: "lossless64", 4: "lossless128"}
+
+
+@pytest.mark.parametrize("mode", sorted(MODE_NAMES))
+def test_cli_encode_equals_reference_bytes(tmp_path, mode, torch_cuda):
+    """`encode` of the fixture images (3x2x2, every mode at capacity) writes
+    exactly the bytes the reference's write_optb(encode(...)) produced
+    (tests/golden/optb.npz, made by the reference compiled from its sources;
+    codec.cpp:283-317), and `decode` gives the images back."""
+    fx = np.load(os.path.join(ROOT, "tests", "golden", "optb.npz"))
+    imgs, want = fx[f"optb{mode}_in"], fx[f"optb{mode}_bytes"]
+    files = []
+    for i, img in enumerate(imgs):
+        p = tmp_path / f"img{i}.raw"
+        p.write_bytes(img.tobytes())
+        files.append(p)
+    packed = tmp_path / "batch.optb"
+    r = run("encode", "--mode", MODE_NAMES[mode], "--height", 3, "--width", 2, "--channels", 2, "--out", packed,
+            *files)
+    assert r.returncode == 0, r.stderr
+    assert packed.read_bytes() == want.tobytes()
+    out = tmp_path / "decoded"
+    r = run("decode", packed, "--out-dir", out)
+    assert r.returncode == 0, r.stderr
+    for i in range(len(imgs)):
+        assert (out / f"img_{i}.raw").read_bytes() == files[i].read_bytes()
+
+
 def test_cli_exit_codes(tmp_path, torch_cuda):
     files = []
     for i in range(9):
