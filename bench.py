@@ -347,7 +347,7 @@ def b2b_time(torch, fn, stream, reps, warm=3):
 
 
 # ---------------------------------------------------------------- the other BASELINE configs
-def config_suite(torch, pkg, dev, stream, peak, quick=False):
+def config_suite(torch, pkg, dev, stream, peak, quick=False, only=None):
     """C1-C4 (and C2 with SBS) on this GPU: the fused round trip
     (optb_roundtrip_dev) and the separate encode / decode launches, each
     timed back to back over a working set larger than L2.  Fractions: HBM
@@ -360,6 +360,8 @@ def config_suite(torch, pkg, dev, stream, peak, quick=False):
     reps = 5 if quick else 10
 
     def case(name, mode, per_chunk, Pp, B, nb, out_dtype=None, scale=1.0, rotate=1):
+        if only and not any(o in name for o in only):
+            return
         out_dtype = out_dtype or torch.uint8
         L = C.layout(mode, per_chunk, Pp, B, nb)
         rows = B * nb
@@ -444,6 +446,8 @@ def config_suite(torch, pkg, dev, stream, peak, quick=False):
     # C2: the CIFAR-100 workload with SBS (the round-1 headline): 50 000
     # images, one epoch = 97 batches per step, draws 4 epochs per sampler call
     N2, nb2 = 50000, 50000 // BATCH
+    if only and not any(o in "C2_sbs" for o in only):
+        return res
     with torch.cuda.stream(stream):
         ctx = pkg._lib.context(dev.index)
         import ctypes as ct

@@ -498,16 +498,13 @@ __device__ __forceinline__ uint2 pack7x8(uint32_t a, uint32_t b) {
 // fields (low, high halves) -> 8 byte lanes holding field << 1 (the pixel
 // without its parity bit), with the same select-and-multiply stages:
 //   28-bit groups -> sel(0x3FFF, g, 4g) -> sel(0x00FF00FF, 2h, 4h).
-// The byte LSBs come out as garbage: the parity merge after the transpose
-// is a select that overwrites them (decode_tile).
+// The byte LSBs come out as garbage: the parity merge (a select, before the
+// transpose) overwrites them (decode_tile).
 __device__ __forceinline__ uint2 unpack7x8_shl1(uint32_t lo, uint32_t hi) {
   const uint32_t gb = __funnelshift_r(lo, hi, 28);
   const uint32_t ha = bsel<0x00003FFFu>(lo, lo * 4u);
   const uint32_t hb = bsel<0x00003FFFu>(gb, gb * 4u);
   return make_uint2(bsel<0x00FF00FFu>(ha * 2u, ha * 4u), bsel<0x00FF00FFu>(hb * 2u, hb * 4u));
-}
-__device__ __forceinline__ uint32_t nibble_lsbs(uint32_t b) {  // 4 bits -> bytes' LSBs
-  return (b * 0x00204081u) & 0x01010101u;
 }
 
 // PTRS: stream row r is read from the absolute address src.ptrs[r] (this
@@ -978,15 +975,92 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
       }
     }
   }
-  uint32_t x16[4] = {0, 0, 0, 0}, x17[4] = {0, 0, 0, 0};
+  // lossless: images NTD.. (lossless64: 8; lossless128: 16, 17) are built as
+  // rows directly (xr), the others go through the 16x16 transpose
+  constexpr int NTD = S::OFFS ? (WC == 8 ? 8 : 16) : S::NT;
+  uint32_t xr[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
   bool bad = false;
-  // lossless: the range check needs only the OR of the lane's 16 words
-  // (every pixel of the item has the same n), one shift test after the loop
-  uint32_t or_w[4] = {0, 0, 0, 0};
+  if constexpr (S::OFFS) {
+    // range check (codec.cpp:189-194): bits >= 7n of every word must be zero;
+    // every pixel of the item has the same n, so only the OR of the lane's
+    // 16 words is tested
+    uint32_t or_w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < 16; ++p)
+#pragma unroll
+      for (int q = 0; q < WC / 4; ++q) or_w[q] |= m[p][q];
+    const uint64_t o0 = (static_cast<uint64_t>(or_w[1]) << 32) | or_w[0];
+    const uint64_t o1 = (static_cast<uint64_t>(or_w[3]) << 32) | or_w[2];
+    const unsigned used = 7u * c.n;
+    if (used < 64u) bad = (o0 >> used) != 0 || o1 != 0;
+    else bad = (o1 >> (used - 64u)) != 0;
+    // the rows of the fields above bit 111 / 55, gathered bytewise from 4
+    // pixels' top words with PRMT (pixel = field << 1; the bit a multiply
+    // shifts into a byte's LSB is overwritten by the parity merge below):
+    //   lossless64 : image 8 = bits 56..62 = byte 3 of word 1 (bits 0..6)
+    //   lossless128: image 16 = bits 112..118 = byte 2 of word 3 (bits 0..6),
+    //                image 17 = bits 119..125 = byte 2 bit 7 + byte 3 bits 0..5
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if constexpr (WC == 8) {
+        const uint32_t t1 = __byte_perm(m[4 * q][1], m[4 * q + 1][1], 0x0073);
+        const uint32_t t2 = __byte_perm(m[4 * q + 2][1], m[4 * q + 3][1], 0x0073);
+        xr[0][q] = __byte_perm(t1, t2, 0x5410) * 2u;
+      } else {
+        const uint32_t t1 = __byte_perm(m[4 * q][3], m[4 * q + 1][3], 0x7632);
+        const uint32_t t2 = __byte_perm(m[4 * q + 2][3], m[4 * q + 3][3], 0x7632);
+        const uint32_t b2 = __byte_perm(t1, t2, 0x6420), b3 = __byte_perm(t1, t2, 0x7531);
+        xr[0][q] = b2 * 2u;
+        xr[1][q] = bsel<0xFCFCFCFCu>(b3 * 4u, b2 >> 6);
+      }
+    }
+    // images 0..7 (and 8..15): byte lanes of field << 1 per pixel
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const uint32_t w0hi = m[p][1], w1lo = m[p][2], w1hi = m[p][3];
+      const uint2 lo = unpack7x8_shl1(m[p][0], w0hi);
+      m[p][0] = lo.x;
+      m[p][1] = lo.y;
+      if constexpr (WC == 16) {  // bits 56..111 = (w0 >> 56) | (w1 << 8)
+        const uint2 hi = unpack7x8_shl1(__funnelshift_r(w0hi, w1lo, 24), __funnelshift_r(w1lo, w1hi, 24));
+        m[p][2] = hi.x;
+        m[p][3] = hi.y;
+      } else {
+        m[p][2] = m[p][3] = 0u;
+      }
+    }
+    // parity bits (codec.cpp:196-201), merged into the byte LSBs BEFORE the
+    // transpose: lane's 16 bits of image i (read for every image: rows past
+    // the chunk's n are never stored); per group of 4 images, PRMT gathers
+    // the bits of pixels 0..7 (L) and 8..15 (H) one byte per image, so pixel
+    // p's 4 parity bits are (L >> p) & 0x01010101 -- the shift as a
+    // multiply-high on the FMA pipe, the merge one LOP3
+    uint32_t bits[S::NI];
+#pragma unroll
+    for (int i = 0; i < S::NI; ++i) bits[i] = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
+#pragma unroll
+    for (int g4 = 0; g4 < NTD / 4; ++g4) {
+      const uint32_t A = __byte_perm(bits[4 * g4], bits[4 * g4 + 1], 0x5140);
+      const uint32_t B = __byte_perm(bits[4 * g4 + 2], bits[4 * g4 + 3], 0x5140);
+      const uint32_t L = __byte_perm(A, B, 0x5410), H = __byte_perm(A, B, 0x7632);
+      m[0][g4] = bsel<0x01010101u>(L, m[0][g4]);
+      m[8][g4] = bsel<0x01010101u>(H, m[8][g4]);
+#pragma unroll
+      for (int p = 1; p < 8; ++p) {
+        m[p][g4] = bsel<0x01010101u>(__umulhi(L, 1u << (32 - p)), m[p][g4]);
+        m[p + 8][g4] = bsel<0x01010101u>(__umulhi(H, 1u << (32 - p)), m[p + 8][g4]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < S::NI - NTD; ++x)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        xr[x][q] = bsel<0x01010101u>(((bits[NTD + x] >> (4 * q)) & 0xFu) * 0x00204081u, xr[x][q]);
+  }
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
-    const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
     if constexpr (S::F64) {
+      const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
       // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
       const double acc = __longlong_as_double(static_cast<long long>(w0));
       bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
@@ -1002,36 +1076,9 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
         m[p][2] = v.z;
         m[p][3] = v.w;
       }
-    } else if constexpr (S::OFFS) {
-#pragma unroll
-      for (int q = 0; q < (WC == 16 ? 4 : 2); ++q) or_w[q] |= m[p][q];
-      // byte lanes hold field << 1: the pixel up to its parity bit
-      const uint2 lo = unpack7x8_shl1(m[p][0], m[p][1]);  // images 0..7 (bits 0..55)
-      const uint32_t w0hi = m[p][1], w1lo = m[p][2], w1hi = m[p][3];
-      m[p][0] = lo.x;
-      m[p][1] = lo.y;
-      if constexpr (WC == 8) {
-        m[p][2] = (w0hi >> 23) & 0xFEu;  // image 8 (bits 56..62)
-        m[p][3] = 0u;
-      } else {
-        // images 8..15: bits 56..111 = (w0 >> 56) | (w1 << 8)
-        const uint2 hi = unpack7x8_shl1(__funnelshift_r(w0hi, w1lo, 24), __funnelshift_r(w1lo, w1hi, 24));
-        m[p][2] = hi.x;
-        m[p][3] = hi.y;
-        x16[p >> 2] |= ((w1hi >> 15) & 0xFEu) << (8 * (p & 3));  // bits 112..118
-        x17[p >> 2] |= ((w1hi >> 22) & 0xFEu) << (8 * (p & 3));  // bits 119..125
-      }
     }
   }
-  if constexpr (S::OFFS) {
-    // range check (codec.cpp:189-194): bits >= 7n of every word must be zero
-    const uint64_t o0 = (static_cast<uint64_t>(or_w[1]) << 32) | or_w[0];
-    const uint64_t o1 = (static_cast<uint64_t>(or_w[3]) << 32) | or_w[2];
-    const unsigned used = 7u * c.n;
-    if (used < 64u) bad = (o0 >> used) != 0 || o1 != 0;
-    else bad = (o1 >> (used - 64u)) != 0;
-  }
-  transpose16<16, S::NT>(m);  // m[i] = 16 pixels of image i (lossless: without their parity bits)
+  transpose16<16, NTD>(m);  // m[i] = 16 pixels of image i < NTD
   if (valid) {
     if constexpr (!S::OFFS && !S::F64) {
       // range check (codec.cpp:189-194): bytes of images >= n must be zero
@@ -1043,28 +1090,19 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
     }
     if (bad) latch_error(err, S::F64 ? kErrF64Range : kErrIntRange, g.chunk_base + k, c.n);
   }
-  if constexpr (S::OFFS) {
-    // pixel = (field << 1) | parity (codec.cpp:196-201); the shift is already in
-#pragma unroll
-    for (int i = 0; i < S::NI; ++i) {
-      uint32_t bits = 0;
-      if (valid && i < static_cast<int>(c.n)) bits = *reinterpret_cast<const uint16_t*>(slot + S::WORDS_B + i * 64 + lane * 2);
-      uint32_t* row = i < 16 ? m[i < 16 ? i : 0] : (i == 16 ? x16 : x17);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) row[q] = bsel<0x01010101u>(nibble_lsbs((bits >> (4 * q)) & 0xFu), row[q]);
-    }
-  }
   auto row_vec = [&](int i) -> uint4 {
-    if (i < 16) return make_uint4(m[i < 16 ? i : 0][0], m[i < 16 ? i : 0][1], m[i < 16 ? i : 0][2], m[i < 16 ? i : 0][3]);
-    if (i == 16) return make_uint4(x16[0], x16[1], x16[2], x16[3]);
-    return make_uint4(x17[0], x17[1], x17[2], x17[3]);
+    if (i < NTD) return make_uint4(m[i < NTD ? i : 0][0], m[i < NTD ? i : 0][1], m[i < NTD ? i : 0][2], m[i < NTD ? i : 0][3]);
+    const int x = i - NTD < 2 ? i - NTD : 0;
+    return make_uint4(xr[x][0], xr[x][1], xr[x][2], xr[x][3]);
   };
   if constexpr (O == OPTB_OUT_U8) {
     if (valid) {
+      uint8_t* dst = static_cast<uint8_t*>(out) + c.r0 * ostride + gi * 16;
 #pragma unroll
-      for (int i = 0; i < S::NI; ++i)
-        if (i < static_cast<int>(c.n))
-          stg16(static_cast<uint8_t*>(out) + (c.r0 + i) * ostride + gi * 16, row_vec(i));
+      for (int i = 0; i < S::NI; ++i) {
+        if (i < static_cast<int>(c.n)) stg16(dst, row_vec(i));
+        dst += ostride;
+      }
     }
   } else {
     __syncwarp();  // all lanes done reading the slot

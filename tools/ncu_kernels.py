@@ -9,6 +9,7 @@ Cases (each launched twice; ncu replays every launch with a cold L2):
   C5  pipeline step (SBS kernels + k_roundtrip_il<exact128,u8>) at 2^20 images
   C1  exact64 fused -> u8 / fp32
   C3  lossless64 n=9 / lossless128 n=18 / f64 n=6: encode, decode, fused
+  C3L lossless64 / lossless128: split encode + decode only
   C4  ImageNet exact128: fused -> bf16, split encode + decode -> bf16
   K7  class index over 2^20 labels
   io  record loader (CHW -> HWC), 4096 CIFAR records
@@ -77,6 +78,9 @@ def main():
             codec(3, 9, 3072, 4096, 16)
             codec(4, 18, 3072, 4096, 16)
             codec(2, 6, 3072, 4096, 16)
+        if want("C3L"):  # lossless split kernels only (source-level captures)
+            codec(3, 9, 3072, 4096, 16, fused=False)
+            codec(4, 18, 3072, 4096, 16, fused=False)
         if want("C4"):
             codec(1, 16, 224 * 224 * 3, 256, 1, torch.bfloat16)
         if want("K7"):
