@@ -580,7 +580,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--sharded-steps", type=int, default=3,
                     help="N > 1 only: steps of the dataset-sharded variants")
     ap.add_argument("--no-cpu-baseline", action="store_true")
