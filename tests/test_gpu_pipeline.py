@@ -301,3 +301,55 @@ def test_pipeline_warm_start_vs_oracle(pkg, oracle_mod, torch_cuda, tmp_path):
         warm.close()
     with pytest.raises(pkg.errors.FormatError):
         Pipeline.warm(1, B, nb, shape, str(tmp_path / "missing"), 0)
+
+
+@pytest.mark.parametrize("mode,n", [(1, 12), (4, 10)])
+def test_pipeline_corrupt_epoch_fails_at_its_step(pkg, oracle_mod, torch_cuda, tmp_path, mode, n):
+    """Failure semantics (pipeline.cpp:60-82, 213-215; the reference's
+    test_pipeline.cpp:200-239): an epoch whose OPTB files pass the header
+    checks but hold a container value out of range for its chunk loads
+    fine, and the step that decodes it reports the reference's FormatError
+    at the next sync -- not earlier steps, which were clean; the latch is
+    cleared, so the pipeline keeps serving after the error."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    C = pkg.codec
+    S, labels, ds, p, offs, mem, ref = _setup(pkg, O, torch)
+    B, nb, P = 64, 3, 768
+    shape = C.ImageShape(16, 16, 3)
+    L = C.layout(mode, n, P, B, nb)
+    ref_ex, _ = ref.next(nb)
+    good_c, good_o = O.encode_stream(ds, ref_ex, mode, n, B, nb)
+    bad_c = good_c.copy()
+    # chunk 2, pixel 5: set a bit above the chunk's n packed images
+    wc = C.container_value_bytes(mode)
+    word = bad_c[(2 * P + 5) * wc:(2 * P + 6) * wc]
+    bit = 8 * 15 if mode == 1 else 7 * 17  # exact128: byte of image 15; lossless128: field of image 17
+    word[bit // 8] |= 1 << (bit % 8)
+    dirs = {}
+    for tag, c in (("good", good_c), ("bad", bad_c)):
+        cont, offs_ = C.alloc_stream(L)
+        cont[: c.size].copy_(torch.from_numpy(c))
+        if good_o is not None:
+            offs_[: good_o.size].copy_(torch.from_numpy(good_o))
+        dirs[tag] = tmp_path / tag
+        C.dump_dev(L, cont, offs_, shape, str(dirs[tag]), 0)
+    want = O.decode_stream(good_c, good_o, mode, n, P, B, nb)
+    o = torch.empty((B * nb, P), dtype=torch.uint8, device="cuda")
+    good = Pipeline.warm(mode, B, nb, shape, str(dirs["good"]), 0, per_chunk=n)
+    for _ in range(2):  # clean steps: no error
+        good.step(o)
+        C.sync()
+        assert np.array_equal(o.cpu().numpy(), want)
+    good.close()
+    bad = Pipeline.warm(mode, B, nb, shape, str(dirs["bad"]), 0, per_chunk=n)  # the header checks pass
+    bad.step(o)
+    with pytest.raises(pkg.errors.FormatError, match=f"^decode: container value exceeds range of {n} packed images$"):
+        C.sync()
+    C.sync()  # the latch is cleared after it was reported
+    bad.close()
+    good = Pipeline.warm(mode, B, nb, shape, str(dirs["good"]), 0, per_chunk=n)
+    good.step(o)
+    C.sync()
+    assert np.array_equal(o.cpu().numpy(), want)
+    good.close()
