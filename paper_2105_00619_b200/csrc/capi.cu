@@ -861,6 +861,7 @@ struct optb_sbs {
   unsigned int* diverged_d = nullptr;
   unsigned int diverged_seen = 0;
   uint8_t* d_static = nullptr;  // counts[C] prefix[C+1] size[C] row_cls[B]
+  uint64_t* d_recip = nullptr;  // [max_m + 1] reciprocals for the Fisher-Yates reductions (launch_recip_table)
   uint8_t* d_call = nullptr;    // per-call block (stream ordered reuse)
   size_t call_cap = 0;
   static constexpr int kRing = 4;  // pinned upload buffers in flight
@@ -1118,6 +1119,7 @@ int run_events(optb_sbs* s, const std::vector<EvKey>& keys, Packer& pk,
   a.expect_start = expect_start;
   a.expect_final = chain;
   a.diverged = s->diverged_d;
+  a.recip = s->d_recip;
   uint64_t max_gen_words = 0;
   for (uint64_t c = 0; c < C; ++c)
     if (!per[c].empty()) max_gen_words = std::max<uint64_t>(max_gen_words, per[c].size() * s->m[c]);
@@ -1220,6 +1222,17 @@ int optb_class_index_host(optb_ctx* c, const int32_t* labels, uint64_t n, uint64
   return rc;
 }
 
+namespace {
+// the reciprocal table of the parallel Fisher-Yates (one per sampler)
+int build_recip(optb_sbs* s, cudaStream_t st) {
+  if (!s->small_ids || s->max_m < 2) return OPTB_OK;
+  if (cudaMalloc(&s->d_recip, (static_cast<size_t>(s->max_m) + 1) * 8) != cudaSuccess)
+    return cuda_err(cudaGetLastError(), "sbs reciprocals");
+  const cudaError_t e = launch_recip_table(s->d_recip, s->max_m, st);
+  return e == cudaSuccess ? OPTB_OK : cuda_err(e, "sbs reciprocals");
+}
+}  // namespace
+
 int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B, uint64_t seed,
                     const uint64_t* class_offsets, const int64_t* members, int32_t on_dev,
                     optb_sbs** out) {
@@ -1297,6 +1310,8 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
         cudaMemcpy(s->d_static, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(cuda_err(cudaGetLastError(), "sbs static"));
   }
+  rc = build_recip(s, st);
+  if (rc) return fail(rc);
   const unsigned long long seed64 = seed;
   if (cudaMemcpy(s->d_chain, &seed64, 8, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(cuda_err(cudaGetLastError(), "sbs seed"));
@@ -1369,6 +1384,9 @@ int optb_sbs_clone(const optb_sbs* src, optb_sbs** out) {
         cudaMemcpy(s->d_static, src->d_static, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess)
       return fail(cuda_err(cudaGetLastError(), "sbs static"));
   }
+  rc = build_recip(s, c->s_compute);
+  if (rc) return fail(rc);
+  if (cudaStreamSynchronize(c->s_compute) != cudaSuccess) return fail(cuda_err(cudaGetLastError(), "sbs clone"));
   *out = s;
   g_err.clear();
   return OPTB_OK;
@@ -1381,6 +1399,7 @@ void optb_sbs_destroy(optb_sbs* s) {
   if (s->d_chain) cudaFree(s->d_chain);
   if (s->diverged_h) cudaFreeHost(s->diverged_h);
   if (s->d_static) cudaFree(s->d_static);
+  if (s->d_recip) cudaFree(s->d_recip);
   if (s->d_call) cudaFree(s->d_call);
   for (int r = 0; r < optb_sbs::kRing; ++r) {
     if (s->h_call[r]) cudaFreeHost(s->h_call[r]);

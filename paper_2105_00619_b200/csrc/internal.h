@@ -153,7 +153,12 @@ struct ChainArgs {
   // call is redone serially from the device state (the authority).
   uint64_t expect_start, expect_final;
   unsigned int* diverged;     // mapped host counter: serial redos that moved the chain off the host's walk
+  // [max_m + 1] floor((2^64 - 1) / i): next_below's x % i as a multiply-high
+  // and one correction in the parallel Fisher-Yates (nullptr: plain %)
+  const uint64_t* recip;
 };
+// fills recip[i] = floor((2^64 - 1) / i) for 2 <= i <= n (the sampler's table)
+cudaError_t launch_recip_table(uint64_t* recip, uint32_t n, cudaStream_t s);
 
 // k_fy_gen (one CTA per reshuffle event) + k_compose (one CTA per reshuffling
 // class), or k_shuffle (one CTA per class, large classes), then k_chain_finish

@@ -51,6 +51,24 @@ __device__ __forceinline__ bool rejected(uint64_t x, uint64_t n) {
   return x > below_limit(n);
 }
 
+// x % i (next_below's reduction, rng.hpp:29-35) for 2 <= i < 2^32: with
+// M = floor((2^64-1)/i), q = mulhi(x, M) is floor(x/i) or one less, so the
+// remainder needs one conditional subtraction (exhaustively edge-checked
+// against %; the sampler's parity tests cover it on the device).
+__device__ __forceinline__ uint32_t mod_below(uint64_t x, uint32_t i, const uint64_t* __restrict__ recip) {
+  if (!recip) return static_cast<uint32_t>(x % i);
+  const uint64_t q = __umul64hi(x, __ldg(recip + i));
+  uint64_t r = x - q * i;
+  if (r >= i) r -= i;
+  return static_cast<uint32_t>(r);
+}
+
+__global__ void k_recip(uint64_t* __restrict__ t, uint32_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i <= n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    t[i] = i >= 2 ? ~0ull / i : 0ull;
+}
+
 // ------------------------------------------------------------------ K7
 // Stable partition of [0,n) by label.  One warp per tile of kTile labels.
 constexpr int kTile = 1024;
@@ -330,7 +348,7 @@ __global__ void __launch_bounds__(T) k_fy_gen(ChainArgs a) {
   for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) {
     const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
     rej |= rejected(x, i);
-    const uint32_t j = static_cast<uint32_t>(x % i);
+    const uint32_t j = mod_below(x, i, a.recip);
     js[i] = j;
     atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
   }
@@ -394,7 +412,7 @@ __global__ void __launch_bounds__(kFyWarps * 32) k_fy_gen_warp(ChainArgs a, uint
   for (uint32_t i = 2 + lane; i <= m; i += 32) {
     const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
     rej |= rejected(x, i);
-    const uint32_t j = static_cast<uint32_t>(x % i);
+    const uint32_t j = mod_below(x, i, a.recip);
     js[i] = j;
     atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
   }
@@ -660,6 +678,12 @@ cudaError_t launch_sbs_events(const ChainArgs& a, uint32_t n_cls, uint32_t n_gen
   }
   k_chain_finish<<<1, 128, 0, s>>>(a, n_cls, force);
   ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_recip_table(uint64_t* recip, uint32_t n, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((static_cast<uint64_t>(n) + 256) / 256, 1184));
+  k_recip<<<grid, 256, 0, s>>>(recip, n);
   return cudaGetLastError();
 }
 
