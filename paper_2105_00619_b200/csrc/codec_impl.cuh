@@ -320,6 +320,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// shared-window address forms, for kernels short of registers: there the
+// generic -> shared conversion of a predicated access is rematerialised
+// (S2R + LEA) per access
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// 16-byte shared load if p, else zeros
+__device__ __forceinline__ uint4 lds16_if(uint32_t a, bool p) {
+  uint4 r = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("{.reg .pred q; setp.ne.b32 q, %4, 0; @q ld.shared.v4.u32 {%0,%1,%2,%3}, [%5];}"
+               : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+               : "r"(static_cast<uint32_t>(p)), "r"(a)
+               : "memory");
+  return r;
+}
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -552,6 +567,11 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   constexpr int WC = S::WC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* ring = smem_base + warp * warp_region;
+  // lossless64 (two CTAs per SM, 128 registers): the lane's shared-window
+  // address derived once, and the parity plane walked by pointer steps
+  // (C3 n=9 encode 76.0 -> 74.1 us); the other modes measured slower with it
+  constexpr bool SADDR = MODE == OPTB_LOSSLESS64;
+  const uint32_t ring_s = SADDR ? smem_u32(ring) + lane * 16 : 0u;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * NW * 32;
@@ -607,7 +627,11 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       if (i < static_cast<int>(pend_n)) {
         const uint8_t* row = PTRS ? reinterpret_cast<const uint8_t*>(static_cast<uintptr_t>(rows[i]))
                                   : images + static_cast<uint64_t>(rows[i]) * row_stride;
-        cp_async16(slot + i * 512 + lane * 16, row + pend_gi * 16);
+        if constexpr (SADDR) {
+          cp_async16_s(ring_s + stage * S::ENC_SLOT + i * 512, row + pend_gi * 16);
+        } else {
+          cp_async16(slot + i * 512 + lane * 16, row + pend_gi * 16);
+        }
       }
     }
     cp_async_commit();
@@ -641,7 +665,11 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
 #pragma unroll
     for (int i = 0; i < S::NI; ++i) {
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (i < static_cast<int>(n)) v = *reinterpret_cast<const uint4*>(slot + i * 512 + lane * 16);
+      if constexpr (SADDR) {
+        v = lds16_if(ring_s + stage * S::ENC_SLOT + i * 512, i < static_cast<int>(n));
+      } else if (i < static_cast<int>(n)) {
+        v = *reinterpret_cast<const uint4*>(slot + i * 512 + lane * 16);
+      }
       if constexpr (S::OFFS) {
         // parity bits of 16 pixels at plane bit i*P + 16*gi (codec.cpp:132-133);
         // images in [n, per_chunk) (partial chunk) write zeros so the padded
@@ -693,12 +721,15 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
       }
       if (t < items) {
         uint8_t* plane = offsets + k * g.ostride + 2 * gi;
+        const uint64_t pstep = g.P >> 3;  // P % 32 == 0 on the vector path
 #pragma unroll
         for (int i = 0; i < S::NT; ++i) {
           if (i < static_cast<int>(g.per_chunk)) {
             const uint32_t bits = __byte_perm(lo[i >> 2], hi[i >> 2], (i & 3) | (((i & 3) + 4) << 4));
-            *reinterpret_cast<uint16_t*>(plane + (static_cast<uint64_t>(i) * g.P) / 8) = static_cast<uint16_t>(bits);
+            uint8_t* dst = SADDR ? plane : offsets + k * g.ostride + 2 * gi + (static_cast<uint64_t>(i) * g.P) / 8;
+            *reinterpret_cast<uint16_t*>(dst) = static_cast<uint16_t>(bits);
           }
+          if constexpr (SADDR) plane += pstep;
         }
       }
     }
