@@ -179,3 +179,25 @@ def test_host_planner_matches_model():
         assert [int(x) for x in ev_g[:len(keys)]] == [k[2] for k in keys], trial
         assert [int(x) for x in ev_s[:len(keys)]] == seeds, trial
         assert ca.value == after, trial
+
+
+def test_reciprocal_reduction_identity():
+    """The parallel Fisher-Yates reduces next_below's x % i (rng.hpp:29-35)
+    as q = mulhi(x, floor((2^64-1)/i)), r = x - q*i, minus i once if r >= i
+    (sbs.cu mod_below): q is floor(x/i) or one less, so this is exact.
+    Checked here on edge values and random draws for every class size the
+    BASELINE configs use and beyond."""
+    import random
+    rng = random.Random(7)
+    M64 = (1 << 64) - 1
+
+    def fast(x, i):
+        q = (x * (M64 // i)) >> 64
+        r = x - q * i
+        assert 0 <= r < 2 * i
+        return r - i if r >= i else r
+    sizes = list(range(2, 2049)) + [10485, 10486, 500, 50000, (1 << 20) + 1, (1 << 31) + 11, (1 << 32) - 1]
+    for i in sizes:
+        edges = [0, 1, i - 1, i, M64, M64 - 1, 1 << 63, (M64 // i) * i, (M64 // i) * i - 1]
+        for x in edges + [rng.getrandbits(64) for _ in range(20)]:
+            assert fast(x, i) == x % i, (x, i)
