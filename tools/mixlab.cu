@@ -11,6 +11,7 @@
 //   r1w2     read N, write 2N          (the round trip's compulsory mix)
 //   r1w3     read N, write 3N
 //   bulk_*   the copy / r1w2 mixes moved by the bulk-copy (TMA) engine
+//   bulkld_* bulk loads into shared memory, 16-byte LSU stores out
 // each back to back over 3 rotating buffer sets (the next launch never finds
 // its inputs in L2), CUDA events, median of 20.
 //
@@ -122,6 +123,85 @@ __global__ void __launch_bounds__(32) k_bulk(const uint8_t* __restrict__ in, uin
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Bulk (TMA) loads, LSU stores: 128 threads; thread 0 streams CH-byte chunks
+// into the ring, every thread then stores its 128 bytes of the stage to the
+// NW outputs with 16-byte st.global.
+template <int NW>
+__global__ void __launch_bounds__(128) k_bulkld(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                uint64_t nbytes) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t bar[kS];
+  const uint64_t nch = nbytes / kCh;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kS; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + s)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto load = [&](uint64_t c, int s) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar + s)), "r"(kCh) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(su32(ring + s * kCh)), "l"(in + c * kCh), "r"(kCh), "r"(su32(bar + s)) : "memory");
+  };
+  const uint64_t c0 = blockIdx.x;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kS && c0 + s * gridDim.x < nch; ++s) load(c0 + s * gridDim.x, s);
+  uint32_t phase = 0;
+  int it = 0;
+  for (uint64_t c = c0; c < nch; c += gridDim.x, ++it) {
+    const int s = it % kS;
+    asm volatile("{.reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W;}"
+                 ::"r"(su32(bar + s)), "r"((phase >> s) & 1u) : "memory");
+    phase ^= 1u << s;
+#pragma unroll
+    for (int u = 0; u < static_cast<int>(kCh / (128 * 16)); ++u) {
+      const uint32_t off = (u * 128 + threadIdx.x) * 16;
+      const uint4 v = *reinterpret_cast<const uint4*>(ring + s * kCh + off);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) st(reinterpret_cast<uint4*>(out + w * nbytes + c * kCh + off), v);
+    }
+    __syncthreads();  // every thread has read the stage
+    const uint64_t cn = c + kS * static_cast<uint64_t>(gridDim.x);
+    if (threadIdx.x == 0 && cn < nch) load(cn, s);
+  }
+}
+
+template <int NW>
+void run_bulkld(const char* name, int sms, int per_sm, uint64_t n16, std::vector<uint4*>& ins,
+                std::vector<uint4*>& outs) {
+  const int grid = sms * per_sm;
+  const size_t smem = kS * kCh;
+  CK(cudaFuncSetAttribute(k_bulkld<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cudaEvent_t ev[21];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  const int sets = static_cast<int>(ins.size());
+  const uint64_t nb = n16 * 16 / kCh * kCh;
+  auto go = [&](int i) {
+    k_bulkld<NW><<<grid, 128, smem>>>(reinterpret_cast<const uint8_t*>(ins[i % sets]),
+                                      reinterpret_cast<uint8_t*>(outs[i % sets]), nb);
+  };
+  for (int i = 0; i < 3; ++i) go(i);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(ev[0]));
+  for (int i = 0; i < 20; ++i) {
+    go(i);
+    CK(cudaEventRecord(ev[i + 1]));
+  }
+  CK(cudaEventSynchronize(ev[20]));
+  CK(cudaGetLastError());
+  std::vector<float> t;
+  for (int i = 0; i < 20; ++i) {
+    float ms;
+    CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+    t.push_back(ms);
+  }
+  std::sort(t.begin(), t.end());
+  const double us = t[10] * 1e3;
+  const double rb = static_cast<double>(nb), wb = static_cast<double>(NW) * nb;
+  printf("{\"kernel\": \"%s\", \"grid\": \"%dx%d\", \"read_mb\": %.1f, \"write_mb\": %.1f, \"us\": %.2f, \"gbs\": %.1f}\n",
+         name, sms, per_sm, rb / 1e6, wb / 1e6, us, (rb + wb) / us / 1e3);
+  for (auto& e : ev) CK(cudaEventDestroy(e));
+}
+
 template <int NW>
 void run_bulk(const char* name, int sms, int per_sm, uint64_t n16, std::vector<uint4*>& ins, std::vector<uint4*>& outs) {
   const int grid = sms * per_sm;
@@ -226,6 +306,8 @@ int main(int argc, char** argv) {
   for (int per_sm : {2, 3}) {  // 64 KB rings: at most 3 CTAs per SM
     run_bulk<1>("bulk_copy", sms, per_sm, n16, ins, outs);
     run_bulk<2>("bulk_r1w2", sms, per_sm, n16, ins, outs);
+    run_bulkld<1>("bulkld_copy", sms, per_sm, n16, ins, outs);
+    run_bulkld<2>("bulkld_r1w2", sms, per_sm, n16, ins, outs);
   }
   for (int per_sm : {4, 8, 16}) {
     run<1, 0>("read", sms, per_sm, n16, ins, outs, sink);
