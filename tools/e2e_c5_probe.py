@@ -10,6 +10,8 @@ rows down per step):
                  double-buffered -- per step, for each K
   raw_chunked  : the same with each copy split into C pieces, the D2H piece j
                  waiting only for H2D piece j (finer interleave of directions)
+  raw_split    : C pieces each way, the step's D2H waiting for its whole H2D
+                 (the leg's real dependency: the kernel needs every row)
   step_host    : optb_pipeline_step_host, for each K
 Prints one JSON line.
 """
@@ -71,7 +73,7 @@ def main():
         torch.cuda.synchronize()
         res[f"raw_{name}_gbs"] = round(nbytes / e0.elapsed_time(e1) / 1e6, 1)
 
-    def pattern(K, C):
+    def pattern(K, C, lockstep=True):
         per = (nbytes + C - 1) // C
         origin, end = ev(), ev()
         # the leg's events: used[b] = "kernel" k done (after H2D(k) and
@@ -99,7 +101,7 @@ def main():
                 cs.wait_event(down_done[b])
             used[b].record(cs)
             for j, e in pieces:
-                down.wait_event(e)
+                down.wait_event(e if lockstep else pieces[-1][1])
                 with torch.cuda.stream(down):
                     host_out[b][j:j + per].copy_(d_out[b][j:j + per], non_blocking=True)
             down_done[b].record(down)
@@ -114,6 +116,7 @@ def main():
         res[f"raw_pattern_K{K}_ms"] = round(pattern(K, 1), 2)
         for C in [int(c) for c in args.chunks.split(",")]:
             res[f"raw_chunked{C}_K{K}_ms"] = round(pattern(K, C), 2)
+            res[f"raw_split{C}_K{K}_ms"] = round(pattern(K, C, lockstep=False), 2)
     del d_out
     if not args.skip_pipeline:
         import paper_2105_00619_b200 as pkg
