@@ -1,3 +1,10 @@
+#!/bin/bash
+# ab_vs_head.sh -- on the GPU box: the config sub-keys and the C5 headline of
+# the working tree's build against a HEAD build, two rounds, plus the codec /
+# pipeline GPU tests.  Prepare here first:
+#   git stash && python tools/build_variant.py head && git stash pop
+#   python -c "import __graft_entry__ as g; g.build()"
+#   gpurun -- 'bash tools/ab_vs_head.sh'
 python -m pytest tests -m gpu -x -q -k "codec or pipeline or fullsize or sharded" 2>&1 | tail -1
 for r in 1 2; do
 for v in new head; do
