@@ -287,9 +287,23 @@ constexpr int kParThreads = 256;
 // the per-CTA time, and these CTAs only run in the gaps the persistent codec
 // kernel leaves.
 constexpr int kParThreadsWide = 1024;
-constexpr uint32_t kParMaxM = 11776;  // 18 bytes of shared memory per element
+constexpr uint32_t kParMaxM = 11776;  // <= 65535: K9a's indices are 16-bit
 
-size_t par_smem_bytes(uint32_t m) { return 4ull * (4ull * m + 2) + 2ull * (m + 2); }
+// K9a's shared memory: four u16 arrays (js, off, bk, cnt) of m + 1 entries,
+// each rounded to an even count so every array is 4-byte aligned for the
+// packed 16-bit-pair atomics -- 8 bytes per element, so two 1024-thread CTAs
+// fit per SM at C5's class size (m ~ 10 486; 14 bytes per element and one
+// CTA per SM with 32-bit indices)
+__host__ __device__ inline uint32_t even_up(uint32_t n) { return (n + 1u) & ~1u; }
+size_t par_smem_bytes(uint32_t m) { return 2ull * 4ull * even_up(m + 1); }
+
+// ++a[x] on a u16 array through the packed u32 word holding it; returns the
+// old value (every entry stays below 2^16, so no carry crosses the halves)
+__device__ __forceinline__ uint32_t inc_u16(uint16_t* a, uint32_t x) {
+  const uint32_t sh = 16u * (x & 1u);
+  const uint32_t old = atomicAdd(reinterpret_cast<uint32_t*>(a) + (x >> 1), 1u << sh);
+  return (old >> sh) & 0xffffu;
+}
 
 template <int T>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot) {
@@ -335,22 +349,23 @@ __global__ void __launch_bounds__(T) k_fy_gen(ChainArgs a) {
   const uint32_t e = a.cls_list[blockIdx.x];
   const SbsEvent E = a.ev[e];
   const uint32_t m = E.m;
-  uint32_t* js = sh;               // [m + 1]  swap target of step i (i = 2..m)
-  uint32_t* off = js + (m + 1);    // [m + 1]  bucket starts, then ends
-  uint32_t* bk = off + (m + 1);    // [m]      steps bucketed by target
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(bk + m);  // [m] bucket sizes
+  const uint32_t span = even_up(m + 1);
+  uint16_t* js = reinterpret_cast<uint16_t*>(sh);  // [m + 1]  swap target of step i (i = 2..m)
+  uint16_t* off = js + span;                       // [m + 1]  bucket starts, then ends
+  uint16_t* bk = off + span;                       // [m]      steps bucketed by target
+  uint16_t* cnt = bk + span;                       // [m]      bucket sizes
   const uint64_t s = a.seeds[e];
   const uint32_t per = (m + T - 1) / T;
   const uint32_t lo = min(m, threadIdx.x * per), hi = min(m, lo + per);
   bool rej = false;
-  for (uint32_t x = threadIdx.x; x < m; x += blockDim.x) cnt[x] = 0;
+  for (uint32_t x = threadIdx.x; x < span / 2; x += blockDim.x) reinterpret_cast<uint32_t*>(cnt)[x] = 0u;
   __syncthreads();
   for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) {
     const uint64_t x = mix64(s + (static_cast<uint64_t>(m) - i + 1) * kGamma);
     rej |= rejected(x, i);
     const uint32_t j = mod_below(x, i, a.recip);
-    js[i] = j;
-    atomicAdd(reinterpret_cast<uint32_t*>(cnt) + (j >> 1), 1u << (16 * (j & 1)));
+    js[i] = static_cast<uint16_t>(j);
+    inc_u16(cnt, j);
   }
   if (__syncthreads_or(rej)) {
     if (threadIdx.x == 0) atomicExch(a.flag, 1u);
@@ -360,11 +375,11 @@ __global__ void __launch_bounds__(T) k_fy_gen(ChainArgs a) {
   for (uint32_t x = lo; x < hi; ++x) local += cnt[x];
   uint32_t run = block_exclusive_scan<T>(local, warp_tot);
   for (uint32_t x = lo; x < hi; ++x) {
-    off[x] = run;
+    off[x] = static_cast<uint16_t>(run);
     run += cnt[x];
   }
   __syncthreads();
-  for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) bk[atomicAdd(&off[js[i]], 1u)] = i;
+  for (uint32_t i = 2 + threadIdx.x; i <= m; i += blockDim.x) bk[inc_u16(off, js[i])] = static_cast<uint16_t>(i);
   __syncthreads();  // off[x] now holds the end of bucket x
   int64_t* gout = a.pool + E.slot;
   for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
