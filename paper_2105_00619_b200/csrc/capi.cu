@@ -1312,6 +1312,12 @@ int optb_sbs_create(optb_ctx* c, const uint64_t* counts, uint64_t C, uint64_t B,
   }
   rc = build_recip(s, st);
   if (rc) return fail(rc);
+  // pool and call blocks sized once for calls of up to 64 Ki draws (the
+  // drop-in cursor's largest ring refill): a growing caller then pays no
+  // synchronising reallocation inside a call (C2 stream: a 128-batch refill
+  // 2.5-11 ms -> the draw time)
+  rc = optb_b200::sbs_reserve(s, std::max<uint64_t>(1, (1ull << 16) / std::max<uint64_t>(B, 1)));
+  if (rc) return fail(rc);
   const unsigned long long seed64 = seed;
   if (cudaMemcpy(s->d_chain, &seed64, 8, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(cuda_err(cudaGetLastError(), "sbs seed"));
@@ -1385,6 +1391,8 @@ int optb_sbs_clone(const optb_sbs* src, optb_sbs** out) {
       return fail(cuda_err(cudaGetLastError(), "sbs static"));
   }
   rc = build_recip(s, c->s_compute);
+  if (rc) return fail(rc);
+  rc = optb_b200::sbs_reserve(s, std::max<uint64_t>(1, (1ull << 16) / std::max<uint64_t>(s->B, 1)));
   if (rc) return fail(rc);
   if (cudaStreamSynchronize(c->s_compute) != cudaSuccess) return fail(cuda_err(cudaGetLastError(), "sbs clone"));
   *out = s;
