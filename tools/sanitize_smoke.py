@@ -101,6 +101,17 @@ def main():
         ex, _ = cur.next_dev(300)
         oc = O.Cursor(O.sbs_plan([1 / 7] * 7, 21), ro, rm, 21, 5)
         assert np.array_equal(ex.cpu().numpy(), oc.next(300)[0])
+    # classes past the warp-per-event limit (m = 4 000): the 1 024-thread
+    # K9a with 16-bit indices and packed atomics, and K9b, several
+    # generations per class in one call
+    labels2 = (np.arange(40000) % 10).astype(np.int32)
+    offs2, mem2 = S.class_index_dev(labels2, 10)
+    ro2, rm2 = O.class_index(labels2, 10)
+    p2 = S.plan([0.1] * 10, 64, 9)
+    cur2 = S.BatchCursor.from_device_index(p2, offs2, mem2)
+    ex2, _ = cur2.next_dev(1500)
+    oc2 = O.Cursor(O.sbs_plan([0.1] * 10, 64), ro2, rm2, 64, 9)
+    assert np.array_equal(ex2.cpu().numpy(), oc2.next(1500)[0])
     ds = torch.randint(0, 256, (3000, 768), dtype=torch.uint8, device=dev)
     cur = S.BatchCursor.from_device_index(p, offs_d, mem_d)
     pipe = Pipeline(cur, ds, 1, 21, 4, steps_per_draw=2)
