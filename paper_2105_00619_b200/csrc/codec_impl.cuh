@@ -1441,7 +1441,8 @@ struct IlShape {
 #if defined(OPTB_IL_WARPS) && defined(OPTB_IL_STAGES)
   static constexpr int NW = OPTB_IL_WARPS, NS = OPTB_IL_STAGES;
 #else
-  static constexpr int NW = DEEP ? 5 : 8;
+  // lossless128: 6 warps (its 10 KB slots: 8 x 30 KB would exceed 227 KB)
+  static constexpr int NW = DEEP ? 5 : (MODE == OPTB_LOSSLESS128 ? 7 : 8);
   static constexpr int NS = DEEP ? 4 : 2;
 #endif
 };
@@ -1455,13 +1456,17 @@ struct IlRegion {
 #define OPTB_IL_DEEP_MAXREG 232  // 5 warps per SM: registers are free (C2 583 -> 591 M img/s)
 #endif
 template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP, bool BULK_ST>
-__global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : RtRegs<MODE, ONE_CTA>::VALUE))
+__global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : MODE == OPTB_LOSSLESS128 ? 255 : RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
   static_assert(IlRegion<MODE, DEEP>::ENC % 1024 == 0, "decode slot must stay 1024-aligned");
-  // exact / f64 only: lossless stays phase-ordered (see rt_vec_t)
-  static_assert(!VecMode<MODE>::OFFS, "interleaved round trip: exact and f64 modes");
   constexpr bool BULK = BULK_ST;
+  constexpr bool OFFS = VecMode<MODE>::OFFS;
+  // lossless: the tile's parity bits are reloaded with cp.async beside the
+  // words' TMA load, committed after the encode's gather of the next stage;
+  // with a 2-stage ring the encode's own wait (all but the newest group)
+  // completes them before the decode (see after_tile)
+  static_assert(!OFFS || (IlShape<MODE, DEEP>::NS == 2 && BULK_ST), "interleaved lossless: 2-stage ring, bulk stores");
   static_assert(IlRegion<MODE, DEEP>::SMEM <= 232448, "interleaved kernel: shared memory over the 227 KB limit");
   constexpr int WC = VecMode<MODE>::WC;
   constexpr int NW = IlShape<MODE, DEEP>::NW, NS = IlShape<MODE, DEEP>::NS;
@@ -1506,6 +1511,25 @@ __global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : RtRegs<MODE, ONE_CTA>:
     if (lane == 0) {
       mbar_expect_tx(bar, 512 * WC);
       tma_load_2d(dslot, &cmap, 0, static_cast<int>((tile * 16 * WC) >> 7), bar);
+    }
+    if constexpr (OFFS) {
+      // tile j's parity bits (written by this warp's lanes in the encode,
+      // ordered by the __syncwarp above): P % 512 == 0 (the launcher's
+      // condition), so image i's 512 bits are 64 contiguous plane bytes --
+      // four 16-byte L2 copies each (.cg: never a stale L1 line).  wd is
+      // tile j here (advanced past j-1 by the decode above).
+      constexpr int NI = VecMode<MODE>::NI;
+      const uint64_t k = wd.k, gi0 = wd.gi - lane;
+      const uint32_t n = walk_chunk(g, wd).n;
+      const uint8_t* plane = offsets + k * g.ostride + 2 * gi0;
+#pragma unroll
+      for (int j = lane; j < 4 * NI; j += 32) {
+        const int i = j >> 2, part = j & 3;
+        if (i < static_cast<int>(n))
+          cp_async16(dslot + VecMode<MODE>::WORDS_B + i * 64 + part * 16,
+                     plane + (static_cast<uint64_t>(i) * g.P) / 8 + part * 16);
+      }
+      cp_async_commit();
     }
     pending = true;
   };
@@ -1892,6 +1916,11 @@ cudaError_t rt_il_launch(const CUtensorMap& cm, const Geom& g, const RowSrc& rs,
   return cudaGetLastError();
 }
 
+bool il_lossless_enabled() {
+  const char* v = getenv("OPTB_IL_LOSSLESS");
+  return !(v && v[0] == '0');
+}
+
 // OPTB_RT_INTERLEAVE=0 selects the phase-ordered fused kernel for every mode
 // (A/B runs; the interleaved one is the default where it applies).
 bool rt_interleave_enabled() {  // read per call (probes switch it at run time)
@@ -1906,6 +1935,14 @@ cudaError_t rt_vec_t(const CUtensorMap& cm, const Geom& g, const RowSrc& rs, voi
   // bits as 64-byte bulk copies beside the words' TMA load) measured slower
   // for these integer-pipe-bound modes (C3 n=9: 138 -> 174 us, n=18: 148 ->
   // 164 us) and was dropped
+  if constexpr (VecMode<MODE>::OFFS) {
+    // lossless, P % 512 == 0: interleaved too (2-stage ring, one CTA per SM
+    // with 184 registers, parity bits reloaded from L2 beside the words).
+    // After the round-2 decode rewrite this beats the phase-ordered kernel
+    // (C3 n=9 132.6 -> 104.9 us); OPTB_IL_LOSSLESS=0 selects the latter.
+    if (rt_interleave_enabled() && il_lossless_enabled() && g.P % 512 == 0)
+      return rt_il_launch<MODE, O, PTRS, true, false>(cm, g, rs, cont, offs, e, out, err, s, sms, launches);
+  }
   if constexpr (!VecMode<MODE>::OFFS) {
     const uint64_t tiles = (g.chunks * (g.P / 16) + 31) / 32;
     const char* f = getenv("OPTB_IL_SHAPE");  // deep | wide: force a shape (tests, probes)

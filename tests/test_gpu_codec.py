@@ -267,7 +267,10 @@ def test_roundtrip_il_shapes_vs_oracle(pkg, oracle_mod, torch_cuda, monkeypatch,
 
 
 def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
-    """Vector geometries take the fused single launch (lossless with P % 512 == 0)."""
+    """Vector geometries take the fused single launch -- the interleaved
+    kernel, lossless included (P % 512 == 0); OPTB_IL_LOSSLESS=0 keeps the
+    lossless modes on the phase-ordered kernel, with identical containers."""
+    import os
     torch, C = torch_cuda, pkg.codec
     P, B, nb = 3072, 512, 2
     ds = torch.randint(0, 256, (B * nb, P), dtype=torch.uint8, device="cuda")
@@ -280,9 +283,20 @@ def test_roundtrip_dev_is_one_launch(pkg, torch_cuda):
         C.roundtrip_dev(L, ds, cont, out, offsets=offs)
         C.sync()
         assert pkg._lib.launches(0) - n0 == launches, mode
-        assert C.last_roundtrip_kind() == ("phase_ordered" if mode >= 3 else "interleaved"), mode
+        assert C.last_roundtrip_kind() == "interleaved", mode
         if pc <= C.capacity(mode):
             assert torch.equal(out, ds)
+        if mode >= 3:
+            cont2, offs2 = C.alloc_stream(L)
+            out2 = torch.empty_like(out)
+            os.environ["OPTB_IL_LOSSLESS"] = "0"
+            try:
+                C.roundtrip_dev(L, ds, cont2, out2, offsets=offs2)
+                C.sync()
+                assert C.last_roundtrip_kind() == "phase_ordered", mode
+            finally:
+                os.environ.pop("OPTB_IL_LOSSLESS", None)
+            assert torch.equal(cont2, cont) and torch.equal(offs2, offs) and torch.equal(out2, out), mode
     # off the vector path: two launches
     L = C.layout(1, 16, 108, 40, 2)
     cont, offs = C.alloc_stream(L)
