@@ -1441,8 +1441,7 @@ struct IlShape {
 #if defined(OPTB_IL_WARPS) && defined(OPTB_IL_STAGES)
   static constexpr int NW = OPTB_IL_WARPS, NS = OPTB_IL_STAGES;
 #else
-  // lossless128: 6 warps (its 10 KB slots: 8 x 30 KB would exceed 227 KB)
-  static constexpr int NW = DEEP ? 5 : (MODE == OPTB_LOSSLESS128 ? 7 : 8);
+  static constexpr int NW = DEEP ? 5 : 8;
   static constexpr int NS = DEEP ? 4 : 2;
 #endif
 };
@@ -1456,6 +1455,8 @@ struct IlRegion {
 #define OPTB_IL_DEEP_MAXREG 232  // 5 warps per SM: registers are free (C2 583 -> 591 M img/s)
 #endif
 template <int MODE, int O, bool PTRS, bool ONE_CTA, bool DEEP, bool BULK_ST>
+// lossless128 (18 staged rows, 2 x 9 KB ring + 10 KB decode slot per warp:
+// 8 warps fit in 225 KB) takes the full register file, 255 per thread
 __global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : MODE == OPTB_LOSSLESS128 ? 255 : RtRegs<MODE, ONE_CTA>::VALUE))
     k_roundtrip_il(const __grid_constant__ CUtensorMap cmap, Geom g, RowSrc src, uint8_t* __restrict__ cont,
                    uint8_t* __restrict__ offsets, Epi e, void* __restrict__ out, DevError* err) {
