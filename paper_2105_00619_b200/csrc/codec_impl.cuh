@@ -567,10 +567,14 @@ __device__ __forceinline__ void encode_body(const Geom& g, const RowSrc& src, ui
   constexpr int WC = S::WC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* ring = smem_base + warp * warp_region;
-  // lossless64 (two CTAs per SM, 128 registers): the lane's shared-window
-  // address derived once, and the parity plane walked by pointer steps
-  // (C3 n=9 encode 76.0 -> 74.1 us); the other modes measured slower with it
-  constexpr bool SADDR = MODE == OPTB_LOSSLESS64;
+  // the register-starved lossless bodies -- lossless64 (128 registers in the
+  // split encode) and lossless128 inside the interleaved kernel: the lane's
+  // shared-window address derived once (ncu: the per-access conversion was
+  // rematerialised, S2R + LEA per predicated row) and the parity plane walked
+  // by pointer steps.  C3 n=9 encode 76.0 -> 74.1 us, the n=18 interleaved
+  // round trip 115.1 -> 105.2 us; the split lossless128 encode (248
+  // registers) and the other modes measured slower with it
+  constexpr bool SADDR = MODE == OPTB_LOSSLESS64 || (MODE == OPTB_LOSSLESS128 && BULK);
   const uint32_t ring_s = SADDR ? smem_u32(ring) + lane * 16 : 0u;
   const uint64_t G = g.P / 16;
   const uint64_t items = g.chunks * G;
