@@ -11,6 +11,7 @@ Cases (each launched twice; ncu replays every launch with a cold L2):
   C3  lossless64 n=9 / lossless128 n=18 / f64 n=6: encode, decode, fused
   C3L lossless64 / lossless128: split encode + decode only
   C3LF lossless64 / lossless128: fused round trips only
+  C3FF f64 (n=6) / exact64 (n=8): fused round trips only
   C4  ImageNet exact128: fused -> bf16, split encode + decode -> bf16
   K7  class index over 2^20 labels
   io  record loader (CHW -> HWC), 4096 CIFAR records
@@ -79,6 +80,9 @@ def main():
             codec(3, 9, 3072, 4096, 16)
             codec(4, 18, 3072, 4096, 16)
             codec(2, 6, 3072, 4096, 16)
+        if want("C3FF"):  # f64 and exact64 fused round trips only (source-level captures)
+            codec(2, 6, 3072, 4096, 16, split=False)
+            codec(0, 8, 3072, 4096, 16, split=False)
         if want("C3LF"):  # lossless fused round trips only (source-level captures)
             codec(3, 9, 3072, 4096, 16, split=False)
             codec(4, 18, 3072, 4096, 16, split=False)
