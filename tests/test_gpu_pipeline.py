@@ -353,3 +353,43 @@ def test_pipeline_corrupt_epoch_fails_at_its_step(pkg, oracle_mod, torch_cuda, t
     C.sync()
     assert np.array_equal(o.cpu().numpy(), want)
     good.close()
+
+
+@pytest.mark.parametrize("mode,spd", [(3, 1), (4, 2)])
+def test_pipeline_lossless_interleaved_steps(pkg, oracle_mod, torch_cuda, mode, spd):
+    """Lossless pipeline steps on the interleaved round trip (P % 512 == 0),
+    enqueued back to back (early gather across steps): every step's rows,
+    containers and parity planes equal the oracle's."""
+    torch, O = torch_cuda, oracle_mod
+    from paper_2105_00619_b200.pipeline import Pipeline
+    C, S = pkg.codec, pkg.sampler
+    N, Ccls, B, nb, P = 4096, 10, 64, 20, 1024
+    labels = (np.arange(N) % Ccls).astype(np.int32)
+    ds = O.synth_pixels(5, 0, N, P)
+    offs, mem = S.class_index_dev(labels, Ccls)
+    cur = S.BatchCursor.from_device_index(S.plan([1.0 / Ccls] * Ccls, B, 77), offs, mem)
+    ro, rm = O.class_index(labels, Ccls)
+    ref = O.Cursor(O.sbs_plan([1.0 / Ccls] * Ccls, B), ro, rm, B, 77)
+    n = C.capacity(mode)
+    pipe = Pipeline(cur, torch.from_numpy(ds).cuda(), mode, B, nb, per_chunk=n, steps_per_draw=spd)
+    assert pipe.fused
+    s = torch.cuda.Stream()
+    outs = [torch.empty((B * nb, P), dtype=torch.uint8, device="cuda") for _ in range(4)]
+    with torch.cuda.stream(s):
+        for o in outs:
+            pipe.step(o, s)
+    s.synchronize()
+    assert C.last_roundtrip_kind() == "interleaved"
+    for k, o in enumerate(outs):
+        ex, _ = ref.next(nb)
+        assert np.array_equal(o.cpu().numpy(), ds[ex]), k
+    # the last step's containers, materialised in HBM as by two calls
+    want_c, _ = O.encode_stream(ds, ex, mode, n, B, nb)
+    nbytes = C.container_bytes(pipe.layout)
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (pipe.containers_ptr(), False),
+                                    "version": 3}
+    cont = torch.as_tensor(_Arr(), device="cuda").cpu().numpy()
+    assert np.array_equal(cont[: want_c.size], want_c)
+    pipe.close()
