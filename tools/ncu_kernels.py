@@ -12,6 +12,7 @@ Cases (each launched twice; ncu replays every launch with a cold L2):
   C3L lossless64 / lossless128: split encode + decode only
   C3LF lossless64 / lossless128: fused round trips only
   C3FF f64 (n=6) / exact64 (n=8): fused round trips only
+  C3S exact128 (n=16) / f64 (n=6): split encode + decode only
   C4  ImageNet exact128: fused -> bf16, split encode + decode -> bf16
   K7  class index over 2^20 labels
   io  record loader (CHW -> HWC), 4096 CIFAR records
@@ -80,6 +81,9 @@ def main():
             codec(3, 9, 3072, 4096, 16)
             codec(4, 18, 3072, 4096, 16)
             codec(2, 6, 3072, 4096, 16)
+        if want("C3S"):  # exact128 / f64 split encode + decode only (source-level captures)
+            codec(1, 16, 3072, 4096, 16, fused=False)
+            codec(2, 6, 3072, 4096, 16, fused=False)
         if want("C3FF"):  # f64 and exact64 fused round trips only (source-level captures)
             codec(2, 6, 3072, 4096, 16, split=False)
             codec(0, 8, 3072, 4096, 16, split=False)
