@@ -953,7 +953,9 @@ struct DecSlot {
 // (lane L: item wc.t + L) are in the warp's slot (TMA: the 128B-swizzled box;
 // else the XOR-swizzled cp.async layout, lossless parity bits after the
 // words).  Range checks, unpack, transpose, epilogue stores.
-template <int MODE, int O, bool TMA>
+// LEAN (the interleaved kernels, register-capped): the f64 peel in one
+// per-pixel pass instead of the two-pass branch-free form
+template <int MODE, int O, bool TMA, bool LEAN = false>
 __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint64_t items, uint8_t* slot,
                                             const Epi& e, void* __restrict__ out, DevError* err) {
   using S = VecMode<MODE>;
@@ -1092,14 +1094,48 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
       for (int q = 0; q < 4; ++q)
         xr[x][q] = bsel<0x01010101u>(((bits[NTD + x] >> (4 * q)) & 0xFu) * 0x00204081u, xr[x][q]);
   }
+  if constexpr (S::F64 && LEAN) {
+    // the interleaved kernels (register-capped): one per-pixel pass
 #pragma unroll
-  for (int p = 0; p < 16; ++p) {
-    if constexpr (S::F64) {
+    for (int p = 0; p < 16; ++p) {
       const uint64_t w0 = (static_cast<uint64_t>(m[p][1]) << 32) | m[p][0];
       // codec.cpp:163-170: negative / NaN always, >= 256^n only within capacity
       const double acc = __longlong_as_double(static_cast<long long>(w0));
       bad |= !(acc >= 0.0) || (c.n <= 6u && acc >= pow256(static_cast<int>(c.n)));
       if (acc < 0x1.0p64) {  // common case: the peel is the integer's bytes
+        const uint64_t iacc = static_cast<uint64_t>(acc);
+        m[p][0] = static_cast<uint32_t>(iacc);
+        m[p][1] = static_cast<uint32_t>(iacc >> 32);
+        m[p][2] = m[p][3] = 0u;
+      } else {
+        const uint4 v = f64_peel_big(acc);
+        m[p][0] = v.x;
+        m[p][1] = v.y;
+        m[p][2] = v.z;
+        m[p][3] = v.w;
+      }
+    }
+  } else if constexpr (S::F64) {
+    // codec.cpp:163-170: negative / NaN always, >= 256^n only within
+    // capacity (the bound hoisted out of the pixel loop; past capacity a NaN,
+    // which no comparison reaches, +inf included).  The peel of a value below
+    // 2^64 is its integer's bytes: a lane whose 16 values all are (the common
+    // case) converts them without a branch per pixel; otherwise the
+    // per-pixel form with the out-of-line >= 2^64 peel.  (Split decode: C3
+    // n=6 85.2 -> 80.1 us; the register-capped interleaved kernel keeps the
+    // one-pass form above, slower with this one.)
+    const double lim = c.n <= 6u ? pow256(static_cast<int>(c.n)) : __longlong_as_double(0x7ff8000000000000ll);
+    bool big = false;
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const double acc = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m[p][1]) << 32) | m[p][0]));
+      bad |= !(acc >= 0.0) | (acc >= lim);
+      big |= !(acc < 0x1.0p64);
+    }
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const double acc = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m[p][1]) << 32) | m[p][0]));
+      if (!big || acc < 0x1.0p64) {
         const uint64_t iacc = static_cast<uint64_t>(acc);
         m[p][0] = static_cast<uint32_t>(iacc);
         m[p][1] = static_cast<uint32_t>(iacc >> 32);
@@ -1504,7 +1540,7 @@ __global__ void __maxnreg__((DEEP ? OPTB_IL_DEEP_MAXREG : MODE == OPTB_LOSSLESS1
   auto decode_pending = [&]() {
     mbar_wait(bar, phase);
     phase ^= 1u;
-    decode_tile<MODE, O, true>(g, wd, items, dslot, e, out, err);  // ends with __syncwarp
+    decode_tile<MODE, O, true, true>(g, wd, items, dslot, e, out, err);  // ends with __syncwarp
     walk_advance(wd, step, g, G);
   };
   auto after_tile = [&](uint64_t tile) {
