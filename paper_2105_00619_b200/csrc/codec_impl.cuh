@@ -954,7 +954,8 @@ struct DecSlot {
 // else the XOR-swizzled cp.async layout, lossless parity bits after the
 // words).  Range checks, unpack, transpose, epilogue stores.
 // LEAN (the interleaved kernels, register-capped): the f64 peel in one
-// per-pixel pass instead of the two-pass branch-free form
+// per-pixel pass instead of the two-pass branch-free form, and the float
+// epilogue's full-chunk rows without per-row predicates
 template <int MODE, int O, bool TMA, bool LEAN = false>
 __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint64_t items, uint8_t* slot,
                                             const Epi& e, void* __restrict__ out, DevError* err) {
@@ -1213,7 +1214,17 @@ __device__ __forceinline__ void decode_tile(const Geom& g, const Walk& wc, uint6
       };
       if (!e.class_scale) {  // one scale for every row (the runner's kPixelScale)
         const PxScale sc = px_scale(e.scale, 0.0f, false);
-        if (sc.fast) {
+        if (LEAN && sc.fast && nL == static_cast<uint32_t>(S::NI)) {
+          // the interleaved kernels, a full chunk (the common case):
+          // straight-line stores, no per-row predicate and branch (ncu: ~100
+          // instructions per tile; C4 bf16 one batch per launch 27.6 -> 26.8
+          // us).  The split decode measured slower with it (deep shape).
+#pragma unroll
+          for (int i = 0; i < S::NI; ++i) {
+            put_row(dst, i, sc, std::true_type{});
+            dst += dstep;
+          }
+        } else if (sc.fast) {
 #pragma unroll
           for (int i = 0; i < S::NI; ++i) {
             if (i < static_cast<int>(nL)) put_row(dst, i, sc, std::true_type{});

@@ -13,6 +13,7 @@ Cases (each launched twice; ncu replays every launch with a cold L2):
   C3LF lossless64 / lossless128: fused round trips only
   C3FF f64 (n=6) / exact64 (n=8): fused round trips only
   C3S exact128 (n=16) / f64 (n=6): split encode + decode only
+  C1S exact64 -> u8 / fp32 and C4 exact128 -> bf16 (8 batches): split only
   C4  ImageNet exact128: fused -> bf16, split encode + decode -> bf16
   K7  class index over 2^20 labels
   io  record loader (CHW -> HWC), 4096 CIFAR records
@@ -81,6 +82,10 @@ def main():
             codec(3, 9, 3072, 4096, 16)
             codec(4, 18, 3072, 4096, 16)
             codec(2, 6, 3072, 4096, 16)
+        if want("C1S"):  # exact64 split encode + decode (u8, fp32) and the C4 bf16 split pair
+            codec(0, 8, 3072, 128, 512, fused=False)
+            codec(0, 8, 3072, 128, 512, torch.float32, fused=False)
+            codec(1, 16, 224 * 224 * 3, 256, 8, torch.bfloat16, fused=False)
         if want("C3S"):  # exact128 / f64 split encode + decode only (source-level captures)
             codec(1, 16, 3072, 4096, 16, fused=False)
             codec(2, 6, 3072, 4096, 16, fused=False)
