@@ -1493,8 +1493,9 @@ __global__ void __maxnreg__((RtRegs<MODE, ONE_CTA>::VALUE))
 // shapes (sweeps).
 template <int MODE, bool DEEP>
 struct IlShape {
-#if defined(OPTB_IL_WARPS) && defined(OPTB_IL_STAGES)
-  static constexpr int NW = OPTB_IL_WARPS, NS = OPTB_IL_STAGES;
+#if defined(OPTB_IL_WARPS) && defined(OPTB_IL_STAGES)  // sweeps of the deep shape
+  static constexpr int NW = DEEP ? OPTB_IL_WARPS : 8;
+  static constexpr int NS = DEEP ? OPTB_IL_STAGES : 2;
 #else
   static constexpr int NW = DEEP ? 5 : 8;
   static constexpr int NS = DEEP ? 4 : 2;
