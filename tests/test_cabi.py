@@ -102,3 +102,22 @@ def test_missing_library_fails_loudly(tmp_path):
     r = subprocess.run([sys.executable, "-c", "import paper_2105_00619_b200"], cwd=tmp_path,
                        capture_output=True, text=True)
     assert r.returncode != 0 and "liboptb_cuda.so is missing" in r.stderr
+
+
+def test_layout_arithmetic_matches_oracle(pkg, oracle_mod):
+    """The C ABI's stream layout (chunks per batch as runner.cpp:77-90 cuts
+    them, container and parity-plane bytes, the plane's 16-byte padded
+    stride) equals the oracle's for every mode over a grid of ragged shapes
+    -- the sizes every caller allocates from."""
+    C, O = pkg.codec, oracle_mod
+    for mode in range(5):
+        cap = C.capacity(mode)
+        for pc in sorted({1, 2, cap // 2 or 1, cap}):
+            for P, B, nb in ((48, 37, 5), (3072, 512, 2), (108, 40, 3), (1024, 7, 1), (150528, 256, 1)):
+                L = C.layout(mode, pc, P, B, nb)
+                chunks = O.stream_chunks(B, nb, pc)
+                assert C.layout_chunks(L) == chunks, (mode, pc, P, B, nb)
+                assert C.container_bytes(L) == chunks * P * C.container_value_bytes(mode)
+                ost = O.offsets_stride(mode, P, pc)
+                assert C.offsets_stride(mode, P, pc) == ost
+                assert C.offsets_bytes(L) == chunks * ost
