@@ -1693,11 +1693,14 @@ __global__ void __launch_bounds__(256) k_decode_generic(Geom g, const uint8_t* _
   constexpr unsigned PER = OFFS ? 7u : 8u;
   const uint64_t items = g.chunks * g.P;
   const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < items;
-       t += gstride) {
-    const uint64_t k = t / g.P;
-    const uint64_t p = t - k * g.P;
-    const ChunkPos c = chunk_pos(g, k);
+  // (chunk, pixel) of the thread's item advanced with adds and compares
+  Walk wk = walk_at(g, g.P, static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+  const WalkStep wstep = walk_step(g, g.P, gstride);
+  for (; wk.t < items; walk_advance(wk, wstep, g, g.P)) {
+    const uint64_t t = wk.t;
+    const uint64_t k = wk.k;
+    const uint64_t p = wk.gi;
+    const ChunkPos c = walk_chunk(g, wk);
     const uint8_t* w = cont + t * WC;
     if constexpr (MODE == OPTB_F64) {
       double acc = *reinterpret_cast<const double*>(w);
